@@ -1,0 +1,185 @@
+/* dfa2c.h — C-ABI drop-in boundary for DiTFastAttnV2's fused head-wise
+ * attention path on B200 (sm_100a).
+ *
+ * The reference (/root/reference/proj) exposes this path as the namespace
+ * `dfa2` C++ free-function API (include/dfa2/*.hpp, linked statically as
+ * dfa2_core). This header is the thin C layer the host C++ (include/dfa2/)
+ * and any FFI (ctypes, cgo, JNI) call. Plain pointers,
+ * sizes and integer status codes; no C++ or torch types cross it.
+ *
+ * Conventions
+ *  - Device tensors are bf16, contiguous row-major [batch, H, N, d] (the
+ *    reference's [H, N, d] per sample, inc/tensor.hpp:86-93, with a leading
+ *    batch axis; the reference runs one sample).
+ *  - Plans are host arrays: kinds[H] (DFA2C_FULL|ARROW|CACHED) and
+ *    windows[H] (Arrow window radius in blocks), mirroring HeadStrategy /
+ *    LayerPlan (inc/dispatch.hpp:12-37).
+ *  - Block masks are host uint8 [nb*nb], row-major, nb = ceil(N/B)
+ *    (BlockMask, inc/arrow.hpp:12-34).
+ *  - Every function returns a dfa2c_status; dfa2c_last_error() holds the
+ *    message of the last failure on the calling thread. Status codes mirror
+ *    the reference exception taxonomy (inc/errors.hpp:8-45). Validation is
+ *    complete before any device work or cache mutation, as in
+ *    src/dispatch.cpp:34-54.
+ *  - Calls that take a cudaStream_t (passed as void*) are asynchronous on
+ *    that stream unless stated otherwise; NULL means the legacy stream.
+ */
+#ifndef DFA2C_H
+#define DFA2C_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    DFA2C_OK = 0,
+    DFA2C_SHAPE = 1,        /* dfa2::ShapeError */
+    DFA2C_NONFINITE = 2,    /* dfa2::NonFiniteError */
+    DFA2C_FULLY_MASKED = 3, /* dfa2::FullyMaskedRowError */
+    DFA2C_CACHE_MISS = 4,   /* dfa2::CacheMissError */
+    DFA2C_DEGENERATE = 5,   /* dfa2::DegenerateReferenceError */
+    DFA2C_PLAN = 6,         /* dfa2::PlanValidationError */
+    DFA2C_IO = 7,           /* dfa2::IoError */
+    DFA2C_ORACLE = 8,       /* dfa2::OracleError */
+    DFA2C_CUDA = 9,         /* CUDA runtime / driver failure */
+    DFA2C_UNSUPPORTED = 10  /* shape outside what the sm_100a kernels support */
+} dfa2c_status;
+
+enum { DFA2C_FULL = 0, DFA2C_ARROW = 1, DFA2C_CACHED = 2 }; /* StrategyKind */
+enum { DFA2C_VISUAL_FIRST = 0, DFA2C_TEXT_FIRST = 1 };     /* TokenOrder */
+enum { DFA2C_BF16 = 0, DFA2C_F32 = 1 };                    /* element type */
+enum { DFA2C_RSE_STANDARD = 0, DFA2C_RSE_LITERAL = 1 };     /* RseMode */
+
+/* AttentionDims (inc/tensor.hpp:56-72). */
+typedef struct {
+    int64_t n_heads;
+    int64_t head_dim;
+    int64_t n_visual;
+    int64_t n_text;
+    int32_t order; /* DFA2C_VISUAL_FIRST | DFA2C_TEXT_FIRST */
+} dfa2c_dims;
+
+const char* dfa2c_last_error(void);
+const char* dfa2c_version(void);
+
+/* ---- host-only plan arithmetic (no GPU needed; bit-exact) -------------- */
+
+/* build_arrow_mask (inc/arrow.hpp:45; src/arrow.cpp:113-153). active may be
+ * NULL to query nb only; otherwise it receives nb*nb bytes. */
+int dfa2c_arrow_mask(const dfa2c_dims* dims, int64_t block, int64_t window,
+                     uint8_t* active, int64_t* nb);
+/* BlockMask::active_positions, flops_count, sparsity_ratio
+ * (inc/arrow.hpp:31-53; src/arrow.cpp:95-104, 155-169). Any output may be NULL. */
+int dfa2c_mask_stats(const uint8_t* active, int64_t seq_len, int64_t block,
+                     int64_t head_dim, int64_t* active_positions, int64_t* flops,
+                     double* sparsity);
+/* dense_flops (inc/arrow.hpp:50; src/arrow.cpp:161-163). */
+int64_t dfa2c_dense_flops(int64_t seq_len, int64_t head_dim);
+/* plan_flops (inc/dispatch.hpp:51-52; src/dispatch.cpp:93-120). */
+int dfa2c_plan_flops(const dfa2c_dims* dims, int64_t block, const int32_t* kinds,
+                     const int64_t* windows, int64_t* flops);
+/* CompressionPlan::validate + flops_total/flops_dense_total/aggregate_sparsity
+ * (inc/plan.hpp:30-42; src/plan.cpp:33-73) over a timestep-major [T*L*H]
+ * plan (layers[t*L + l], src/plan.cpp:25-31). Outputs may be NULL. */
+int dfa2c_plan_aggregate(const dfa2c_dims* dims, int64_t n_timesteps, int64_t n_layers,
+                         int64_t block, const int32_t* kinds, const int64_t* windows,
+                         int64_t* flops_total, int64_t* flops_dense, double* sparsity);
+/* The per-head tile scheduler's tile set for one head strategy: for every
+ * 128-row query tile i, the 128-key KV tiles the kernel will compute, in
+ * ascending order. row_ptr[n_qtiles+1] (CSR), cols[] (kv tile | 1<<31 when
+ * the tile needs element masking: mask block size != 128 or ragged tail).
+ * Pass cols == NULL to query the count in *n_tiles. kind FULL or ARROW. */
+int dfa2c_tile_set(const dfa2c_dims* dims, int64_t block, int32_t kind, int64_t window,
+                   int64_t* row_ptr, uint32_t* cols, int64_t* n_tiles);
+
+/* ---- HeadCache (inc/cache.hpp:15-32; src/cache.cpp) --------------------
+ * Device-resident: one bf16 slot [batch, N, d] per (layer, head), laid out
+ * per layer as [batch, H, N, d] so cached heads copy back with the same
+ * offsets as the output. produced_at bookkeeping is host-side. */
+typedef struct dfa2c_cache dfa2c_cache;
+int dfa2c_cache_create(int64_t n_layers, int64_t n_heads, int64_t batch,
+                       int64_t seq_len, int64_t head_dim, dfa2c_cache** cache);
+int dfa2c_cache_destroy(dfa2c_cache* cache);
+int dfa2c_cache_has(const dfa2c_cache* cache, int64_t layer, int64_t head, int32_t* has);
+int dfa2c_cache_produced_at(const dfa2c_cache* cache, int64_t layer, int64_t head,
+                            int64_t* t); /* DFA2C_CACHE_MISS when empty */
+int dfa2c_cache_staleness(const dfa2c_cache* cache, int64_t layer, int64_t head,
+                          int64_t t, int64_t* staleness);
+/* store: copies a device bf16 [batch, N, d] tensor into the slot (deep copy,
+ * HeadCache::store). fetch: slot -> device [batch, N, d]. */
+int dfa2c_cache_store(dfa2c_cache* cache, int64_t layer, int64_t head, const void* src,
+                      int64_t t, void* stream);
+int dfa2c_cache_fetch(const dfa2c_cache* cache, int64_t layer, int64_t head, void* dst,
+                      void* stream);
+int dfa2c_cache_clear(dfa2c_cache* cache);
+int dfa2c_cache_size(const dfa2c_cache* cache, int64_t* n_entries);
+int dfa2c_cache_bytes(const dfa2c_cache* cache, int64_t* bytes);
+
+/* ---- the fused joint-attention call ------------------------------------
+ * multi_strategy_attention (inc/dispatch.hpp:44-47; src/dispatch.cpp:30-91):
+ * ONE kernel launch computes every Full and Arrow head with the sm_100a
+ * tcgen05/TMA flash kernel over only the tiles the head's mask keeps, copies
+ * every Cached head's stored slot into `out`, and commits computed heads to
+ * the cache (dual store) — cached heads read the pre-call slot state and
+ * keep their produced_at. `cache` may be NULL only if no head is Cached (then
+ * nothing is committed). q/k/v/out: device bf16 [batch, H, N, d]. */
+int dfa2c_mha_forward(const void* q, const void* k, const void* v, int64_t batch,
+                      const dfa2c_dims* dims, int64_t block, const int32_t* kinds,
+                      const int64_t* windows, dfa2c_cache* cache, int64_t layer,
+                      int64_t t, void* out, void* stream);
+
+/* sparse_attention_forward (inc/arrow.hpp:59-63; src/arrow.cpp:171-208) for
+ * `n_heads` independent [N, d] heads sharing one arbitrary block mask
+ * (host bytes, nb*nb). Empty mask rows -> DFA2C_FULLY_MASKED. */
+int dfa2c_sparse_attention_forward(const void* q, const void* k, const void* v,
+                                   void* out, int64_t n_heads, int64_t seq_len,
+                                   int64_t head_dim, const uint8_t* active,
+                                   int64_t block, void* stream);
+/* dense_tiled_attention (inc/arrow.hpp:67-69; src/arrow.cpp:210-228). */
+int dfa2c_dense_attention_forward(const void* q, const void* k, const void* v, void* out,
+                                  int64_t n_heads, int64_t seq_len, int64_t head_dim,
+                                  void* stream);
+
+/* ---- calibration RSE query ---------------------------------------------
+ * rse (inc/calibrate.hpp:18-20; src/calibrate.cpp:18-87) for `n_heads`
+ * contiguous heads of `numel` elements each (y_m, y_o device, dtype
+ * DFA2C_BF16 or DFA2C_F32): fp64 accumulation, deterministic fixed-order
+ * reduction. Writes out[n_heads] (HOST doubles) and synchronizes the
+ * stream; DFA2C_DEGENERATE if any head's reference has zero variance. */
+int dfa2c_rse(const void* y_m, const void* y_o, int32_t dtype, int64_t n_heads,
+              int64_t numel, int32_t mode, double* out, void* stream);
+/* Asynchronous variant: out_dev is a DEVICE double[n_heads]; degenerate
+ * heads yield NaN instead of an error. */
+int dfa2c_rse_async(const void* y_m, const void* y_o, int32_t dtype, int64_t n_heads,
+                    int64_t numel, int32_t mode, double* out_dev, void* stream);
+
+/* influence_for_layer (inc/calibrate.hpp:80-86; src/calibrate.cpp:193-253)
+ * for one sample (batch 1): 1 original (all Full) + |M| candidate
+ * evaluations, M = n_windows Arrow(w) candidates then Cached when
+ * include_cached != 0 (make_candidates, src/calibrate.cpp:89-103).
+ * influence[H*M] host (h*M + m), +inf where ineligible (Cached at t == 0 or
+ * empty slot). original / method_outputs are optional device outputs
+ * ([H,N,d] and [M,H,N,d] bf16); evals (optional) += 1 + M. Synchronous. */
+int dfa2c_influence_for_layer(const void* q, const void* k, const void* v,
+                              const dfa2c_dims* dims, int64_t block,
+                              const int64_t* windows, int64_t n_windows,
+                              int32_t include_cached, const dfa2c_cache* cache,
+                              int64_t layer, int64_t t, int32_t mode, double* influence,
+                              void* original, void* method_outputs, int64_t* evals,
+                              void* stream);
+
+/* Kernel launches issued by this library since load (evidence counter). */
+int64_t dfa2c_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+#endif /* DFA2C_H */

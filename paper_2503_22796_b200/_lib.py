@@ -1,0 +1,155 @@
+"""ctypes binding of the C-ABI in include/dfa2c.h (libdfa2_b200.so, in-tree).
+
+The product path has no fallback: if the native library is missing or a
+call fails, an exception mirroring the reference's error taxonomy
+(/root/reference/proj/include/dfa2/errors.hpp:8-45) is raised.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from ctypes import POINTER, c_char_p, c_double, c_int32, c_int64, c_uint8, c_uint32, c_void_p
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libdfa2_b200.so")
+
+
+class Dfa2Error(RuntimeError):
+    """Base of the mapped status codes."""
+
+
+class ShapeError(Dfa2Error, ValueError):
+    """dfa2::ShapeError (a std::invalid_argument in the reference)."""
+
+
+class NonFiniteError(Dfa2Error):
+    pass
+
+
+class FullyMaskedRowError(Dfa2Error):
+    pass
+
+
+class CacheMissError(Dfa2Error):
+    pass
+
+
+class DegenerateReferenceError(Dfa2Error):
+    pass
+
+
+class PlanValidationError(Dfa2Error):
+    pass
+
+
+class IoError(Dfa2Error):
+    pass
+
+
+class OracleError(Dfa2Error):
+    pass
+
+
+class CudaError(Dfa2Error):
+    pass
+
+
+class UnsupportedError(Dfa2Error):
+    pass
+
+
+_ERRORS = {
+    1: ShapeError,
+    2: NonFiniteError,
+    3: FullyMaskedRowError,
+    4: CacheMissError,
+    5: DegenerateReferenceError,
+    6: PlanValidationError,
+    7: IoError,
+    8: OracleError,
+    9: CudaError,
+    10: UnsupportedError,
+}
+
+
+class Dims(ctypes.Structure):
+    """dfa2c_dims (AttentionDims, inc/tensor.hpp:56-72)."""
+
+    _fields_ = [
+        ("n_heads", c_int64),
+        ("head_dim", c_int64),
+        ("n_visual", c_int64),
+        ("n_text", c_int64),
+        ("order", c_int32),
+    ]
+
+
+# name -> (restype, argtypes)
+_SIGS = {
+    "dfa2c_last_error": (c_char_p, []),
+    "dfa2c_version": (c_char_p, []),
+    "dfa2c_launch_count": (c_int64, []),
+    "dfa2c_arrow_mask": (c_int32, [POINTER(Dims), c_int64, c_int64, POINTER(c_uint8), POINTER(c_int64)]),
+    "dfa2c_mask_stats": (c_int32, [POINTER(c_uint8), c_int64, c_int64, c_int64, POINTER(c_int64),
+                                   POINTER(c_int64), POINTER(c_double)]),
+    "dfa2c_dense_flops": (c_int64, [c_int64, c_int64]),
+    "dfa2c_plan_flops": (c_int32, [POINTER(Dims), c_int64, POINTER(c_int32), POINTER(c_int64), POINTER(c_int64)]),
+    "dfa2c_plan_aggregate": (c_int32, [POINTER(Dims), c_int64, c_int64, c_int64, POINTER(c_int32),
+                                       POINTER(c_int64), POINTER(c_int64), POINTER(c_int64), POINTER(c_double)]),
+    "dfa2c_tile_set": (c_int32, [POINTER(Dims), c_int64, c_int32, c_int64, POINTER(c_int64),
+                                 POINTER(c_uint32), POINTER(c_int64)]),
+    "dfa2c_cache_create": (c_int32, [c_int64, c_int64, c_int64, c_int64, c_int64, POINTER(c_void_p)]),
+    "dfa2c_cache_destroy": (c_int32, [c_void_p]),
+    "dfa2c_cache_has": (c_int32, [c_void_p, c_int64, c_int64, POINTER(c_int32)]),
+    "dfa2c_cache_produced_at": (c_int32, [c_void_p, c_int64, c_int64, POINTER(c_int64)]),
+    "dfa2c_cache_staleness": (c_int32, [c_void_p, c_int64, c_int64, c_int64, POINTER(c_int64)]),
+    "dfa2c_cache_store": (c_int32, [c_void_p, c_int64, c_int64, c_void_p, c_int64, c_void_p]),
+    "dfa2c_cache_fetch": (c_int32, [c_void_p, c_int64, c_int64, c_void_p, c_void_p]),
+    "dfa2c_cache_clear": (c_int32, [c_void_p]),
+    "dfa2c_cache_size": (c_int32, [c_void_p, POINTER(c_int64)]),
+    "dfa2c_cache_bytes": (c_int32, [c_void_p, POINTER(c_int64)]),
+    "dfa2c_mha_forward": (c_int32, [c_void_p, c_void_p, c_void_p, c_int64, POINTER(Dims), c_int64,
+                                    POINTER(c_int32), POINTER(c_int64), c_void_p, c_int64, c_int64,
+                                    c_void_p, c_void_p]),
+    "dfa2c_sparse_attention_forward": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int64,
+                                                 c_int64, POINTER(c_uint8), c_int64, c_void_p]),
+    "dfa2c_dense_attention_forward": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int64,
+                                                c_int64, c_void_p]),
+    "dfa2c_rse": (c_int32, [c_void_p, c_void_p, c_int32, c_int64, c_int64, c_int32, POINTER(c_double),
+                            c_void_p]),
+    "dfa2c_rse_async": (c_int32, [c_void_p, c_void_p, c_int32, c_int64, c_int64, c_int32, c_void_p,
+                                  c_void_p]),
+    "dfa2c_influence_for_layer": (c_int32, [c_void_p, c_void_p, c_void_p, POINTER(Dims), c_int64,
+                                            POINTER(c_int64), c_int64, c_int32, c_void_p, c_int64, c_int64,
+                                            c_int32, POINTER(c_double), c_void_p, c_void_p, POINTER(c_int64),
+                                            c_void_p]),
+}
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Loads libdfa2_b200.so (raising loudly if it was not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} is missing: build it with `python -m paper_2503_22796_b200.build` "
+                "(there is no CPU fallback for the attention path)")
+        L = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in _SIGS.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def check(status: int) -> None:
+    if status != 0:
+        msg = lib().dfa2c_last_error().decode(errors="replace")
+        raise _ERRORS.get(status, Dfa2Error)(msg)
+
+
+def exported_symbols():
+    return list(_SIGS)

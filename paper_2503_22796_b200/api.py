@@ -1,0 +1,673 @@
+"""Python mirror of the reference's `dfa2` operator API for the fused head-wise
+attention path, on top of the C-ABI (include/dfa2c.h).
+
+Names, argument meaning and error behaviour follow
+/root/reference/proj/include/dfa2/{tensor,arrow,dispatch,cache,plan,calibrate}.hpp
+so tests read like the reference's own (tests/test_*.cpp). Tensors are torch
+CUDA tensors: bf16 is the compute type; f32 inputs are rounded to bf16 at the
+boundary (the reference computes in f32; see DESIGN.md for the tolerance).
+There is no CPU fallback: every attention / RSE value comes from the sm_100a
+kernels of libdfa2_b200.so.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+from ctypes import POINTER, byref, c_double, c_int32, c_int64, c_uint8, c_uint32, c_void_p
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+from ._lib import (  # noqa: F401  (re-exported error taxonomy)
+    CacheMissError,
+    CudaError,
+    DegenerateReferenceError,
+    Dfa2Error,
+    FullyMaskedRowError,
+    IoError,
+    NonFiniteError,
+    OracleError,
+    PlanValidationError,
+    ShapeError,
+    UnsupportedError,
+    check,
+    lib,
+)
+
+VISUAL_FIRST = "visual_first"
+TEXT_FIRST = "text_first"
+
+
+# --------------------------------------------------------------- geometry
+@dataclass
+class AttentionDims:
+    """AttentionDims (inc/tensor.hpp:56-72)."""
+
+    n_heads: int = 0
+    head_dim: int = 0
+    n_visual: int = 0
+    n_text: int = 0
+    order: str = VISUAL_FIRST
+
+    def seq_len(self) -> int:
+        return self.n_visual + self.n_text
+
+    def text_begin(self) -> int:
+        return self.n_visual if self.order == VISUAL_FIRST else 0
+
+    def text_end(self) -> int:
+        return self.seq_len() if self.order == VISUAL_FIRST else self.n_text
+
+    def c(self) -> _lib.Dims:
+        if self.order not in (VISUAL_FIRST, TEXT_FIRST):
+            raise ShapeError(f"unknown token order {self.order!r}")
+        return _lib.Dims(self.n_heads, self.head_dim, self.n_visual, self.n_text,
+                         0 if self.order == VISUAL_FIRST else 1)
+
+    def validate(self) -> None:
+        if self.n_heads < 1 or self.head_dim < 1:
+            raise ShapeError("n_heads and head_dim must be >= 1")
+        if self.n_visual < 1 or self.n_text < 0:
+            raise ShapeError("need n_visual >= 1 and n_text >= 0")
+
+
+def _ceil_div(a: int, b: int) -> int:
+    return (a + b - 1) // b
+
+
+# --------------------------------------------------------------- masks
+@dataclass
+class BlockMask:
+    """BlockMask (inc/arrow.hpp:12-34): row-major uint8 [nqb * nkb]."""
+
+    block_size: int = 0
+    seq_len: int = 0
+    n_query_blocks: int = 0
+    n_key_blocks: int = 0
+    active: np.ndarray = field(default_factory=lambda: np.zeros(0, np.uint8))
+
+    @staticmethod
+    def all_active(seq_len: int, block_size: int) -> "BlockMask":
+        if block_size < 1:
+            raise ShapeError("block_size must be >= 1")
+        if seq_len < 1:
+            raise ShapeError("seq_len must be >= 1")
+        nb = _ceil_div(seq_len, block_size)
+        return BlockMask(block_size, seq_len, nb, nb, np.ones(nb * nb, np.uint8))
+
+    def is_active(self, i: int, j: int) -> bool:
+        return bool(self.active[i * self.n_key_blocks + j])
+
+    def set(self, i: int, j: int, v: bool) -> None:
+        self.active[i * self.n_key_blocks + j] = 1 if v else 0
+
+    def block_begin(self, i: int) -> int:
+        return i * self.block_size
+
+    def block_len(self, i: int) -> int:
+        return min(self.block_size, self.seq_len - i * self.block_size)
+
+    def _stats(self, head_dim: int = 1):
+        a = np.ascontiguousarray(self.active, dtype=np.uint8)
+        ap, fl, sp = c_int64(), c_int64(), c_double()
+        check(lib().dfa2c_mask_stats(a.ctypes.data_as(POINTER(c_uint8)), self.seq_len, self.block_size,
+                                     head_dim, byref(ap), byref(fl), byref(sp)))
+        return ap.value, fl.value, sp.value
+
+    def active_positions(self) -> int:
+        return self._stats()[0]
+
+    def row_has_active(self, i: int) -> bool:
+        return bool(self.active[i * self.n_key_blocks:(i + 1) * self.n_key_blocks].any())
+
+    def grid(self) -> np.ndarray:
+        return self.active.reshape(self.n_query_blocks, self.n_key_blocks)
+
+
+@dataclass
+class ArrowSpec:
+    """ArrowSpec (inc/arrow.hpp:39-43)."""
+
+    dims: AttentionDims
+    block_size: int = 0
+    window_blocks: int = 0
+
+
+def build_arrow_mask(spec: ArrowSpec) -> BlockMask:
+    """build_arrow_mask (inc/arrow.hpp:45; src/arrow.cpp:113-153), bit-exact."""
+    d = spec.dims.c()
+    nb = c_int64()
+    check(lib().dfa2c_arrow_mask(byref(d), spec.block_size, spec.window_blocks, None, byref(nb)))
+    active = np.zeros(nb.value * nb.value, np.uint8)
+    check(lib().dfa2c_arrow_mask(byref(d), spec.block_size, spec.window_blocks,
+                                 active.ctypes.data_as(POINTER(c_uint8)), byref(nb)))
+    return BlockMask(spec.block_size, spec.dims.seq_len(), nb.value, nb.value, active)
+
+
+def flops_count(mask: BlockMask, head_dim: int) -> int:
+    """4*d per active (query, key) position (src/arrow.cpp:155-159)."""
+    if head_dim < 1:
+        raise ShapeError("head_dim must be >= 1")
+    return mask._stats(head_dim)[1]
+
+
+def dense_flops(seq_len: int, head_dim: int) -> int:
+    return int(lib().dfa2c_dense_flops(seq_len, head_dim))
+
+
+def sparsity_ratio(mask: BlockMask) -> float:
+    return mask._stats()[2]
+
+
+def tile_set(dims: AttentionDims, block_size: int, strategy: "HeadStrategy"):
+    """The scheduler's KV tile list per 128-row query tile (CSR row_ptr, cols)."""
+    d = dims.c()
+    kind = {StrategyKind.full: 0, StrategyKind.arrow: 1}.get(strategy.kind)
+    if kind is None:
+        raise ShapeError("tile sets exist for Full and Arrow heads only")
+    n = c_int64()
+    check(lib().dfa2c_tile_set(byref(d), block_size, kind, strategy.window_blocks, None, None, byref(n)))
+    nqt = _ceil_div(dims.seq_len(), 128)
+    row_ptr = np.zeros(nqt + 1, np.int64)
+    cols = np.zeros(max(n.value, 1), np.uint32)
+    check(lib().dfa2c_tile_set(byref(d), block_size, kind, strategy.window_blocks,
+                               row_ptr.ctypes.data_as(POINTER(c_int64)), cols.ctypes.data_as(POINTER(c_uint32)),
+                               byref(n)))
+    return row_ptr, cols[: n.value]
+
+
+# --------------------------------------------------------------- plans
+class StrategyKind:
+    full = "full"
+    arrow = "arrow"
+    cached = "cached"
+
+
+_KIND_CODE = {StrategyKind.full: 0, StrategyKind.arrow: 1, StrategyKind.cached: 2}
+
+
+@dataclass(frozen=True)
+class HeadStrategy:
+    """HeadStrategy (inc/dispatch.hpp:14-25)."""
+
+    kind: str = StrategyKind.full
+    window_blocks: int = 0
+
+    @staticmethod
+    def Full() -> "HeadStrategy":
+        return HeadStrategy(StrategyKind.full, 0)
+
+    @staticmethod
+    def Arrow(w: int) -> "HeadStrategy":
+        return HeadStrategy(StrategyKind.arrow, int(w))
+
+    @staticmethod
+    def Cached() -> "HeadStrategy":
+        return HeadStrategy(StrategyKind.cached, 0)
+
+
+@dataclass
+class LayerPlan:
+    """LayerPlan (inc/dispatch.hpp:28-37)."""
+
+    strategies: List[HeadStrategy] = field(default_factory=list)
+
+    @staticmethod
+    def all_full(n_heads: int) -> "LayerPlan":
+        return LayerPlan([HeadStrategy.Full() for _ in range(n_heads)])
+
+    def n_heads(self) -> int:
+        return len(self.strategies)
+
+    def arrays(self):
+        kinds = (c_int32 * max(1, len(self.strategies)))(*[_KIND_CODE[s.kind] for s in self.strategies])
+        wins = (c_int64 * max(1, len(self.strategies)))(*[s.window_blocks for s in self.strategies])
+        return kinds, wins
+
+    @staticmethod
+    def parse(text: str) -> "LayerPlan":
+        """'F A8 C A0' -> LayerPlan (bench / test shorthand)."""
+        out = []
+        for tok in text.split():
+            if tok == "F":
+                out.append(HeadStrategy.Full())
+            elif tok == "C":
+                out.append(HeadStrategy.Cached())
+            elif tok.startswith("A"):
+                out.append(HeadStrategy.Arrow(int(tok[1:])))
+            else:
+                raise ShapeError(f"bad plan token {tok!r}")
+        return LayerPlan(out)
+
+
+def plan_flops(plan: LayerPlan, dims: AttentionDims, block_size: int) -> int:
+    """plan_flops (inc/dispatch.hpp:51-52; src/dispatch.cpp:93-120)."""
+    d = dims.c()
+    if plan.n_heads() != dims.n_heads:
+        raise ShapeError("plan must assign exactly one strategy per head")
+    kinds, wins = plan.arrays()
+    out = c_int64()
+    check(lib().dfa2c_plan_flops(byref(d), block_size, kinds, wins, byref(out)))
+    return out.value
+
+
+# --------------------------------------------------------------- tensors
+def _torch():
+    import torch
+
+    return torch
+
+
+def _stream_ptr(stream=None) -> Optional[int]:
+    torch = _torch()
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def _as_bf16_cuda(x, name: str):
+    torch = _torch()
+    if not isinstance(x, torch.Tensor):
+        raise ShapeError(f"{name} must be a torch tensor")
+    if not x.is_cuda:
+        raise ShapeError(f"{name} must be a CUDA tensor (the path has no CPU implementation)")
+    if x.dtype == torch.float32:
+        x = x.to(torch.bfloat16)
+    elif x.dtype != torch.bfloat16:
+        raise ShapeError(f"{name} must be bf16 (or f32, rounded to bf16)")
+    return x.contiguous()
+
+
+# --------------------------------------------------------------- cache
+class HeadCache:
+    """HeadCache (inc/cache.hpp:15-32), device resident.
+
+    One bf16 slot [batch, N, d] per (layer, head). store() deep-copies,
+    fetch() returns a fresh tensor, produced_at/staleness follow
+    src/cache.cpp:7-41 (CacheMissError on empty slots).
+    """
+
+    def __init__(self, n_layers: int, n_heads: int, seq_len: int, head_dim: int, batch: int = 1):
+        self.n_layers, self.n_heads, self.seq_len, self.head_dim, self.batch = (
+            n_layers, n_heads, seq_len, head_dim, batch)
+        h = c_void_p()
+        check(lib().dfa2c_cache_create(n_layers, n_heads, batch, seq_len, head_dim, byref(h)))
+        self._h = h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                lib().dfa2c_cache_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+    @property
+    def handle(self) -> c_void_p:
+        return self._h
+
+    def store(self, layer: int, head: int, output, t: int) -> None:
+        x = _as_bf16_cuda(output, "output")
+        if x.dim() == 2:
+            x = x.unsqueeze(0)
+        if tuple(x.shape) != (self.batch, self.seq_len, self.head_dim):
+            raise ShapeError("cache entries are per-head [N, d] tensors")
+        check(lib().dfa2c_cache_store(self._h, layer, head, c_void_p(x.data_ptr()), t, c_void_p(_stream_ptr())))
+
+    def fetch(self, layer: int, head: int):
+        torch = _torch()
+        out = torch.empty(self.batch, self.seq_len, self.head_dim, dtype=torch.bfloat16, device="cuda")
+        check(lib().dfa2c_cache_fetch(self._h, layer, head, c_void_p(out.data_ptr()), c_void_p(_stream_ptr())))
+        return out[0] if self.batch == 1 else out
+
+    def has(self, layer: int, head: int) -> bool:
+        v = c_int32()
+        check(lib().dfa2c_cache_has(self._h, layer, head, byref(v)))
+        return bool(v.value)
+
+    def produced_at(self, layer: int, head: int) -> int:
+        v = c_int64()
+        check(lib().dfa2c_cache_produced_at(self._h, layer, head, byref(v)))
+        return v.value
+
+    def staleness(self, layer: int, head: int, t: int) -> int:
+        v = c_int64()
+        check(lib().dfa2c_cache_staleness(self._h, layer, head, t, byref(v)))
+        return v.value
+
+    def clear(self) -> None:
+        check(lib().dfa2c_cache_clear(self._h))
+
+    def size(self) -> int:
+        v = c_int64()
+        check(lib().dfa2c_cache_size(self._h, byref(v)))
+        return v.value
+
+    def nbytes(self) -> int:
+        v = c_int64()
+        check(lib().dfa2c_cache_bytes(self._h, byref(v)))
+        return v.value
+
+
+# --------------------------------------------------------------- attention
+def multi_strategy_attention(q, k, v, plan: LayerPlan, cache: Optional[HeadCache], layer: int, t: int,
+                             dims: AttentionDims, block_size: int, out=None, stream=None):
+    """multi_strategy_attention (inc/dispatch.hpp:44-47; src/dispatch.cpp:30-91).
+
+    q/k/v: [H, N, d] or [batch, H, N, d] CUDA tensors. One fused sm_100a
+    launch: Full/Arrow heads computed, Cached heads copied from `cache`,
+    computed heads committed to `cache` (produced_at = t).
+    """
+    torch = _torch()
+    q = _as_bf16_cuda(q, "q")
+    k = _as_bf16_cuda(k, "k")
+    v = _as_bf16_cuda(v, "v")
+    squeeze = q.dim() == 3
+    if squeeze:
+        q, k, v = q.unsqueeze(0), k.unsqueeze(0), v.unsqueeze(0)
+    if q.dim() != 4 or q.shape != k.shape or q.shape != v.shape:
+        raise ShapeError("q/k/v must be identical [H, N, d] tensors")
+    if tuple(q.shape[1:]) != (dims.n_heads, dims.seq_len(), dims.head_dim):
+        raise ShapeError("tensor shape disagrees with dims")
+    if plan.n_heads() != dims.n_heads:
+        raise ShapeError("plan must assign exactly one strategy per head")
+    if out is None:
+        out = torch.empty_like(q)
+    d = dims.c()
+    kinds, wins = plan.arrays()
+    check(lib().dfa2c_mha_forward(c_void_p(q.data_ptr()), c_void_p(k.data_ptr()), c_void_p(v.data_ptr()),
+                                  q.shape[0], byref(d), block_size, kinds, wins,
+                                  cache.handle if cache is not None else None, layer, t,
+                                  c_void_p(out.data_ptr()), c_void_p(_stream_ptr(stream))))
+    return out[0] if squeeze else out
+
+
+def sparse_attention_forward(q, k, v, mask: BlockMask, out=None, stream=None):
+    """sparse_attention_forward (inc/arrow.hpp:59-63): [N, d] or [H, N, d] heads."""
+    torch = _torch()
+    q = _as_bf16_cuda(q, "q")
+    k = _as_bf16_cuda(k, "k")
+    v = _as_bf16_cuda(v, "v")
+    if q.shape != k.shape or q.shape != v.shape or q.dim() not in (2, 3):
+        raise ShapeError("sparse attention expects per-head [N, d] tensors")
+    n, d = q.shape[-2], q.shape[-1]
+    heads = 1 if q.dim() == 2 else q.shape[0]
+    if mask.seq_len != n:
+        raise ShapeError("mask sequence length disagrees with tensors")
+    if out is None:
+        out = torch.empty_like(q)
+    a = np.ascontiguousarray(mask.active, dtype=np.uint8)
+    check(lib().dfa2c_sparse_attention_forward(
+        c_void_p(q.data_ptr()), c_void_p(k.data_ptr()), c_void_p(v.data_ptr()), c_void_p(out.data_ptr()),
+        heads, n, d, a.ctypes.data_as(POINTER(c_uint8)), mask.block_size, c_void_p(_stream_ptr(stream))))
+    return out
+
+
+def dense_tiled_attention(q, k, v, out=None, stream=None):
+    """dense_tiled_attention (inc/arrow.hpp:67-69): unmasked [N, d] / [H, N, d]."""
+    torch = _torch()
+    q = _as_bf16_cuda(q, "q")
+    k = _as_bf16_cuda(k, "k")
+    v = _as_bf16_cuda(v, "v")
+    n, d = q.shape[-2], q.shape[-1]
+    heads = 1 if q.dim() == 2 else q.shape[0]
+    if out is None:
+        out = torch.empty_like(q)
+    check(lib().dfa2c_dense_attention_forward(c_void_p(q.data_ptr()), c_void_p(k.data_ptr()),
+                                              c_void_p(v.data_ptr()), c_void_p(out.data_ptr()), heads, n, d,
+                                              c_void_p(_stream_ptr(stream))))
+    return out
+
+
+# --------------------------------------------------------------- RSE
+class RseMode:
+    standard = 0
+    literal = 1
+
+
+def _rse_operands(y_m, y_o):
+    torch = _torch()
+    if y_m.shape != y_o.shape or y_m.dtype != y_o.dtype:
+        raise ShapeError("rse operands must share shape and dtype")
+    if y_m.numel() == 0:
+        raise ShapeError("rse needs at least one element")
+    if not (y_m.is_cuda and y_o.is_cuda):
+        raise ShapeError("rse operands must be CUDA tensors")
+    if y_m.dtype == torch.bfloat16:
+        dt = 0
+    elif y_m.dtype == torch.float32:
+        dt = 1
+    else:
+        raise ShapeError("rse operands must be bf16 or f32")
+    return y_m.contiguous(), y_o.contiguous(), dt
+
+
+def rse(y_m, y_o, mode: int = RseMode.standard, stream=None) -> float:
+    """rse (inc/calibrate.hpp:18-20; src/calibrate.cpp:75-87) of one tensor pair."""
+    return float(rse_per_head(y_m.reshape(1, -1), y_o.reshape(1, -1), mode, stream)[0])
+
+
+def rse_per_head(y_m, y_o, mode: int = RseMode.standard, stream=None) -> np.ndarray:
+    """RSE of every leading-axis slice ([H, ...] -> [H] doubles), one launch."""
+    y_m, y_o, dt = _rse_operands(y_m, y_o)
+    H = y_m.shape[0]
+    numel = y_m.numel() // H
+    out = np.zeros(H, np.float64)
+    check(lib().dfa2c_rse(c_void_p(y_m.data_ptr()), c_void_p(y_o.data_ptr()), dt, H, numel, mode,
+                          out.ctypes.data_as(POINTER(c_double)), c_void_p(_stream_ptr(stream))))
+    return out
+
+
+# --------------------------------------------------------------- calibration
+@dataclass
+class MethodCandidate:
+    """MethodCandidate (inc/calibrate.hpp:24-28)."""
+
+    id: str
+    strategy: HeadStrategy
+
+
+def method_id(s: HeadStrategy) -> str:
+    """method_id (src/plan.cpp:86-96)."""
+    if s.kind == StrategyKind.arrow:
+        return f"arrow_w{s.window_blocks}"
+    if s.kind == StrategyKind.cached:
+        return "cached"
+    return "full"
+
+
+def make_candidates(windows: Sequence[int], include_cached: bool = True) -> List[MethodCandidate]:
+    """make_candidates (src/calibrate.cpp:89-103)."""
+    out = []
+    for w in windows:
+        if w < 0:
+            raise ShapeError("window radii must be >= 0")
+        s = HeadStrategy.Arrow(w)
+        out.append(MethodCandidate(method_id(s), s))
+    if include_cached:
+        out.append(MethodCandidate("cached", HeadStrategy.Cached()))
+    if not out:
+        raise ShapeError("candidate set must be nonempty")
+    return out
+
+
+@dataclass
+class CalibrationStats:
+    attention_evals: int = 0
+
+
+@dataclass
+class LayerInfluence:
+    """LayerInfluence (inc/calibrate.hpp:74-78)."""
+
+    original: object
+    method_outputs: object  # [M, H, N, d]
+    influence: np.ndarray   # [H * M], h*M + m, +inf where ineligible
+
+
+def influence_for_layer(q, k, v, methods: Sequence[MethodCandidate], cache: Optional[HeadCache], layer: int,
+                        t: int, dims: AttentionDims, block_size: int, mode: int = RseMode.standard,
+                        stats: Optional[CalibrationStats] = None, keep_outputs: bool = True,
+                        stream=None) -> LayerInfluence:
+    """influence_for_layer (inc/calibrate.hpp:80-86; src/calibrate.cpp:193-253).
+
+    Candidates must be Arrow(w)* followed by at most one Cached, the order
+    make_candidates produces."""
+    torch = _torch()
+    if not methods:
+        raise ShapeError("candidate set must be nonempty")
+    windows, include_cached = [], False
+    for i, m in enumerate(methods):
+        if m.strategy.kind == StrategyKind.arrow:
+            if include_cached:
+                raise ShapeError("Cached must be the last candidate")
+            windows.append(m.strategy.window_blocks)
+        elif m.strategy.kind == StrategyKind.cached:
+            include_cached = True
+        else:
+            raise ShapeError("Full is not a compression candidate")
+    q = _as_bf16_cuda(q, "q")
+    k = _as_bf16_cuda(k, "k")
+    v = _as_bf16_cuda(v, "v")
+    M = len(methods)
+    H, n, dd = dims.n_heads, dims.seq_len(), dims.head_dim
+    original = torch.empty(H, n, dd, dtype=torch.bfloat16, device="cuda")
+    outs = torch.zeros(M, H, n, dd, dtype=torch.bfloat16, device="cuda") if keep_outputs else None
+    infl = np.zeros(H * M, np.float64)
+    evals = c_int64(0)
+    d = dims.c()
+    w_arr = (c_int64 * max(1, len(windows)))(*windows)
+    check(lib().dfa2c_influence_for_layer(
+        c_void_p(q.data_ptr()), c_void_p(k.data_ptr()), c_void_p(v.data_ptr()), byref(d), block_size,
+        w_arr, len(windows), 1 if include_cached else 0, cache.handle if cache is not None else None,
+        layer, t, mode, infl.ctypes.data_as(POINTER(c_double)), c_void_p(original.data_ptr()),
+        c_void_p(outs.data_ptr()) if outs is not None else None, byref(evals), c_void_p(_stream_ptr(stream))))
+    if stats is not None:
+        stats.attention_evals += evals.value
+    return LayerInfluence(original, outs, infl)
+
+
+# --------------------------------------------------------------- compression plan
+@dataclass
+class CompressionPlan:
+    """CompressionPlan (inc/plan.hpp:14-42): layers[t*L + l], timestep-major."""
+
+    dims: AttentionDims
+    n_timesteps: int = 0
+    n_layers: int = 0
+    block_size: int = 0
+    delta: float = 0.0
+    coeff: float = 1.5
+    window_set: List[int] = field(default_factory=list)
+    layers: List[LayerPlan] = field(default_factory=list)
+
+    @staticmethod
+    def all_full(dims: AttentionDims, timesteps: int, layers: int, block_size: int) -> "CompressionPlan":
+        return CompressionPlan(dims, timesteps, layers, block_size,
+                               layers=[LayerPlan.all_full(dims.n_heads) for _ in range(timesteps * layers)])
+
+    def at(self, t: int, layer: int) -> LayerPlan:
+        return self.layers[t * self.n_layers + layer]
+
+    def _arrays(self):
+        H = self.dims.n_heads
+        if len(self.layers) != self.n_timesteps * self.n_layers:
+            raise PlanValidationError("plan must cover every (t, layer) exactly once")
+        kinds, wins = [], []
+        for lp in self.layers:
+            if lp.n_heads() != H:
+                raise PlanValidationError("head array length must equal H")
+            kinds += [_KIND_CODE[s.kind] for s in lp.strategies]
+            wins += [s.window_blocks for s in lp.strategies]
+        n = max(1, len(kinds))
+        return (c_int32 * n)(*kinds), (c_int64 * n)(*wins)
+
+    def _aggregate(self):
+        if not (self.delta >= 0.0):
+            raise PlanValidationError("delta must be >= 0")
+        if not (self.coeff >= 1.0):
+            raise PlanValidationError("coeff must be >= 1")
+        kinds, wins = self._arrays()
+        d = self.dims.c()
+        ft, fd, sp = c_int64(), c_int64(), c_double()
+        check(lib().dfa2c_plan_aggregate(byref(d), self.n_timesteps, self.n_layers, self.block_size, kinds, wins,
+                                         byref(ft), byref(fd), byref(sp)))
+        return ft.value, fd.value, sp.value
+
+    def validate(self) -> None:
+        self.dims.validate()
+        self._aggregate()
+
+    def flops_total(self) -> int:
+        return self._aggregate()[0]
+
+    def flops_dense_total(self) -> int:
+        return self._aggregate()[1]
+
+    def aggregate_sparsity(self) -> float:
+        return self._aggregate()[2]
+
+
+@dataclass
+class RunStats:
+    """RunStats (inc/workload.hpp:59-69)."""
+
+    flops_total: int = 0
+    flops_dense: int = 0
+    sparsity: float = 0.0
+    outputs: list = field(default_factory=list)
+
+    def output(self, t: int, layer: int, n_layers: int):
+        return self.outputs[t * n_layers + layer]
+
+
+def run_pipeline(q_stream, k_stream, v_stream, plan: CompressionPlan, batch: int = 1, keep_outputs: bool = True,
+                 cache: Optional[HeadCache] = None) -> RunStats:
+    """run_pipeline (inc/workload.hpp:71; src/workload.cpp:230-262): t-major
+    (t, l) loop over multi_strategy_attention with one shared device cache.
+    q_stream(t, l) etc. return the [H, N, d] (or [batch, H, N, d]) inputs."""
+    plan.validate()
+    dims = plan.dims
+    if cache is None:
+        cache = HeadCache(plan.n_layers, dims.n_heads, dims.seq_len(), dims.head_dim, batch)
+    stats = RunStats()
+    dense = dims.n_heads * dense_flops(dims.seq_len(), dims.head_dim)
+    for t in range(plan.n_timesteps):
+        for l in range(plan.n_layers):
+            lp = plan.at(t, l)
+            o = multi_strategy_attention(q_stream(t, l), k_stream(t, l), v_stream(t, l), lp, cache, l, t, dims,
+                                         plan.block_size)
+            if keep_outputs:
+                stats.outputs.append(o)
+            stats.flops_total += plan_flops(lp, dims, plan.block_size)
+            stats.flops_dense += dense
+    stats.sparsity = 1.0 - stats.flops_total / stats.flops_dense
+    return stats
+
+
+def flux68_plan(n_heads: int = 24) -> LayerPlan:
+    """The survey's FLUX68 head pattern: head h,
+    g = h // 4, r = h % 4 -> r0 Full, r1 Arrow(8), r2 Cached,
+    r3 Arrow(0 if g % 3 != 1 else 8)."""
+    out = []
+    for h in range(n_heads):
+        g, r = divmod(h, 4)
+        if r == 0:
+            out.append(HeadStrategy.Full())
+        elif r == 1:
+            out.append(HeadStrategy.Arrow(8))
+        elif r == 2:
+            out.append(HeadStrategy.Cached())
+        else:
+            out.append(HeadStrategy.Arrow(0 if g % 3 != 1 else 8))
+    return LayerPlan(out)
+
+
+def launch_count() -> int:
+    return int(lib().dfa2c_launch_count())
+
+
+__all__ = [n for n in dir() if not n.startswith("_")]
+_ = (math, ctypes)

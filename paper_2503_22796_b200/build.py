@@ -1,0 +1,61 @@
+"""Builds the in-tree native library (no JIT cache; the .so travels with the repo).
+
+    python -m paper_2503_22796_b200.build
+
+Produces paper_2503_22796_b200/libdfa2_b200.so: the sm_100a kernels
+(tcgen05 / TMA / TMEM), the C-ABI of include/dfa2c.h and the host C++
+dfa2:: API of include/dfa2/ (csrc/host/), with the CUDA runtime linked
+statically so the library is self-contained for ctypes / cgo / JNI callers.
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+CSRC = os.path.join(HERE, "csrc")
+LIB = os.path.join(HERE, "libdfa2_b200.so")
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+CU_SOURCES = ["attn_sm100.cu", "rse_sm100.cu"]
+CPP_SOURCES = ["dfa2c.cpp"]
+
+
+def _sources():
+    srcs = [os.path.join(CSRC, s) for s in CU_SOURCES + CPP_SOURCES]
+    host = os.path.join(CSRC, "host")
+    if os.path.isdir(host):
+        srcs += sorted(os.path.join(host, f) for f in os.listdir(host) if f.endswith(".cpp"))
+    return srcs
+
+
+def _stale(target, deps):
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    deps = _sources()
+    for d in (CSRC, os.path.join(ROOT, "include"), os.path.join(ROOT, "include", "dfa2")):
+        if os.path.isdir(d):
+            deps += [os.path.join(d, f) for f in os.listdir(d) if f.endswith((".h", ".cuh", ".hpp"))]
+    if not force and not _stale(LIB, deps):
+        return LIB
+    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-cudart", "static",
+           "-Xcompiler", "-fPIC,-fvisibility=hidden,-fvisibility-inlines-hidden", "-Xptxas", "-v" if verbose else "-O3",
+           "-I", os.path.join(ROOT, "include"), "-I", CSRC,
+           "-o", LIB + ".tmp", *_sources(), "-lcuda" if False else "-ldl"]
+    if verbose:
+        print(" ".join(cmd), file=sys.stderr)
+    subprocess.run(cmd, check=True)
+    os.replace(LIB + ".tmp", LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

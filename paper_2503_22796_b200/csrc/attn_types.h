@@ -1,0 +1,48 @@
+// attn_types.h — work-list records shared by the host tile scheduler
+// (dfa2c.cpp) and the sm_100a fused head-wise attention kernel.
+#pragma once
+#include <cstdint>
+#include <cuda_bf16.h>
+
+namespace dfa2k {
+
+// One unit of the per-head tile scheduler: a 128-row query tile of one
+// (sample, head), either computed over its mask's KV tile list or (Cached
+// heads) copied back from the head cache.
+struct WorkItem {
+    int32_t bh;          // sample * H + head: row of the [batch*H, N, d] view
+    int32_t qtile;       // 128-row query tile index
+    int32_t tile_begin;  // offset into the tile list (compute items)
+    int32_t n_tiles;     // KV tiles to fold (0 for copy items)
+    int32_t mask_off;    // byte offset of this head's nb*nb block mask
+    int32_t flags;       // ITEM_COPY | ITEM_COMMIT
+};
+
+enum : int32_t {
+    ITEM_COPY = 1,    // Cached head: out <- cache slot (src/dispatch.cpp:77-81)
+    ITEM_COMMIT = 2,  // computed head: also store O into the cache slot (:85-88)
+};
+
+// Tile-list word: KV tile index in the low 31 bits; the top bit marks tiles
+// that need element masking (block size != 128 or a ragged tail).
+constexpr uint32_t TILE_PARTIAL = 0x80000000u;
+constexpr uint32_t TILE_INDEX_MASK = 0x7FFFFFFFu;
+
+// Kernel arguments (besides the three TMA tensor maps).
+struct AttnArgs {
+    const WorkItem* items;
+    const int32_t* cta_begin;  // [gridDim.x + 1]
+    const uint32_t* tiles;
+    const uint8_t* masks;      // concatenated nb*nb block masks
+    __nv_bfloat16* out;        // [batch*H, N, D]
+    __nv_bfloat16* cache;      // layer slot array [batch*H, N, D] or null
+    int32_t n;
+    int32_t block;
+    int32_t nb;
+    float scale_log2;          // log2(e) / sqrt(d)
+};
+
+constexpr int TILE_M = 128;  // query rows per tile (tcgen05 M)
+constexpr int TILE_N = 128;  // keys per KV tile (tcgen05 N of S = Q K^T)
+
+}  // namespace dfa2k

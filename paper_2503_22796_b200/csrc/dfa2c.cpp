@@ -1,0 +1,989 @@
+// dfa2c.cpp — host side of the C-ABI (include/dfa2c.h): bit-exact plan
+// arithmetic, the per-head tile scheduler, the device-resident head cache,
+// TMA descriptor creation and kernel launches. No CPU attention fallback
+// exists here: every attention / RSE result comes from the sm_100a kernels.
+#include "dfa2c.h"
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <queue>
+#include <string>
+#include <vector>
+
+#include "attn_types.h"
+
+namespace dfa2k {
+cudaError_t launch_attn(int d, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
+                        const AttnArgs& args, int grid, cudaStream_t stream);
+cudaError_t launch_rse(const void* ym, const void* yo, int dtype, int64_t n_heads, int64_t numel,
+                       int mode, double* out_dev, double* scratch, int nblk, cudaStream_t stream);
+}  // namespace dfa2k
+
+using dfa2k::WorkItem;
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<int64_t> g_launches{0};
+
+struct Failure {
+    int code;
+    std::string msg;
+};
+
+[[noreturn]] void fail(int code, const std::string& msg) { throw Failure{code, msg}; }
+
+#define DFA2C_CUDA_CHECK(expr)                                                             \
+    do {                                                                                   \
+        const cudaError_t e_ = (expr);                                                     \
+        if (e_ != cudaSuccess)                                                             \
+            fail(DFA2C_CUDA, std::string(#expr) + " failed: " + cudaGetErrorString(e_)); \
+    } while (0)
+
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return DFA2C_OK;
+    } catch (const Failure& e) {
+        g_err = e.msg;
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_err = "host allocation failed";
+        return DFA2C_CUDA;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return DFA2C_CUDA;
+    }
+}
+
+int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// AttentionDims::validate (src/tensor.cpp:225-230).
+void validate_dims(const dfa2c_dims* d) {
+    if (!d)
+        fail(DFA2C_SHAPE, "dims must not be NULL");
+    if (d->n_heads < 1 || d->head_dim < 1)
+        fail(DFA2C_SHAPE, "n_heads and head_dim must be >= 1");
+    if (d->n_visual < 1 || d->n_text < 0)
+        fail(DFA2C_SHAPE, "need n_visual >= 1 and n_text >= 0");
+    if (d->order != DFA2C_VISUAL_FIRST && d->order != DFA2C_TEXT_FIRST)
+        fail(DFA2C_SHAPE, "unknown token order");
+}
+
+int64_t seq_len(const dfa2c_dims* d) { return d->n_visual + d->n_text; }
+int64_t text_begin(const dfa2c_dims* d) { return d->order == DFA2C_VISUAL_FIRST ? d->n_visual : 0; }
+int64_t text_end(const dfa2c_dims* d) { return d->order == DFA2C_VISUAL_FIRST ? seq_len(d) : d->n_text; }
+
+// build_arrow_mask (src/arrow.cpp:113-153): a block is text if it overlaps
+// the text span; the window clamps to the visual block count;
+// active(i,j) = text(i) | text(j) | |i-j| <= w_eff.
+std::vector<uint8_t> arrow_mask(const dfa2c_dims* dims, int64_t B, int64_t w) {
+    validate_dims(dims);
+    if (B < 1)
+        fail(DFA2C_SHAPE, "block_size must be >= 1");
+    if (w < 0)
+        fail(DFA2C_SHAPE, "window_blocks must be >= 0");
+    const int64_t n = seq_len(dims);
+    const int64_t nb = ceil_div(n, B);
+    const int64_t lo_t = text_begin(dims), hi_t = text_end(dims);
+    std::vector<uint8_t> is_text(static_cast<size_t>(nb));
+    for (int64_t i = 0; i < nb; ++i) {
+        const int64_t lo = i * B, hi = std::min(lo + B, n);
+        is_text[i] = (lo < hi_t && hi > lo_t) ? 1 : 0;
+    }
+    const int64_t weff = std::min(w, std::max<int64_t>(0, ceil_div(dims->n_visual, B) - 1));
+    std::vector<uint8_t> m(static_cast<size_t>(nb * nb));
+    for (int64_t i = 0; i < nb; ++i)
+        for (int64_t j = 0; j < nb; ++j)
+            m[i * nb + j] = (is_text[i] || is_text[j] || std::llabs(i - j) <= weff) ? 1 : 0;
+    return m;
+}
+
+// BlockMask::active_positions (src/arrow.cpp:95-104).
+int64_t active_positions(const uint8_t* m, int64_t n, int64_t B) {
+    const int64_t nb = ceil_div(n, B);
+    int64_t total = 0;
+    for (int64_t i = 0; i < nb; ++i) {
+        const int64_t li = std::min(B, n - i * B);
+        for (int64_t j = 0; j < nb; ++j)
+            if (m[i * nb + j])
+                total += li * std::min(B, n - j * B);
+    }
+    return total;
+}
+
+void validate_plan(const dfa2c_dims* dims, const int32_t* kinds, const int64_t* windows) {
+    if (!kinds)
+        fail(DFA2C_SHAPE, "plan must assign exactly one strategy per head");
+    for (int64_t h = 0; h < dims->n_heads; ++h) {
+        if (kinds[h] < DFA2C_FULL || kinds[h] > DFA2C_CACHED)
+            fail(DFA2C_SHAPE, "unknown strategy kind for head " + std::to_string(h));
+        if (kinds[h] == DFA2C_ARROW && (!windows || windows[h] < 0))
+            fail(DFA2C_SHAPE, "window_blocks must be >= 0");
+    }
+}
+
+// plan_flops (src/dispatch.cpp:93-120).
+int64_t plan_flops(const dfa2c_dims* dims, int64_t B, const int32_t* kinds, const int64_t* windows) {
+    validate_dims(dims);
+    validate_plan(dims, kinds, windows);
+    const int64_t n = seq_len(dims), d = dims->head_dim;
+    std::map<int64_t, int64_t> arrow;
+    int64_t total = 0;
+    for (int64_t h = 0; h < dims->n_heads; ++h) {
+        if (kinds[h] == DFA2C_FULL) {
+            total += 4 * d * n * n;
+        } else if (kinds[h] == DFA2C_ARROW) {
+            auto it = arrow.find(windows[h]);
+            if (it == arrow.end()) {
+                const auto m = arrow_mask(dims, B, windows[h]);
+                it = arrow.emplace(windows[h], 4 * d * active_positions(m.data(), n, B)).first;
+            }
+            total += it->second;
+        }
+    }
+    return total;
+}
+
+// ------------------------------------------------------------ tile sets
+// For every 128-row query tile, the 128-key KV tiles holding at least one
+// active (query, key) pair, ascending (the reference folds key blocks in
+// ascending order, src/arrow.cpp:184-186). A tile is PARTIAL when some pair
+// inside [rows < n] x [keys < n] is inactive, or keys run past n.
+struct TileSet {
+    std::vector<int64_t> row_ptr;
+    std::vector<uint32_t> cols;
+};
+
+TileSet build_tile_set(const uint8_t* m, int64_t n, int64_t B) {
+    const int64_t nb = ceil_div(n, B);
+    const int64_t nt = ceil_div(n, dfa2k::TILE_M);
+    TileSet ts;
+    ts.row_ptr.assign(static_cast<size_t>(nt + 1), 0);
+    for (int64_t i = 0; i < nt; ++i) {
+        const int64_t r0 = i * 128, r1 = std::min(r0 + 128, n);
+        const int64_t qb0 = r0 / B, qb1 = (r1 - 1) / B;
+        for (int64_t t = 0; t < nt; ++t) {
+            const int64_t c0 = t * 128, c1 = std::min(c0 + 128, n);
+            const int64_t kb0 = c0 / B, kb1 = (c1 - 1) / B;
+            bool any = false, all = true;
+            for (int64_t qb = qb0; qb <= qb1; ++qb)
+                for (int64_t kb = kb0; kb <= kb1; ++kb) {
+                    const bool a = m[qb * nb + kb] != 0;
+                    any |= a;
+                    all &= a;
+                }
+            if (!any)
+                continue;
+            const bool partial = !all || (c1 - c0) < 128;
+            ts.cols.push_back(static_cast<uint32_t>(t) | (partial ? dfa2k::TILE_PARTIAL : 0u));
+        }
+        ts.row_ptr[i + 1] = static_cast<int64_t>(ts.cols.size());
+    }
+    return ts;
+}
+
+void check_rows_nonempty(const uint8_t* m, int64_t nb) {
+    for (int64_t i = 0; i < nb; ++i) {
+        bool any = false;
+        for (int64_t j = 0; j < nb && !any; ++j)
+            any = m[i * nb + j] != 0;
+        if (!any)
+            fail(DFA2C_FULLY_MASKED, "query block " + std::to_string(i) + " has no active key blocks");
+    }
+}
+
+// ------------------------------------------------------------ device plan
+struct DevPlan {
+    int grid = 0;
+    WorkItem* items = nullptr;
+    int32_t* cta_begin = nullptr;
+    uint32_t* tiles = nullptr;
+    uint8_t* masks = nullptr;
+    ~DevPlan() {
+        cudaFree(items);
+        cudaFree(cta_begin);
+        cudaFree(tiles);
+        cudaFree(masks);
+    }
+};
+
+// Head strategy for the scheduler: mask_id < 0 => cached (copy items).
+struct HeadJob {
+    int mask_id;
+    bool commit;
+};
+
+int num_sms(int device) {
+    int v = 0;
+    DFA2C_CUDA_CHECK(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device));
+    return v;
+}
+
+// Builds the LPT-scheduled work list: each (sample, head, query tile) is one
+// item costing (#KV tiles + 0.5) tile-units (compute) or 1 (copy); items are
+// sorted by cost (desc), then (bh, qtile) so concurrently running CTAs share
+// a head's K/V in L2, and greedily assigned to the least-loaded CTA. The
+// schedule is static, so every run (and every GPU count) folds the same
+// tiles in the same order: outputs are bitwise reproducible.
+std::unique_ptr<DevPlan> build_dev_plan(int device, int64_t batch, int64_t H, int64_t n, int64_t B,
+                                        const std::vector<std::vector<uint8_t>>& masks,
+                                        const std::vector<HeadJob>& jobs) {
+    const int64_t nb = ceil_div(n, B);
+    const int64_t nqt = ceil_div(n, dfa2k::TILE_M);
+    std::vector<uint32_t> tiles;
+    std::vector<uint8_t> mask_bytes;
+    std::vector<int64_t> mask_tile_base, mask_off;
+    std::vector<TileSet> sets;
+    for (const auto& m : masks) {
+        sets.push_back(build_tile_set(m.data(), n, B));
+        mask_tile_base.push_back(static_cast<int64_t>(tiles.size()));
+        tiles.insert(tiles.end(), sets.back().cols.begin(), sets.back().cols.end());
+        mask_off.push_back(static_cast<int64_t>(mask_bytes.size()));
+        mask_bytes.insert(mask_bytes.end(), m.begin(), m.end());
+    }
+    if (mask_bytes.empty())
+        mask_bytes.push_back(0);
+    if (tiles.empty())
+        tiles.push_back(0);
+    if (mask_bytes.size() > static_cast<size_t>(std::numeric_limits<int32_t>::max()) ||
+        tiles.size() > static_cast<size_t>(std::numeric_limits<int32_t>::max()))
+        fail(DFA2C_UNSUPPORTED, "work list too large");
+
+    struct Cand {
+        WorkItem w;
+        double cost;
+    };
+    std::vector<Cand> cands;
+    cands.reserve(static_cast<size_t>(batch * H * nqt));
+    for (int64_t b = 0; b < batch; ++b)
+        for (int64_t h = 0; h < H; ++h) {
+            const HeadJob& j = jobs[h];
+            for (int64_t i = 0; i < nqt; ++i) {
+                WorkItem w{};
+                w.bh = static_cast<int32_t>(b * H + h);
+                w.qtile = static_cast<int32_t>(i);
+                if (j.mask_id < 0) {
+                    w.flags = dfa2k::ITEM_COPY;
+                    cands.push_back({w, 1.0});
+                } else {
+                    const TileSet& ts = sets[j.mask_id];
+                    w.tile_begin = static_cast<int32_t>(mask_tile_base[j.mask_id] + ts.row_ptr[i]);
+                    w.n_tiles = static_cast<int32_t>(ts.row_ptr[i + 1] - ts.row_ptr[i]);
+                    w.mask_off = static_cast<int32_t>(mask_off[j.mask_id]);
+                    w.flags = j.commit ? dfa2k::ITEM_COMMIT : 0;
+                    cands.push_back({w, w.n_tiles + 0.5});
+                }
+            }
+        }
+    std::stable_sort(cands.begin(), cands.end(), [](const Cand& a, const Cand& b) {
+        if (a.cost != b.cost)
+            return a.cost > b.cost;
+        if (a.w.bh != b.w.bh)
+            return a.w.bh < b.w.bh;
+        return a.w.qtile < b.w.qtile;
+    });
+    const int grid = static_cast<int>(std::min<int64_t>(num_sms(device), static_cast<int64_t>(cands.size())));
+    using Slot = std::pair<double, int>;
+    std::priority_queue<Slot, std::vector<Slot>, std::greater<Slot>> pq;
+    for (int c = 0; c < grid; ++c)
+        pq.push({0.0, c});
+    std::vector<std::vector<WorkItem>> per_cta(static_cast<size_t>(grid));
+    for (const Cand& c : cands) {
+        Slot s = pq.top();
+        pq.pop();
+        per_cta[s.second].push_back(c.w);
+        s.first += c.cost;
+        pq.push(s);
+    }
+    std::vector<WorkItem> items;
+    std::vector<int32_t> cta_begin(static_cast<size_t>(grid + 1), 0);
+    for (int c = 0; c < grid; ++c) {
+        items.insert(items.end(), per_cta[c].begin(), per_cta[c].end());
+        cta_begin[c + 1] = static_cast<int32_t>(items.size());
+    }
+    (void)nb;
+
+    auto p = std::make_unique<DevPlan>();
+    p->grid = grid;
+    DFA2C_CUDA_CHECK(cudaMalloc(&p->items, items.size() * sizeof(WorkItem)));
+    DFA2C_CUDA_CHECK(cudaMalloc(&p->cta_begin, cta_begin.size() * sizeof(int32_t)));
+    DFA2C_CUDA_CHECK(cudaMalloc(&p->tiles, tiles.size() * sizeof(uint32_t)));
+    DFA2C_CUDA_CHECK(cudaMalloc(&p->masks, mask_bytes.size()));
+    DFA2C_CUDA_CHECK(cudaMemcpy(p->items, items.data(), items.size() * sizeof(WorkItem), cudaMemcpyHostToDevice));
+    DFA2C_CUDA_CHECK(cudaMemcpy(p->cta_begin, cta_begin.data(), cta_begin.size() * sizeof(int32_t),
+                                cudaMemcpyHostToDevice));
+    DFA2C_CUDA_CHECK(cudaMemcpy(p->tiles, tiles.data(), tiles.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    DFA2C_CUDA_CHECK(cudaMemcpy(p->masks, mask_bytes.data(), mask_bytes.size(), cudaMemcpyHostToDevice));
+    return p;
+}
+
+// Plans are cached per (device, geometry, plan) so steady-state calls only
+// encode three tensor maps and launch.
+std::mutex g_plan_mu;
+std::map<std::string, std::unique_ptr<DevPlan>> g_plans;
+
+template <class T>
+void put(std::string& key, const T& v) {
+    key.append(reinterpret_cast<const char*>(&v), sizeof(T));
+}
+
+// ------------------------------------------------------------ TMA maps
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        cudaDriverEntryPointQueryResult q{};
+        void* p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    });
+    if (!fn)
+        fail(DFA2C_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
+    return fn;
+}
+
+// [rows=batch*H][n][d] bf16, box {64 cols, 128 rows, 1}, 128-byte swizzle:
+// the canonical K-major SW128 UMMA layout (and MN-major for V).
+CUtensorMap make_map(const void* base, int64_t bh, int64_t n, int64_t d) {
+    CUtensorMap m;
+    const cuuint64_t dims[3] = {static_cast<cuuint64_t>(d), static_cast<cuuint64_t>(n),
+                                static_cast<cuuint64_t>(bh)};
+    const cuuint64_t strides[2] = {static_cast<cuuint64_t>(d * 2), static_cast<cuuint64_t>(n * d * 2)};
+    const cuuint32_t box[3] = {64, 128, 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims,
+                                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+        fail(DFA2C_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(r)) + ")");
+    return m;
+}
+
+void check_ptr(const void* p, const char* what) {
+    if (!p)
+        fail(DFA2C_SHAPE, std::string(what) + " must not be NULL");
+    if (reinterpret_cast<uintptr_t>(p) % 16 != 0)
+        fail(DFA2C_SHAPE, std::string(what) + " must be 16-byte aligned");
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- cache
+struct dfa2c_cache {
+    int64_t L = 0, H = 0, batch = 0, n = 0, d = 0;
+    int device = 0;
+    std::vector<void*> layer_buf;    // [L] -> [batch, H, n, d] bf16, lazily allocated
+    std::vector<int64_t> produced;   // [L*H], INT64_MIN = empty slot
+
+    ~dfa2c_cache() {
+        for (void* p : layer_buf)
+            if (p)
+                cudaFree(p);
+    }
+    size_t slot_elems() const { return static_cast<size_t>(n * d); }
+    size_t layer_bytes() const { return static_cast<size_t>(batch * H * n * d) * 2; }
+    void check(int64_t layer, int64_t head) const {
+        if (layer < 0 || layer >= L || head < 0 || head >= H)
+            fail(DFA2C_SHAPE, "cache slot (" + std::to_string(layer) + ", " + std::to_string(head) +
+                                  ") out of range");
+    }
+    bool has(int64_t layer, int64_t head) const {
+        return produced[static_cast<size_t>(layer * H + head)] != std::numeric_limits<int64_t>::min();
+    }
+    void* layer_ptr(int64_t layer) {
+        if (!layer_buf[layer]) {
+            DFA2C_CUDA_CHECK(cudaMalloc(&layer_buf[layer], layer_bytes()));
+            DFA2C_CUDA_CHECK(cudaMemset(layer_buf[layer], 0, layer_bytes()));
+        }
+        return layer_buf[layer];
+    }
+};
+
+namespace {
+
+struct ForwardSpec {
+    const void *q, *k, *v;
+    void* out;
+    int64_t batch;
+    const dfa2c_dims* dims;
+    int64_t block;
+    std::vector<std::vector<uint8_t>> masks;  // distinct masks
+    std::vector<HeadJob> jobs;                // per head
+    std::string mask_key;                     // identifies the masks in the plan cache
+    dfa2c_cache* cache;                       // slots read (copy) / written (commit)
+    int64_t layer;
+};
+
+void run_forward(const ForwardSpec& s, cudaStream_t stream) {
+    const int64_t n = seq_len(s.dims), d = s.dims->head_dim, H = s.dims->n_heads;
+    if (d != 64 && d != 128)
+        fail(DFA2C_UNSUPPORTED, "head_dim must be 64 or 128 on the sm_100a path (got " + std::to_string(d) + ")");
+    if (s.batch < 1)
+        fail(DFA2C_SHAPE, "batch must be >= 1");
+    if (s.batch * H > std::numeric_limits<int32_t>::max() / 2 || n > (1 << 24))
+        fail(DFA2C_UNSUPPORTED, "problem too large for the 32-bit tile coordinates");
+    check_ptr(s.q, "q");
+    check_ptr(s.k, "k");
+    check_ptr(s.v, "v");
+    check_ptr(s.out, "out");
+    int device = 0;
+    DFA2C_CUDA_CHECK(cudaGetDevice(&device));
+
+    std::string key;
+    put(key, device);
+    put(key, s.batch);
+    put(key, H);
+    put(key, n);
+    put(key, d);
+    put(key, s.block);
+    for (const HeadJob& j : s.jobs) {
+        put(key, j.mask_id);
+        put(key, j.commit);
+    }
+    key += s.mask_key;
+
+    DevPlan* plan = nullptr;
+    {
+        std::lock_guard<std::mutex> lk(g_plan_mu);
+        auto it = g_plans.find(key);
+        if (it == g_plans.end()) {
+            if (g_plans.size() >= 256)
+                g_plans.clear();
+            it = g_plans.emplace(key, build_dev_plan(device, s.batch, H, n, s.block, s.masks, s.jobs)).first;
+        }
+        plan = it->second.get();
+    }
+
+    void* cache_layer = nullptr;
+    bool need_cache = false;
+    for (const HeadJob& j : s.jobs)
+        need_cache |= (j.mask_id < 0) || j.commit;
+    if (need_cache) {
+        if (!s.cache)
+            fail(DFA2C_CACHE_MISS, "cached heads need a cache");
+        cache_layer = s.cache->layer_ptr(s.layer);
+    }
+
+    const int64_t bh = s.batch * H;
+    const CUtensorMap tq = make_map(s.q, bh, n, d);
+    const CUtensorMap tk = make_map(s.k, bh, n, d);
+    const CUtensorMap tv = make_map(s.v, bh, n, d);
+    dfa2k::AttnArgs a{};
+    a.items = plan->items;
+    a.cta_begin = plan->cta_begin;
+    a.tiles = plan->tiles;
+    a.masks = plan->masks;
+    a.out = static_cast<__nv_bfloat16*>(s.out);
+    a.cache = static_cast<__nv_bfloat16*>(cache_layer);
+    a.n = static_cast<int32_t>(n);
+    a.block = static_cast<int32_t>(std::min<int64_t>(s.block, int64_t{1} << 30));
+    a.nb = static_cast<int32_t>(ceil_div(n, s.block));
+    a.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(d)));
+    DFA2C_CUDA_CHECK(dfa2k::launch_attn(static_cast<int>(d), tq, tk, tv, a, plan->grid, stream));
+    g_launches.fetch_add(1);
+}
+
+cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+// Standard per-call mask bookkeeping for a LayerPlan: one mask per distinct
+// window (src/dispatch.cpp:38-54) plus the all-active mask for Full heads.
+void plan_jobs(const dfa2c_dims* dims, int64_t block, const int32_t* kinds, const int64_t* windows,
+               bool commit, ForwardSpec& s) {
+    const int64_t n = seq_len(dims);
+    const int64_t nb = ceil_div(n, block);
+    std::map<int64_t, int> ids;  // -1 = full, else window
+    for (int64_t h = 0; h < dims->n_heads; ++h) {
+        if (kinds[h] == DFA2C_CACHED) {
+            s.jobs.push_back({-1, false});
+            continue;
+        }
+        const int64_t key = kinds[h] == DFA2C_FULL ? -1 : windows[h];
+        auto it = ids.find(key);
+        if (it == ids.end()) {
+            it = ids.emplace(key, static_cast<int>(s.masks.size())).first;
+            if (key < 0)
+                s.masks.emplace_back(static_cast<size_t>(nb * nb), uint8_t{1});
+            else
+                s.masks.push_back(arrow_mask(dims, block, key));
+            put(s.mask_key, key);
+        }
+        s.jobs.push_back({it->second, commit});
+    }
+    put(s.mask_key, dims->n_visual);
+    put(s.mask_key, dims->n_text);
+    put(s.mask_key, dims->order);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* dfa2c_last_error(void) { return g_err.c_str(); }
+const char* dfa2c_version(void) { return "dfa2c 0.1 (sm_100a tcgen05/TMA fused head-wise attention)"; }
+int64_t dfa2c_launch_count(void) { return g_launches.load(); }
+
+int dfa2c_arrow_mask(const dfa2c_dims* dims, int64_t block, int64_t window, uint8_t* active, int64_t* nb) {
+    return guard([&] {
+        const auto m = arrow_mask(dims, block, window);
+        if (nb)
+            *nb = ceil_div(seq_len(dims), block);
+        if (active)
+            std::memcpy(active, m.data(), m.size());
+    });
+}
+
+int dfa2c_mask_stats(const uint8_t* active, int64_t n, int64_t block, int64_t head_dim, int64_t* ap,
+                     int64_t* flops, double* sparsity) {
+    return guard([&] {
+        if (!active || n < 1 || block < 1)
+            fail(DFA2C_SHAPE, "mask stats need a mask, seq_len >= 1 and block >= 1");
+        const int64_t a = active_positions(active, n, block);
+        if (ap)
+            *ap = a;
+        if (flops) {
+            if (head_dim < 1)
+                fail(DFA2C_SHAPE, "head_dim must be >= 1");
+            *flops = 4 * head_dim * a;
+        }
+        if (sparsity)
+            *sparsity = 1.0 - static_cast<double>(a) / (static_cast<double>(n) * static_cast<double>(n));
+    });
+}
+
+int64_t dfa2c_dense_flops(int64_t n, int64_t d) { return 4 * d * n * n; }
+
+int dfa2c_plan_flops(const dfa2c_dims* dims, int64_t block, const int32_t* kinds, const int64_t* windows,
+                     int64_t* flops) {
+    return guard([&] {
+        if (block < 1)
+            fail(DFA2C_SHAPE, "block_size must be >= 1");
+        const int64_t f = plan_flops(dims, block, kinds, windows);
+        if (flops)
+            *flops = f;
+    });
+}
+
+int dfa2c_plan_aggregate(const dfa2c_dims* dims, int64_t T, int64_t L, int64_t block, const int32_t* kinds,
+                         const int64_t* windows, int64_t* flops_total, int64_t* flops_dense, double* sparsity) {
+    return guard([&] {
+        // CompressionPlan::validate (src/plan.cpp:33-56)
+        validate_dims(dims);
+        if (T < 1 || L < 1 || block < 1)
+            fail(DFA2C_PLAN, "plan needs T >= 1, L >= 1, block >= 1");
+        if (!kinds)
+            fail(DFA2C_PLAN, "plan must cover every (t, layer) exactly once");
+        const int64_t H = dims->n_heads;
+        for (int64_t t = 0; t < T; ++t)
+            for (int64_t l = 0; l < L; ++l)
+                for (int64_t h = 0; h < H; ++h) {
+                    const int64_t i = (t * L + l) * H + h;
+                    if (kinds[i] < DFA2C_FULL || kinds[i] > DFA2C_CACHED)
+                        fail(DFA2C_PLAN, "unknown strategy kind");
+                    if (kinds[i] == DFA2C_ARROW && (!windows || windows[i] < 0))
+                        fail(DFA2C_PLAN, "arrow window must be >= 0");
+                    if (kinds[i] == DFA2C_CACHED && t == 0)
+                        fail(DFA2C_PLAN, "cached must not appear at the first timestep");
+                }
+        int64_t total = 0;
+        for (int64_t s = 0; s < T * L; ++s)
+            total += plan_flops(dims, block, kinds + s * H, windows ? windows + s * H : nullptr);
+        const int64_t n = seq_len(dims);
+        const int64_t dense = T * L * H * (4 * dims->head_dim * n * n);
+        if (flops_total)
+            *flops_total = total;
+        if (flops_dense)
+            *flops_dense = dense;
+        if (sparsity)
+            *sparsity = 1.0 - static_cast<double>(total) / static_cast<double>(dense);
+    });
+}
+
+int dfa2c_tile_set(const dfa2c_dims* dims, int64_t block, int32_t kind, int64_t window, int64_t* row_ptr,
+                   uint32_t* cols, int64_t* n_tiles) {
+    return guard([&] {
+        validate_dims(dims);
+        if (block < 1)
+            fail(DFA2C_SHAPE, "block_size must be >= 1");
+        const int64_t n = seq_len(dims);
+        std::vector<uint8_t> m;
+        if (kind == DFA2C_FULL)
+            m.assign(static_cast<size_t>(ceil_div(n, block) * ceil_div(n, block)), 1);
+        else if (kind == DFA2C_ARROW)
+            m = arrow_mask(dims, block, window);
+        else
+            fail(DFA2C_SHAPE, "tile sets exist for Full and Arrow heads only");
+        const TileSet ts = build_tile_set(m.data(), n, block);
+        if (n_tiles)
+            *n_tiles = static_cast<int64_t>(ts.cols.size());
+        if (row_ptr)
+            std::memcpy(row_ptr, ts.row_ptr.data(), ts.row_ptr.size() * sizeof(int64_t));
+        if (cols)
+            std::memcpy(cols, ts.cols.data(), ts.cols.size() * sizeof(uint32_t));
+    });
+}
+
+int dfa2c_cache_create(int64_t L, int64_t H, int64_t batch, int64_t n, int64_t d, dfa2c_cache** out) {
+    return guard([&] {
+        if (!out || L < 1 || H < 1 || batch < 1 || n < 1 || d < 1)
+            fail(DFA2C_SHAPE, "cache needs layers, heads, batch, seq_len, head_dim >= 1");
+        auto c = std::make_unique<dfa2c_cache>();
+        c->L = L;
+        c->H = H;
+        c->batch = batch;
+        c->n = n;
+        c->d = d;
+        DFA2C_CUDA_CHECK(cudaGetDevice(&c->device));
+        c->layer_buf.assign(static_cast<size_t>(L), nullptr);
+        c->produced.assign(static_cast<size_t>(L * H), std::numeric_limits<int64_t>::min());
+        *out = c.release();
+    });
+}
+
+int dfa2c_cache_destroy(dfa2c_cache* c) {
+    return guard([&] { delete c; });
+}
+
+int dfa2c_cache_has(const dfa2c_cache* c, int64_t layer, int64_t head, int32_t* has) {
+    return guard([&] {
+        if (!c || !has)
+            fail(DFA2C_SHAPE, "NULL cache");
+        *has = (layer >= 0 && layer < c->L && head >= 0 && head < c->H && c->has(layer, head)) ? 1 : 0;
+    });
+}
+
+int dfa2c_cache_produced_at(const dfa2c_cache* c, int64_t layer, int64_t head, int64_t* t) {
+    return guard([&] {
+        if (!c || !t)
+            fail(DFA2C_SHAPE, "NULL cache");
+        if (layer < 0 || layer >= c->L || head < 0 || head >= c->H || !c->has(layer, head))
+            fail(DFA2C_CACHE_MISS, "no cached output for layer " + std::to_string(layer) + ", head " +
+                                       std::to_string(head));
+        *t = c->produced[static_cast<size_t>(layer * c->H + head)];
+    });
+}
+
+int dfa2c_cache_staleness(const dfa2c_cache* c, int64_t layer, int64_t head, int64_t t, int64_t* st) {
+    int64_t p = 0;
+    const int rc = dfa2c_cache_produced_at(c, layer, head, &p);
+    if (rc == DFA2C_OK && st)
+        *st = t - p;
+    return rc;
+}
+
+int dfa2c_cache_store(dfa2c_cache* c, int64_t layer, int64_t head, const void* src, int64_t t, void* stream) {
+    return guard([&] {
+        if (!c || !src)
+            fail(DFA2C_SHAPE, "NULL cache or source");
+        c->check(layer, head);
+        char* dst = static_cast<char*>(c->layer_ptr(layer)) + static_cast<size_t>(head) * c->slot_elems() * 2;
+        const size_t row = c->slot_elems() * 2;
+        DFA2C_CUDA_CHECK(cudaMemcpy2DAsync(dst, row * c->H, src, row, row, static_cast<size_t>(c->batch),
+                                           cudaMemcpyDeviceToDevice, as_stream(stream)));
+        c->produced[static_cast<size_t>(layer * c->H + head)] = t;
+    });
+}
+
+int dfa2c_cache_fetch(const dfa2c_cache* c, int64_t layer, int64_t head, void* dst, void* stream) {
+    return guard([&] {
+        if (!c || !dst)
+            fail(DFA2C_SHAPE, "NULL cache or destination");
+        c->check(layer, head);
+        if (!c->has(layer, head))
+            fail(DFA2C_CACHE_MISS, "no cached output for layer " + std::to_string(layer) + ", head " +
+                                       std::to_string(head));
+        const char* src =
+            static_cast<const char*>(c->layer_buf[layer]) + static_cast<size_t>(head) * c->slot_elems() * 2;
+        const size_t row = c->slot_elems() * 2;
+        DFA2C_CUDA_CHECK(cudaMemcpy2DAsync(dst, row, src, row * c->H, row, static_cast<size_t>(c->batch),
+                                           cudaMemcpyDeviceToDevice, as_stream(stream)));
+    });
+}
+
+int dfa2c_cache_clear(dfa2c_cache* c) {
+    return guard([&] {
+        if (!c)
+            fail(DFA2C_SHAPE, "NULL cache");
+        std::fill(c->produced.begin(), c->produced.end(), std::numeric_limits<int64_t>::min());
+    });
+}
+
+int dfa2c_cache_size(const dfa2c_cache* c, int64_t* n) {
+    return guard([&] {
+        if (!c || !n)
+            fail(DFA2C_SHAPE, "NULL cache");
+        *n = 0;
+        for (int64_t l = 0; l < c->L; ++l)
+            for (int64_t h = 0; h < c->H; ++h)
+                *n += c->has(l, h) ? 1 : 0;
+    });
+}
+
+int dfa2c_cache_bytes(const dfa2c_cache* c, int64_t* bytes) {
+    return guard([&] {
+        if (!c || !bytes)
+            fail(DFA2C_SHAPE, "NULL cache");
+        *bytes = 0;
+        for (void* p : c->layer_buf)
+            if (p)
+                *bytes += static_cast<int64_t>(c->layer_bytes());
+    });
+}
+
+int dfa2c_mha_forward(const void* q, const void* k, const void* v, int64_t batch, const dfa2c_dims* dims,
+                      int64_t block, const int32_t* kinds, const int64_t* windows, dfa2c_cache* cache,
+                      int64_t layer, int64_t t, void* out, void* stream) {
+    return guard([&] {
+        // validate_plan_inputs + cached-head checks (src/dispatch.cpp:11-54),
+        // all before any device work or cache mutation.
+        validate_dims(dims);
+        if (block < 1)
+            fail(DFA2C_SHAPE, "block_size must be >= 1");
+        validate_plan(dims, kinds, windows);
+        const int64_t H = dims->n_heads;
+        if (cache) {
+            if (cache->H != H || cache->n != seq_len(dims) || cache->d != dims->head_dim || cache->batch != batch)
+                fail(DFA2C_SHAPE, "cache geometry disagrees with dims/batch");
+            if (layer < 0 || layer >= cache->L)
+                fail(DFA2C_SHAPE, "layer out of the cache's range");
+        }
+        for (int64_t h = 0; h < H; ++h)
+            if (kinds[h] == DFA2C_CACHED && (!cache || !cache->has(layer, h)))
+                fail(DFA2C_CACHE_MISS, "plan marks head " + std::to_string(h) + " Cached before it ever computed");
+        ForwardSpec s{};
+        s.q = q;
+        s.k = k;
+        s.v = v;
+        s.out = out;
+        s.batch = batch;
+        s.dims = dims;
+        s.block = block;
+        s.cache = cache;
+        s.layer = layer;
+        plan_jobs(dims, block, kinds, windows, cache != nullptr, s);
+        run_forward(s, as_stream(stream));
+        if (cache)  // phase 2: computed heads now hold output produced at t
+            for (int64_t h = 0; h < H; ++h)
+                if (kinds[h] != DFA2C_CACHED)
+                    cache->produced[static_cast<size_t>(layer * H + h)] = t;
+    });
+}
+
+int dfa2c_sparse_attention_forward(const void* q, const void* k, const void* v, void* out, int64_t n_heads,
+                                   int64_t n, int64_t d, const uint8_t* active, int64_t block, void* stream) {
+    return guard([&] {
+        if (n_heads < 1 || n < 1 || d < 1 || block < 1 || !active)
+            fail(DFA2C_SHAPE, "sparse attention needs heads, seq_len, head_dim, block >= 1 and a mask");
+        const int64_t nb = ceil_div(n, block);
+        check_rows_nonempty(active, nb);
+        dfa2c_dims dims{n_heads, d, n, 0, DFA2C_VISUAL_FIRST};
+        ForwardSpec s{};
+        s.q = q;
+        s.k = k;
+        s.v = v;
+        s.out = out;
+        s.batch = 1;
+        s.dims = &dims;
+        s.block = block;
+        s.cache = nullptr;
+        s.masks.emplace_back(active, active + nb * nb);
+        // key the plan cache on the mask bytes themselves
+        s.mask_key.assign(reinterpret_cast<const char*>(active), static_cast<size_t>(nb * nb));
+        s.jobs.assign(static_cast<size_t>(n_heads), HeadJob{0, false});
+        run_forward(s, as_stream(stream));
+    });
+}
+
+int dfa2c_dense_attention_forward(const void* q, const void* k, const void* v, void* out, int64_t n_heads,
+                                  int64_t n, int64_t d, void* stream) {
+    return guard([&] {
+        if (n_heads < 1 || n < 1 || d < 1)
+            fail(DFA2C_SHAPE, "dense attention needs heads, seq_len, head_dim >= 1");
+        dfa2c_dims dims{n_heads, d, n, 0, DFA2C_VISUAL_FIRST};
+        std::vector<int32_t> kinds(static_cast<size_t>(n_heads), DFA2C_FULL);
+        ForwardSpec s{};
+        s.q = q;
+        s.k = k;
+        s.v = v;
+        s.out = out;
+        s.batch = 1;
+        s.dims = &dims;
+        s.block = 128;
+        s.cache = nullptr;
+        plan_jobs(&dims, 128, kinds.data(), nullptr, false, s);
+        run_forward(s, as_stream(stream));
+    });
+}
+
+int dfa2c_rse_async(const void* y_m, const void* y_o, int32_t dtype, int64_t n_heads, int64_t numel, int32_t mode,
+                    double* out_dev, void* stream) {
+    return guard([&] {
+        if (!y_m || !y_o || !out_dev)
+            fail(DFA2C_SHAPE, "rse operands must not be NULL");
+        if (dtype != DFA2C_BF16 && dtype != DFA2C_F32)
+            fail(DFA2C_SHAPE, "rse operands must be bf16 or f32");
+        if (n_heads < 1 || numel < 1)
+            fail(DFA2C_SHAPE, "rse needs at least one element");
+        if (mode != DFA2C_RSE_STANDARD && mode != DFA2C_RSE_LITERAL)
+            fail(DFA2C_SHAPE, "unknown rse mode");
+        if (n_heads > 65535)
+            fail(DFA2C_UNSUPPORTED, "too many heads for one rse launch");
+        const cudaStream_t st = as_stream(stream);
+        int device = 0;
+        DFA2C_CUDA_CHECK(cudaGetDevice(&device));
+        const int64_t target = std::max<int64_t>(1, 4 * num_sms(device) / n_heads);
+        const int nblk = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(target, ceil_div(numel, 8192))));
+        double* scratch = nullptr;
+        DFA2C_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&scratch),
+                                         static_cast<size_t>(n_heads * nblk * 5) * sizeof(double), st));
+        DFA2C_CUDA_CHECK(dfa2k::launch_rse(y_m, y_o, dtype, n_heads, numel, mode, out_dev, scratch, nblk, st));
+        g_launches.fetch_add(2);
+        DFA2C_CUDA_CHECK(cudaFreeAsync(scratch, st));
+    });
+}
+
+int dfa2c_rse(const void* y_m, const void* y_o, int32_t dtype, int64_t n_heads, int64_t numel, int32_t mode,
+              double* out, void* stream) {
+    return guard([&] {
+        if (!out)
+            fail(DFA2C_SHAPE, "rse output must not be NULL");
+        const cudaStream_t st = as_stream(stream);
+        double* dev = nullptr;
+        DFA2C_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&dev), static_cast<size_t>(n_heads) * sizeof(double), st));
+        const int rc = dfa2c_rse_async(y_m, y_o, dtype, n_heads, numel, mode, dev, stream);
+        if (rc != DFA2C_OK) {
+            cudaFreeAsync(dev, st);
+            fail(rc, g_err);
+        }
+        DFA2C_CUDA_CHECK(cudaMemcpyAsync(out, dev, static_cast<size_t>(n_heads) * sizeof(double),
+                                         cudaMemcpyDeviceToHost, st));
+        DFA2C_CUDA_CHECK(cudaFreeAsync(dev, st));
+        DFA2C_CUDA_CHECK(cudaStreamSynchronize(st));
+        for (int64_t h = 0; h < n_heads; ++h)
+            if (std::isnan(out[h]))
+                fail(DFA2C_DEGENERATE, "reference output has zero variance (head " + std::to_string(h) + ")");
+    });
+}
+
+int dfa2c_influence_for_layer(const void* q, const void* k, const void* v, const dfa2c_dims* dims, int64_t block,
+                              const int64_t* windows, int64_t n_windows, int32_t include_cached,
+                              const dfa2c_cache* cache, int64_t layer, int64_t t, int32_t mode, double* influence,
+                              void* original, void* method_outputs, int64_t* evals, void* stream) {
+    return guard([&] {
+        validate_dims(dims);
+        if (block < 1)
+            fail(DFA2C_SHAPE, "block_size must be >= 1");
+        if (n_windows < 0 || (n_windows > 0 && !windows))
+            fail(DFA2C_SHAPE, "bad candidate windows");
+        for (int64_t i = 0; i < n_windows; ++i)
+            if (windows[i] < 0)
+                fail(DFA2C_SHAPE, "window radii must be >= 0");
+        const int64_t M = n_windows + (include_cached ? 1 : 0);
+        if (M == 0)
+            fail(DFA2C_SHAPE, "candidate set must be nonempty");
+        if (!influence)
+            fail(DFA2C_SHAPE, "influence output must not be NULL");
+        const int64_t H = dims->n_heads, n = seq_len(dims), d = dims->head_dim;
+        const size_t head_elems = static_cast<size_t>(n * d);
+        const size_t layer_bytes = static_cast<size_t>(H) * head_elems * 2;
+        if (include_cached && cache &&
+            (cache->H != H || cache->n != n || cache->d != d || cache->batch != 1))
+            fail(DFA2C_SHAPE, "cache geometry disagrees with dims");
+        const cudaStream_t st = as_stream(stream);
+
+        void* orig = original;
+        void* scratch_orig = nullptr;
+        if (!orig) {
+            DFA2C_CUDA_CHECK(cudaMallocAsync(&scratch_orig, layer_bytes, st));
+            orig = scratch_orig;
+        }
+        void* scratch_cand = nullptr;
+        if (!method_outputs)
+            DFA2C_CUDA_CHECK(cudaMallocAsync(&scratch_cand, layer_bytes, st));
+        double* rse_dev = nullptr;
+        DFA2C_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&rse_dev),
+                                         static_cast<size_t>(M * H) * sizeof(double), st));
+        std::vector<uint8_t> eligible(static_cast<size_t>(M * H), 0);
+
+        // 1 original evaluation: all heads Full (src/calibrate.cpp:206).
+        std::vector<int32_t> kinds(static_cast<size_t>(H), DFA2C_FULL);
+        std::vector<int64_t> wins(static_cast<size_t>(H), 0);
+        {
+            ForwardSpec s{};
+            s.q = q; s.k = k; s.v = v; s.out = orig; s.batch = 1; s.dims = dims; s.block = block;
+            plan_jobs(dims, block, kinds.data(), wins.data(), false, s);
+            run_forward(s, st);
+        }
+        for (int64_t m = 0; m < M; ++m) {
+            void* cand = method_outputs ? static_cast<char*>(method_outputs) + m * layer_bytes : scratch_cand;
+            if (m < n_windows) {
+                // Arrow(w) over every head, then per-head RSE (src/calibrate.cpp:238-250).
+                std::fill(kinds.begin(), kinds.end(), DFA2C_ARROW);
+                std::fill(wins.begin(), wins.end(), windows[m]);
+                ForwardSpec s{};
+                s.q = q; s.k = k; s.v = v; s.out = cand; s.batch = 1; s.dims = dims; s.block = block;
+                plan_jobs(dims, block, kinds.data(), wins.data(), false, s);
+                run_forward(s, st);
+                const int rc = dfa2c_rse_async(cand, orig, DFA2C_BF16, H, static_cast<int64_t>(head_elems), mode,
+                                               rse_dev + m * H, stream);
+                if (rc != DFA2C_OK)
+                    fail(rc, g_err);
+                for (int64_t h = 0; h < H; ++h)
+                    eligible[m * H + h] = 1;
+            } else if (t > 0 && cache) {
+                // Cached: slot vs original for heads with a slot (src/calibrate.cpp:222-235).
+                if (method_outputs)
+                    DFA2C_CUDA_CHECK(cudaMemsetAsync(cand, 0, layer_bytes, st));
+                for (int64_t h = 0; h < H; ++h) {
+                    if (layer < 0 || layer >= cache->L || !cache->has(layer, h))
+                        continue;
+                    const char* slot = static_cast<const char*>(cache->layer_buf[layer]) + h * head_elems * 2;
+                    if (method_outputs)
+                        DFA2C_CUDA_CHECK(cudaMemcpyAsync(static_cast<char*>(cand) + h * head_elems * 2, slot,
+                                                         head_elems * 2, cudaMemcpyDeviceToDevice, st));
+                    const int rc = dfa2c_rse_async(slot, static_cast<const char*>(orig) + h * head_elems * 2,
+                                                   DFA2C_BF16, 1, static_cast<int64_t>(head_elems), mode,
+                                                   rse_dev + m * H + h, stream);
+                    if (rc != DFA2C_OK)
+                        fail(rc, g_err);
+                    eligible[m * H + h] = 1;
+                }
+            }
+        }
+        std::vector<double> host(static_cast<size_t>(M * H));
+        DFA2C_CUDA_CHECK(cudaMemcpyAsync(host.data(), rse_dev, host.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+        DFA2C_CUDA_CHECK(cudaFreeAsync(rse_dev, st));
+        if (scratch_orig)
+            DFA2C_CUDA_CHECK(cudaFreeAsync(scratch_orig, st));
+        if (scratch_cand)
+            DFA2C_CUDA_CHECK(cudaFreeAsync(scratch_cand, st));
+        DFA2C_CUDA_CHECK(cudaStreamSynchronize(st));
+        for (int64_t h = 0; h < H; ++h)
+            for (int64_t m = 0; m < M; ++m) {
+                double val = std::numeric_limits<double>::infinity();
+                if (eligible[m * H + h]) {
+                    val = host[m * H + h];
+                    if (std::isnan(val))
+                        fail(DFA2C_DEGENERATE, "reference output has zero variance (head " + std::to_string(h) + ")");
+                }
+                influence[h * M + m] = val;
+            }
+        if (evals)
+            *evals += 1 + M;
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,387 @@
+"""GPU parity of the sm_100a path against the oracle / the reference itself.
+
+Stated tolerance for attention outputs (bf16 in, fp32 accumulate, bf16 out)
+against the f64 two-pass oracle evaluated on the SAME bf16-rounded inputs
+(attention_head_impl<double>, src/tensor.cpp:73-114, pinned bit-exact in
+tests/test_oracle.py):
+    max|gpu - ref| / max|ref| <= 1e-2   and   RSE(gpu, ref) <= 5e-5   per head.
+Bit-exact: cached-head copies, cache commits, Full == Arrow(max window),
+run-to-run determinism, head isolation, CacheMiss-before-compute.
+"""
+import ctypes
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2503_22796_b200 import api
+from paper_2503_22796_b200.api import (AttentionDims, ArrowSpec, BlockMask, CacheMissError, FullyMaskedRowError,
+                                       HeadCache, HeadStrategy, LayerPlan, ShapeError)
+
+pytestmark = pytest.mark.gpu
+
+MAX_REL = 1e-2
+MAX_RSE = 5e-5
+
+
+def torch():
+    import torch as t
+
+    return t
+
+
+def bf16_inputs(shape, seed):
+    """Seeded gaussian -> (bf16 CUDA tensor, the same values as f32 numpy)."""
+    t = torch()
+    x = oracle.round_bf16(oracle.gaussian(shape, seed))
+    return t.from_numpy(x).to("cuda").to(t.bfloat16), x
+
+
+def to_np(x):
+    return x.float().cpu().numpy()
+
+
+def head_mask(dims, B, s):
+    n = dims.seq_len()
+    nb = (n + B - 1) // B
+    if s.kind == "full":
+        return np.ones(nb * nb, np.uint8)
+    return oracle.arrow_mask(dims.n_visual, dims.n_text, 1 if dims.order == api.TEXT_FIRST else 0, B,
+                             s.window_blocks)
+
+
+def check_close(got, want, what=""):
+    got = np.asarray(got, np.float64)
+    rel = np.abs(got - want).max() / np.abs(want).max()
+    den = ((want - want.mean()) ** 2).sum()
+    r = ((got - want) ** 2).sum() / den
+    assert rel <= MAX_REL and r <= MAX_RSE, f"{what}: max-rel {rel:.3e} rse {r:.3e}"
+    return rel, r
+
+
+def oracle_head(qn, kn, vn, dims, B, s, rows=None):
+    return oracle.attention_rows_f64(qn, kn, vn, head_mask(dims, B, s), B, rows)
+
+
+CASES = [
+    # (H, nv, nt, d, B, order, plan)
+    (4, 1024, 77, 64, 128, 0, "F A0 A2 F"),     # cfg1 geometry (ragged 77-token tail)
+    (4, 1024, 77, 64, 64, 0, "F A0 A2 A1"),     # cfg1 at B=64 (element masks inside 128 tiles)
+    (3, 256, 32, 128, 32, 0, "A0 A1 F"),        # test_arrow.cpp:154-166 geometry, d=128
+    (3, 300, 44, 64, 48, 1, "A0 A2 F"),         # text-first, B not dividing 128
+    (2, 130, 17, 128, 16, 0, "A0 A3"),          # small ragged
+    (2, 600, 50, 64, 200, 0, "A0 A1"),          # B > 128
+    (2, 17, 3, 64, 8, 0, "A0 F"),               # N < one tile
+]
+
+
+@pytest.mark.parametrize("H,nv,nt,d,B,order,plan", CASES)
+def test_multi_strategy_matches_oracle(H, nv, nt, d, B, order, plan):
+    t = torch()
+    dims = AttentionDims(H, d, nv, nt, api.TEXT_FIRST if order else api.VISUAL_FIRST)
+    n = nv + nt
+    q, qn = bf16_inputs((H, n, d), 11)
+    k, kn = bf16_inputs((H, n, d), 12)
+    v, vn = bf16_inputs((H, n, d), 13)
+    lp = LayerPlan.parse(plan)
+    out = api.multi_strategy_attention(q, k, v, lp, None, 0, 0, dims, B)
+    t.cuda.synchronize()
+    o = to_np(out)
+    for h, s in enumerate(lp.strategies):
+        check_close(o[h], oracle_head(qn[h], kn[h], vn[h], dims, B, s), f"head {h} {s}")
+
+
+def test_cached_heads_and_cache_commit_semantics():
+    """dispatch.cpp:62-88 + test_dispatch.cpp:63-88: cached heads splice the
+    stored slot bit-exactly and keep produced_at; computed heads commit."""
+    t = torch()
+    H, nv, nt, d, B = 4, 1024, 77, 64, 128
+    dims = AttentionDims(H, d, nv, nt)
+    n = nv + nt
+    cache = HeadCache(2, H, n, d)
+    q0, _ = bf16_inputs((H, n, d), 21)
+    k0, _ = bf16_inputs((H, n, d), 22)
+    v0, _ = bf16_inputs((H, n, d), 23)
+    o0 = api.multi_strategy_attention(q0, k0, v0, LayerPlan.all_full(H), cache, 1, 0, dims, B)
+    t.cuda.synchronize()
+    for h in range(H):
+        assert cache.has(1, h) and cache.produced_at(1, h) == 0
+        assert t.equal(cache.fetch(1, h), o0[h])
+    assert not cache.has(0, 0)
+    q1, q1n = bf16_inputs((H, n, d), 31)
+    k1, k1n = bf16_inputs((H, n, d), 32)
+    v1, v1n = bf16_inputs((H, n, d), 33)
+    lp = LayerPlan.parse("F A0 A2 C")
+    o1 = api.multi_strategy_attention(q1, k1, v1, lp, cache, 1, 1, dims, B)
+    t.cuda.synchronize()
+    assert t.equal(o1[3], o0[3])                      # spliced bit-exactly
+    assert cache.produced_at(1, 3) == 0               # cached head keeps its slot
+    assert [cache.produced_at(1, h) for h in range(3)] == [1, 1, 1]
+    for h in range(3):
+        assert t.equal(cache.fetch(1, h), o1[h])      # commit == output, bitwise
+        check_close(to_np(o1[h]), oracle_head(q1n[h], k1n[h], v1n[h], dims, B, lp.strategies[h]))
+    assert cache.staleness(1, 3, 5) == 5
+    assert cache.size() == 4
+
+
+def test_cache_miss_is_raised_before_any_compute():
+    t = torch()
+    H, n, d = 3, 300, 64
+    dims = AttentionDims(H, d, 280, 20)
+    cache = HeadCache(1, H, n, d)
+    q, _ = bf16_inputs((H, n, d), 1)
+    out = t.full((H, n, d), 7.0, dtype=t.bfloat16, device="cuda")
+    with pytest.raises(CacheMissError):
+        api.multi_strategy_attention(q, q, q, LayerPlan.parse("F C F"), cache, 0, 1, dims, 64, out=out)
+    t.cuda.synchronize()
+    assert bool((out == 7.0).all()) and cache.size() == 0
+    with pytest.raises(ShapeError):
+        api.multi_strategy_attention(q, q, q, LayerPlan.parse("F F"), cache, 0, 1, dims, 64)
+
+
+def test_full_equals_max_window_arrow_bitwise_and_deterministic():
+    t = torch()
+    H, nv, nt, d, B = 3, 2048, 120, 128, 128
+    dims = AttentionDims(H, d, nv, nt)
+    n = nv + nt
+    q, _ = bf16_inputs((H, n, d), 41)
+    k, _ = bf16_inputs((H, n, d), 42)
+    v, _ = bf16_inputs((H, n, d), 43)
+    full = api.multi_strategy_attention(q, k, v, LayerPlan.all_full(H), None, 0, 0, dims, B)
+    maxw = api.multi_strategy_attention(q, k, v, LayerPlan([HeadStrategy.Arrow(100)] * H), None, 0, 0, dims, B)
+    again = api.multi_strategy_attention(q, k, v, LayerPlan.all_full(H), None, 0, 0, dims, B)
+    t.cuda.synchronize()
+    assert t.equal(full, maxw) and t.equal(full, again)
+    # head isolation (test_dispatch.cpp:98-109)
+    a = api.multi_strategy_attention(q, k, v, LayerPlan.parse("F F A1"), None, 0, 0, dims, B)
+    b = api.multi_strategy_attention(q, k, v, LayerPlan.parse("F A0 A1"), None, 0, 0, dims, B)
+    t.cuda.synchronize()
+    assert t.equal(a[0], b[0]) and t.equal(a[2], b[2])
+
+
+def test_batched_samples_match_single_sample_calls():
+    t = torch()
+    Bt, H, nv, nt, d, B = 3, 4, 1024, 77, 64, 128
+    dims = AttentionDims(H, d, nv, nt)
+    n = nv + nt
+    q, _ = bf16_inputs((Bt, H, n, d), 51)
+    k, _ = bf16_inputs((Bt, H, n, d), 52)
+    v, _ = bf16_inputs((Bt, H, n, d), 53)
+    lp = LayerPlan.parse("F A0 A2 A1")
+    ob = api.multi_strategy_attention(q, k, v, lp, None, 0, 0, dims, B)
+    for s in range(Bt):
+        os_ = api.multi_strategy_attention(q[s], k[s], v[s], lp, None, 0, 0, dims, B)
+        t.cuda.synchronize()
+        assert t.equal(ob[s], os_)
+
+
+def test_sparse_attention_forward_arbitrary_masks():
+    t = torch()
+    rng = np.random.default_rng(3)
+    for n, d, B in ((300, 64, 16), (513, 128, 64), (1000, 64, 100)):
+        nb = (n + B - 1) // B
+        m = (rng.random((nb, nb)) < 0.3).astype(np.uint8)
+        m[np.arange(nb), np.arange(nb)] = 1
+        mask = BlockMask(B, n, nb, nb, m.ravel().copy())
+        q, qn = bf16_inputs((2, n, d), 61)
+        k, kn = bf16_inputs((2, n, d), 62)
+        v, vn = bf16_inputs((2, n, d), 63)
+        out = api.sparse_attention_forward(q, k, v, mask)
+        t.cuda.synchronize()
+        for h in range(2):
+            check_close(to_np(out[h]), oracle.attention_rows_f64(qn[h], kn[h], vn[h], mask.active, B))
+        dense = api.dense_tiled_attention(q, k, v)
+        t.cuda.synchronize()
+        check_close(to_np(dense[0]), oracle.attention_rows_f64(qn[0], kn[0], vn[0]))
+    bad = BlockMask.all_active(64, 16)
+    for j in range(4):
+        bad.set(2, j, False)
+    x, _ = bf16_inputs((64, 64), 1)
+    with pytest.raises(FullyMaskedRowError):
+        api.sparse_attention_forward(x, x, x, bad)
+
+
+def test_against_reference_multi_strategy_golden():
+    """The reference's own multi_strategy_attention outputs (golden, f32 on the
+    same bf16-rounded inputs): t=0 all Full, t=1 [F, A0, A2, C] with its cache."""
+    import os
+
+    t = torch()
+    G = np.load(os.path.join(os.path.dirname(__file__), "golden", "reference_golden.npz"))
+    H, nv, nt, d, B = (int(x) for x in G["msa_geom"])
+    n = nv + nt
+    xs = [oracle.round_bf16(oracle.gaussian((H, n, d), 7000 + tt * 10 + j)) for tt in range(2) for j in range(3)]
+    dev = [t.from_numpy(x).cuda().to(t.bfloat16) for x in xs]
+    dims = AttentionDims(H, d, nv, nt)
+    cache = HeadCache(1, H, n, d)
+    o0 = api.multi_strategy_attention(dev[0], dev[1], dev[2], LayerPlan.all_full(H), cache, 0, 0, dims, B)
+    o1 = api.multi_strategy_attention(dev[3], dev[4], dev[5], LayerPlan.parse("F A0 A2 C"), cache, 0, 1, dims, B)
+    t.cuda.synchronize()
+    for h in range(H):
+        check_close(to_np(o0[h]), G["msa_out_t0"][h].astype(np.float64), f"t0 head {h}")
+        check_close(to_np(o1[h]), G["msa_out_t1"][h].astype(np.float64), f"t1 head {h}")
+    assert [cache.produced_at(0, h) for h in range(H)] == list(G["msa_produced_at"])
+
+
+@pytest.mark.parametrize("plan_kind", ["flux68"])
+def test_flux_2k_sampled_rows(plan_kind):
+    """Config 3 at full size (16384+512, H=24, d=128, B=128, FLUX68 after an
+    all-Full t=0): every head checked on sampled rows (incl. text rows) against
+    the f64 oracle; cached heads bit-exact."""
+    t = torch()
+    H, nv, nt, d, B = 24, 16384, 512, 128, 128
+    n = nv + nt
+    dims = AttentionDims(H, d, nv, nt)
+    cache = HeadCache(1, H, n, d)
+    q, qn = bf16_inputs((H, n, d), 1)
+    k, kn = bf16_inputs((H, n, d), 2)
+    v, vn = bf16_inputs((H, n, d), 3)
+    slots = {}
+    for h in range(H):
+        s, _ = bf16_inputs((n, d), 100 + h)
+        cache.store(0, h, s, 0)
+        slots[h] = s
+    lp = api.flux68_plan(H)
+    out = api.multi_strategy_attention(q, k, v, lp, cache, 0, 1, dims, B)
+    t.cuda.synchronize()
+    rows = np.concatenate([np.arange(0, nv, 997), np.arange(nv, n, 61), [n - 1]]).astype(np.int64)
+    o = out.float().cpu().numpy()
+    for h, s in enumerate(lp.strategies):
+        if s.kind == "cached":
+            assert t.equal(out[h], slots[h])
+            continue
+        want = oracle_head(qn[h], kn[h], vn[h], dims, B, s, rows)
+        check_close(o[h][rows], want, f"head {h} {s}")
+
+
+def test_rse_kernel_against_oracle_and_reference_semantics():
+    t = torch()
+    # f32 operands: fp64 accumulation, within 1e-9 of the reference's sequential rse
+    for n, scale in ((2, 1.0), (1000, 0.1), (16896 * 128, 0.01), (12345, 3.0)):
+        a = oracle.gaussian((n,), 7) + 2.5
+        b = a + scale * oracle.gaussian((n,), 8)
+        for mode in (0, 1):
+            want = oracle.rse_f32(b, a, mode)
+            got = api.rse(t.from_numpy(b).cuda(), t.from_numpy(a).cuda(), mode)
+            assert abs(got - want) <= 1e-9 * abs(want), (n, mode, got, want)
+    # bf16 operands, several heads in one launch
+    H, n = 24, 16896 * 128
+    a, an = bf16_inputs((H, n), 9)
+    b, bn = bf16_inputs((H, n), 10)
+    b = (a.float() + 0.05 * b.float()).to(t.bfloat16)
+    bn = to_np(b)
+    got = api.rse_per_head(b, a)
+    for h in (0, 7, 23):
+        want = oracle.rse_f32(bn[h], an[h])
+        assert abs(got[h] - want) <= 1e-9 * want
+    # hand values and the degenerate case (test_calibrate.cpp:48-72)
+    y_o = t.tensor([1.0, 3.0], device="cuda")
+    assert api.rse(t.tensor([2.0, 2.0], device="cuda"), y_o) == pytest.approx(1.0)
+    assert api.rse(y_o, y_o) == 0.0
+    assert api.rse(y_o, y_o, api.RseMode.literal) == pytest.approx(1.0)
+    with pytest.raises(api.DegenerateReferenceError):
+        api.rse(t.tensor([5.0, 6.0], device="cuda"), t.tensor([5.0, 5.0], device="cuda"))
+
+
+def test_influence_for_layer_semantics():
+    """calibrate.cpp:193-253 + test_calibrate.cpp:85-146."""
+    t = torch()
+    H, nv, nt, d, B = 4, 1024, 77, 64, 128
+    dims = AttentionDims(H, d, nv, nt)
+    n = nv + nt
+    q, _ = bf16_inputs((H, n, d), 71)
+    k, _ = bf16_inputs((H, n, d), 72)
+    v, _ = bf16_inputs((H, n, d), 73)
+    cache = HeadCache(1, H, n, d)
+    stats = api.CalibrationStats()
+    methods = api.make_candidates([0, 2, 100], include_cached=True)
+    li = api.influence_for_layer(q, k, v, methods, cache, 0, 0, dims, B, stats=stats)
+    M = len(methods)
+    assert stats.attention_evals == 1 + M
+    infl = li.influence.reshape(H, M)
+    assert np.isinf(infl[:, 3]).all()          # Cached ineligible at t = 0
+    assert (infl[:, 2] == 0.0).all()           # max window == Full, bitwise
+    assert (infl[:, 0] >= infl[:, 1]).all()    # narrower window, larger error
+    for h in range(H):                          # independent recomputation
+        want = oracle.rse_f32(to_np(li.method_outputs[0][h]), to_np(li.original[h]))
+        assert infl[h, 0] == pytest.approx(want, rel=1e-12)
+    full = api.multi_strategy_attention(q, k, v, LayerPlan.all_full(H), None, 0, 0, dims, B)
+    t.cuda.synchronize()
+    assert t.equal(full, li.original)
+    # Cached candidate against identical entries measures 0 (test_calibrate.cpp:97-109)
+    for h in range(H):
+        cache.store(0, h, li.original[h], 0)
+    li2 = api.influence_for_layer(q, k, v, api.make_candidates([], True), cache, 0, 1, dims, B)
+    assert (li2.influence == 0.0).all()
+
+
+def test_influence_matches_reference_values():
+    """Same bf16-rounded inputs through the reference's influence_for_layer
+    (f32) and ours (bf16): per-head influences agree to a few percent."""
+    if not oracle.ref_available():
+        pytest.skip("oracle/_ref not available")
+    from oracle import c_double, c_float, c_int64, ptr
+    t = torch()
+    H, nv, nt, d, B = 4, 512, 64, 64, 64
+    dims = AttentionDims(H, d, nv, nt)
+    n = nv + nt
+    q, qn = bf16_inputs((H, n, d), 81)
+    k, kn = bf16_inputs((H, n, d), 82)
+    v, vn = bf16_inputs((H, n, d), 83)
+    wins = np.array([0, 1, 3], np.int64)
+    infl_ref = np.zeros(H * 3, np.float64)
+    c = oracle.ref().ref_cache_create()
+    oracle.ref_check(oracle.ref().ref_influence_for_layer(
+        ptr(qn, c_float), ptr(kn, c_float), ptr(vn, c_float), H, d, nv, nt, 0, ptr(wins, c_int64), 3, 0, c, 0, 0,
+        B, 0, ptr(infl_ref, c_double), None, None, None))
+    oracle.ref().ref_cache_destroy(c)
+    li = api.influence_for_layer(q, k, v, api.make_candidates([0, 1, 3], False), None, 0, 0, dims, B)
+    np.testing.assert_allclose(li.influence, infl_ref, rtol=0.05)
+
+
+def test_run_pipeline_on_reference_workload():
+    """run_pipeline (workload.cpp:230-262) over the reference generator's
+    drifting streams: every (t, l) within tolerance of the reference's own
+    pipeline; cached heads replay their last computed output bitwise."""
+    if not oracle.ref_available():
+        pytest.skip("oracle/_ref not available")
+    from oracle import c_float, c_int32, c_int64, ptr
+    t = torch()
+    H, nv, nt, d, L, T, B = 4, 512, 64, 64, 2, 3, 64
+    n = nv + nt
+    per = H * n * d
+    qs, ks, vs = (np.zeros((T * L, H, n, d), np.float32) for _ in range(3))
+    oracle.ref_check(oracle.ref().ref_generate(H, d, nv, nt, 0, L, T, B, 1234, ptr(qs, c_float), ptr(ks, c_float),
+                                               ptr(vs, c_float)))
+    qs, ks, vs = (oracle.round_bf16(x).reshape(T * L, H, n, d) for x in (qs, ks, vs))
+    dims = AttentionDims(H, d, nv, nt)
+    plan = api.CompressionPlan.all_full(dims, T, L, B)
+    plan.layers[1 * L + 0] = LayerPlan.parse("F A0 A2 C")
+    plan.layers[2 * L + 1] = LayerPlan.parse("C A1 F C")
+    plan.layers[2 * L + 0] = LayerPlan.parse("A0 C C F")
+    dq, dk, dv = (t.from_numpy(x).cuda().to(t.bfloat16) for x in (qs, ks, vs))
+    stats = api.run_pipeline(lambda tt, l: dq[tt * L + l], lambda tt, l: dk[tt * L + l],
+                             lambda tt, l: dv[tt * L + l], plan)
+    t.cuda.synchronize()
+    assert stats.flops_total == plan.flops_total()
+    assert stats.sparsity == pytest.approx(plan.aggregate_sparsity(), abs=1e-15)
+    c = oracle.ref().ref_cache_create()
+    for tt in range(T):
+        for l in range(L):
+            lp = plan.at(tt, l)
+            kinds = np.array([api._KIND_CODE[s.kind] for s in lp.strategies], np.int32)
+            wins = np.array([s.window_blocks for s in lp.strategies], np.int64)
+            o = np.zeros((H, n, d), np.float32)
+            s = tt * L + l
+            oracle.ref_check(oracle.ref().ref_multi_strategy_attention(
+                ptr(np.ascontiguousarray(qs[s]), c_float), ptr(np.ascontiguousarray(ks[s]), c_float),
+                ptr(np.ascontiguousarray(vs[s]), c_float), H, d, nv, nt, 0, ptr(kinds, c_int32),
+                ptr(wins, c_int64), c, l, tt, B, ptr(o, c_float)))
+            got = to_np(stats.output(tt, l, L))
+            for h in range(H):
+                check_close(got[h], o[h].astype(np.float64), f"t{tt} l{l} h{h}")
+    oracle.ref().ref_cache_destroy(c)
+    # cached replay: (t=2, l=0) head 1 is Cached -> equals (t=1, l=0) head 1 output... which was A0 at t=1
+    assert t.equal(stats.output(2, 0, L)[1], stats.output(1, 0, L)[1])
+    assert t.equal(stats.output(2, 1, L)[0], stats.output(1, 1, L)[0])
+    _ = (ctypes, per, ArrowSpec)
