@@ -11,7 +11,7 @@ import os
 from ctypes import POINTER, c_char_p, c_double, c_int32, c_int64, c_uint8, c_uint32, c_void_p
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libdfa2_b200.so")
+LIB_PATH = os.environ.get("DFA2_LIB") or os.path.join(HERE, "libdfa2_b200.so")  # DFA2_LIB: A/B builds
 
 
 class Dfa2Error(RuntimeError):

@@ -39,23 +39,27 @@ def _stale(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=()) -> str:
     deps = _sources()
     for d in (CSRC, os.path.join(ROOT, "include"), os.path.join(ROOT, "include", "dfa2")):
         if os.path.isdir(d):
             deps += [os.path.join(d, f) for f in os.listdir(d) if f.endswith((".h", ".cuh", ".hpp"))]
-    if not force and not _stale(LIB, deps):
-        return LIB
+    if not force and not _stale(out, deps):
+        return out
     cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-cudart", "static",
            "-Xcompiler", "-fPIC,-fvisibility=hidden,-fvisibility-inlines-hidden", "-Xptxas", "-v" if verbose else "-O3",
            "-I", os.path.join(ROOT, "include"), "-I", CSRC,
-           "-o", LIB + ".tmp", *_sources(), "-lcuda" if False else "-ldl"]
+           *[f"-D{d}" for d in defines], "-o", out + ".tmp", *_sources(), "-ldl"]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(out + ".tmp", out)
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    # python -m paper_2503_22796_b200.build [--force] [-v] [--out PATH] [-DNAME=VAL ...]
+    argv = sys.argv[1:]
+    out = argv[argv.index("--out") + 1] if "--out" in argv else LIB
+    defs = [a[2:] for a in argv if a.startswith("-D")]
+    print(build(force="--force" in argv or bool(defs), verbose="-v" in argv, out=out, defines=defs))

@@ -8,18 +8,22 @@
 //                  the KV tiles build_arrow_mask keeps (src/arrow.cpp:113-153)
 //   Cached heads-> copy of the stored slot  (src/dispatch.cpp:77-81)
 //
-// Structure (persistent, one CTA per SM, static LPT work list built on the
-// host, see dfa2c.cpp):
-//   warp 0      TMA producer: Q tile (double-buffered) + K/V tiles (ring)
-//   warp 1      tcgen05 issuer: S = Q K^T (SS, into TMEM, double-buffered)
-//               and O += P V (TS: P read from TMEM, V from smem)
+// Structure: persistent, one CTA per SM, static LPT work list (dfa2c.cpp).
+// A work item is a PAIR of 128-row query tiles (lanes A, B) of one head
+// sharing one K/V stream (the union of their mask rows, ascending key order).
+//   warp 0      TMA producer: Q_A/Q_B, K ring (runs ahead), V ring
+//   warp 1      tcgen05 issuer, per union tile u and lane L:
+//                 [wait P_L(u-1)] O_L += P_L V(u-1)   (TS: P from TMEM)
+//                 S_L = Q_L K(u)^T                      (SS, into TMEM)
+//               so one lane's MMAs overlap the other lane's softmax.
 //   warp 2      TMEM allocator
-//   warps 4-7   softmax warpgroup: one query row per thread; tcgen05.ld of
-//               S, online softmax in the exp2 domain with lazy (threshold 8)
-//               rescaling of O in TMEM, P written back to TMEM as bf16,
-//               epilogue O/l -> bf16 -> out (+ cache slot); also executes the
-//               Cached heads' copy items.
-// TMEM (512 cols): S0 [0,128)  S1 [128,256)  O [256,256+D)
+//   warps 4-7   softmax lane A, warps 8-11 softmax lane B: one query row per
+//               thread; S read from TMEM twice (row max, then exp2 -> bf16 P
+//               written back over S), lazy rescale (threshold 2^8) of O in
+//               TMEM, part of the exp2s on the FMA pipe (Cody-Waite +
+//               degree-3 polynomial) to unload MUFU; epilogue O/l -> bf16 ->
+//               out (+ cache slot); Cached heads' copy items.
+// TMEM (512 cols): S_A [0,128) S_B [128,256) O_A [256,256+D) O_B [384,384+D)
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -31,28 +35,65 @@ namespace dfa2k {
 
 template <int D>
 struct Cfg {
-    static constexpr int STAGES = D == 128 ? 2 : 4;
+    static constexpr int KSTAGES = D == 128 ? 3 : 5;
+    static constexpr int VSTAGES = D == 128 ? 2 : 4;
     static constexpr int BOXES = D / 64;                       // 128-byte column boxes
     static constexpr uint32_t BOX_BYTES = 128u * 128u;         // 128 rows x 128 B
     static constexpr uint32_t TILE_BYTES = BOXES * BOX_BYTES;  // one Q, K or V tile
-    static constexpr uint32_t Q_OFF = 0;
-    static constexpr uint32_t K_OFF = Q_OFF + 2 * TILE_BYTES;
-    static constexpr uint32_t V_OFF = K_OFF + STAGES * TILE_BYTES;
-    static constexpr uint32_t BAR_OFF = V_OFF + STAGES * TILE_BYTES;
-    static constexpr int NBARS = 2 + 2 + 3 * STAGES + 2 + 2 + 2;
+    static constexpr uint32_t Q_OFF = 0;                       // Q_A, Q_B
+    static constexpr uint32_t K_OFF = 2 * TILE_BYTES;
+    static constexpr uint32_t V_OFF = K_OFF + KSTAGES * TILE_BYTES;
+    static constexpr uint32_t BAR_OFF = V_OFF + VSTAGES * TILE_BYTES;
+    static constexpr int NBARS = 2 + 2 * KSTAGES + 2 * VSTAGES + 8;
     static constexpr uint32_t SMEM_BYTES = BAR_OFF + NBARS * 8 + 16 + 1024;
     static constexpr uint32_t TMEM_COLS = 512;
-    static constexpr uint32_t O_COL = 256;
+    static constexpr int THREADS = 384;
 };
+
+// Every EMU_EVERY-th column of a 32-column chunk computes exp2 on the FMA
+// pipe instead of MUFU (0 disables).
+#ifndef DFA2_EMU_EVERY
+#define DFA2_EMU_EVERY 0
+#endif
 
 namespace {
 
-__device__ __forceinline__ uint32_t s_col(int sb) { return sb ? 128u : 0u; }
+__device__ __forceinline__ uint32_t s_col(int lane) { return lane ? 128u : 0u; }
+__device__ __forceinline__ uint32_t o_col(int lane) { return lane ? 384u : 256u; }
+
+// 2^x on the FMA/ALU pipes: x = j + f, j = floor(x) by the round-down
+// magic-number add, 2^f by a degree-3 minimax polynomial (max rel. error
+// 8.6e-5, far below the bf16 rounding P is stored with), exponent added as
+// an integer.
+__device__ __forceinline__ float ex2_poly(float x) {
+    x = fmaxf(x, -127.f);
+    const float t = __fadd_rd(x, 12582912.f);
+    const float f = x - (t - 12582912.f);
+    float p = fmaf(0.0770652f, f, 0.227647f);
+    p = fmaf(p, f, 0.69511634f);
+    p = fmaf(p, f, 1.0f);
+    return __uint_as_float(__float_as_uint(p) + (__float_as_uint(t) << 23));
+}
+
+// Two exp2s on the FMA/ALU pipes with packed fp32x2 arithmetic.
+__device__ __forceinline__ float2 ex2_poly2(float2 x) {
+    x.x = fmaxf(x.x, -127.f);
+    x.y = fmaxf(x.y, -127.f);
+    const float2 magic = make_float2(12582912.f, 12582912.f);
+    const float2 t = __fadd2_rd(x, magic);
+    const float2 tm = __fadd2_rn(t, make_float2(-12582912.f, -12582912.f));  // floor(x)
+    const float2 f = __ffma2_rn(tm, make_float2(-1.f, -1.f), x);              // x - floor(x)
+    float2 p = __ffma2_rn(make_float2(0.0770652f, 0.0770652f), f, make_float2(0.227647f, 0.227647f));
+    p = __ffma2_rn(p, f, make_float2(0.69511634f, 0.69511634f));
+    p = __ffma2_rn(p, f, make_float2(1.0f, 1.0f));
+    return make_float2(__uint_as_float(__float_as_uint(p.x) + (__float_as_uint(t.x) << 23)),
+                       __uint_as_float(__float_as_uint(p.y) + (__float_as_uint(t.y) << 23)));
+}
 
 // Per-row 128-column validity bitmap for a partial tile: key < N and the
 // (query block, key block) pair active in the head's block mask.
-__device__ __forceinline__ void tile_valid_bits(const AttnArgs& a, const uint8_t* mask, int row,
-                                                int k0, uint32_t (&vm)[4]) {
+__device__ __forceinline__ void tile_valid_bits(const AttnArgs& a, const uint8_t* mask, int row, int k0,
+                                                uint32_t (&vm)[4]) {
     vm[0] = vm[1] = vm[2] = vm[3] = 0u;
     const int B = a.block;
     const int rr = row < a.n ? row : a.n - 1;
@@ -75,14 +116,155 @@ __device__ __forceinline__ void tile_valid_bits(const AttnArgs& a, const uint8_t
     }
 }
 
+
+// Partial tiles: overwrite the masked scores in TMEM with -inf before the
+// common softmax pass (only tiles with block size != 128 or a ragged tail).
+__device__ __forceinline__ void mask_tile_in_tmem(uint32_t sc, const uint32_t (&vm)[4]) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        uint32_t s[32];
+        tmem_ld32(sc + 32 * c, s);
+        tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+            if (!((vm[c] >> i) & 1u))
+                s[i] = 0xFF800000u;  // -inf
+        tmem_st32(sc + 32 * c, s);
+    }
+    tmem_st_wait();
+}
+
+// One S tile of one lane. All 128 scores of the thread's row are loaded
+// once (4 x tcgen05.ld, one wait): row max, lazy O rescale, then
+// P = exp2(s*scale - m) as bf16 written back into the lane's S columns:
+// keys 64..127 -> cols [64,96) (a region whose scores are already in
+// registers) and signalled on p_half, so the MMA warp starts the first half
+// of O += P V while keys 0..63 -> cols [0,32) are still being computed
+// (signalled on p_full). Masked scores arrive as -inf and give P == 0
+// exactly (MUFU ex2(-inf) = 0; the polynomial path selects 0 below 2^-126).
+template <int D>
+__device__ __forceinline__ void softmax_half(const uint32_t* s, float2 scale2, float2 neg_m, float2& sum,
+                                             uint32_t dst) {
+#pragma unroll
+    for (int cc = 0; cc < 2; ++cc) {
+        uint32_t pk[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            const float2 x = __ffma2_rn(
+                make_float2(__uint_as_float(s[32 * cc + 2 * i]), __uint_as_float(s[32 * cc + 2 * i + 1])), scale2,
+                neg_m);
+            float2 p;
+            if (DFA2_EMU_EVERY > 0 && (i % DFA2_EMU_EVERY) == DFA2_EMU_EVERY - 1) {
+                p = ex2_poly2(x);
+                p.x = x.x < -126.f ? 0.f : p.x;
+                p.y = x.y < -126.f ? 0.f : p.y;
+            } else {
+                p = make_float2(ex2_approx(x.x), ex2_approx(x.y));
+            }
+            sum = __fadd2_rn(sum, p);
+            pk[i] = pack_bf16x2(p.x, p.y);
+        }
+        tmem_st16(dst + 16 * cc, pk);
+    }
+}
+
+template <int D>
+__device__ __forceinline__ void softmax_tile(uint32_t sc, uint32_t oc, float sl2, float& m_ref, float& l,
+                                             bool first, uint32_t bar_half, uint32_t bar_full) {
+    uint32_t hi[64];
+    float mx;
+    {
+        uint32_t lo[64];
+        tmem_ld32(sc, lo);
+        tmem_ld32(sc + 32, lo + 32);
+        tmem_ld32(sc + 64, hi);
+        tmem_ld32(sc + 96, hi + 32);
+        tmem_ld_wait();
+        float m0 = -INFINITY, m1 = -INFINITY;
+#pragma unroll
+        for (int c = 0; c < 64; c += 2) {  // two independent 3-input max chains
+            m0 = fmaxf(m0, fmaxf(__uint_as_float(lo[c]), __uint_as_float(lo[c + 1])));
+            m1 = fmaxf(m1, fmaxf(__uint_as_float(hi[c]), __uint_as_float(hi[c + 1])));
+        }
+        mx = fmaxf(m0, m1) * sl2;
+    }
+    // lazy rescale: keep the reference max unless the tile max exceeds it by
+    // more than 8 (P <= 2^8 stays exact in fp32 and representable in bf16)
+    float factor = 1.f;
+    bool need = false;
+    if (first) {
+        m_ref = mx;
+    } else if (mx > m_ref + 8.f) {
+        factor = (m_ref == -INFINITY) ? 0.f : ex2_approx(m_ref - mx);
+        m_ref = mx;
+        need = true;
+    }
+    l *= factor;
+    if (__any_sync(0xFFFFFFFFu, need)) {
+        // O holds every earlier PV of this lane: this S was issued after them,
+        // so they completed before s_full fired.
+#pragma unroll
+        for (int c = 0; c < D / 32; ++c) {
+            uint32_t o[32];
+            tmem_ld32(oc + 32 * c, o);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+                o[i] = __float_as_uint(__uint_as_float(o[i]) * factor);
+            tmem_st32(oc + 32 * c, o);
+        }
+    }
+    const float msub = (m_ref == -INFINITY) ? 0.f : m_ref;
+    const float2 scale2 = make_float2(sl2, sl2);
+    const float2 neg_m = make_float2(-msub, -msub);
+    float2 sum = make_float2(0.f, 0.f);
+    // keys 64..127 from registers -> cols [64,96): the MMA warp starts on them
+    softmax_half<D>(hi, scale2, neg_m, sum, sc + 64);
+    tmem_st_wait();
+    tc_fence_before();
+    mbar_arrive(bar_half);
+    // keys 0..63 re-read (cols [0,64) untouched so far) -> cols [0,32)
+    uint32_t lo[64];
+    tmem_ld32(sc, lo);
+    tmem_ld32(sc + 32, lo + 32);
+    tmem_ld_wait();
+    softmax_half<D>(lo, scale2, neg_m, sum, sc);
+    tmem_st_wait();
+    tc_fence_before();
+    mbar_arrive(bar_full);
+    l += sum.x + sum.y;
+}
+
+// Flat cursor over the union tiles of a CTA's compute items.
+struct Cursor {
+    int it;
+    int j;
+};
+
+__device__ __forceinline__ void skip_copies(const WorkItem* items, int it1, Cursor& c) {
+    while (c.it < it1 && ((items[c.it].flags & ITEM_COPY) || items[c.it].n_tiles == 0)) {
+        ++c.it;
+        c.j = 0;
+    }
+}
+
+__device__ __forceinline__ void advance(const WorkItem* items, int it1, Cursor& c) {
+    if (++c.j >= items[c.it].n_tiles) {
+        ++c.it;
+        c.j = 0;
+        skip_copies(items, it1, c);
+    }
+}
+
 }  // namespace
 
 template <int D>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(384, 1)
     attn_fwd_sm100(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtensorMap tmk,
                    const __grid_constant__ CUtensorMap tmv, const AttnArgs args) {
     using C = Cfg<D>;
-    constexpr int S = C::STAGES;
+    constexpr int KS = C::KSTAGES;
+    constexpr int VS = C::VSTAGES;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t sbase = (raw + 1023u) & ~1023u;
@@ -92,28 +274,34 @@ __global__ void __launch_bounds__(256, 1)
     const int lane = threadIdx.x & 31;
 
     const uint32_t bars = sbase + C::BAR_OFF;
-    auto q_full = [&](int i) { return bars + 8u * i; };
-    auto q_empty = [&](int i) { return bars + 8u * (2 + i); };
-    auto k_full = [&](int s) { return bars + 8u * (4 + s); };
-    auto v_full = [&](int s) { return bars + 8u * (4 + S + s); };
-    auto kv_empty = [&](int s) { return bars + 8u * (4 + 2 * S + s); };
-    auto s_full = [&](int i) { return bars + 8u * (4 + 3 * S + i); };
-    auto p_full = [&](int i) { return bars + 8u * (6 + 3 * S + i); };
-    auto pv_done = [&](int i) { return bars + 8u * (8 + 3 * S + i); };
+    const uint32_t q_full = bars;
+    const uint32_t q_empty = bars + 8;
+    auto k_full = [&](int s) { return bars + 8u * (2 + s); };
+    auto k_empty = [&](int s) { return bars + 8u * (2 + KS + s); };
+    auto v_full = [&](int s) { return bars + 8u * (2 + 2 * KS + s); };
+    auto v_empty = [&](int s) { return bars + 8u * (2 + 2 * KS + VS + s); };
+    auto s_full = [&](int l) { return bars + 8u * (2 + 2 * KS + 2 * VS + l); };
+    auto p_full = [&](int l) { return bars + 8u * (4 + 2 * KS + 2 * VS + l); };
+    auto o_full = [&](int l) { return bars + 8u * (6 + 2 * KS + 2 * VS + l); };
+    auto p_half = [&](int l) { return bars + 8u * (8 + 2 * KS + 2 * VS + l); };
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::BAR_OFF + C::NBARS * 8);
 
     if (threadIdx.x == 0) {
-        for (int i = 0; i < 2; ++i) {
-            mbar_init(q_full(i), 1);
-            mbar_init(q_empty(i), 1);
-            mbar_init(s_full(i), 1);
-            mbar_init(p_full(i), 128);
-            mbar_init(pv_done(i), 1);
-        }
-        for (int s = 0; s < S; ++s) {
+        mbar_init(q_full, 1);
+        mbar_init(q_empty, 1);
+        for (int s = 0; s < KS; ++s) {
             mbar_init(k_full(s), 1);
+            mbar_init(k_empty(s), 1);
+        }
+        for (int s = 0; s < VS; ++s) {
             mbar_init(v_full(s), 1);
-            mbar_init(kv_empty(s), 1);
+            mbar_init(v_empty(s), 1);
+        }
+        for (int l = 0; l < 2; ++l) {
+            mbar_init(s_full(l), 1);
+            mbar_init(p_full(l), 128);
+            mbar_init(p_half(l), 128);
+            mbar_init(o_full(l), 1);
         }
         fence_mbar_init();
     }
@@ -133,40 +321,57 @@ __global__ void __launch_bounds__(256, 1)
 
     const int it0 = args.cta_begin[blockIdx.x];
     const int it1 = args.cta_begin[blockIdx.x + 1];
+    const WorkItem* items = args.items;
 
     if (warp == 0) {
         // ------------------------------------------------ TMA producer
         if (lane == 0) {
-            uint32_t kv_it = 0, q_it = 0;
-            for (int it = it0; it < it1; ++it) {
-                const WorkItem w = args.items[it];
-                if (w.flags & ITEM_COPY)
-                    continue;
-                const int qb = q_it & 1;
-                mbar_wait(q_empty(qb), ((q_it >> 1) & 1) ^ 1);
-                mbar_arrive_expect_tx(q_full(qb), C::TILE_BYTES);
+            Cursor kc{it0, 0}, vc{it0, 0};
+            skip_copies(items, it1, kc);
+            skip_copies(items, it1, vc);
+            uint32_t kcount = 0, vcount = 0, qcount = 0;
+            while (vc.it < it1) {
+                // K runs up to KS-1 tiles ahead of V, but never into the next
+                // item before every V of the current one is issued (the Q pair
+                // buffer is single and freed by the current item's last S).
+                while (kc.it < it1 && kcount < vcount + (KS - 1) && !(kc.j == 0 && kc.it > vc.it)) {
+                    const WorkItem& w = items[kc.it];
+                    if (kc.j == 0) {
+                        mbar_wait(q_empty, (qcount & 1) ^ 1);
+                        const int nq = w.qtile_b >= 0 ? 2 : 1;
+                        mbar_arrive_expect_tx(q_full, nq * C::TILE_BYTES);
 #pragma unroll
-                for (int b = 0; b < C::BOXES; ++b)
-                    tma_load_3d(sbase + C::Q_OFF + qb * C::TILE_BYTES + b * C::BOX_BYTES, &tmq,
-                                q_full(qb), b * 64, w.qtile * TILE_M, w.bh);
-                ++q_it;
-                for (int j = 0; j < w.n_tiles; ++j) {
-                    const int kt = static_cast<int>(args.tiles[w.tile_begin + j] & TILE_INDEX_MASK);
-                    const int st = kv_it % S;
-                    const uint32_t ph = (kv_it / S) & 1;
-                    mbar_wait(kv_empty(st), ph ^ 1);
+                        for (int b = 0; b < C::BOXES; ++b) {
+                            tma_load_3d(sbase + C::Q_OFF + b * C::BOX_BYTES, &tmq, q_full, b * 64,
+                                        w.qtile_a * TILE_M, w.bh);
+                            if (nq == 2)
+                                tma_load_3d(sbase + C::Q_OFF + C::TILE_BYTES + b * C::BOX_BYTES, &tmq, q_full,
+                                            b * 64, w.qtile_b * TILE_M, w.bh);
+                        }
+                        ++qcount;
+                    }
+                    const int kt = static_cast<int>(args.tiles[w.tile_begin + kc.j] & TILE_INDEX_MASK);
+                    const int st = kcount % KS;
+                    mbar_wait(k_empty(st), ((kcount / KS) & 1) ^ 1);
                     mbar_arrive_expect_tx(k_full(st), C::TILE_BYTES);
 #pragma unroll
                     for (int b = 0; b < C::BOXES; ++b)
-                        tma_load_3d(sbase + C::K_OFF + st * C::TILE_BYTES + b * C::BOX_BYTES, &tmk,
-                                    k_full(st), b * 64, kt * TILE_N, w.bh);
-                    mbar_arrive_expect_tx(v_full(st), C::TILE_BYTES);
-#pragma unroll
-                    for (int b = 0; b < C::BOXES; ++b)
-                        tma_load_3d(sbase + C::V_OFF + st * C::TILE_BYTES + b * C::BOX_BYTES, &tmv,
-                                    v_full(st), b * 64, kt * TILE_N, w.bh);
-                    ++kv_it;
+                        tma_load_3d(sbase + C::K_OFF + st * C::TILE_BYTES + b * C::BOX_BYTES, &tmk, k_full(st),
+                                    b * 64, kt * TILE_N, w.bh);
+                    ++kcount;
+                    advance(items, it1, kc);
                 }
+                const WorkItem& w = items[vc.it];
+                const int kt = static_cast<int>(args.tiles[w.tile_begin + vc.j] & TILE_INDEX_MASK);
+                const int st = vcount % VS;
+                mbar_wait(v_empty(st), ((vcount / VS) & 1) ^ 1);
+                mbar_arrive_expect_tx(v_full(st), C::TILE_BYTES);
+#pragma unroll
+                for (int b = 0; b < C::BOXES; ++b)
+                    tma_load_3d(sbase + C::V_OFF + st * C::TILE_BYTES + b * C::BOX_BYTES, &tmv, v_full(st),
+                                b * 64, kt * TILE_N, w.bh);
+                ++vcount;
+                advance(items, it1, vc);
             }
         }
     } else if (warp == 1) {
@@ -174,176 +379,155 @@ __global__ void __launch_bounds__(256, 1)
         if (lane == 0) {
             constexpr uint32_t IDESC_S = idesc_bf16_f32(128, 128, false);
             constexpr uint32_t IDESC_O = idesc_bf16_f32(128, D, true);
-            uint32_t kv_it = 0, q_it = 0, g = 0;
+            uint32_t kcount = 0, vcount = 0, qcount = 0;
+            uint32_t pcnt[2] = {0, 0};
             for (int it = it0; it < it1; ++it) {
-                const WorkItem w = args.items[it];
-                if (w.flags & ITEM_COPY)
+                const WorkItem w = items[it];
+                if ((w.flags & ITEM_COPY) || w.n_tiles == 0)
                     continue;
-                const int qb = q_it & 1;
-                mbar_wait(q_full(qb), (q_it >> 1) & 1);
+                mbar_wait(q_full, qcount & 1);
                 tc_fence_after();
-                const uint32_t q_addr = sbase + C::Q_OFF + qb * C::TILE_BYTES;
-                const int n = w.n_tiles;
-                for (int j = 0; j <= n; ++j) {
-                    if (j < n) {
-                        // S_j = Q K_j^T  (M=128, N=128, K=D in steps of 16)
-                        const uint32_t gj = g + j;
-                        const int sb = gj & 1;
-                        const uint32_t kv = kv_it + j;
-                        const int st = kv % S;
-                        mbar_wait(k_full(st), (kv / S) & 1);
-                        tc_fence_after();
-                        const uint32_t k_addr = sbase + C::K_OFF + st * C::TILE_BYTES;
+                bool first_pv[2] = {true, true};
+                uint32_t prev = 0;
+                const int U = w.n_tiles;
+                for (int u = 0; u <= U; ++u) {
+                    const uint32_t word = u < U ? args.tiles[w.tile_begin + u] : 0u;
+                    const int vst = vcount % VS;
+                    const int kst = kcount % KS;
+                    const uint32_t v_addr = sbase + C::V_OFF + vst * C::TILE_BYTES;
+                    const uint32_t k_addr = sbase + C::K_OFF + kst * C::TILE_BYTES;
+                    bool v_ready = false, k_ready = false;
+                    // lane by lane: O_L += P_L(u-1) V(u-1), then S_L = Q_L K(u)^T, so
+                    // lane A's next S overlaps lane B's softmax and vice versa.
 #pragma unroll
-                        for (int kk = 0; kk < D / 16; ++kk) {
-                            const uint32_t off = (kk >> 2) * C::BOX_BYTES + (kk & 3) * 32;
-                            const uint64_t ad = smem_desc_sw128(q_addr + off, 16, 1024);
-                            const uint64_t bd = smem_desc_sw128(k_addr + off, 16, 1024);
-                            mma_bf16_ss(tmem + s_col(sb), ad, bd, IDESC_S, kk > 0 ? 1u : 0u);
-                        }
-                        mma_commit(s_full(sb));
-                        if (j == n - 1)
-                            mma_commit(q_empty(qb));
-                    }
-                    if (j >= 1) {
-                        // O += P_{j-1} V_{j-1}  (M=128, N=D, K=128 keys in steps of 16)
-                        const uint32_t gp = g + j - 1;
-                        const int sb = gp & 1;
-                        const uint32_t kv = kv_it + j - 1;
-                        const int st = kv % S;
-                        mbar_wait(p_full(sb), (gp >> 1) & 1);
-                        mbar_wait(v_full(st), (kv / S) & 1);
-                        tc_fence_after();
-                        const uint32_t v_addr = sbase + C::V_OFF + st * C::TILE_BYTES;
+                    for (int L = 0; L < 2; ++L) {
+                        const uint32_t need = L ? TILE_NEED_B : TILE_NEED_A;
+                        if (u >= 1 && (prev & need)) {
+                            if (!v_ready) {
+                                mbar_wait(v_full(vst), (vcount / VS) & 1);
+                                v_ready = true;
+                            }
+                            // keys 64..127 (P in cols [64,96)) as soon as that half is ready,
+                            // then keys 0..63 (cols [0,32))
+                            mbar_wait(p_half(L), pcnt[L] & 1);
+                            tc_fence_after();
 #pragma unroll
-                        for (int kk = 0; kk < 128 / 16; ++kk) {
-                            const uint64_t bd = smem_desc_sw128(v_addr + kk * 2048, C::BOX_BYTES, 1024);
-                            mma_bf16_ts(tmem + C::O_COL, tmem + s_col(sb) + kk * 8, bd, IDESC_O,
-                                        (j > 1 || kk > 0) ? 1u : 0u);
+                            for (int kk = 4; kk < 8; ++kk) {
+                                const uint64_t bd = smem_desc_sw128(v_addr + kk * 2048, C::BOX_BYTES, 1024);
+                                mma_bf16_ts(tmem + o_col(L), tmem + s_col(L) + 64 + (kk - 4) * 8, bd, IDESC_O,
+                                            (!first_pv[L] || kk > 4) ? 1u : 0u);
+                            }
+                            mbar_wait(p_full(L), pcnt[L] & 1);
+                            tc_fence_after();
+#pragma unroll
+                            for (int kk = 0; kk < 4; ++kk) {
+                                const uint64_t bd = smem_desc_sw128(v_addr + kk * 2048, C::BOX_BYTES, 1024);
+                                mma_bf16_ts(tmem + o_col(L), tmem + s_col(L) + kk * 8, bd, IDESC_O, 1u);
+                            }
+                            first_pv[L] = false;
+                            ++pcnt[L];
                         }
-                        mma_commit(kv_empty(st));
-                        mma_commit(pv_done(sb));
+                        if (u < U && (word & need)) {
+                            if (!k_ready) {
+                                mbar_wait(k_full(kst), (kcount / KS) & 1);
+                                k_ready = true;
+                            }
+                            tc_fence_after();
+                            const uint32_t q_addr = sbase + C::Q_OFF + L * C::TILE_BYTES;
+#pragma unroll
+                            for (int kk = 0; kk < D / 16; ++kk) {
+                                const uint32_t off = (kk >> 2) * C::BOX_BYTES + (kk & 3) * 32;
+                                const uint64_t ad = smem_desc_sw128(q_addr + off, 16, 1024);
+                                const uint64_t bd = smem_desc_sw128(k_addr + off, 16, 1024);
+                                mma_bf16_ss(tmem + s_col(L), ad, bd, IDESC_S, kk > 0 ? 1u : 0u);
+                            }
+                            mma_commit(s_full(L));
+                        }
                     }
+                    if (u >= 1) {
+                        mma_commit(v_empty(vst));  // V(u-1) free once its PVs complete
+                        ++vcount;
+                    }
+                    if (u < U) {
+                        mma_commit(k_empty(kst));  // K(u) free once its S MMAs complete
+                        ++kcount;
+                        if (u == U - 1)
+                            mma_commit(q_empty);
+                    }
+                    prev = word;
                 }
-                g += n;
-                kv_it += n;
-                ++q_it;
+                // both lanes' O final once every MMA issued so far completes
+                mma_commit(o_full(0));
+                if (w.qtile_b >= 0)
+                    mma_commit(o_full(1));
+                ++qcount;
             }
         }
     } else if (warp >= 4) {
-        // ------------------------------------------------ softmax warpgroup
-        const int wq = warp & 3;
-        const int r = wq * 32 + lane;
+        // ------------------------------------------------ softmax lanes
+        const int L = (warp - 4) >> 2;              // 0 = lane A, 1 = lane B
+        const int wq = warp & 3;                    // TMEM lane quarter
+        const int r = wq * 32 + lane;               // row within the query tile
+        const int tid2 = threadIdx.x - 128;         // 0..255 across both lanes
         const uint32_t lrow = static_cast<uint32_t>(wq * 32) << 16;
+        const uint32_t need_bit = L ? TILE_NEED_B : TILE_NEED_A;
+        const uint32_t part_bit = L ? TILE_PART_B : TILE_PART_A;
         const float sl2 = args.scale_log2;
         const int N = args.n;
-        uint32_t g = 0;
+        const uint32_t sc = tmem + lrow + s_col(L);
+        const uint32_t oc = tmem + lrow + o_col(L);
+        uint32_t scnt = 0, icnt = 0;
         for (int it = it0; it < it1; ++it) {
-            const WorkItem w = args.items[it];
-            const int row = w.qtile * TILE_M + r;
+            const WorkItem w = items[it];
             if (w.flags & ITEM_COPY) {
-                // Cached head: out <- stored slot, 16 B per thread-step.
-                const int rows = min(TILE_M, N - w.qtile * TILE_M);
-                const size_t base = (static_cast<size_t>(w.bh) * N + static_cast<size_t>(w.qtile) * TILE_M) * D;
+                // Cached head: out <- stored slot over the pair's rows.
+                const int r0 = w.qtile_a * TILE_M;
+                const int r1 = min(N, (w.qtile_b >= 0 ? w.qtile_b : w.qtile_a) * TILE_M + TILE_M);
+                const size_t base = (static_cast<size_t>(w.bh) * N + r0) * D;
                 const uint4* src = reinterpret_cast<const uint4*>(args.cache + base);
                 uint4* dst = reinterpret_cast<uint4*>(args.out + base);
-                const int nvec = rows * D / 8;
-                for (int i = r; i < nvec; i += 128)
+                const int nvec = (r1 - r0) * D / 8;
+                for (int i = tid2; i < nvec; i += 256)
                     dst[i] = src[i];
                 continue;
             }
+            const int qt = L ? w.qtile_b : w.qtile_a;
+            if (qt < 0 || w.n_tiles == 0)
+                continue;
+            const int row = qt * TILE_M + r;
             const uint8_t* mask = args.masks + w.mask_off;
             float m_ref = -INFINITY;
             float l = 0.f;
-            for (int j = 0; j < w.n_tiles; ++j, ++g) {
-                const int sb = g & 1;
-                const uint32_t word = args.tiles[w.tile_begin + j];
-                mbar_wait(s_full(sb), (g >> 1) & 1);
-                tc_fence_after();
-                float s[128];
-#pragma unroll
-                for (int c = 0; c < 4; ++c)
-                    tmem_ld32(tmem + lrow + s_col(sb) + 32 * c, reinterpret_cast<uint32_t*>(s) + 32 * c);
-                tmem_ld_wait();
-                if (word & TILE_PARTIAL) {
-                    uint32_t vm[4];
+            bool first = true;
+            for (int u = 0; u < w.n_tiles; ++u) {
+                const uint32_t word = args.tiles[w.tile_begin + u];
+                if (!(word & need_bit))
+                    continue;
+                uint32_t vm[4] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu};
+                const bool partial = (word & part_bit) != 0;
+                if (partial)
                     tile_valid_bits(args, mask, row, static_cast<int>(word & TILE_INDEX_MASK) * TILE_N, vm);
-#pragma unroll
-                    for (int c = 0; c < 128; ++c)
-                        if (!((vm[c >> 5] >> (c & 31)) & 1u))
-                            s[c] = -INFINITY;
-                }
-                float m0 = s[0], m1 = s[1], m2 = s[2], m3 = s[3];
-#pragma unroll
-                for (int c = 4; c < 128; c += 4) {
-                    m0 = fmaxf(m0, s[c]);
-                    m1 = fmaxf(m1, s[c + 1]);
-                    m2 = fmaxf(m2, s[c + 2]);
-                    m3 = fmaxf(m3, s[c + 3]);
-                }
-                const float mx = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3)) * sl2;
-                float factor = 1.f;
-                bool need = false;
-                if (j == 0) {
-                    m_ref = mx;
-                } else if (mx > m_ref + 8.f) {
-                    factor = (m_ref == -INFINITY) ? 0.f : ex2_approx(m_ref - mx);
-                    m_ref = mx;
-                    need = true;
-                }
-                l *= factor;
-                if (__any_sync(0xFFFFFFFFu, need)) {
-                    // O (through PV_{g-1}) must be final before rescaling it.
-                    const uint32_t gp = g - 1;
-                    mbar_wait(pv_done(gp & 1), (gp >> 1) & 1);
-                    tc_fence_after();
-#pragma unroll
-                    for (int c = 0; c < D / 32; ++c) {
-                        uint32_t o[32];
-                        tmem_ld32(tmem + lrow + C::O_COL + 32 * c, o);
-                        tmem_ld_wait();
-#pragma unroll
-                        for (int i = 0; i < 32; ++i)
-                            o[i] = __float_as_uint(__uint_as_float(o[i]) * factor);
-                        tmem_st32(tmem + lrow + C::O_COL + 32 * c, o);
-                    }
-                    tmem_st_wait();
-                }
-                const float msub = (m_ref == -INFINITY) ? 0.f : m_ref;
-                float sum0 = 0.f, sum1 = 0.f;
-#pragma unroll
-                for (int c = 0; c < 4; ++c) {
-                    uint32_t pk[16];
-#pragma unroll
-                    for (int i = 0; i < 16; ++i) {
-                        const float p0 = ex2_approx(fmaf(s[32 * c + 2 * i], sl2, -msub));
-                        const float p1 = ex2_approx(fmaf(s[32 * c + 2 * i + 1], sl2, -msub));
-                        sum0 += p0;
-                        sum1 += p1;
-                        pk[i] = pack_bf16x2(p0, p1);
-                    }
-                    tmem_st16(tmem + lrow + s_col(sb) + 16 * c, pk);
-                }
-                l += sum0 + sum1;
-                tmem_st_wait();
-                tc_fence_before();
-                mbar_arrive(p_full(sb));
+                mbar_wait(s_full(L), scnt & 1);
+                tc_fence_after();
+                if (partial)
+                    mask_tile_in_tmem(sc, vm);
+                softmax_tile<D>(sc, oc, sl2, m_ref, l, first, p_half(L), p_full(L));
+                ++scnt;
+                first = false;
             }
             // ---- epilogue: O / l -> bf16 -> out (+ cache slot)
-            const uint32_t gp = g - 1;
-            mbar_wait(pv_done(gp & 1), (gp >> 1) & 1);
+            mbar_wait(o_full(L), icnt & 1);
+            ++icnt;
             tc_fence_after();
             const float inv = 1.f / l;
             const bool valid = row < N;
             const size_t off = (static_cast<size_t>(w.bh) * N + row) * D;
             uint4* orow = reinterpret_cast<uint4*>(args.out + off);
-            uint4* crow = (w.flags & ITEM_COMMIT) && args.cache
-                              ? reinterpret_cast<uint4*>(args.cache + off)
-                              : nullptr;
+            uint4* crow = (w.flags & ITEM_COMMIT) && args.cache ? reinterpret_cast<uint4*>(args.cache + off) : nullptr;
 #pragma unroll
             for (int c = 0; c < D / 32; ++c) {
                 uint32_t o[32];
-                tmem_ld32(tmem + lrow + C::O_COL + 32 * c, o);
+                tmem_ld32(oc + 32 * c, o);
                 tmem_ld_wait();
                 uint32_t pk[16];
 #pragma unroll
@@ -377,27 +561,30 @@ template __global__ void attn_fwd_sm100<128>(const __grid_constant__ CUtensorMap
                                              const __grid_constant__ CUtensorMap,
                                              const __grid_constant__ CUtensorMap, const AttnArgs);
 
+namespace {
+template <int D>
+cudaError_t launch_d(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const AttnArgs& args,
+                     int grid, cudaStream_t stream) {
+    using C = Cfg<D>;
+    static int configured_for = -1;  // device the smem attribute was set on
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (configured_for != dev) {
+        const cudaError_t e =
+            cudaFuncSetAttribute(attn_fwd_sm100<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
+        if (e != cudaSuccess)
+            return e;
+        configured_for = dev;
+    }
+    attn_fwd_sm100<D><<<grid, C::THREADS, C::SMEM_BYTES, stream>>>(tq, tk, tv, args);
+    return cudaGetLastError();
+}
+}  // namespace
+
 // Host-side launcher (called from dfa2c.cpp).
 cudaError_t launch_attn(int d, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                         const AttnArgs& args, int grid, cudaStream_t stream) {
-    if (d == 128) {
-        using C = Cfg<128>;
-        static bool init = false;
-        if (!init) {
-            cudaFuncSetAttribute(attn_fwd_sm100<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
-            init = true;
-        }
-        attn_fwd_sm100<128><<<grid, 256, C::SMEM_BYTES, stream>>>(tq, tk, tv, args);
-    } else {
-        using C = Cfg<64>;
-        static bool init = false;
-        if (!init) {
-            cudaFuncSetAttribute(attn_fwd_sm100<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
-            init = true;
-        }
-        attn_fwd_sm100<64><<<grid, 256, C::SMEM_BYTES, stream>>>(tq, tk, tv, args);
-    }
-    return cudaGetLastError();
+    return d == 128 ? launch_d<128>(tq, tk, tv, args, grid, stream) : launch_d<64>(tq, tk, tv, args, grid, stream);
 }
 
 }  // namespace dfa2k

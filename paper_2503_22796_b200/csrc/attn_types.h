@@ -6,16 +6,19 @@
 
 namespace dfa2k {
 
-// One unit of the per-head tile scheduler: a 128-row query tile of one
-// (sample, head), either computed over its mask's KV tile list or (Cached
-// heads) copied back from the head cache.
+// One unit of the per-head tile scheduler: a PAIR of 128-row query tiles
+// (lanes A and B) of one (sample, head) that share one K/V tile stream — the
+// union of the two tiles' mask rows, in ascending key order — or, for Cached
+// heads, a 256-row copy-back from the head cache.
 struct WorkItem {
     int32_t bh;          // sample * H + head: row of the [batch*H, N, d] view
-    int32_t qtile;       // 128-row query tile index
-    int32_t tile_begin;  // offset into the tile list (compute items)
-    int32_t n_tiles;     // KV tiles to fold (0 for copy items)
+    int32_t qtile_a;     // lane A query tile
+    int32_t qtile_b;     // lane B query tile, -1 when the pair is a single tile
+    int32_t tile_begin;  // offset into the tile-word list (compute items)
+    int32_t n_tiles;     // union length (0 for copy items)
     int32_t mask_off;    // byte offset of this head's nb*nb block mask
     int32_t flags;       // ITEM_COPY | ITEM_COMMIT
+    int32_t pad;
 };
 
 enum : int32_t {
@@ -23,10 +26,16 @@ enum : int32_t {
     ITEM_COMMIT = 2,  // computed head: also store O into the cache slot (:85-88)
 };
 
-// Tile-list word: KV tile index in the low 31 bits; the top bit marks tiles
-// that need element masking (block size != 128 or a ragged tail).
-constexpr uint32_t TILE_PARTIAL = 0x80000000u;
-constexpr uint32_t TILE_INDEX_MASK = 0x7FFFFFFFu;
+// Tile word: KV tile index in bits [0,24); bit 24/25: lane A/B folds this
+// tile; bit 26/27: lane A/B needs element masking (mask block size != 128 or
+// a ragged tail).
+constexpr uint32_t TILE_INDEX_MASK = 0x00FFFFFFu;
+constexpr uint32_t TILE_NEED_A = 1u << 24;
+constexpr uint32_t TILE_NEED_B = 1u << 25;
+constexpr uint32_t TILE_PART_A = 1u << 26;
+constexpr uint32_t TILE_PART_B = 1u << 27;
+// Per-query-tile tile-set word (dfa2c_tile_set): bit 31 = needs element masking.
+constexpr uint32_t TILE_SET_PARTIAL = 0x80000000u;
 
 // Kernel arguments (besides the three TMA tensor maps).
 struct AttnArgs {

@@ -187,7 +187,7 @@ TileSet build_tile_set(const uint8_t* m, int64_t n, int64_t B) {
             if (!any)
                 continue;
             const bool partial = !all || (c1 - c0) < 128;
-            ts.cols.push_back(static_cast<uint32_t>(t) | (partial ? dfa2k::TILE_PARTIAL : 0u));
+            ts.cols.push_back(static_cast<uint32_t>(t) | (partial ? dfa2k::TILE_SET_PARTIAL : 0u));
         }
         ts.row_ptr[i + 1] = static_cast<int64_t>(ts.cols.size());
     }
@@ -231,25 +231,63 @@ int num_sms(int device) {
     return v;
 }
 
-// Builds the LPT-scheduled work list: each (sample, head, query tile) is one
-// item costing (#KV tiles + 0.5) tile-units (compute) or 1 (copy); items are
-// sorted by cost (desc), then (bh, qtile) so concurrently running CTAs share
-// a head's K/V in L2, and greedily assigned to the least-loaded CTA. The
-// schedule is static, so every run (and every GPU count) folds the same
-// tiles in the same order: outputs are bitwise reproducible.
+// Pair lists: for every pair of query tiles (2p, 2p+1) the union of their
+// KV tile rows (ascending), each word tagged with the lanes that fold it.
+struct PairSet {
+    std::vector<int64_t> row_ptr;  // [n_pairs + 1]
+    std::vector<uint32_t> words;
+    std::vector<int32_t> n_a, n_b;  // per pair: tiles lane A / lane B fold
+};
+
+PairSet build_pair_set(const TileSet& ts, int64_t nqt) {
+    PairSet ps;
+    const int64_t np = (nqt + 1) / 2;
+    ps.row_ptr.assign(static_cast<size_t>(np + 1), 0);
+    for (int64_t p = 0; p < np; ++p) {
+        const int64_t qa = 2 * p, qb = 2 * p + 1;
+        std::map<uint32_t, uint32_t> u;  // kv tile -> flags
+        for (int64_t i = ts.row_ptr[qa]; i < ts.row_ptr[qa + 1]; ++i) {
+            const uint32_t c = ts.cols[i];
+            u[c & ~dfa2k::TILE_SET_PARTIAL] |=
+                dfa2k::TILE_NEED_A | ((c & dfa2k::TILE_SET_PARTIAL) ? dfa2k::TILE_PART_A : 0u);
+        }
+        int32_t nb_ = 0;
+        if (qb < nqt)
+            for (int64_t i = ts.row_ptr[qb]; i < ts.row_ptr[qb + 1]; ++i) {
+                const uint32_t c = ts.cols[i];
+                u[c & ~dfa2k::TILE_SET_PARTIAL] |=
+                    dfa2k::TILE_NEED_B | ((c & dfa2k::TILE_SET_PARTIAL) ? dfa2k::TILE_PART_B : 0u);
+                ++nb_;
+            }
+        for (const auto& kv : u)
+            ps.words.push_back(kv.first | kv.second);
+        ps.row_ptr[p + 1] = static_cast<int64_t>(ps.words.size());
+        ps.n_a.push_back(static_cast<int32_t>(ts.row_ptr[qa + 1] - ts.row_ptr[qa]));
+        ps.n_b.push_back(nb_);
+    }
+    return ps;
+}
+
+// Builds the LPT-scheduled work list: each (sample, head, query-tile pair)
+// is one item costing (#lane-A tiles + #lane-B tiles + 1) tile-units
+// (compute) or #rows/128 (copy); items are sorted by cost (desc), then
+// (bh, pair) so concurrently running CTAs share a head's K/V in L2, and
+// greedily assigned to the least-loaded CTA. The schedule is static, so
+// every run (and every GPU count) folds the same tiles in the same order:
+// outputs are bitwise reproducible.
 std::unique_ptr<DevPlan> build_dev_plan(int device, int64_t batch, int64_t H, int64_t n, int64_t B,
                                         const std::vector<std::vector<uint8_t>>& masks,
                                         const std::vector<HeadJob>& jobs) {
-    const int64_t nb = ceil_div(n, B);
     const int64_t nqt = ceil_div(n, dfa2k::TILE_M);
+    const int64_t np = (nqt + 1) / 2;
     std::vector<uint32_t> tiles;
     std::vector<uint8_t> mask_bytes;
     std::vector<int64_t> mask_tile_base, mask_off;
-    std::vector<TileSet> sets;
+    std::vector<PairSet> sets;
     for (const auto& m : masks) {
-        sets.push_back(build_tile_set(m.data(), n, B));
+        sets.push_back(build_pair_set(build_tile_set(m.data(), n, B), nqt));
         mask_tile_base.push_back(static_cast<int64_t>(tiles.size()));
-        tiles.insert(tiles.end(), sets.back().cols.begin(), sets.back().cols.end());
+        tiles.insert(tiles.end(), sets.back().words.begin(), sets.back().words.end());
         mask_off.push_back(static_cast<int64_t>(mask_bytes.size()));
         mask_bytes.insert(mask_bytes.end(), m.begin(), m.end());
     }
@@ -258,7 +296,7 @@ std::unique_ptr<DevPlan> build_dev_plan(int device, int64_t batch, int64_t H, in
     if (tiles.empty())
         tiles.push_back(0);
     if (mask_bytes.size() > static_cast<size_t>(std::numeric_limits<int32_t>::max()) ||
-        tiles.size() > static_cast<size_t>(std::numeric_limits<int32_t>::max()))
+        tiles.size() > static_cast<size_t>(std::numeric_limits<int32_t>::max()) || nqt > (1 << 24))
         fail(DFA2C_UNSUPPORTED, "work list too large");
 
     struct Cand {
@@ -266,24 +304,31 @@ std::unique_ptr<DevPlan> build_dev_plan(int device, int64_t batch, int64_t H, in
         double cost;
     };
     std::vector<Cand> cands;
-    cands.reserve(static_cast<size_t>(batch * H * nqt));
+    cands.reserve(static_cast<size_t>(batch * H * np));
     for (int64_t b = 0; b < batch; ++b)
         for (int64_t h = 0; h < H; ++h) {
             const HeadJob& j = jobs[h];
-            for (int64_t i = 0; i < nqt; ++i) {
+            for (int64_t p = 0; p < np; ++p) {
                 WorkItem w{};
                 w.bh = static_cast<int32_t>(b * H + h);
-                w.qtile = static_cast<int32_t>(i);
+                w.qtile_a = static_cast<int32_t>(2 * p);
+                w.qtile_b = 2 * p + 1 < nqt ? static_cast<int32_t>(2 * p + 1) : -1;
                 if (j.mask_id < 0) {
                     w.flags = dfa2k::ITEM_COPY;
-                    cands.push_back({w, 1.0});
+                    const int64_t rows = std::min<int64_t>(n, (w.qtile_b >= 0 ? w.qtile_b : w.qtile_a) * 128 + 128) -
+                                         w.qtile_a * 128;
+                    cands.push_back({w, static_cast<double>(rows) / 128.0});
                 } else {
-                    const TileSet& ts = sets[j.mask_id];
-                    w.tile_begin = static_cast<int32_t>(mask_tile_base[j.mask_id] + ts.row_ptr[i]);
-                    w.n_tiles = static_cast<int32_t>(ts.row_ptr[i + 1] - ts.row_ptr[i]);
+                    const PairSet& ps = sets[j.mask_id];
+                    w.tile_begin = static_cast<int32_t>(mask_tile_base[j.mask_id] + ps.row_ptr[p]);
+                    w.n_tiles = static_cast<int32_t>(ps.row_ptr[p + 1] - ps.row_ptr[p]);
                     w.mask_off = static_cast<int32_t>(mask_off[j.mask_id]);
                     w.flags = j.commit ? dfa2k::ITEM_COMMIT : 0;
-                    cands.push_back({w, w.n_tiles + 0.5});
+                    if (ps.n_a[p] < 1)
+                        fail(DFA2C_FULLY_MASKED, "query tile " + std::to_string(2 * p) + " has no active key tiles");
+                    if (w.qtile_b >= 0 && ps.n_b[p] < 1)
+                        fail(DFA2C_FULLY_MASKED, "query tile " + std::to_string(2 * p + 1) + " has no active key tiles");
+                    cands.push_back({w, ps.n_a[p] + ps.n_b[p] + 1.0});
                 }
             }
         }
@@ -292,7 +337,7 @@ std::unique_ptr<DevPlan> build_dev_plan(int device, int64_t batch, int64_t H, in
             return a.cost > b.cost;
         if (a.w.bh != b.w.bh)
             return a.w.bh < b.w.bh;
-        return a.w.qtile < b.w.qtile;
+        return a.w.qtile_a < b.w.qtile_a;
     });
     const int grid = static_cast<int>(std::min<int64_t>(num_sms(device), static_cast<int64_t>(cands.size())));
     using Slot = std::pair<double, int>;
@@ -313,7 +358,6 @@ std::unique_ptr<DevPlan> build_dev_plan(int device, int64_t batch, int64_t H, in
         items.insert(items.end(), per_cta[c].begin(), per_cta[c].end());
         cta_begin[c + 1] = static_cast<int32_t>(items.size());
     }
-    (void)nb;
 
     auto p = std::make_unique<DevPlan>();
     p->grid = grid;
