@@ -325,7 +325,9 @@ __global__ void __launch_bounds__(384, 1)
 
     if (warp == 0) {
         // ------------------------------------------------ TMA producer
-        if (lane == 0) {
+        // The whole warp walks the schedule (warp-uniform control flow keeps
+        // coordinates in uniform registers); one elected lane issues.
+        {
             Cursor kc{it0, 0}, vc{it0, 0};
             skip_copies(items, it1, kc);
             skip_copies(items, it1, vc);
@@ -339,25 +341,31 @@ __global__ void __launch_bounds__(384, 1)
                     if (kc.j == 0) {
                         mbar_wait(q_empty, (qcount & 1) ^ 1);
                         const int nq = w.qtile_b >= 0 ? 2 : 1;
-                        mbar_arrive_expect_tx(q_full, nq * C::TILE_BYTES);
+                        if (elect_one()) {
+                            mbar_arrive_expect_tx(q_full, nq * C::TILE_BYTES);
 #pragma unroll
-                        for (int b = 0; b < C::BOXES; ++b) {
-                            tma_load_3d(sbase + C::Q_OFF + b * C::BOX_BYTES, &tmq, q_full, b * 64,
-                                        w.qtile_a * TILE_M, w.bh);
-                            if (nq == 2)
-                                tma_load_3d(sbase + C::Q_OFF + C::TILE_BYTES + b * C::BOX_BYTES, &tmq, q_full,
-                                            b * 64, w.qtile_b * TILE_M, w.bh);
+                            for (int b = 0; b < C::BOXES; ++b) {
+                                tma_load_3d(sbase + C::Q_OFF + b * C::BOX_BYTES, &tmq, q_full, b * 64,
+                                            w.qtile_a * TILE_M, w.bh);
+                                if (nq == 2)
+                                    tma_load_3d(sbase + C::Q_OFF + C::TILE_BYTES + b * C::BOX_BYTES, &tmq, q_full,
+                                                b * 64, w.qtile_b * TILE_M, w.bh);
+                            }
                         }
+                        __syncwarp();
                         ++qcount;
                     }
                     const int kt = static_cast<int>(args.tiles[w.tile_begin + kc.j] & TILE_INDEX_MASK);
                     const int st = kcount % KS;
                     mbar_wait(k_empty(st), ((kcount / KS) & 1) ^ 1);
-                    mbar_arrive_expect_tx(k_full(st), C::TILE_BYTES);
+                    if (elect_one()) {
+                        mbar_arrive_expect_tx(k_full(st), C::TILE_BYTES);
 #pragma unroll
-                    for (int b = 0; b < C::BOXES; ++b)
-                        tma_load_3d(sbase + C::K_OFF + st * C::TILE_BYTES + b * C::BOX_BYTES, &tmk, k_full(st),
-                                    b * 64, kt * TILE_N, w.bh);
+                        for (int b = 0; b < C::BOXES; ++b)
+                            tma_load_3d(sbase + C::K_OFF + st * C::TILE_BYTES + b * C::BOX_BYTES, &tmk, k_full(st),
+                                        b * 64, kt * TILE_N, w.bh);
+                    }
+                    __syncwarp();
                     ++kcount;
                     advance(items, it1, kc);
                 }
@@ -365,18 +373,23 @@ __global__ void __launch_bounds__(384, 1)
                 const int kt = static_cast<int>(args.tiles[w.tile_begin + vc.j] & TILE_INDEX_MASK);
                 const int st = vcount % VS;
                 mbar_wait(v_empty(st), ((vcount / VS) & 1) ^ 1);
-                mbar_arrive_expect_tx(v_full(st), C::TILE_BYTES);
+                if (elect_one()) {
+                    mbar_arrive_expect_tx(v_full(st), C::TILE_BYTES);
 #pragma unroll
-                for (int b = 0; b < C::BOXES; ++b)
-                    tma_load_3d(sbase + C::V_OFF + st * C::TILE_BYTES + b * C::BOX_BYTES, &tmv, v_full(st),
-                                b * 64, kt * TILE_N, w.bh);
+                    for (int b = 0; b < C::BOXES; ++b)
+                        tma_load_3d(sbase + C::V_OFF + st * C::TILE_BYTES + b * C::BOX_BYTES, &tmv, v_full(st),
+                                    b * 64, kt * TILE_N, w.bh);
+                }
+                __syncwarp();
                 ++vcount;
                 advance(items, it1, vc);
             }
         }
     } else if (warp == 1) {
         // ------------------------------------------------ tcgen05 issuer
-        if (lane == 0) {
+        // Whole warp walks the schedule and waits; one elected lane (the same
+        // lane every time, so tcgen05.commit tracks all its MMAs) issues.
+        {
             constexpr uint32_t IDESC_S = idesc_bf16_f32(128, 128, false);
             constexpr uint32_t IDESC_O = idesc_bf16_f32(128, D, true);
             uint32_t kcount = 0, vcount = 0, qcount = 0;
@@ -409,21 +422,25 @@ __global__ void __launch_bounds__(384, 1)
                             }
                             // keys 64..127 (P in cols [64,96)) as soon as that half is ready,
                             // then keys 0..63 (cols [0,32))
+                            const uint64_t vdesc = smem_desc_sw128(v_addr, C::BOX_BYTES, 1024);
                             mbar_wait(p_half(L), pcnt[L] & 1);
                             tc_fence_after();
+                            if (elect_one()) {
 #pragma unroll
-                            for (int kk = 4; kk < 8; ++kk) {
-                                const uint64_t bd = smem_desc_sw128(v_addr + kk * 2048, C::BOX_BYTES, 1024);
-                                mma_bf16_ts(tmem + o_col(L), tmem + s_col(L) + 64 + (kk - 4) * 8, bd, IDESC_O,
-                                            (!first_pv[L] || kk > 4) ? 1u : 0u);
+                                for (int kk = 4; kk < 8; ++kk)
+                                    mma_bf16_ts(tmem + o_col(L), tmem + s_col(L) + 64 + (kk - 4) * 8,
+                                                vdesc + (kk * 2048 >> 4), IDESC_O, (!first_pv[L] || kk > 4) ? 1u : 0u);
                             }
+                            __syncwarp();
                             mbar_wait(p_full(L), pcnt[L] & 1);
                             tc_fence_after();
+                            if (elect_one()) {
 #pragma unroll
-                            for (int kk = 0; kk < 4; ++kk) {
-                                const uint64_t bd = smem_desc_sw128(v_addr + kk * 2048, C::BOX_BYTES, 1024);
-                                mma_bf16_ts(tmem + o_col(L), tmem + s_col(L) + kk * 8, bd, IDESC_O, 1u);
+                                for (int kk = 0; kk < 4; ++kk)
+                                    mma_bf16_ts(tmem + o_col(L), tmem + s_col(L) + kk * 8, vdesc + (kk * 2048 >> 4),
+                                                IDESC_O, 1u);
                             }
+                            __syncwarp();
                             first_pv[L] = false;
                             ++pcnt[L];
                         }
@@ -433,33 +450,42 @@ __global__ void __launch_bounds__(384, 1)
                                 k_ready = true;
                             }
                             tc_fence_after();
-                            const uint32_t q_addr = sbase + C::Q_OFF + L * C::TILE_BYTES;
+                            const uint64_t qdesc = smem_desc_sw128(sbase + C::Q_OFF + L * C::TILE_BYTES, 16, 1024);
+                            const uint64_t kdesc = smem_desc_sw128(k_addr, 16, 1024);
+                            if (elect_one()) {
 #pragma unroll
-                            for (int kk = 0; kk < D / 16; ++kk) {
-                                const uint32_t off = (kk >> 2) * C::BOX_BYTES + (kk & 3) * 32;
-                                const uint64_t ad = smem_desc_sw128(q_addr + off, 16, 1024);
-                                const uint64_t bd = smem_desc_sw128(k_addr + off, 16, 1024);
-                                mma_bf16_ss(tmem + s_col(L), ad, bd, IDESC_S, kk > 0 ? 1u : 0u);
+                                for (int kk = 0; kk < D / 16; ++kk) {
+                                    const uint32_t off = ((kk >> 2) * C::BOX_BYTES + (kk & 3) * 32) >> 4;
+                                    mma_bf16_ss(tmem + s_col(L), qdesc + off, kdesc + off, IDESC_S, kk > 0 ? 1u : 0u);
+                                }
+                                mma_commit(s_full(L));
                             }
-                            mma_commit(s_full(L));
+                            __syncwarp();
                         }
                     }
-                    if (u >= 1) {
-                        mma_commit(v_empty(vst));  // V(u-1) free once its PVs complete
+                    if (elect_one()) {
+                        if (u >= 1)
+                            mma_commit(v_empty(vst));  // V(u-1) free once its PVs complete
+                        if (u < U) {
+                            mma_commit(k_empty(kst));  // K(u) free once its S MMAs complete
+                            if (u == U - 1)
+                                mma_commit(q_empty);
+                        }
+                    }
+                    __syncwarp();
+                    if (u >= 1)
                         ++vcount;
-                    }
-                    if (u < U) {
-                        mma_commit(k_empty(kst));  // K(u) free once its S MMAs complete
+                    if (u < U)
                         ++kcount;
-                        if (u == U - 1)
-                            mma_commit(q_empty);
-                    }
                     prev = word;
                 }
                 // both lanes' O final once every MMA issued so far completes
-                mma_commit(o_full(0));
-                if (w.qtile_b >= 0)
-                    mma_commit(o_full(1));
+                if (elect_one()) {
+                    mma_commit(o_full(0));
+                    if (w.qtile_b >= 0)
+                        mma_commit(o_full(1));
+                }
+                __syncwarp();
                 ++qcount;
             }
         }
