@@ -35,7 +35,10 @@ namespace dfa2k {
 
 template <int D>
 struct Cfg {
-    static constexpr int KSTAGES = D == 128 ? 3 : 5;
+#ifndef DFA2_KSTAGES128
+#define DFA2_KSTAGES128 2
+#endif
+    static constexpr int KSTAGES = D == 128 ? DFA2_KSTAGES128 : 5;
     static constexpr int VSTAGES = D == 128 ? 2 : 4;
     static constexpr int BOXES = D / 64;                       // 128-byte column boxes
     static constexpr uint32_t BOX_BYTES = 128u * 128u;         // 128 rows x 128 B
@@ -43,9 +46,15 @@ struct Cfg {
     static constexpr uint32_t Q_OFF = 0;                       // Q_A, Q_B
     static constexpr uint32_t K_OFF = 2 * TILE_BYTES;
     static constexpr uint32_t V_OFF = K_OFF + KSTAGES * TILE_BYTES;
-    static constexpr uint32_t BAR_OFF = V_OFF + VSTAGES * TILE_BYTES;
-    static constexpr int NBARS = 2 + 2 * KSTAGES + 2 * VSTAGES + 8;
-    static constexpr uint32_t SMEM_BYTES = BAR_OFF + NBARS * 8 + 16 + 1024;
+    // two 16 KB staging boxes (128 rows x 64 cols bf16, 128B swizzle), one per
+    // lane: O epilogue and cached-head copies go smem -> TMA bulk store
+    static constexpr uint32_t STG_OFF = V_OFF + VSTAGES * TILE_BYTES;
+    static constexpr uint32_t BAR_OFF = STG_OFF + 2 * BOX_BYTES;
+    static constexpr int NBARS = 2 + 2 * KSTAGES + 2 * VSTAGES + 10;
+    // The dynamic window starts 1024-aligned (the 1 KB system reservation
+    // precedes it); the kernel traps otherwise, so no alignment slack.
+    static constexpr uint32_t SMEM_BYTES = BAR_OFF + NBARS * 8 + 16;
+    static_assert(SMEM_BYTES <= 232448, "shared memory budget");
     static constexpr uint32_t TMEM_COLS = 512;
     static constexpr int THREADS = 384;
 };
@@ -261,14 +270,15 @@ __device__ __forceinline__ void advance(const WorkItem* items, int it1, Cursor& 
 template <int D>
 __global__ void __launch_bounds__(384, 1)
     attn_fwd_sm100(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtensorMap tmk,
-                   const __grid_constant__ CUtensorMap tmv, const AttnArgs args) {
+                   const __grid_constant__ CUtensorMap tmv, const __grid_constant__ CUtensorMap tmo,
+                   const __grid_constant__ CUtensorMap tmc, const AttnArgs args) {
     using C = Cfg<D>;
     constexpr int KS = C::KSTAGES;
     constexpr int VS = C::VSTAGES;
-    extern __shared__ uint8_t smem_raw[];
-    const uint32_t raw = smem_u32(smem_raw);
-    const uint32_t sbase = (raw + 1023u) & ~1023u;
-    uint8_t* smem = smem_raw + (sbase - raw);
+    extern __shared__ __align__(1024) uint8_t smem[];
+    const uint32_t sbase = smem_u32(smem);
+    if (sbase & 1023u)
+        __trap();
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -284,6 +294,7 @@ __global__ void __launch_bounds__(384, 1)
     auto p_full = [&](int l) { return bars + 8u * (4 + 2 * KS + 2 * VS + l); };
     auto o_full = [&](int l) { return bars + 8u * (6 + 2 * KS + 2 * VS + l); };
     auto p_half = [&](int l) { return bars + 8u * (8 + 2 * KS + 2 * VS + l); };
+    auto c_full = [&](int l) { return bars + 8u * (10 + 2 * KS + 2 * VS + l); };  // copy-box landed
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::BAR_OFF + C::NBARS * 8);
 
     if (threadIdx.x == 0) {
@@ -301,6 +312,7 @@ __global__ void __launch_bounds__(384, 1)
             mbar_init(s_full(l), 1);
             mbar_init(p_full(l), 128);
             mbar_init(p_half(l), 128);
+            mbar_init(c_full(l), 1);
             mbar_init(o_full(l), 1);
         }
         fence_mbar_init();
@@ -309,6 +321,8 @@ __global__ void __launch_bounds__(384, 1)
         tma_prefetch_desc(&tmq);
         tma_prefetch_desc(&tmk);
         tma_prefetch_desc(&tmv);
+        tma_prefetch_desc(&tmo);
+        tma_prefetch_desc(&tmc);
     }
     if (warp == 2) {
         tmem_alloc(smem_u32(tmem_slot), C::TMEM_COLS);
@@ -494,7 +508,6 @@ __global__ void __launch_bounds__(384, 1)
         const int L = (warp - 4) >> 2;              // 0 = lane A, 1 = lane B
         const int wq = warp & 3;                    // TMEM lane quarter
         const int r = wq * 32 + lane;               // row within the query tile
-        const int tid2 = threadIdx.x - 128;         // 0..255 across both lanes
         const uint32_t lrow = static_cast<uint32_t>(wq * 32) << 16;
         const uint32_t need_bit = L ? TILE_NEED_B : TILE_NEED_A;
         const uint32_t part_bit = L ? TILE_PART_B : TILE_PART_A;
@@ -502,19 +515,27 @@ __global__ void __launch_bounds__(384, 1)
         const int N = args.n;
         const uint32_t sc = tmem + lrow + s_col(L);
         const uint32_t oc = tmem + lrow + o_col(L);
-        uint32_t scnt = 0, icnt = 0;
+        const uint32_t stg = sbase + C::STG_OFF + L * C::BOX_BYTES;  // this lane's staging box
+        const bool issuer = r == 0;  // issues this lane's bulk copies / stores
+        uint32_t scnt = 0, icnt = 0, ccnt = 0;
         for (int it = it0; it < it1; ++it) {
             const WorkItem w = items[it];
             if (w.flags & ITEM_COPY) {
-                // Cached head: out <- stored slot over the pair's rows.
-                const int r0 = w.qtile_a * TILE_M;
-                const int r1 = min(N, (w.qtile_b >= 0 ? w.qtile_b : w.qtile_a) * TILE_M + TILE_M);
-                const size_t base = (static_cast<size_t>(w.bh) * N + r0) * D;
-                const uint4* src = reinterpret_cast<const uint4*>(args.cache + base);
-                uint4* dst = reinterpret_cast<uint4*>(args.out + base);
-                const int nvec = (r1 - r0) * D / 8;
-                for (int i = tid2; i < nvec; i += 256)
-                    dst[i] = src[i];
+                // Cached head: out <- stored slot, one 128-row tile per lane,
+                // 64-column boxes through the lane's staging buffer by TMA.
+                const int qt = L ? w.qtile_b : w.qtile_a;
+                if (issuer && qt >= 0) {
+#pragma unroll
+                    for (int b = 0; b < D / 64; ++b) {
+                        bulk_wait_read0();  // staging free
+                        mbar_arrive_expect_tx(c_full(L), C::BOX_BYTES);
+                        tma_load_3d(stg, &tmc, c_full(L), b * 64, qt * TILE_M, w.bh);
+                        mbar_wait(c_full(L), ccnt & 1);
+                        ++ccnt;
+                        tma_store_3d(&tmo, stg, b * 64, qt * TILE_M, w.bh);
+                        bulk_commit();
+                    }
+                }
                 continue;
             }
             const int qt = L ? w.qtile_b : w.qtile_a;
@@ -541,36 +562,44 @@ __global__ void __launch_bounds__(384, 1)
                 ++scnt;
                 first = false;
             }
-            // ---- epilogue: O / l -> bf16 -> out (+ cache slot)
+            // ---- epilogue: O / l -> bf16 -> staging (128B swizzle) -> TMA
+            // bulk stores to out and, for computed heads, the cache slot
             mbar_wait(o_full(L), icnt & 1);
             ++icnt;
             tc_fence_after();
             const float inv = 1.f / l;
-            const bool valid = row < N;
-            const size_t off = (static_cast<size_t>(w.bh) * N + row) * D;
-            uint4* orow = reinterpret_cast<uint4*>(args.out + off);
-            uint4* crow = (w.flags & ITEM_COMMIT) && args.cache ? reinterpret_cast<uint4*>(args.cache + off) : nullptr;
+            const bool commit = (w.flags & ITEM_COMMIT) && args.cache;
 #pragma unroll
-            for (int c = 0; c < D / 32; ++c) {
-                uint32_t o[32];
-                tmem_ld32(oc + 32 * c, o);
+            for (int b = 0; b < D / 64; ++b) {
+                uint32_t o[64];
+                tmem_ld32(oc + 64 * b, o);
+                tmem_ld32(oc + 64 * b + 32, o + 32);
+                if (issuer)
+                    bulk_wait_read0();  // previous store from this buffer has read smem
+                named_bar_sync(1 + L, 128);
                 tmem_ld_wait();
-                uint32_t pk[16];
+                const uint32_t rbase = stg + static_cast<uint32_t>(r) * 128u;
 #pragma unroll
-                for (int i = 0; i < 16; ++i)
-                    pk[i] = pack_bf16x2(__uint_as_float(o[2 * i]) * inv, __uint_as_float(o[2 * i + 1]) * inv);
-                if (valid) {
-#pragma unroll
-                    for (int v4 = 0; v4 < 4; ++v4) {
-                        const uint4 val = make_uint4(pk[4 * v4], pk[4 * v4 + 1], pk[4 * v4 + 2], pk[4 * v4 + 3]);
-                        orow[4 * c + v4] = val;
-                        if (crow)
-                            crow[4 * c + v4] = val;
-                    }
+                for (int c = 0; c < 8; ++c) {
+                    const uint32_t p0 = pack_bf16x2(__uint_as_float(o[8 * c + 0]) * inv, __uint_as_float(o[8 * c + 1]) * inv);
+                    const uint32_t p1 = pack_bf16x2(__uint_as_float(o[8 * c + 2]) * inv, __uint_as_float(o[8 * c + 3]) * inv);
+                    const uint32_t p2 = pack_bf16x2(__uint_as_float(o[8 * c + 4]) * inv, __uint_as_float(o[8 * c + 5]) * inv);
+                    const uint32_t p3 = pack_bf16x2(__uint_as_float(o[8 * c + 6]) * inv, __uint_as_float(o[8 * c + 7]) * inv);
+                    st_shared_v4(rbase + static_cast<uint32_t>((c ^ (r & 7)) * 16), p0, p1, p2, p3);
+                }
+                fence_proxy_async_smem();
+                named_bar_sync(1 + L, 128);
+                if (issuer) {
+                    tma_store_3d(&tmo, stg, b * 64, qt * TILE_M, w.bh);  // rows >= N are clipped
+                    if (commit)
+                        tma_store_3d(&tmc, stg, b * 64, qt * TILE_M, w.bh);
+                    bulk_commit();
                 }
             }
             tc_fence_before();
         }
+        if (issuer)
+            bulk_wait0();  // every bulk store of this lane has completed
     }
 
     tc_fence_before();
@@ -580,17 +609,18 @@ __global__ void __launch_bounds__(384, 1)
         tmem_dealloc(tmem, C::TMEM_COLS);
 }
 
-template __global__ void attn_fwd_sm100<64>(const __grid_constant__ CUtensorMap,
-                                            const __grid_constant__ CUtensorMap,
-                                            const __grid_constant__ CUtensorMap, const AttnArgs);
-template __global__ void attn_fwd_sm100<128>(const __grid_constant__ CUtensorMap,
-                                             const __grid_constant__ CUtensorMap,
-                                             const __grid_constant__ CUtensorMap, const AttnArgs);
+#define DFA2_MAPS                                                                                 \
+    const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap,                     \
+        const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap,                 \
+        const __grid_constant__ CUtensorMap
+template __global__ void attn_fwd_sm100<64>(DFA2_MAPS, const AttnArgs);
+template __global__ void attn_fwd_sm100<128>(DFA2_MAPS, const AttnArgs);
+#undef DFA2_MAPS
 
 namespace {
 template <int D>
-cudaError_t launch_d(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const AttnArgs& args,
-                     int grid, cudaStream_t stream) {
+cudaError_t launch_d(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const CUtensorMap& to,
+                     const CUtensorMap& tc, const AttnArgs& args, int grid, cudaStream_t stream) {
     using C = Cfg<D>;
     static int configured_for = -1;  // device the smem attribute was set on
     int dev = 0;
@@ -602,15 +632,18 @@ cudaError_t launch_d(const CUtensorMap& tq, const CUtensorMap& tk, const CUtenso
             return e;
         configured_for = dev;
     }
-    attn_fwd_sm100<D><<<grid, C::THREADS, C::SMEM_BYTES, stream>>>(tq, tk, tv, args);
+    attn_fwd_sm100<D><<<grid, C::THREADS, C::SMEM_BYTES, stream>>>(tq, tk, tv, to, tc, args);
     return cudaGetLastError();
 }
 }  // namespace
 
-// Host-side launcher (called from dfa2c.cpp).
+// Host-side launcher (called from dfa2c.cpp). `to` / `tc` map the output and
+// the cache layer buffer with the same [batch*H, N, d] geometry as q/k/v.
 cudaError_t launch_attn(int d, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
-                        const AttnArgs& args, int grid, cudaStream_t stream) {
-    return d == 128 ? launch_d<128>(tq, tk, tv, args, grid, stream) : launch_d<64>(tq, tk, tv, args, grid, stream);
+                        const CUtensorMap& to, const CUtensorMap& tc, const AttnArgs& args, int grid,
+                        cudaStream_t stream) {
+    return d == 128 ? launch_d<128>(tq, tk, tv, to, tc, args, grid, stream)
+                    : launch_d<64>(tq, tk, tv, to, tc, args, grid, stream);
 }
 
 }  // namespace dfa2k

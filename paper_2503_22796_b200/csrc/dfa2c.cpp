@@ -24,7 +24,8 @@
 
 namespace dfa2k {
 cudaError_t launch_attn(int d, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
-                        const AttnArgs& args, int grid, cudaStream_t stream);
+                        const CUtensorMap& to, const CUtensorMap& tc, const AttnArgs& args, int grid,
+                        cudaStream_t stream);
 cudaError_t launch_rse(const void* ym, const void* yo, int dtype, int64_t n_heads, int64_t numel,
                        int mode, double* out_dev, double* scratch, int nblk, cudaStream_t stream);
 }  // namespace dfa2k
@@ -526,6 +527,8 @@ void run_forward(const ForwardSpec& s, cudaStream_t stream) {
     const CUtensorMap tq = make_map(s.q, bh, n, d);
     const CUtensorMap tk = make_map(s.k, bh, n, d);
     const CUtensorMap tv = make_map(s.v, bh, n, d);
+    const CUtensorMap to = make_map(s.out, bh, n, d);
+    const CUtensorMap tc = cache_layer ? make_map(cache_layer, bh, n, d) : to;
     dfa2k::AttnArgs a{};
     a.items = plan->items;
     a.cta_begin = plan->cta_begin;
@@ -537,7 +540,7 @@ void run_forward(const ForwardSpec& s, cudaStream_t stream) {
     a.block = static_cast<int32_t>(std::min<int64_t>(s.block, int64_t{1} << 30));
     a.nb = static_cast<int32_t>(ceil_div(n, s.block));
     a.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(d)));
-    DFA2C_CUDA_CHECK(dfa2k::launch_attn(static_cast<int>(d), tq, tk, tv, a, plan->grid, stream));
+    DFA2C_CUDA_CHECK(dfa2k::launch_attn(static_cast<int>(d), tq, tk, tv, to, tc, a, plan->grid, stream));
     g_launches.fetch_add(1);
 }
 
