@@ -175,6 +175,9 @@ int dfa2c_influence_for_layer(const void* q, const void* k, const void* v,
 
 /* Kernel launches issued by this library since load (evidence counter). */
 int64_t dfa2c_launch_count(void);
+/* Debug: device buffer (int64 [2][4096][8]) receiving per-tile clock64 stamps
+ * of CTA 0 from kernels built with -DDFA2_TRACE=1 (NULL disables). */
+void dfa2c_debug_set_trace(void* dev_buffer);
 
 #ifdef __cplusplus
 }

@@ -65,6 +65,16 @@ struct Cfg {
 #define DFA2_EMU_EVERY 0
 #endif
 
+#ifndef DFA2_TRACE
+#define DFA2_TRACE 0
+#endif
+// trace[((lane * 4096) + tile) * 8 + slot] = clock64() for CTA 0 (debug builds)
+#define DFA2_STAMP(L_, j_, k_)                                                          \
+    do {                                                                                \
+        if (DFA2_TRACE && args.trace && blockIdx.x == 0 && (j_) < 4096)                 \
+            args.trace[((static_cast<int>(L_) * 4096) + static_cast<int>(j_)) * 8 + (k_)] = clock64(); \
+    } while (0)
+
 namespace {
 
 __device__ __forceinline__ uint32_t s_col(int lane) { return lane ? 128u : 0u; }
@@ -408,6 +418,7 @@ __global__ void __launch_bounds__(384, 1)
             constexpr uint32_t IDESC_O = idesc_bf16_f32(128, D, true);
             uint32_t kcount = 0, vcount = 0, qcount = 0;
             uint32_t pcnt[2] = {0, 0};
+            uint32_t scount[2] = {0, 0};
             for (int it = it0; it < it1; ++it) {
                 const WorkItem w = items[it];
                 if ((w.flags & ITEM_COPY) || w.n_tiles == 0)
@@ -439,6 +450,7 @@ __global__ void __launch_bounds__(384, 1)
                             const uint64_t vdesc = smem_desc_sw128(v_addr, C::BOX_BYTES, 1024);
                             mbar_wait(p_half(L), pcnt[L] & 1);
                             tc_fence_after();
+                            if (lane == 0) DFA2_STAMP(L, pcnt[L], 3);
                             if (elect_one()) {
 #pragma unroll
                                 for (int kk = 4; kk < 8; ++kk)
@@ -455,6 +467,7 @@ __global__ void __launch_bounds__(384, 1)
                                                 IDESC_O, 1u);
                             }
                             __syncwarp();
+                            if (lane == 0) DFA2_STAMP(L, pcnt[L], 4);
                             first_pv[L] = false;
                             ++pcnt[L];
                         }
@@ -475,6 +488,8 @@ __global__ void __launch_bounds__(384, 1)
                                 mma_commit(s_full(L));
                             }
                             __syncwarp();
+                            if (lane == 0) DFA2_STAMP(L, scount[L], 5);
+                            ++scount[L];
                         }
                     }
                     if (elect_one()) {
@@ -554,11 +569,14 @@ __global__ void __launch_bounds__(384, 1)
                 const bool partial = (word & part_bit) != 0;
                 if (partial)
                     tile_valid_bits(args, mask, row, static_cast<int>(word & TILE_INDEX_MASK) * TILE_N, vm);
+                if (r == 0) DFA2_STAMP(L, scnt, 0);
                 mbar_wait(s_full(L), scnt & 1);
                 tc_fence_after();
+                if (r == 0) DFA2_STAMP(L, scnt, 1);
                 if (partial)
                     mask_tile_in_tmem(sc, vm);
                 softmax_tile<D>(sc, oc, sl2, m_ref, l, first, p_half(L), p_full(L));
+                if (r == 0) DFA2_STAMP(L, scnt, 2);
                 ++scnt;
                 first = false;
             }

@@ -49,6 +49,7 @@ struct AttnArgs {
     int32_t block;
     int32_t nb;
     float scale_log2;          // log2(e) / sqrt(d)
+    long long* trace;          // debug builds (-DDFA2_TRACE=1): per-tile clock64 stamps of CTA 0
 };
 
 constexpr int TILE_M = 128;  // query rows per tile (tcgen05 M)

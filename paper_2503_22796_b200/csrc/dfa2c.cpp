@@ -35,6 +35,7 @@ using dfa2k::WorkItem;
 namespace {
 
 thread_local std::string g_err;
+long long* g_trace = nullptr;  // debug: per-tile timestamps (kernels built with -DDFA2_TRACE=1)
 std::atomic<int64_t> g_launches{0};
 
 struct Failure {
@@ -540,6 +541,7 @@ void run_forward(const ForwardSpec& s, cudaStream_t stream) {
     a.block = static_cast<int32_t>(std::min<int64_t>(s.block, int64_t{1} << 30));
     a.nb = static_cast<int32_t>(ceil_div(n, s.block));
     a.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(d)));
+    a.trace = g_trace;
     DFA2C_CUDA_CHECK(dfa2k::launch_attn(static_cast<int>(d), tq, tk, tv, to, tc, a, plan->grid, stream));
     g_launches.fetch_add(1);
 }
@@ -582,6 +584,7 @@ extern "C" {
 const char* dfa2c_last_error(void) { return g_err.c_str(); }
 const char* dfa2c_version(void) { return "dfa2c 0.1 (sm_100a tcgen05/TMA fused head-wise attention)"; }
 int64_t dfa2c_launch_count(void) { return g_launches.load(); }
+void dfa2c_debug_set_trace(void* dev_buffer) { g_trace = static_cast<long long*>(dev_buffer); }
 
 int dfa2c_arrow_mask(const dfa2c_dims* dims, int64_t block, int64_t window, uint8_t* active, int64_t* nb) {
     return guard([&] {

@@ -1,0 +1,46 @@
+"""Per-tile timeline of CTA 0 from a -DDFA2_TRACE=1 build (cycles, medians).
+
+    python -m paper_2503_22796_b200.build --out /tmp/libtrace.so -DDFA2_TRACE=1
+    DFA2_LIB=/tmp/libtrace.so python tools/trace_tiles.py [plan]
+"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+
+from paper_2503_22796_b200 import _lib, api
+
+plan = sys.argv[1] if len(sys.argv) > 1 else "F"
+sd3 = "--sd3" in sys.argv
+H, NV, NT, D, B = (24, 4096, 333, 64, 128) if sd3 else (24, 16384, 512, 128, 128)
+N = NV + NT
+dims = api.AttentionDims(H, D, NV, NT)
+q, k, v = (torch.randn(1, H, N, D, device="cuda").to(torch.bfloat16) for _ in range(3))
+out = torch.empty_like(q)
+lp = api.LayerPlan.parse(" ".join([plan] * H) if len(plan.split()) == 1 else plan)
+trace = torch.zeros(2 * 4096 * 8, dtype=torch.int64, device="cuda")
+for _ in range(3):
+    api.multi_strategy_attention(q, k, v, lp, None, 0, 0, dims, B, out=out)
+_lib.lib().dfa2c_debug_set_trace(ctypes_ptr := __import__("ctypes").c_void_p(trace.data_ptr()))
+api.multi_strategy_attention(q, k, v, lp, None, 0, 0, dims, B, out=out)
+torch.cuda.synchronize()
+_lib.lib().dfa2c_debug_set_trace(None)
+t = trace.view(2, 4096, 8).cpu().numpy()
+for L in range(2):
+    n = int((t[L, :, 1] > 0).sum())
+    x = t[L, :n].astype(np.float64)
+    if n < 3:
+        continue
+    wait = x[:, 1] - x[:, 0]
+    soft = x[:, 2] - x[:, 1]
+    pseen = x[:, 3] - x[:, 2]                    # P(j) arrive -> MMA warp sees it
+    pv_issue = x[:, 4] - x[:, 3]
+    s_next = x[1:, 5] - x[:-1, 4]                # PV(j) issued -> S(j+1) issued
+    s_ready = x[1:, 1] - x[1:, 5]                # S(j+1) issued -> softmax sees it
+    period = np.diff(x[:, 1])
+    med = lambda a: float(np.median(a))
+    print(f"lane {L}: tiles {n}  period {med(period):.0f}  softmax {med(soft):.0f}  wait_S {med(wait):.0f}  "
+          f"P->MMA {med(pseen):.0f}  PV issue {med(pv_issue):.0f}  PV->S issue {med(s_next):.0f}  "
+          f"S issue->ready {med(s_ready):.0f}")
