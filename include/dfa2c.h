@@ -90,10 +90,12 @@ int dfa2c_plan_aggregate(const dfa2c_dims* dims, int64_t n_timesteps, int64_t n_
                          int64_t block, const int32_t* kinds, const int64_t* windows,
                          int64_t* flops_total, int64_t* flops_dense, double* sparsity);
 /* The per-head tile scheduler's tile set for one head strategy: for every
- * 128-row query tile i, the 128-key KV tiles the kernel will compute, in
- * ascending order. row_ptr[n_qtiles+1] (CSR), cols[] (kv tile | 1<<31 when
- * the tile needs element masking: mask block size != 128 or ragged tail).
- * Pass cols == NULL to query the count in *n_tiles. kind FULL or ARROW. */
+ * 128-row query tile i, the KV tiles (dfa2c_kv_tile_keys() keys each) the
+ * kernel will compute, in ascending order. row_ptr[n_qtiles+1] (CSR),
+ * cols[] (kv tile | 1<<31 when the tile needs element masking: a mask block
+ * boundary inside the tile or a ragged tail). Pass cols == NULL to query
+ * the count in *n_tiles. kind FULL or ARROW. */
+int64_t dfa2c_kv_tile_keys(void);
 int dfa2c_tile_set(const dfa2c_dims* dims, int64_t block, int32_t kind, int64_t window,
                    int64_t* row_ptr, uint32_t* cols, int64_t* n_tiles);
 

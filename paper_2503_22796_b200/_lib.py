@@ -94,6 +94,7 @@ _SIGS = {
     "dfa2c_mask_stats": (c_int32, [POINTER(c_uint8), c_int64, c_int64, c_int64, POINTER(c_int64),
                                    POINTER(c_int64), POINTER(c_double)]),
     "dfa2c_dense_flops": (c_int64, [c_int64, c_int64]),
+    "dfa2c_kv_tile_keys": (c_int64, []),
     "dfa2c_plan_flops": (c_int32, [POINTER(Dims), c_int64, POINTER(c_int32), POINTER(c_int64), POINTER(c_int64)]),
     "dfa2c_plan_aggregate": (c_int32, [POINTER(Dims), c_int64, c_int64, c_int64, POINTER(c_int32),
                                        POINTER(c_int64), POINTER(c_int64), POINTER(c_int64), POINTER(c_double)]),

@@ -72,7 +72,8 @@ struct Cfg {
 #define DFA2_STAMP(L_, j_, k_)                                                          \
     do {                                                                                \
         if (DFA2_TRACE && args.trace && blockIdx.x == 0 && (j_) < 4096)                 \
-            args.trace[((static_cast<int>(L_) * 4096) + static_cast<int>(j_)) * 8 + (k_)] = clock64(); \
+            if (DFA2_TRACE == 1 || (k_) < 3)                                                  \
+                args.trace[((static_cast<int>(L_) * 4096) + static_cast<int>(j_)) * 8 + (k_)] = clock64(); \
     } while (0)
 
 namespace {
@@ -80,33 +81,21 @@ namespace {
 __device__ __forceinline__ uint32_t s_col(int lane) { return lane ? 128u : 0u; }
 __device__ __forceinline__ uint32_t o_col(int lane) { return lane ? 384u : 256u; }
 
-// 2^x on the FMA/ALU pipes: x = j + f, j = floor(x) by the round-down
-// magic-number add, 2^f by a degree-3 minimax polynomial (max rel. error
-// 8.6e-5, far below the bf16 rounding P is stored with), exponent added as
-// an integer.
-__device__ __forceinline__ float ex2_poly(float x) {
-    x = fmaxf(x, -127.f);
-    const float t = __fadd_rd(x, 12582912.f);
-    const float f = x - (t - 12582912.f);
-    float p = fmaf(0.0770652f, f, 0.227647f);
-    p = fmaf(p, f, 0.69511634f);
-    p = fmaf(p, f, 1.0f);
-    return __uint_as_float(__float_as_uint(p) + (__float_as_uint(t) << 23));
-}
-
-// Two exp2s on the FMA/ALU pipes with packed fp32x2 arithmetic.
+// Two exp2s on the FMA/ALU pipes with packed fp32x2 arithmetic: x = j + f,
+// j = floor(x) by the round-down magic-number add, 2^f by a degree-3
+// minimax polynomial (max rel. error 8.6e-5, far below the bf16 rounding P
+// is stored with), the exponent added as an integer; 0 below 2^-126, so
+// masked (-inf) scores still give P == 0 exactly.
 __device__ __forceinline__ float2 ex2_poly2(float2 x) {
-    x.x = fmaxf(x.x, -127.f);
-    x.y = fmaxf(x.y, -127.f);
-    const float2 magic = make_float2(12582912.f, 12582912.f);
-    const float2 t = __fadd2_rd(x, magic);
+    const float2 xc = make_float2(fmaxf(x.x, -127.f), fmaxf(x.y, -127.f));
+    const float2 t = __fadd2_rd(xc, make_float2(12582912.f, 12582912.f));
     const float2 tm = __fadd2_rn(t, make_float2(-12582912.f, -12582912.f));  // floor(x)
-    const float2 f = __ffma2_rn(tm, make_float2(-1.f, -1.f), x);              // x - floor(x)
+    const float2 f = __ffma2_rn(tm, make_float2(-1.f, -1.f), xc);             // x - floor(x)
     float2 p = __ffma2_rn(make_float2(0.0770652f, 0.0770652f), f, make_float2(0.227647f, 0.227647f));
     p = __ffma2_rn(p, f, make_float2(0.69511634f, 0.69511634f));
     p = __ffma2_rn(p, f, make_float2(1.0f, 1.0f));
-    return make_float2(__uint_as_float(__float_as_uint(p.x) + (__float_as_uint(t.x) << 23)),
-                       __uint_as_float(__float_as_uint(p.y) + (__float_as_uint(t.y) << 23)));
+    return make_float2(x.x < -126.f ? 0.f : __uint_as_float(__float_as_uint(p.x) + (__float_as_uint(t.x) << 23)),
+                       x.y < -126.f ? 0.f : __uint_as_float(__float_as_uint(p.y) + (__float_as_uint(t.y) << 23)));
 }
 
 // Per-row 128-column validity bitmap for a partial tile: key < N and the
@@ -173,10 +162,8 @@ __device__ __forceinline__ void softmax_half(const uint32_t* s, float2 scale2, f
                 make_float2(__uint_as_float(s[32 * cc + 2 * i]), __uint_as_float(s[32 * cc + 2 * i + 1])), scale2,
                 neg_m);
             float2 p;
-            if (DFA2_EMU_EVERY > 0 && (i % DFA2_EMU_EVERY) == DFA2_EMU_EVERY - 1) {
+            if (DFA2_EMU_EVERY > 0 && (i % (DFA2_EMU_EVERY > 0 ? DFA2_EMU_EVERY : 1)) == DFA2_EMU_EVERY - 1) {
                 p = ex2_poly2(x);
-                p.x = x.x < -126.f ? 0.f : p.x;
-                p.y = x.y < -126.f ? 0.f : p.y;
             } else {
                 p = make_float2(ex2_approx(x.x), ex2_approx(x.y));
             }
@@ -187,9 +174,17 @@ __device__ __forceinline__ void softmax_half(const uint32_t* s, float2 scale2, f
     }
 }
 
+// DFA2_TRACE == 2: in-softmax stamps (slots 3..7 of the lane's trace rows)
+#define DFA2_SSTAMP(k_)                                        \
+    do {                                                       \
+        if (DFA2_TRACE == 2 && stamp)                          \
+            stamp[k_] = clock64();                             \
+    } while (0)
+
 template <int D>
 __device__ __forceinline__ void softmax_tile(uint32_t sc, uint32_t oc, float sl2, float& m_ref, float& l,
-                                             bool first, uint32_t bar_half, uint32_t bar_full) {
+                                             bool first, uint32_t bar_half, uint32_t bar_full,
+                                             long long* stamp = nullptr) {
     uint32_t hi[64];
     float mx;
     {
@@ -199,13 +194,16 @@ __device__ __forceinline__ void softmax_tile(uint32_t sc, uint32_t oc, float sl2
         tmem_ld32(sc + 64, hi);
         tmem_ld32(sc + 96, hi + 32);
         tmem_ld_wait();
-        float m0 = -INFINITY, m1 = -INFINITY;
+        DFA2_SSTAMP(3);
+        float m0 = -INFINITY, m1 = -INFINITY, m2 = -INFINITY, m3 = -INFINITY;
 #pragma unroll
-        for (int c = 0; c < 64; c += 2) {  // two independent 3-input max chains
+        for (int c = 0; c < 64; c += 4) {  // four independent 3-input max chains
             m0 = fmaxf(m0, fmaxf(__uint_as_float(lo[c]), __uint_as_float(lo[c + 1])));
             m1 = fmaxf(m1, fmaxf(__uint_as_float(hi[c]), __uint_as_float(hi[c + 1])));
+            m2 = fmaxf(m2, fmaxf(__uint_as_float(lo[c + 2]), __uint_as_float(lo[c + 3])));
+            m3 = fmaxf(m3, fmaxf(__uint_as_float(hi[c + 2]), __uint_as_float(hi[c + 3])));
         }
-        mx = fmaxf(m0, m1) * sl2;
+        mx = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3)) * sl2;
     }
     // lazy rescale: keep the reference max unless the tile max exceeds it by
     // more than 8 (P <= 2^8 stays exact in fp32 and representable in bf16)
@@ -219,6 +217,7 @@ __device__ __forceinline__ void softmax_tile(uint32_t sc, uint32_t oc, float sl2
         need = true;
     }
     l *= factor;
+    DFA2_SSTAMP(4);
     if (__any_sync(0xFFFFFFFFu, need)) {
         // O holds every earlier PV of this lane: this S was issued after them,
         // so they completed before s_full fired.
@@ -239,14 +238,17 @@ __device__ __forceinline__ void softmax_tile(uint32_t sc, uint32_t oc, float sl2
     float2 sum = make_float2(0.f, 0.f);
     // keys 64..127 from registers -> cols [64,96): the MMA warp starts on them
     softmax_half<D>(hi, scale2, neg_m, sum, sc + 64);
+    DFA2_SSTAMP(5);
     tmem_st_wait();
     tc_fence_before();
     mbar_arrive(bar_half);
+    DFA2_SSTAMP(6);
     // keys 0..63 re-read (cols [0,64) untouched so far) -> cols [0,32)
     uint32_t lo[64];
     tmem_ld32(sc, lo);
     tmem_ld32(sc + 32, lo + 32);
     tmem_ld_wait();
+    DFA2_SSTAMP(7);
     softmax_half<D>(lo, scale2, neg_m, sum, sc);
     tmem_st_wait();
     tc_fence_before();
@@ -575,7 +577,10 @@ __global__ void __launch_bounds__(384, 1)
                 if (r == 0) DFA2_STAMP(L, scnt, 1);
                 if (partial)
                     mask_tile_in_tmem(sc, vm);
-                softmax_tile<D>(sc, oc, sl2, m_ref, l, first, p_half(L), p_full(L));
+                long long* stamp = nullptr;
+                if (DFA2_TRACE == 2 && args.trace && blockIdx.x == 0 && r == 0 && scnt < 4096)
+                    stamp = args.trace + ((L * 4096) + scnt) * 8;
+                softmax_tile<D>(sc, oc, sl2, m_ref, l, first, p_half(L), p_full(L), stamp);
                 if (r == 0) DFA2_STAMP(L, scnt, 2);
                 ++scnt;
                 first = false;

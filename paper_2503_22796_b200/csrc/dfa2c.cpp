@@ -159,7 +159,7 @@ int64_t plan_flops(const dfa2c_dims* dims, int64_t B, const int32_t* kinds, cons
 }
 
 // ------------------------------------------------------------ tile sets
-// For every 128-row query tile, the 128-key KV tiles holding at least one
+// For every 128-row query tile, the 64-key KV tiles holding at least one
 // active (query, key) pair, ascending (the reference folds key blocks in
 // ascending order, src/arrow.cpp:184-186). A tile is PARTIAL when some pair
 // inside [rows < n] x [keys < n] is inactive, or keys run past n.
@@ -170,14 +170,15 @@ struct TileSet {
 
 TileSet build_tile_set(const uint8_t* m, int64_t n, int64_t B) {
     const int64_t nb = ceil_div(n, B);
-    const int64_t nt = ceil_div(n, dfa2k::TILE_M);
+    const int64_t nqt = ceil_div(n, dfa2k::TILE_M);
+    const int64_t nkt = ceil_div(n, dfa2k::TILE_N);
     TileSet ts;
-    ts.row_ptr.assign(static_cast<size_t>(nt + 1), 0);
-    for (int64_t i = 0; i < nt; ++i) {
-        const int64_t r0 = i * 128, r1 = std::min(r0 + 128, n);
+    ts.row_ptr.assign(static_cast<size_t>(nqt + 1), 0);
+    for (int64_t i = 0; i < nqt; ++i) {
+        const int64_t r0 = i * dfa2k::TILE_M, r1 = std::min(r0 + dfa2k::TILE_M, n);
         const int64_t qb0 = r0 / B, qb1 = (r1 - 1) / B;
-        for (int64_t t = 0; t < nt; ++t) {
-            const int64_t c0 = t * 128, c1 = std::min(c0 + 128, n);
+        for (int64_t t = 0; t < nkt; ++t) {
+            const int64_t c0 = t * dfa2k::TILE_N, c1 = std::min(c0 + dfa2k::TILE_N, n);
             const int64_t kb0 = c0 / B, kb1 = (c1 - 1) / B;
             bool any = false, all = true;
             for (int64_t qb = qb0; qb <= qb1; ++qb)
@@ -188,7 +189,7 @@ TileSet build_tile_set(const uint8_t* m, int64_t n, int64_t B) {
                 }
             if (!any)
                 continue;
-            const bool partial = !all || (c1 - c0) < 128;
+            const bool partial = !all || (c1 - c0) < dfa2k::TILE_N;
             ts.cols.push_back(static_cast<uint32_t>(t) | (partial ? dfa2k::TILE_SET_PARTIAL : 0u));
         }
         ts.row_ptr[i + 1] = static_cast<int64_t>(ts.cols.size());
@@ -330,7 +331,7 @@ std::unique_ptr<DevPlan> build_dev_plan(int device, int64_t batch, int64_t H, in
                         fail(DFA2C_FULLY_MASKED, "query tile " + std::to_string(2 * p) + " has no active key tiles");
                     if (w.qtile_b >= 0 && ps.n_b[p] < 1)
                         fail(DFA2C_FULLY_MASKED, "query tile " + std::to_string(2 * p + 1) + " has no active key tiles");
-                    cands.push_back({w, ps.n_a[p] + ps.n_b[p] + 1.0});
+                    cands.push_back({w, (ps.n_a[p] + ps.n_b[p]) * (dfa2k::TILE_N / 128.0) + 1.0});
                 }
             }
         }
@@ -401,14 +402,14 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
-// [rows=batch*H][n][d] bf16, box {64 cols, 128 rows, 1}, 128-byte swizzle:
-// the canonical K-major SW128 UMMA layout (and MN-major for V).
-CUtensorMap make_map(const void* base, int64_t bh, int64_t n, int64_t d) {
+// [rows=batch*H][n][d] bf16, box {64 cols, box_rows rows, 1}, 128-byte
+// swizzle: the canonical K-major SW128 UMMA layout (and MN-major for V).
+CUtensorMap make_map(const void* base, int64_t bh, int64_t n, int64_t d, int box_rows) {
     CUtensorMap m;
     const cuuint64_t dims[3] = {static_cast<cuuint64_t>(d), static_cast<cuuint64_t>(n),
                                 static_cast<cuuint64_t>(bh)};
     const cuuint64_t strides[2] = {static_cast<cuuint64_t>(d * 2), static_cast<cuuint64_t>(n * d * 2)};
-    const cuuint32_t box[3] = {64, 128, 1};
+    const cuuint32_t box[3] = {64, static_cast<cuuint32_t>(box_rows), 1};
     const cuuint32_t estr[3] = {1, 1, 1};
     const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims,
                                    strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -525,11 +526,11 @@ void run_forward(const ForwardSpec& s, cudaStream_t stream) {
     }
 
     const int64_t bh = s.batch * H;
-    const CUtensorMap tq = make_map(s.q, bh, n, d);
-    const CUtensorMap tk = make_map(s.k, bh, n, d);
-    const CUtensorMap tv = make_map(s.v, bh, n, d);
-    const CUtensorMap to = make_map(s.out, bh, n, d);
-    const CUtensorMap tc = cache_layer ? make_map(cache_layer, bh, n, d) : to;
+    const CUtensorMap tq = make_map(s.q, bh, n, d, dfa2k::TILE_M);
+    const CUtensorMap tk = make_map(s.k, bh, n, d, dfa2k::TILE_N);
+    const CUtensorMap tv = make_map(s.v, bh, n, d, dfa2k::TILE_N);
+    const CUtensorMap to = make_map(s.out, bh, n, d, dfa2k::TILE_M);
+    const CUtensorMap tc = cache_layer ? make_map(cache_layer, bh, n, d, dfa2k::TILE_M) : to;
     dfa2k::AttnArgs a{};
     a.items = plan->items;
     a.cta_begin = plan->cta_begin;
@@ -615,6 +616,7 @@ int dfa2c_mask_stats(const uint8_t* active, int64_t n, int64_t block, int64_t he
 }
 
 int64_t dfa2c_dense_flops(int64_t n, int64_t d) { return 4 * d * n * n; }
+int64_t dfa2c_kv_tile_keys(void) { return dfa2k::TILE_N; }
 
 int dfa2c_plan_flops(const dfa2c_dims* dims, int64_t block, const int32_t* kinds, const int64_t* windows,
                      int64_t* flops) {

@@ -117,16 +117,21 @@ def test_plan_aggregate_matches_live_reference():
     assert plan.aggregate_sparsity() == sp.value
 
 
+def kv_tile():
+    return int(api.lib().dfa2c_kv_tile_keys())
+
+
 def _expand(row_ptr, cols, n):
     """Token-pair coverage of a tile set: bool [n, n] of pairs inside listed tiles."""
+    kt = kv_tile()
     cov = np.zeros((n, n), bool)
     part = np.zeros((n, n), bool)
     for i in range(len(row_ptr) - 1):
         for c in cols[row_ptr[i]:row_ptr[i + 1]]:
             t = int(c) & 0x7FFFFFFF
-            cov[i * 128:(i + 1) * 128, t * 128:(t + 1) * 128] = True
+            cov[i * 128:(i + 1) * 128, t * kt:(t + 1) * kt] = True
             if int(c) >> 31:
-                part[i * 128:(i + 1) * 128, t * 128:(t + 1) * 128] = True
+                part[i * 128:(i + 1) * 128, t * kt:(t + 1) * kt] = True
     return cov, part
 
 
@@ -141,15 +146,16 @@ def test_tile_set_covers_exactly_the_active_token_pairs(nv, nt, order, B, w):
     blk = np.arange(n) // B
     active = m.reshape(nb, nb)[blk[:, None], blk[None, :]].astype(bool)  # token-level predicate
     row_ptr, cols = api.tile_set(d, B, HeadStrategy.Arrow(w))
+    kt = kv_tile()
     cov, part = _expand(row_ptr, cols, n)
     assert not (active & ~cov).any(), "an active pair lies outside every scheduled tile"
     # every scheduled tile holds >= 1 active pair; non-partial tiles hold only active pairs
     for i in range(len(row_ptr) - 1):
         for c in cols[row_ptr[i]:row_ptr[i + 1]]:
             t = int(c) & 0x7FFFFFFF
-            blk_act = active[i * 128:(i + 1) * 128, t * 128:(t + 1) * 128]
+            blk_act = active[i * 128:(i + 1) * 128, t * kt:(t + 1) * kt]
             assert blk_act.any()
-            full_tile = blk_act.shape[1] == 128 and blk_act.all()  # rows past n are never stored
+            full_tile = blk_act.shape[1] == kt and blk_act.all()  # rows past n are never stored
             assert bool(int(c) >> 31) == (not full_tile)
         ts = [int(c) & 0x7FFFFFFF for c in cols[row_ptr[i]:row_ptr[i + 1]]]
         assert ts == sorted(ts)  # ascending key order (arrow.cpp:184-186)
@@ -165,4 +171,4 @@ def test_flux68_tile_counts():
         total += len(cols)
         assert not any(int(c) >> 31 for c in cols)  # block-aligned: no element masking at FLUX 2K
     # 134,368 computed 128x128 tiles of 418,176 dense
-    assert total == 134368 and 24 * 132 * 132 == 418176
+    assert total * kv_tile() == 134368 * 128 and 24 * 132 * 132 == 418176

@@ -36,11 +36,23 @@ for L in range(2):
     wait = x[:, 1] - x[:, 0]
     soft = x[:, 2] - x[:, 1]
     pseen = x[:, 3] - x[:, 2]                    # P(j) arrive -> MMA warp sees it
-    pv_issue = x[:, 4] - x[:, 3]
-    s_next = x[1:, 5] - x[:-1, 4]                # PV(j) issued -> S(j+1) issued
-    s_ready = x[1:, 1] - x[1:, 5]                # S(j+1) issued -> softmax sees it
     period = np.diff(x[:, 1])
     med = lambda a: float(np.median(a))
+    extra = ""
+    if (x[:, 4] > 0).all() and (x[:, 5] > 0).all():
+        extra = (f"  PV issue {med(x[:, 4] - x[:, 3]):.0f}  PV->S issue {med(x[1:, 5] - x[:-1, 4]):.0f}  "
+                 f"S issue->ready {med(x[1:, 1] - x[1:, 5]):.0f}")
+    if os.environ.get("DFA2_TRACE_MODE") == "2":
+        d = lambda a_, b_: med(x[:, b_] - x[:, a_])
+        extra = (f"\n   softmax detail: ld+wait {d(1, 3):.0f}  max+decide {d(3, 4):.0f}  P(hi) {d(4, 5):.0f}  "
+                 f"st.wait+arrive {d(5, 6):.0f}  reload lo {d(6, 7):.0f}  P(lo)+st+arrive {d(7, 2):.0f}")
+    elif L == 1 and (x[:, 7] > 0).sum() > 3:
+        # MMA warp, union step u: 4 = before K wait, 5 = K ready, 6 = S issued, 7 = PV(u-1)... issued
+        kw = x[:, 5] - x[:, 4]
+        si = x[:, 6] - x[:, 5]
+        pv = x[1:, 7] - x[1:, 6]
+        nxt = x[1:, 4] - x[:-1, 7]
+        extra += (f"\n   MMA warp: K wait {med(kw):.0f}  S issue {med(si):.0f}  S->PV done {med(pv):.0f}  "
+                  f"PV done->next step {med(nxt):.0f}")
     print(f"lane {L}: tiles {n}  period {med(period):.0f}  softmax {med(soft):.0f}  wait_S {med(wait):.0f}  "
-          f"P->MMA {med(pseen):.0f}  PV issue {med(pv_issue):.0f}  PV->S issue {med(s_next):.0f}  "
-          f"S issue->ready {med(s_ready):.0f}")
+          f"P->MMA {med(pseen):.0f}" + extra)
