@@ -52,7 +52,7 @@ typedef enum {
 
 enum { DFA2C_FULL = 0, DFA2C_ARROW = 1, DFA2C_CACHED = 2 }; /* StrategyKind */
 enum { DFA2C_VISUAL_FIRST = 0, DFA2C_TEXT_FIRST = 1 };     /* TokenOrder */
-enum { DFA2C_BF16 = 0, DFA2C_F32 = 1 };                    /* element type */
+enum { DFA2C_BF16 = 0, DFA2C_F32 = 1, DFA2C_F64 = 2 };    /* element type */
 enum { DFA2C_RSE_STANDARD = 0, DFA2C_RSE_LITERAL = 1 };     /* RseMode */
 
 /* AttentionDims (inc/tensor.hpp:56-72). */
@@ -102,7 +102,9 @@ int dfa2c_tile_set(const dfa2c_dims* dims, int64_t block, int32_t kind, int64_t 
 /* ---- HeadCache (inc/cache.hpp:15-32; src/cache.cpp) --------------------
  * Device-resident: one bf16 slot [batch, N, d] per (layer, head), laid out
  * per layer as [batch, H, N, d] so cached heads copy back with the same
- * offsets as the output. produced_at bookkeeping is host-side. */
+ * offsets as the output. produced_at bookkeeping is host-side. n_layers is
+ * a capacity hint: any layer index >= 0 is accepted (storage grows), as in
+ * the reference's map-backed cache. */
 typedef struct dfa2c_cache dfa2c_cache;
 int dfa2c_cache_create(int64_t n_layers, int64_t n_heads, int64_t batch,
                        int64_t seq_len, int64_t head_dim, dfa2c_cache** cache);
@@ -150,7 +152,7 @@ int dfa2c_dense_attention_forward(const void* q, const void* k, const void* v, v
 /* ---- calibration RSE query ---------------------------------------------
  * rse (inc/calibrate.hpp:18-20; src/calibrate.cpp:18-87) for `n_heads`
  * contiguous heads of `numel` elements each (y_m, y_o device, dtype
- * DFA2C_BF16 or DFA2C_F32): fp64 accumulation, deterministic fixed-order
+ * DFA2C_BF16, DFA2C_F32 or DFA2C_F64): fp64 accumulation, deterministic fixed-order
  * reduction. Writes out[n_heads] (HOST doubles) and synchronizes the
  * stream; DFA2C_DEGENERATE if any head's reference has zero variance. */
 int dfa2c_rse(const void* y_m, const void* y_o, int32_t dtype, int64_t n_heads,

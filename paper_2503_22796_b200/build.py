@@ -46,7 +46,7 @@ def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=()
             deps += [os.path.join(d, f) for f in os.listdir(d) if f.endswith((".h", ".cuh", ".hpp"))]
     if not force and not _stale(out, deps):
         return out
-    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-cudart", "static",
+    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++20", "-shared", "-cudart", "static",
            "-Xcompiler", "-fPIC,-fvisibility=hidden,-fvisibility-inlines-hidden", "-Xptxas", "-v" if verbose else "-O3",
            "-I", os.path.join(ROOT, "include"), "-I", CSRC,
            *[f"-D{d}" for d in defines], "-o", out + ".tmp", *_sources(), "-ldl"]

@@ -443,13 +443,26 @@ struct dfa2c_cache {
     }
     size_t slot_elems() const { return static_cast<size_t>(n * d); }
     size_t layer_bytes() const { return static_cast<size_t>(batch * H * n * d) * 2; }
-    void check(int64_t layer, int64_t head) const {
-        if (layer < 0 || layer >= L || head < 0 || head >= H)
+    // n_layers is a capacity hint: like the reference's map-backed HeadCache
+    // (src/cache.cpp), any layer index >= 0 is accepted; storage grows.
+    void ensure(int64_t layer) {
+        if (layer >= L) {
+            layer_buf.resize(static_cast<size_t>(layer + 1), nullptr);
+            std::vector<int64_t> p(static_cast<size_t>((layer + 1) * H), std::numeric_limits<int64_t>::min());
+            std::copy(produced.begin(), produced.end(), p.begin());
+            produced.swap(p);
+            L = layer + 1;
+        }
+    }
+    void check(int64_t layer, int64_t head) {
+        if (layer < 0 || head < 0 || head >= H)
             fail(DFA2C_SHAPE, "cache slot (" + std::to_string(layer) + ", " + std::to_string(head) +
                                   ") out of range");
+        ensure(layer);
     }
     bool has(int64_t layer, int64_t head) const {
-        return produced[static_cast<size_t>(layer * H + head)] != std::numeric_limits<int64_t>::min();
+        return layer >= 0 && layer < L && head >= 0 && head < H &&
+               produced[static_cast<size_t>(layer * H + head)] != std::numeric_limits<int64_t>::min();
     }
     void* layer_ptr(int64_t layer) {
         if (!layer_buf[layer]) {
@@ -522,6 +535,7 @@ void run_forward(const ForwardSpec& s, cudaStream_t stream) {
     if (need_cache) {
         if (!s.cache)
             fail(DFA2C_CACHE_MISS, "cached heads need a cache");
+        s.cache->ensure(s.layer);
         cache_layer = s.cache->layer_ptr(s.layer);
     }
 
@@ -753,7 +767,6 @@ int dfa2c_cache_fetch(const dfa2c_cache* c, int64_t layer, int64_t head, void* d
     return guard([&] {
         if (!c || !dst)
             fail(DFA2C_SHAPE, "NULL cache or destination");
-        c->check(layer, head);
         if (!c->has(layer, head))
             fail(DFA2C_CACHE_MISS, "no cached output for layer " + std::to_string(layer) + ", head " +
                                        std::to_string(head));
@@ -809,8 +822,8 @@ int dfa2c_mha_forward(const void* q, const void* k, const void* v, int64_t batch
         if (cache) {
             if (cache->H != H || cache->n != seq_len(dims) || cache->d != dims->head_dim || cache->batch != batch)
                 fail(DFA2C_SHAPE, "cache geometry disagrees with dims/batch");
-            if (layer < 0 || layer >= cache->L)
-                fail(DFA2C_SHAPE, "layer out of the cache's range");
+            if (layer < 0)
+                fail(DFA2C_SHAPE, "layer index must be >= 0");
         }
         for (int64_t h = 0; h < H; ++h)
             if (kinds[h] == DFA2C_CACHED && (!cache || !cache->has(layer, h)))
@@ -885,8 +898,8 @@ int dfa2c_rse_async(const void* y_m, const void* y_o, int32_t dtype, int64_t n_h
     return guard([&] {
         if (!y_m || !y_o || !out_dev)
             fail(DFA2C_SHAPE, "rse operands must not be NULL");
-        if (dtype != DFA2C_BF16 && dtype != DFA2C_F32)
-            fail(DFA2C_SHAPE, "rse operands must be bf16 or f32");
+        if (dtype != DFA2C_BF16 && dtype != DFA2C_F32 && dtype != DFA2C_F64)
+            fail(DFA2C_SHAPE, "rse operands must be bf16, f32 or f64");
         if (n_heads < 1 || numel < 1)
             fail(DFA2C_SHAPE, "rse needs at least one element");
         if (mode != DFA2C_RSE_STANDARD && mode != DFA2C_RSE_LITERAL)

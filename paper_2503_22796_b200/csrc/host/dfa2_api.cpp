@@ -1,0 +1,677 @@
+// dfa2_api.cpp — the reference's C++ operator API (namespace dfa2,
+// include/dfa2/*.hpp) implemented on top of the C-ABI (include/dfa2c.h).
+//
+// A caller of /root/reference/proj/include/dfa2/*.hpp relinks against
+// libdfa2_b200.so and keeps its code: host f32 Tensors go in, the work runs
+// on the sm_100a kernels (bf16 inputs, fp32 accumulation), f32 Tensors come
+// back. Validation and the exception taxonomy follow the reference
+// (src/dispatch.cpp:11-54, inc/errors.hpp:8-45).
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <string>
+#include <vector>
+
+#include "dfa2/arrow.hpp"
+#include "dfa2/cache.hpp"
+#include "dfa2/calibrate.hpp"
+#include "dfa2/dispatch.hpp"
+#include "dfa2/errors.hpp"
+#include "dfa2/plan.hpp"
+#include "dfa2/tensor.hpp"
+#include "dfa2c.h"
+
+#define DFA2_API __attribute__((visibility("default")))
+
+namespace dfa2 {
+
+DFA2_API void throw_status(int status) {
+    if (status == DFA2C_OK)
+        return;
+    const std::string msg = dfa2c_last_error();
+    switch (status) {
+    case DFA2C_SHAPE: throw ShapeError(msg);
+    case DFA2C_NONFINITE: throw NonFiniteError(msg);
+    case DFA2C_FULLY_MASKED: throw FullyMaskedRowError(msg);
+    case DFA2C_CACHE_MISS: throw CacheMissError(msg);
+    case DFA2C_DEGENERATE: throw DegenerateReferenceError(msg);
+    case DFA2C_PLAN: throw PlanValidationError(msg);
+    case DFA2C_IO: throw IoError(msg);
+    case DFA2C_ORACLE: throw OracleError(msg);
+    default: throw DeviceError(msg);
+    }
+}
+
+namespace {
+
+void check(int status) { throw_status(status); }
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess)
+        throw DeviceError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+int64_t shape_numel(const std::vector<int64_t>& shape) {
+    int64_t n = 1;
+    for (int64_t d : shape) {
+        if (d < 0)
+            throw ShapeError("negative dimension");
+        n *= d;
+    }
+    return n;
+}
+
+uint16_t to_bf16(float f) {
+    uint32_t u;
+    std::memcpy(&u, &f, 4);
+    if ((u & 0x7f800000u) != 0x7f800000u)
+        u += 0x7fffu + ((u >> 16) & 1u);
+    else if (u & 0x007fffffu)
+        u |= 0x00400000u;  // quiet NaN
+    return static_cast<uint16_t>(u >> 16);
+}
+
+float from_bf16(uint16_t b) {
+    const uint32_t u = static_cast<uint32_t>(b) << 16;
+    float f;
+    std::memcpy(&f, &u, 4);
+    return f;
+}
+
+// Owning device buffer.
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    explicit DevBuf(size_t n) : bytes(n) { cuda_check(cudaMalloc(&p, n ? n : 16), "cudaMalloc"); }
+    ~DevBuf() { cudaFree(p); }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+};
+
+// f32 host values -> bf16 device buffer.
+void upload_bf16(const float* src, int64_t n, void* dst) {
+    std::vector<uint16_t> h(static_cast<size_t>(n));
+    for (int64_t i = 0; i < n; ++i)
+        h[i] = to_bf16(src[i]);
+    cuda_check(cudaMemcpy(dst, h.data(), h.size() * 2, cudaMemcpyHostToDevice), "upload");
+}
+
+void download_bf16(const void* src, int64_t n, float* dst) {
+    std::vector<uint16_t> h(static_cast<size_t>(n));
+    cuda_check(cudaMemcpy(h.data(), src, h.size() * 2, cudaMemcpyDeviceToHost), "download");
+    for (int64_t i = 0; i < n; ++i)
+        dst[i] = from_bf16(h[i]);
+}
+
+// f32 view of a tensor (f64 narrowed).
+std::vector<float> as_f32(const Tensor& t) {
+    if (t.dtype() == Dtype::f32)
+        return std::vector<float>(t.f32(), t.f32() + t.numel());
+    std::vector<float> v(static_cast<size_t>(t.numel()));
+    for (int64_t i = 0; i < t.numel(); ++i)
+        v[i] = static_cast<float>(t.f64()[i]);
+    return v;
+}
+
+dfa2c_dims cdims(const AttentionDims& d) {
+    return dfa2c_dims{d.n_heads, d.head_dim, d.n_visual, d.n_text,
+                      d.order == TokenOrder::visual_first ? DFA2C_VISUAL_FIRST : DFA2C_TEXT_FIRST};
+}
+
+void plan_arrays(const LayerPlan& plan, std::vector<int32_t>& kinds, std::vector<int64_t>& wins) {
+    kinds.clear();
+    wins.clear();
+    for (const HeadStrategy& s : plan.strategies) {
+        kinds.push_back(s.kind == StrategyKind::full ? DFA2C_FULL
+                        : s.kind == StrategyKind::arrow ? DFA2C_ARROW
+                                                        : DFA2C_CACHED);
+        wins.push_back(s.window_blocks);
+    }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- Tensor
+DFA2_API Tensor Tensor::zeros(std::vector<int64_t> shape, Dtype dt) {
+    Tensor t;
+    const int64_t n = shape_numel(shape);
+    t.shape_ = std::move(shape);
+    t.dtype_ = dt;
+    if (dt == Dtype::f32)
+        t.f32_.assign(static_cast<size_t>(n), 0.0f);
+    else
+        t.f64_.assign(static_cast<size_t>(n), 0.0);
+    return t;
+}
+DFA2_API Tensor Tensor::from_f32(std::vector<int64_t> shape, std::vector<float> data) {
+    if (shape_numel(shape) != static_cast<int64_t>(data.size()))
+        throw ShapeError("data length does not match shape");
+    Tensor t;
+    t.shape_ = std::move(shape);
+    t.f32_ = std::move(data);
+    return t;
+}
+DFA2_API Tensor Tensor::from_f64(std::vector<int64_t> shape, std::vector<double> data) {
+    if (shape_numel(shape) != static_cast<int64_t>(data.size()))
+        throw ShapeError("data length does not match shape");
+    Tensor t;
+    t.shape_ = std::move(shape);
+    t.dtype_ = Dtype::f64;
+    t.f64_ = std::move(data);
+    return t;
+}
+DFA2_API int64_t Tensor::dim(int64_t i) const {
+    if (i < 0 || i >= ndim())
+        throw ShapeError("dimension index out of range");
+    return shape_[static_cast<size_t>(i)];
+}
+DFA2_API int64_t Tensor::numel() const {
+    return dtype_ == Dtype::f32 ? static_cast<int64_t>(f32_.size()) : static_cast<int64_t>(f64_.size());
+}
+DFA2_API float* Tensor::f32() {
+    if (dtype_ != Dtype::f32)
+        throw ShapeError("tensor is not float32");
+    return f32_.data();
+}
+DFA2_API const float* Tensor::f32() const {
+    if (dtype_ != Dtype::f32)
+        throw ShapeError("tensor is not float32");
+    return f32_.data();
+}
+DFA2_API double* Tensor::f64() {
+    if (dtype_ != Dtype::f64)
+        throw ShapeError("tensor is not float64");
+    return f64_.data();
+}
+DFA2_API const double* Tensor::f64() const {
+    if (dtype_ != Dtype::f64)
+        throw ShapeError("tensor is not float64");
+    return f64_.data();
+}
+DFA2_API Tensor Tensor::to_f64() const {
+    if (dtype_ == Dtype::f64)
+        return *this;
+    Tensor t = zeros(shape_, Dtype::f64);
+    for (size_t i = 0; i < f32_.size(); ++i)
+        t.f64_[i] = static_cast<double>(f32_[i]);
+    return t;
+}
+DFA2_API bool Tensor::operator==(const Tensor& o) const {
+    if (dtype_ != o.dtype_ || shape_ != o.shape_)
+        return false;
+    if (dtype_ == Dtype::f32)
+        return std::memcmp(f32_.data(), o.f32_.data(), f32_.size() * sizeof(float)) == 0;
+    return std::memcmp(f64_.data(), o.f64_.data(), f64_.size() * sizeof(double)) == 0;
+}
+DFA2_API bool Tensor::all_finite() const {
+    for (float v : f32_)
+        if (!std::isfinite(v))
+            return false;
+    for (double v : f64_)
+        if (!std::isfinite(v))
+            return false;
+    return true;
+}
+DFA2_API void Tensor::check_finite(const char* what) const {
+    if (!all_finite())
+        throw NonFiniteError(std::string(what) + ": non-finite scalar");
+}
+
+DFA2_API void AttentionDims::validate() const {
+    if (n_heads < 1 || head_dim < 1)
+        throw ShapeError("n_heads and head_dim must be >= 1");
+    if (n_visual < 1 || n_text < 0)
+        throw ShapeError("need n_visual >= 1 and n_text >= 0");
+}
+
+DFA2_API Tensor head_slice(const Tensor& x, int64_t head) {
+    if (x.ndim() != 3)
+        throw ShapeError("head_slice expects [H, N, d]");
+    if (head < 0 || head >= x.dim(0))
+        throw ShapeError("head index out of range");
+    const int64_t n = x.dim(1), d = x.dim(2);
+    Tensor s = Tensor::zeros({n, d}, x.dtype());
+    if (x.dtype() == Dtype::f32)
+        std::memcpy(s.f32(), x.f32() + head * n * d, sizeof(float) * n * d);
+    else
+        std::memcpy(s.f64(), x.f64() + head * n * d, sizeof(double) * n * d);
+    return s;
+}
+
+DFA2_API void copy_into_head(Tensor& dst, int64_t head, const Tensor& src) {
+    if (dst.ndim() != 3 || src.ndim() != 2)
+        throw ShapeError("copy_into_head expects [H, N, d] and [N, d]");
+    if (dst.dtype() != src.dtype())
+        throw ShapeError("copy_into_head dtype mismatch");
+    if (src.dim(0) != dst.dim(1) || src.dim(1) != dst.dim(2))
+        throw ShapeError("copy_into_head shape mismatch");
+    if (head < 0 || head >= dst.dim(0))
+        throw ShapeError("head index out of range");
+    const int64_t n = dst.dim(1), d = dst.dim(2);
+    if (dst.dtype() == Dtype::f32)
+        std::memcpy(dst.f32() + head * n * d, src.f32(), sizeof(float) * n * d);
+    else
+        std::memcpy(dst.f64() + head * n * d, src.f64(), sizeof(double) * n * d);
+}
+
+// ---------------------------------------------------------------- masks
+DFA2_API BlockMask BlockMask::all_active(int64_t seq_len, int64_t block_size) {
+    if (block_size < 1)
+        throw ShapeError("block_size must be >= 1");
+    if (seq_len < 1)
+        throw ShapeError("seq_len must be >= 1");
+    BlockMask m;
+    m.block_size = block_size;
+    m.seq_len = seq_len;
+    m.n_query_blocks = (seq_len + block_size - 1) / block_size;
+    m.n_key_blocks = m.n_query_blocks;
+    m.active.assign(static_cast<size_t>(m.n_query_blocks * m.n_key_blocks), 1);
+    return m;
+}
+DFA2_API int64_t BlockMask::block_len(int64_t i) const { return std::min(block_size, seq_len - i * block_size); }
+DFA2_API int64_t BlockMask::active_positions() const {
+    int64_t ap = 0;
+    check(dfa2c_mask_stats(active.data(), seq_len, block_size, 1, &ap, nullptr, nullptr));
+    return ap;
+}
+DFA2_API bool BlockMask::row_has_active(int64_t i) const {
+    for (int64_t j = 0; j < n_key_blocks; ++j)
+        if (is_active(i, j))
+            return true;
+    return false;
+}
+
+DFA2_API BlockMask build_arrow_mask(const ArrowSpec& spec) {
+    const dfa2c_dims d = cdims(spec.dims);
+    int64_t nb = 0;
+    check(dfa2c_arrow_mask(&d, spec.block_size, spec.window_blocks, nullptr, &nb));
+    BlockMask m;
+    m.block_size = spec.block_size;
+    m.seq_len = spec.dims.seq_len();
+    m.n_query_blocks = m.n_key_blocks = nb;
+    m.active.resize(static_cast<size_t>(nb * nb));
+    check(dfa2c_arrow_mask(&d, spec.block_size, spec.window_blocks, m.active.data(), &nb));
+    return m;
+}
+DFA2_API int64_t flops_count(const BlockMask& mask, int64_t head_dim) {
+    int64_t f = 0;
+    check(dfa2c_mask_stats(mask.active.data(), mask.seq_len, mask.block_size, head_dim, nullptr, &f, nullptr));
+    return f;
+}
+DFA2_API int64_t dense_flops(int64_t seq_len, int64_t head_dim) { return dfa2c_dense_flops(seq_len, head_dim); }
+DFA2_API double sparsity_ratio(const BlockMask& mask) {
+    double s = 0.0;
+    check(dfa2c_mask_stats(mask.active.data(), mask.seq_len, mask.block_size, 1, nullptr, nullptr, &s));
+    return s;
+}
+
+// ---------------------------------------------------------------- attention
+namespace {
+void sparse_heads(const float* q, const float* k, const float* v, float* out, int64_t heads, int64_t n, int64_t d,
+                  const BlockMask* mask) {
+    const int64_t numel = heads * n * d;
+    DevBuf dq(numel * 2), dk(numel * 2), dv(numel * 2), dout(numel * 2);
+    upload_bf16(q, numel, dq.p);
+    upload_bf16(k, numel, dk.p);
+    upload_bf16(v, numel, dv.p);
+    if (mask) {
+        if (mask->seq_len != n)
+            throw ShapeError("mask sequence length disagrees with tensors");
+        check(dfa2c_sparse_attention_forward(dq.p, dk.p, dv.p, dout.p, heads, n, d, mask->active.data(),
+                                             mask->block_size, nullptr));
+    } else {
+        check(dfa2c_dense_attention_forward(dq.p, dk.p, dv.p, dout.p, heads, n, d, nullptr));
+    }
+    download_bf16(dout.p, numel, out);
+}
+}  // namespace
+
+DFA2_API void sparse_attention_forward(const float* q, const float* k, const float* v, float* out, int64_t n,
+                                       int64_t d, const BlockMask& mask, bool /*parallel*/) {
+    sparse_heads(q, k, v, out, 1, n, d, &mask);
+}
+
+DFA2_API Tensor sparse_attention_forward(const Tensor& q, const Tensor& k, const Tensor& v, const BlockMask& mask) {
+    if (q.ndim() != 2 || k.ndim() != 2 || v.ndim() != 2)
+        throw ShapeError("sparse attention expects per-head [N, d] tensors");
+    if (q.shape() != k.shape() || q.shape() != v.shape())
+        throw ShapeError("q/k/v shapes disagree");
+    if (q.dtype() != Dtype::f32)
+        throw ShapeError("sparse attention runs in float32");
+    Tensor out = Tensor::zeros(q.shape(), Dtype::f32);
+    sparse_attention_forward(q.f32(), k.f32(), v.f32(), out.f32(), q.dim(0), q.dim(1), mask);
+    return out;
+}
+
+DFA2_API void dense_tiled_attention(const float* q, const float* k, const float* v, float* out, int64_t n, int64_t d,
+                                    int64_t block_size, bool /*parallel*/) {
+    if (block_size < 1)
+        throw ShapeError("block_size must be >= 1");
+    sparse_heads(q, k, v, out, 1, n, d, nullptr);
+}
+
+DFA2_API Tensor attention_reference(const Tensor& q, const Tensor& k, const Tensor& v, const BlockMask* mask) {
+    if (q.ndim() != 3 || k.ndim() != 3 || v.ndim() != 3)
+        throw ShapeError("attention expects [H, N, d] tensors");
+    if (q.shape() != k.shape() || q.shape() != v.shape())
+        throw ShapeError("q/k/v shapes disagree");
+    if (q.dtype() != k.dtype() || q.dtype() != v.dtype())
+        throw ShapeError("q/k/v dtypes disagree");
+    q.check_finite("attention q");
+    k.check_finite("attention k");
+    v.check_finite("attention v");
+    const std::vector<float> qf = as_f32(q), kf = as_f32(k), vf = as_f32(v);
+    std::vector<float> of(qf.size());
+    sparse_heads(qf.data(), kf.data(), vf.data(), of.data(), q.dim(0), q.dim(1), q.dim(2), mask);
+    Tensor out = Tensor::from_f32(q.shape(), std::move(of));
+    return q.dtype() == Dtype::f64 ? out.to_f64() : out;
+}
+
+// ---------------------------------------------------------------- cache
+DFA2_API HeadCache::~HeadCache() {
+    if (dev_)
+        dfa2c_cache_destroy(dev_);
+}
+
+DFA2_API dfa2c_cache* HeadCache::bind(int64_t n_heads, int64_t n, int64_t d) {
+    if (dev_) {
+        if (n_heads != heads_ || n != n_ || d != d_)
+            throw ShapeError("cached output shape disagrees with dims");
+    } else {
+        int64_t layers = 1;
+        for (const auto& kv : slots_)
+            layers = std::max(layers, kv.first.first + 1);
+        check(dfa2c_cache_create(layers, n_heads, 1, n, d, &dev_));
+        heads_ = n_heads;
+        n_ = n;
+        d_ = d;
+        layers_ = layers;
+    }
+    for (auto& kv : slots_) {
+        Slot& s = kv.second;
+        if (s.on_device)
+            continue;
+        if (kv.first.second >= heads_)
+            throw ShapeError("cached head index outside the layer's heads");
+        if (s.host.ndim() != 2 || s.host.dim(0) != n || s.host.dim(1) != d)
+            throw ShapeError("cached output shape disagrees with dims");
+        DevBuf tmp(static_cast<size_t>(n * d) * 2);
+        upload_bf16(s.host.f32(), n * d, tmp.p);
+        check(dfa2c_cache_store(dev_, kv.first.first, kv.first.second, tmp.p, s.produced_at, nullptr));
+        cuda_check(cudaDeviceSynchronize(), "cache upload");
+        s.on_device = true;
+        s.host_fresh = false;
+    }
+    return dev_;
+}
+
+DFA2_API void HeadCache::store(int64_t layer, int64_t head, Tensor output, int64_t t) {
+    if (output.ndim() != 2)
+        throw ShapeError("cache entries are per-head [N, d] tensors");
+    Slot& s = slots_[{layer, head}];
+    s.produced_at = t;
+    s.host = output.dtype() == Dtype::f32 ? std::move(output)
+                                          : Tensor::from_f32(output.shape(), as_f32(output));
+    s.on_device = false;
+    s.host_fresh = true;
+    if (dev_)
+        bind(heads_, n_, d_);  // upload now (bf16 slot)
+}
+
+DFA2_API const HeadCache::Slot& HeadCache::slot(int64_t layer, int64_t head) const {
+    const auto it = slots_.find({layer, head});
+    if (it == slots_.end())
+        throw CacheMissError("no cached output for layer " + std::to_string(layer) + ", head " + std::to_string(head));
+    return it->second;
+}
+
+DFA2_API const Tensor& HeadCache::fetch(int64_t layer, int64_t head) const {
+    const Slot& s = slot(layer, head);
+    if (!s.host_fresh) {
+        DevBuf tmp(static_cast<size_t>(n_ * d_) * 2);
+        check(dfa2c_cache_fetch(dev_, layer, head, tmp.p, nullptr));
+        s.host = Tensor::zeros({n_, d_});
+        download_bf16(tmp.p, n_ * d_, s.host.f32());
+        s.host_fresh = true;
+    }
+    return s.host;
+}
+
+DFA2_API bool HeadCache::has(int64_t layer, int64_t head) const { return slots_.count({layer, head}) != 0; }
+DFA2_API int64_t HeadCache::produced_at(int64_t layer, int64_t head) const { return slot(layer, head).produced_at; }
+DFA2_API int64_t HeadCache::staleness(int64_t layer, int64_t head, int64_t t) const {
+    return t - slot(layer, head).produced_at;
+}
+DFA2_API void HeadCache::clear() {
+    slots_.clear();
+    if (dev_)
+        check(dfa2c_cache_clear(dev_));
+}
+DFA2_API int64_t HeadCache::size() const { return static_cast<int64_t>(slots_.size()); }
+
+// Access for multi_strategy_attention / influence_for_layer.
+class CacheAccess {
+public:
+    static void committed(HeadCache& c, int64_t layer, int64_t head, int64_t t) {
+        HeadCache::Slot& s = c.slots_[{layer, head}];
+        s.produced_at = t;
+        s.on_device = true;
+        s.host_fresh = false;
+    }
+};
+
+// ---------------------------------------------------------------- dispatch
+DFA2_API Tensor multi_strategy_attention(const Tensor& q, const Tensor& k, const Tensor& v, const LayerPlan& plan,
+                                         HeadCache& cache, int64_t layer, int64_t t, const AttentionDims& dims,
+                                         int64_t block_size) {
+    // validate_plan_inputs (src/dispatch.cpp:11-26)
+    dims.validate();
+    if (block_size < 1)
+        throw ShapeError("block_size must be >= 1");
+    if (q.ndim() != 3 || q.shape() != k.shape() || q.shape() != v.shape())
+        throw ShapeError("q/k/v must be identical [H, N, d] tensors");
+    if (q.dtype() != Dtype::f32 || k.dtype() != Dtype::f32 || v.dtype() != Dtype::f32)
+        throw ShapeError("multi-strategy attention runs in float32");
+    if (q.dim(0) != dims.n_heads || q.dim(1) != dims.seq_len() || q.dim(2) != dims.head_dim)
+        throw ShapeError("tensor shape disagrees with dims");
+    if (plan.n_heads() != dims.n_heads)
+        throw ShapeError("plan must assign exactly one strategy per head");
+    // cached heads checked before any compute (src/dispatch.cpp:38-48)
+    for (int64_t h = 0; h < plan.n_heads(); ++h)
+        if (plan.strategies[h].kind == StrategyKind::cached && !cache.has(layer, h))
+            throw CacheMissError("plan marks head " + std::to_string(h) + " Cached before it ever computed");
+    const int64_t H = dims.n_heads, n = dims.seq_len(), d = dims.head_dim, numel = H * n * d;
+    dfa2c_cache* dev = cache.bind(H, n, d);
+    DevBuf dq(numel * 2), dk(numel * 2), dv(numel * 2), dout(numel * 2);
+    upload_bf16(q.f32(), numel, dq.p);
+    upload_bf16(k.f32(), numel, dk.p);
+    upload_bf16(v.f32(), numel, dv.p);
+    std::vector<int32_t> kinds;
+    std::vector<int64_t> wins;
+    plan_arrays(plan, kinds, wins);
+    const dfa2c_dims cd = cdims(dims);
+    check(dfa2c_mha_forward(dq.p, dk.p, dv.p, 1, &cd, block_size, kinds.data(), wins.data(), dev, layer, t, dout.p,
+                            nullptr));
+    Tensor out = Tensor::zeros(q.shape(), Dtype::f32);
+    download_bf16(dout.p, numel, out.f32());
+    for (int64_t h = 0; h < H; ++h)
+        if (plan.strategies[h].kind != StrategyKind::cached)
+            CacheAccess::committed(cache, layer, h, t);
+    return out;
+}
+
+DFA2_API int64_t plan_flops(const LayerPlan& plan, const AttentionDims& dims, int64_t block_size) {
+    if (plan.n_heads() != dims.n_heads)
+        throw ShapeError("plan must assign exactly one strategy per head");
+    std::vector<int32_t> kinds;
+    std::vector<int64_t> wins;
+    plan_arrays(plan, kinds, wins);
+    const dfa2c_dims cd = cdims(dims);
+    int64_t f = 0;
+    check(dfa2c_plan_flops(&cd, block_size, kinds.data(), wins.data(), &f));
+    return f;
+}
+
+// ---------------------------------------------------------------- calibration
+DFA2_API double rse(const Tensor& y_m, const Tensor& y_o, RseMode mode) {
+    if (y_m.shape() != y_o.shape() || y_m.dtype() != y_o.dtype())
+        throw ShapeError("rse operands must share shape and dtype");
+    if (y_m.numel() == 0)
+        throw ShapeError("rse needs at least one element");
+    const int64_t n = y_m.numel();
+    const bool f64 = y_m.dtype() == Dtype::f64;
+    const size_t bytes = static_cast<size_t>(n) * (f64 ? 8 : 4);
+    DevBuf dm(bytes), dO(bytes);
+    cuda_check(cudaMemcpy(dm.p, f64 ? static_cast<const void*>(y_m.f64()) : y_m.f32(), bytes, cudaMemcpyHostToDevice),
+               "rse upload");
+    cuda_check(cudaMemcpy(dO.p, f64 ? static_cast<const void*>(y_o.f64()) : y_o.f32(), bytes, cudaMemcpyHostToDevice),
+               "rse upload");
+    double out = 0.0;
+    check(dfa2c_rse(dm.p, dO.p, f64 ? DFA2C_F64 : DFA2C_F32, 1, n,
+                    mode == RseMode::standard ? DFA2C_RSE_STANDARD : DFA2C_RSE_LITERAL, &out, nullptr));
+    return out;
+}
+
+DFA2_API std::string method_id(const HeadStrategy& s) {
+    switch (s.kind) {
+    case StrategyKind::arrow: return "arrow_w" + std::to_string(s.window_blocks);
+    case StrategyKind::cached: return "cached";
+    default: return "full";
+    }
+}
+
+DFA2_API std::vector<MethodCandidate> make_candidates(const std::vector<int64_t>& windows, bool include_cached) {
+    std::vector<MethodCandidate> methods;
+    for (int64_t w : windows) {
+        if (w < 0)
+            throw ShapeError("window radii must be >= 0");
+        methods.push_back({method_id(HeadStrategy::Arrow(w)), HeadStrategy::Arrow(w)});
+    }
+    if (include_cached)
+        methods.push_back({"cached", HeadStrategy::Cached()});
+    if (methods.empty())
+        throw ShapeError("candidate set must be nonempty");
+    return methods;
+}
+
+DFA2_API LayerInfluence influence_for_layer(const Tensor& q, const Tensor& k, const Tensor& v,
+                                            const std::vector<MethodCandidate>& methods, HeadCache& cache,
+                                            int64_t layer, int64_t t, const AttentionDims& dims, int64_t block_size,
+                                            RseMode mode, CalibrationStats* stats) {
+    if (methods.empty())
+        throw ShapeError("candidate set must be nonempty");
+    std::vector<int64_t> windows;
+    bool cached = false;
+    for (const MethodCandidate& m : methods) {
+        if (m.strategy.kind == StrategyKind::arrow) {
+            if (cached)
+                throw ShapeError("Cached must be the last candidate");
+            windows.push_back(m.strategy.window_blocks);
+        } else if (m.strategy.kind == StrategyKind::cached) {
+            cached = true;
+        } else {
+            throw ShapeError("Full is not a compression candidate");
+        }
+    }
+    dims.validate();
+    const int64_t H = dims.n_heads, n = dims.seq_len(), d = dims.head_dim, numel = H * n * d;
+    const int64_t M = static_cast<int64_t>(methods.size());
+    if (q.ndim() != 3 || q.dim(0) != H || q.dim(1) != n || q.dim(2) != d || q.shape() != k.shape() ||
+        q.shape() != v.shape())
+        throw ShapeError("tensor shape disagrees with dims");
+    dfa2c_cache* dev = cache.size() > 0 ? cache.bind(H, n, d) : nullptr;
+    DevBuf dq(numel * 2), dk(numel * 2), dv(numel * 2), dorig(numel * 2), douts(numel * 2 * M);
+    upload_bf16(as_f32(q).data(), numel, dq.p);
+    upload_bf16(as_f32(k).data(), numel, dk.p);
+    upload_bf16(as_f32(v).data(), numel, dv.p);
+    LayerInfluence li;
+    li.influence.assign(static_cast<size_t>(H * M), 0.0);
+    int64_t evals = 0;
+    const dfa2c_dims cd = cdims(dims);
+    check(dfa2c_influence_for_layer(dq.p, dk.p, dv.p, &cd, block_size, windows.data(),
+                                    static_cast<int64_t>(windows.size()), cached ? 1 : 0, dev, layer, t,
+                                    mode == RseMode::standard ? DFA2C_RSE_STANDARD : DFA2C_RSE_LITERAL,
+                                    li.influence.data(), dorig.p, douts.p, &evals, nullptr));
+    li.original = Tensor::zeros({H, n, d});
+    download_bf16(dorig.p, numel, li.original.f32());
+    li.method_outputs.resize(static_cast<size_t>(M));
+    for (int64_t m = 0; m < M; ++m) {
+        if (methods[m].strategy.kind == StrategyKind::cached && t == 0)
+            continue;  // ineligible: left unset, as in the reference
+        li.method_outputs[m] = Tensor::zeros({H, n, d});
+        download_bf16(static_cast<const char*>(douts.p) + m * numel * 2, numel, li.method_outputs[m].f32());
+    }
+    if (stats)
+        stats->attention_evals += evals;
+    return li;
+}
+
+// ---------------------------------------------------------------- plan
+DFA2_API CompressionPlan CompressionPlan::all_full(const AttentionDims& dims, int64_t timesteps, int64_t layers,
+                                                   int64_t block_size) {
+    CompressionPlan p;
+    p.dims = dims;
+    p.n_timesteps = timesteps;
+    p.n_layers = layers;
+    p.block_size = block_size;
+    p.layers.assign(static_cast<size_t>(timesteps * layers), LayerPlan::all_full(dims.n_heads));
+    return p;
+}
+DFA2_API const LayerPlan& CompressionPlan::at(int64_t t, int64_t layer) const {
+    return layers.at(static_cast<size_t>(t * n_layers + layer));
+}
+DFA2_API LayerPlan& CompressionPlan::at(int64_t t, int64_t layer) {
+    return layers.at(static_cast<size_t>(t * n_layers + layer));
+}
+
+namespace {
+void plan_flat(const CompressionPlan& p, std::vector<int32_t>& kinds, std::vector<int64_t>& wins) {
+    if (static_cast<int64_t>(p.layers.size()) != p.n_timesteps * p.n_layers)
+        throw PlanValidationError("plan must cover every (t, layer) exactly once");
+    kinds.clear();
+    wins.clear();
+    for (const LayerPlan& lp : p.layers) {
+        if (lp.n_heads() != p.dims.n_heads)
+            throw PlanValidationError("head array length must equal H");
+        std::vector<int32_t> k;
+        std::vector<int64_t> w;
+        plan_arrays(lp, k, w);
+        kinds.insert(kinds.end(), k.begin(), k.end());
+        wins.insert(wins.end(), w.begin(), w.end());
+    }
+}
+}  // namespace
+
+DFA2_API void CompressionPlan::validate() const {
+    dims.validate();
+    if (!(delta >= 0.0))
+        throw PlanValidationError("delta must be >= 0");
+    if (!(coeff >= 1.0))
+        throw PlanValidationError("coeff must be >= 1");
+    std::vector<int32_t> kinds;
+    std::vector<int64_t> wins;
+    plan_flat(*this, kinds, wins);
+    const dfa2c_dims cd = cdims(dims);
+    check(dfa2c_plan_aggregate(&cd, n_timesteps, n_layers, block_size, kinds.data(), wins.data(), nullptr, nullptr,
+                               nullptr));
+}
+DFA2_API int64_t CompressionPlan::flops_total() const {
+    std::vector<int32_t> kinds;
+    std::vector<int64_t> wins;
+    plan_flat(*this, kinds, wins);
+    const dfa2c_dims cd = cdims(dims);
+    int64_t f = 0;
+    check(dfa2c_plan_aggregate(&cd, n_timesteps, n_layers, block_size, kinds.data(), wins.data(), &f, nullptr,
+                               nullptr));
+    return f;
+}
+DFA2_API int64_t CompressionPlan::flops_dense_total() const {
+    return n_timesteps * n_layers * dims.n_heads * dense_flops(dims.seq_len(), dims.head_dim);
+}
+DFA2_API double CompressionPlan::aggregate_sparsity() const {
+    return 1.0 - static_cast<double>(flops_total()) / static_cast<double>(flops_dense_total());
+}
+
+}  // namespace dfa2

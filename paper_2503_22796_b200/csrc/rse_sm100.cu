@@ -54,6 +54,17 @@ struct Vec<float> {
     __device__ static double one(const float* p) { return static_cast<double>(*p); }
 };
 
+template <>
+struct Vec<double> {
+    static constexpr int W = 2;
+    __device__ static void load(const double* p, double (&x)[2]) {
+        const double2 u = __ldg(reinterpret_cast<const double2*>(p));
+        x[0] = u.x;
+        x[1] = u.y;
+    }
+    __device__ static double one(const double* p) { return *p; }
+};
+
 __device__ __forceinline__ void accum(double m, double o, double K, double (&a)[NACC]) {
     const double dO = o - K;
     const double dM = m - K;
@@ -144,7 +155,7 @@ __global__ void rse_finalize(const T* __restrict__ yo, const double* __restrict_
 
 cudaError_t launch_rse(const void* ym, const void* yo, int dtype, int64_t n_heads, int64_t numel,
                        int mode, double* out_dev, double* scratch, int nblk, cudaStream_t stream) {
-    const int64_t W = dtype == 0 ? 8 : 4;
+    const int64_t W = dtype == 0 ? 8 : dtype == 1 ? 4 : 2;
     int64_t chunk = (numel + nblk - 1) / nblk;
     chunk = (chunk + W - 1) / W * W;
     const dim3 grid(nblk, static_cast<unsigned>(n_heads));
@@ -156,6 +167,12 @@ cudaError_t launch_rse(const void* ym, const void* yo, int dtype, int64_t n_head
             static_cast<const __nv_bfloat16*>(ym), static_cast<const __nv_bfloat16*>(yo), numel, chunk, vec_ok, scratch);
         rse_finalize<__nv_bfloat16><<<fin_blocks, 128, 0, stream>>>(
             static_cast<const __nv_bfloat16*>(yo), scratch, nblk, static_cast<int>(n_heads), numel, mode, out_dev);
+    } else if (dtype == 2) {
+        rse_partial<double><<<grid, RSE_THREADS, 0, stream>>>(static_cast<const double*>(ym),
+                                                              static_cast<const double*>(yo), numel, chunk, vec_ok,
+                                                              scratch);
+        rse_finalize<double><<<fin_blocks, 128, 0, stream>>>(static_cast<const double*>(yo), scratch, nblk,
+                                                             static_cast<int>(n_heads), numel, mode, out_dev);
     } else {
         rse_partial<float><<<grid, RSE_THREADS, 0, stream>>>(static_cast<const float*>(ym),
                                                              static_cast<const float*>(yo), numel, chunk, vec_ok, scratch);
