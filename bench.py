@@ -197,6 +197,71 @@ def run_reference(args):
     print(json.dumps(line))
 
 
+def run_head_mode(args, rank, world, barrier, max_over_ranks):
+    """One FLUX sample on `world` GPUs: heads LPT-sharded by plan cost, one
+    fused launch per rank over its heads, NCCL all-gather of the bf16 output
+    heads (paper_2503_22796_b200.parallel). Strong scaling."""
+    import torch
+
+    from paper_2503_22796_b200 import api, parallel
+
+    dims = api.AttentionDims(H, D, NV, NT)
+    lp = api.LayerPlan.parse(PLAN)
+    shard = parallel.make_head_shard(lp, dims, BLOCK, world, rank)
+    gen = torch.Generator(device="cuda")
+
+    def randn(seed, *shape):
+        gen.manual_seed(seed)
+        return torch.randn(*shape, device="cuda", dtype=torch.float32, generator=gen).to(torch.bfloat16)
+
+    q, k, v = (randn(s, H, N, D) for s in (1, 2, 3))  # the same sample on every rank
+    idx = torch.tensor(shard.heads, device="cuda", dtype=torch.long)
+    ql, kl, vl = (x.index_select(0, idx).contiguous() for x in (q, k, v))
+    nh = len(shard.heads)
+    ldims = api.AttentionDims(max(nh, 1), D, NV, NT)
+    lplan = parallel.sub_plan(lp, shard.heads)
+    cache = api.HeadCache(1, max(nh, 1), N, D)
+    for i, h in enumerate(shard.heads):
+        cache.store(0, i, randn(100 + h, N, D), 0)
+    local = torch.empty_like(ql)
+    full = torch.empty_like(q)
+    stream = torch.cuda.current_stream()
+
+    def compute():
+        if nh:
+            api.multi_strategy_attention(ql, kl, vl, lplan, cache, 0, 1, ldims, BLOCK, out=local)
+
+    def step():
+        compute()
+        parallel.gather_heads(local, shard, full)
+
+    def timed(fn, steps):
+        for _ in range(args.warmup):
+            fn()
+        torch.cuda.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        return max_over_ranks(e0.elapsed_time(e1) / steps)
+
+    compute_ms = timed(compute, args.steps)
+    ms = timed(step, args.steps)
+    dense_fl = dense_layer_flops()
+    line = {"metric": METRIC, "value": dense_fl / (ms * 1e-3) / 1e12, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded N(0,1) bf16)",
+            "config": config({"parallelism": f"head-sharded x{world} (LPT on plan cost) + NCCL all-gather"}),
+            "layer_ms": ms, "compute_only_ms": compute_ms, "heads_per_rank": [len(o) for o in shard.all_heads]}
+    if rank == 0:
+        print(json.dumps(line))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -205,6 +270,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--ncu", action="store_true", help="short run for profiler captures (no e2e/cpu legs)")
+    ap.add_argument("--mode", default="sample", choices=["sample", "head"],
+                    help="sample: one FLUX sample per GPU (weak scaling, no collective); "
+                         "head: one sample split over the GPUs by LPT head sharding + NCCL all-gather (strong)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -234,6 +302,8 @@ def main():
         return float(t.item())
 
     dims = api.AttentionDims(H, D, NV, NT)
+    if args.mode == "head":
+        return run_head_mode(args, rank, world, barrier, max_over_ranks)
     seed0 = 1000 * rank
     gen = torch.Generator(device="cuda")
 

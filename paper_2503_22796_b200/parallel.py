@@ -1,0 +1,125 @@
+"""Multi-GPU execution of the fused head-wise attention layer.
+
+One process per GPU (torch.distributed, NCCL on GPUs / gloo in CPU tests).
+Every (sample, head) is independent (/root/reference/proj/src/dispatch.cpp:62-83),
+so no data-path collective is needed inside the layer:
+
+* sample sharding (configs 4, weak scaling): rank r owns samples
+  r, r + W, ... with their own cache slots; zero cross-GPU traffic.
+* head sharding (configs 2/3, one sample on W GPUs, strong scaling): heads
+  are assigned to ranks longest-processing-time-first on their plan cost
+  (Full and Arrow heads carry very different FLOPs, Cached heads are copies),
+  each rank runs ONE fused launch over its heads, and the per-rank outputs
+  are assembled with an all-gather over NVLink (all_gather_into_tensor on
+  equal-size padded shards). Each rank owns the cache slots of its heads.
+
+Outputs are bitwise identical for any W: a head's result depends only on
+its own tile sequence, which the static schedule fixes.
+"""
+from __future__ import annotations
+
+import heapq
+from dataclasses import dataclass
+from typing import List, Optional, Sequence
+
+from . import api
+
+
+def head_costs(plan: api.LayerPlan, dims: api.AttentionDims, block_size: int) -> List[float]:
+    """Relative cost per head: plan FLOPs of the head, Cached heads as their
+    copy traffic expressed in FLOP-equivalents (bytes x 100)."""
+    costs = []
+    d1 = api.AttentionDims(1, dims.head_dim, dims.n_visual, dims.n_text, dims.order)
+    for s in plan.strategies:
+        one = api.LayerPlan([s])
+        if s.kind == api.StrategyKind.cached:
+            costs.append(float(2 * dims.seq_len() * dims.head_dim * 2) * 100.0)
+        else:
+            costs.append(float(api.plan_flops(one, d1, block_size)))
+    return costs
+
+
+def assign_heads(costs: Sequence[float], world: int) -> List[List[int]]:
+    """LPT: heads in descending cost order, each to the least-loaded rank
+    (ties to the lower rank); heads within a rank stay ascending."""
+    heap = [(0.0, r) for r in range(world)]
+    heapq.heapify(heap)
+    owner = [[] for _ in range(world)]
+    for h in sorted(range(len(costs)), key=lambda i: (-costs[i], i)):
+        load, r = heapq.heappop(heap)
+        owner[r].append(h)
+        heapq.heappush(heap, (load + costs[h], r))
+    return [sorted(o) for o in owner]
+
+
+def shard_samples(batch: int, world: int, rank: int) -> List[int]:
+    """Sample sharding: rank r owns samples r, r + world, ..."""
+    return list(range(rank, batch, world))
+
+
+@dataclass
+class HeadShard:
+    rank: int
+    world: int
+    heads: List[int]          # heads this rank computes / owns, ascending
+    max_heads: int            # padding so every rank's shard has equal size
+    all_heads: List[List[int]]
+
+
+def make_head_shard(plan: api.LayerPlan, dims: api.AttentionDims, block_size: int, world: int,
+                    rank: int) -> HeadShard:
+    owner = assign_heads(head_costs(plan, dims, block_size), world)
+    return HeadShard(rank, world, owner[rank], max(len(o) for o in owner), owner)
+
+
+def sub_plan(plan: api.LayerPlan, heads: Sequence[int]) -> api.LayerPlan:
+    return api.LayerPlan([plan.strategies[h] for h in heads])
+
+
+def gather_heads(local_out, shard: HeadShard, full_out, group=None):
+    """Assemble [H, N, d] from every rank's [len(heads), N, d] shard.
+
+    All-gather of equal-size (padded to max_heads) shards, then a scatter
+    into head order. Works on any torch.distributed backend (NCCL over
+    NVLink on GPUs, gloo in CPU tests)."""
+    import torch
+    import torch.distributed as dist
+
+    n, d = local_out.shape[-2], local_out.shape[-1]
+    padded = local_out.new_zeros((shard.max_heads, n, d))
+    if len(shard.heads):
+        padded[: len(shard.heads)] = local_out
+    gathered = local_out.new_empty((shard.world * shard.max_heads, n, d))
+    if shard.world == 1:
+        gathered.copy_(padded)
+    elif dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(gathered, padded, group=group)
+    else:  # gloo (CPU tests): list form
+        parts = list(gathered.chunk(shard.world))
+        dist.all_gather(parts, padded, group=group)
+        gathered = torch.cat(parts)
+    for r, hs in enumerate(shard.all_heads):
+        for i, h in enumerate(hs):
+            full_out[h].copy_(gathered[r * shard.max_heads + i])
+    return full_out
+
+
+def sharded_multi_strategy_attention(q, k, v, plan: api.LayerPlan, cache: Optional[api.HeadCache], layer: int,
+                                     t: int, dims: api.AttentionDims, block_size: int, shard: HeadShard,
+                                     gather: bool = True, out=None):
+    """One sample on W GPUs: this rank runs ONE fused launch over its heads
+    (cache holds only this rank's heads, indexed locally), then the output
+    heads are all-gathered. q/k/v: the full [H, N, d] sample (replicated)."""
+    import torch
+
+    heads = shard.heads
+    local_dims = api.AttentionDims(len(heads), dims.head_dim, dims.n_visual, dims.n_text, dims.order)
+    idx = torch.tensor(heads, device=q.device, dtype=torch.long)
+    ql, kl, vl = (x.index_select(0, idx).contiguous() for x in (q, k, v))
+    local = api.multi_strategy_attention(ql, kl, vl, sub_plan(plan, heads), cache, layer, t, local_dims,
+                                         block_size) if heads else q.new_empty((0,) + tuple(q.shape[1:]))
+    if not gather:
+        return local
+    if out is None:
+        out = torch.empty_like(q)
+    return gather_heads(local, shard, out)

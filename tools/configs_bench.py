@@ -1,0 +1,160 @@
+"""BASELINE.json configs 1, 2, 4, 5 on one B200 (config 3 is bench.py).
+
+    python tools/configs_bench.py [--out gpurun_out/configs.json]
+
+  cfg1  1024+77 tok, H=4, d=64, plan [F, A0, A2, C] at t=1 (B=128 and 64)
+  cfg2  SD3 4096+333, H=24, d=64: all-Arrow(w) window sweep + all Full
+  cfg4  FLUX 2K 28-step x 57-layer schedule with one shared device cache
+        (5 F, 9 A8, 4 A0, 6 C per layer for t >= 1, rotated per (t, l);
+        all Full at t = 0), one sample per GPU (batch 8 over 8 GPUs = 8x this)
+  cfg5  FLUX-shaped calibration sweep: influence_for_layer over 57 layers,
+        candidates Arrow {0, 2, 8, 16, 32} + Cached, plus the RSE kernel alone
+All timings: CUDA events, warm-up first; inputs resident in HBM.
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+
+from paper_2503_22796_b200 import api
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--out", default="gpurun_out/configs.json")
+ap.add_argument("--only", default="1,2,4,5")
+args = ap.parse_args()
+only = set(args.only.split(","))
+res = {}
+ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+
+
+def randn(seed, *shape):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    return torch.randn(*shape, device="cuda", generator=g).to(torch.bfloat16)
+
+
+def time_calls(fn, steps=20, warmup=5):
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    e0, e1 = ev(), ev()
+    e0.record()
+    for _ in range(steps):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / steps
+
+
+if "1" in only:
+    out = {}
+    for B in (128, 64):
+        H, nv, nt, d = 4, 1024, 77, 64
+        n = nv + nt
+        dims = api.AttentionDims(H, d, nv, nt)
+        q, k, v = (randn(s, H, n, d) for s in (1, 2, 3))
+        cache = api.HeadCache(1, H, n, d)
+        api.multi_strategy_attention(q, k, v, api.LayerPlan.all_full(H), cache, 0, 0, dims, B)
+        lp = api.LayerPlan.parse("F A0 A2 C")
+        o = torch.empty_like(q)
+        ms = time_calls(lambda: api.multi_strategy_attention(q, k, v, lp, cache, 0, 1, dims, B, out=o), 50)
+        fl = api.plan_flops(lp, dims, B)
+        out[f"B{B}"] = {"ms": ms, "plan_gflop": fl / 1e9, "computed_tflops": fl / ms / 1e9,
+                        "reduction": 1 - fl / (H * api.dense_flops(n, d))}
+    res["cfg1"] = out
+    print("cfg1", json.dumps(out))
+
+if "2" in only:
+    H, nv, nt, d, B = 24, 4096, 333, 64, 128
+    n = nv + nt
+    dims = api.AttentionDims(H, d, nv, nt)
+    q, k, v = (randn(s, H, n, d) for s in (1, 2, 3))
+    o = torch.empty_like(q)
+    dense = H * api.dense_flops(n, d)
+    full_ms = time_calls(lambda: api.multi_strategy_attention(q, k, v, api.LayerPlan.all_full(H), None, 0, 0, dims,
+                                                              B, out=o))
+    rows = [{"plan": "all Full", "ms": full_ms, "sparsity": 0.0, "computed_tflops": dense / full_ms / 1e9,
+             "effective_tflops": dense / full_ms / 1e9, "speedup_vs_full": 1.0}]
+    for w in (0, 1, 2, 4, 8, 16, 31):
+        lp = api.LayerPlan([api.HeadStrategy.Arrow(w)] * H)
+        fl = api.plan_flops(lp, dims, B)
+        ms = time_calls(lambda: api.multi_strategy_attention(q, k, v, lp, None, 0, 0, dims, B, out=o))
+        rows.append({"plan": f"all Arrow({w})", "ms": ms, "sparsity": 1 - fl / dense,
+                     "computed_tflops": fl / ms / 1e9, "effective_tflops": dense / ms / 1e9,
+                     "speedup_vs_full": full_ms / ms, "ideal_speedup": dense / fl})
+    res["cfg2_sd3_window_sweep"] = rows
+    for r in rows:
+        print("cfg2", json.dumps(r))
+
+if "4" in only:
+    T, L, H, nv, nt, d, B = 28, 57, 24, 16384, 512, 128, 128
+    n = nv + nt
+    dims = api.AttentionDims(H, d, nv, nt)
+    base = api.LayerPlan.parse(" ".join(["F"] * 5 + ["A8"] * 9 + ["A0"] * 4 + ["C"] * 6)).strategies
+    plan = api.CompressionPlan.all_full(dims, T, L, B)
+    for t in range(1, T):
+        for l in range(L):
+            r = (7 * t + 3 * l) % H
+            plan.layers[t * L + l] = api.LayerPlan(base[r:] + base[:r])
+    agg = plan.aggregate_sparsity()
+    # 4 rotating input sets stand in for the per-(t, l) activations (kernel time is data-independent)
+    qs = [tuple(randn(100 * i + s, H, n, d) for s in (1, 2, 3)) for i in range(4)]
+    o = torch.empty_like(qs[0][0])
+    cache = api.HeadCache(L, H, n, d)
+
+    def run_schedule(p):
+        e0, e1 = ev(), ev()
+        e0.record()
+        for t in range(T):
+            for l in range(L):
+                q, k, v = qs[(t + l) % 4]
+                api.multi_strategy_attention(q, k, v, p.at(t, l), cache, l, t, dims, B, out=o)
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1)
+
+    run_schedule(plan)  # warm-up (also fills every slot)
+    ms = run_schedule(plan)
+    full_ms = run_schedule(api.CompressionPlan.all_full(dims, T, L, B))
+    out = {"T": T, "L": L, "aggregate_sparsity": agg, "schedule_ms": ms, "per_layer_ms": ms / (T * L),
+           "all_full_schedule_ms": full_ms, "speedup_vs_full": full_ms / ms,
+           "effective_tflops": plan.flops_dense_total() / ms / 1e9,
+           "computed_tflops": plan.flops_total() / ms / 1e9, "cache_gb": cache.nbytes() / 1e9,
+           "note": "one sample per GPU; batch 8 on 8 GPUs shards samples (no inter-GPU traffic)"}
+    res["cfg4_flux_schedule"] = out
+    print("cfg4", json.dumps(out))
+    del qs, cache
+
+if "5" in only:
+    L, H, nv, nt, d, B = 57, 24, 16384, 512, 128, 128
+    n = nv + nt
+    dims = api.AttentionDims(H, d, nv, nt)
+    q, k, v = (randn(s, H, n, d) for s in (1, 2, 3))
+    cache = api.HeadCache(L, H, n, d)
+    for l in range(L):  # t = 0: every slot produced
+        api.multi_strategy_attention(q, k, v, api.LayerPlan.all_full(H), cache, l, 0, dims, B)
+    methods = api.make_candidates([0, 2, 8, 16, 32], include_cached=True)
+    stats = api.CalibrationStats()
+    api.influence_for_layer(q, k, v, methods, cache, 0, 1, dims, B, stats=stats, keep_outputs=False)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for l in range(L):
+        li = api.influence_for_layer(q, k, v, methods, cache, l, 1, dims, B, stats=stats, keep_outputs=False)
+    torch.cuda.synchronize()
+    sweep_s = time.perf_counter() - t0
+    # the RSE kernel alone: 24 heads x [N, d] bf16, 2 operands
+    a, b = randn(7, H, n, d), randn(8, H, n, d)
+    ms = time_calls(lambda: api.rse_per_head(a, b), 20)
+    bytes_ = 2 * a.numel() * 2
+    out = {"layers": L, "candidates": [m.id for m in methods], "sweep_s": sweep_s, "per_layer_ms": 1e3 * sweep_s / L,
+           "attention_evals": stats.attention_evals, "influence_example": [float(x) for x in li.influence[:6]],
+           "rse_ms": ms, "rse_bytes": bytes_, "rse_gbs": bytes_ / ms / 1e6}
+    res["cfg5_calibration"] = out
+    print("cfg5", json.dumps(out))
+
+os.makedirs(os.path.dirname(args.out) or ".", exist_ok=True)
+with open(args.out, "w") as f:
+    json.dump(res, f, indent=1)
