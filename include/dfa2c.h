@@ -137,6 +137,24 @@ int dfa2c_mha_forward(const void* q, const void* k, const void* v, int64_t batch
                       const int64_t* windows, dfa2c_cache* cache, int64_t layer,
                       int64_t t, void* out, void* stream);
 
+/* Same call with HOST buffers (the reference's host-tensor calling
+ * convention, inc/dispatch.hpp:44-47): q/k/v/out are host bf16
+ * [batch, H, N, d] (pinned for full overlap; pageable works, slower). Only
+ * the computed heads' q/k/v are uploaded, in head groups on a copy stream;
+ * each group's fused launch starts as soon as its inputs land and its
+ * outputs download while later groups upload and compute. Cached heads'
+ * outputs go straight from the cache slot to `out`. The call is
+ * asynchronous on `stream`: `out` is final once the stream reaches it.
+ * Host inputs are read from the moment of the call (uploads may start
+ * before earlier work on `stream` completes, overlapping the previous
+ * call's download), so they must be ready when the call is made — as with
+ * the reference's synchronous call.
+ * Same validation, cache semantics and results as dfa2c_mha_forward. */
+int dfa2c_mha_forward_host(const void* q, const void* k, const void* v, int64_t batch,
+                           const dfa2c_dims* dims, int64_t block, const int32_t* kinds,
+                           const int64_t* windows, dfa2c_cache* cache, int64_t layer,
+                           int64_t t, void* out, void* stream);
+
 /* sparse_attention_forward (inc/arrow.hpp:59-63; src/arrow.cpp:171-208) for
  * `n_heads` independent [N, d] heads sharing one arbitrary block mask
  * (host bytes, nb*nb). Empty mask rows -> DFA2C_FULLY_MASKED. */

@@ -113,6 +113,9 @@ _SIGS = {
     "dfa2c_mha_forward": (c_int32, [c_void_p, c_void_p, c_void_p, c_int64, POINTER(Dims), c_int64,
                                     POINTER(c_int32), POINTER(c_int64), c_void_p, c_int64, c_int64,
                                     c_void_p, c_void_p]),
+    "dfa2c_mha_forward_host": (c_int32, [c_void_p, c_void_p, c_void_p, c_int64, POINTER(Dims), c_int64,
+                                         POINTER(c_int32), POINTER(c_int64), c_void_p, c_int64, c_int64,
+                                         c_void_p, c_void_p]),
     "dfa2c_sparse_attention_forward": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int64,
                                                  c_int64, POINTER(c_uint8), c_int64, c_void_p]),
     "dfa2c_dense_attention_forward": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int64,

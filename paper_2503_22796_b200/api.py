@@ -384,6 +384,41 @@ def multi_strategy_attention(q, k, v, plan: LayerPlan, cache: Optional[HeadCache
     return out[0] if squeeze else out
 
 
+def multi_strategy_attention_host(q, k, v, plan: LayerPlan, cache: Optional[HeadCache], layer: int, t: int,
+                                  dims: AttentionDims, block_size: int, out=None, stream=None):
+    """multi_strategy_attention with HOST tensors (the reference's calling
+    convention, inc/dispatch.hpp:44-47) through dfa2c_mha_forward_host:
+    q/k/v are host bf16 [H, N, d] or [batch, H, N, d] (pin them for
+    copy/compute overlap); only computed heads are uploaded, in head groups
+    pipelined against their fused launches and the output download. Returns
+    the host output tensor; it is final once `stream` (default: the current
+    stream) is synchronized."""
+    torch = _torch()
+    for name, x in (("q", q), ("k", k), ("v", v)):
+        if not isinstance(x, torch.Tensor) or x.is_cuda or x.dtype != torch.bfloat16 or not x.is_contiguous():
+            raise ShapeError(f"{name} must be a contiguous host bf16 tensor")
+    squeeze = q.dim() == 3
+    if squeeze:
+        q, k, v = q.unsqueeze(0), k.unsqueeze(0), v.unsqueeze(0)
+    if q.dim() != 4 or q.shape != k.shape or q.shape != v.shape:
+        raise ShapeError("q/k/v must be identical [H, N, d] tensors")
+    if tuple(q.shape[1:]) != (dims.n_heads, dims.seq_len(), dims.head_dim):
+        raise ShapeError("tensor shape disagrees with dims")
+    if plan.n_heads() != dims.n_heads:
+        raise ShapeError("plan must assign exactly one strategy per head")
+    if out is None:
+        out = torch.empty(q.shape, dtype=torch.bfloat16, pin_memory=True)
+    elif out.is_cuda or out.dtype != torch.bfloat16 or out.shape != q.shape or not out.is_contiguous():
+        raise ShapeError("out must be a contiguous host bf16 tensor shaped like q")
+    d = dims.c()
+    kinds, wins = plan.arrays()
+    check(lib().dfa2c_mha_forward_host(c_void_p(q.data_ptr()), c_void_p(k.data_ptr()), c_void_p(v.data_ptr()),
+                                       q.shape[0], byref(d), block_size, kinds, wins,
+                                       cache.handle if cache is not None else None, layer, t,
+                                       c_void_p(out.data_ptr()), c_void_p(_stream_ptr(stream))))
+    return out[0] if squeeze else out
+
+
 def sparse_attention_forward(q, k, v, mask: BlockMask, out=None, stream=None):
     """sparse_attention_forward (inc/arrow.hpp:59-63): [N, d] or [H, N, d] heads."""
     torch = _torch()
@@ -457,6 +492,20 @@ def rse_per_head(y_m, y_o, mode: int = RseMode.standard, stream=None) -> np.ndar
     out = np.zeros(H, np.float64)
     check(lib().dfa2c_rse(c_void_p(y_m.data_ptr()), c_void_p(y_o.data_ptr()), dt, H, numel, mode,
                           out.ctypes.data_as(POINTER(c_double)), c_void_p(_stream_ptr(stream))))
+    return out
+
+
+def rse_per_head_async(y_m, y_o, out, mode: int = RseMode.standard, stream=None):
+    """RSE of every leading-axis slice into the DEVICE float64 tensor `out`
+    ([H]), asynchronously on `stream` (dfa2c_rse_async): no host sync, and a
+    zero-variance reference yields NaN instead of DegenerateReferenceError."""
+    torch = _torch()
+    y_m, y_o, dt = _rse_operands(y_m, y_o)
+    H = y_m.shape[0]
+    if not (out.is_cuda and out.dtype == torch.float64 and out.numel() == H and out.is_contiguous()):
+        raise ShapeError("out must be a contiguous CUDA float64 tensor with one entry per head")
+    check(lib().dfa2c_rse_async(c_void_p(y_m.data_ptr()), c_void_p(y_o.data_ptr()), dt, H, y_m.numel() // H, mode,
+                                c_void_p(out.data_ptr()), c_void_p(_stream_ptr(stream))))
     return out
 
 

@@ -26,6 +26,7 @@ namespace dfa2k {
 cudaError_t launch_attn(int d, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
                         const CUtensorMap& to, const CUtensorMap& tc, const AttnArgs& args, int grid,
                         cudaStream_t stream);
+int rse_ctas_per_sm();
 cudaError_t launch_rse(const void* ym, const void* yo, int dtype, int64_t n_heads, int64_t numel,
                        int mode, double* out_dev, double* scratch, int nblk, cudaStream_t stream);
 }  // namespace dfa2k
@@ -222,7 +223,10 @@ struct DevPlan {
     }
 };
 
-// Head strategy for the scheduler: mask_id < 0 => cached (copy items).
+// Head strategy for the scheduler: mask_id >= 0 => computed over that mask;
+// JOB_COPY => cached (copy items); JOB_SKIP => not part of this launch.
+constexpr int JOB_COPY = -1;
+constexpr int JOB_SKIP = -2;
 struct HeadJob {
     int mask_id;
     bool commit;
@@ -232,6 +236,35 @@ int num_sms(int device) {
     int v = 0;
     DFA2C_CUDA_CHECK(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device));
     return v;
+}
+
+// Stream-ordered scratch comes from a library-owned pool per device that
+// never returns memory to the driver (release threshold = max), so
+// steady-state calls allocate without driver round trips.
+cudaMemPool_t scratch_pool(int device) {
+    static std::mutex mu;
+    static std::map<int, cudaMemPool_t> pools;
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = pools.find(device);
+    if (it != pools.end())
+        return it->second;
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = device;
+    cudaMemPool_t pool{};
+    DFA2C_CUDA_CHECK(cudaMemPoolCreate(&pool, &props));
+    uint64_t keep = std::numeric_limits<uint64_t>::max();
+    DFA2C_CUDA_CHECK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    pools[device] = pool;
+    return pool;
+}
+
+template <class T>
+void scratch_alloc(T** p, size_t bytes, cudaStream_t st) {
+    int device = 0;
+    DFA2C_CUDA_CHECK(cudaGetDevice(&device));
+    DFA2C_CUDA_CHECK(cudaMallocFromPoolAsync(reinterpret_cast<void**>(p), bytes, scratch_pool(device), st));
 }
 
 // Pair lists: for every pair of query tiles (2p, 2p+1) the union of their
@@ -311,12 +344,14 @@ std::unique_ptr<DevPlan> build_dev_plan(int device, int64_t batch, int64_t H, in
     for (int64_t b = 0; b < batch; ++b)
         for (int64_t h = 0; h < H; ++h) {
             const HeadJob& j = jobs[h];
+            if (j.mask_id == JOB_SKIP)
+                continue;
             for (int64_t p = 0; p < np; ++p) {
                 WorkItem w{};
                 w.bh = static_cast<int32_t>(b * H + h);
                 w.qtile_a = static_cast<int32_t>(2 * p);
                 w.qtile_b = 2 * p + 1 < nqt ? static_cast<int32_t>(2 * p + 1) : -1;
-                if (j.mask_id < 0) {
+                if (j.mask_id == JOB_COPY) {
                     w.flags = dfa2k::ITEM_COPY;
                     const int64_t rows = std::min<int64_t>(n, (w.qtile_b >= 0 ? w.qtile_b : w.qtile_a) * 128 + 128) -
                                          w.qtile_a * 128;
@@ -531,7 +566,7 @@ void run_forward(const ForwardSpec& s, cudaStream_t stream) {
     void* cache_layer = nullptr;
     bool need_cache = false;
     for (const HeadJob& j : s.jobs)
-        need_cache |= (j.mask_id < 0) || j.commit;
+        need_cache |= (j.mask_id == JOB_COPY) || j.commit;
     if (need_cache) {
         if (!s.cache)
             fail(DFA2C_CACHE_MISS, "cached heads need a cache");
@@ -557,6 +592,8 @@ void run_forward(const ForwardSpec& s, cudaStream_t stream) {
     a.nb = static_cast<int32_t>(ceil_div(n, s.block));
     a.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(d)));
     a.trace = g_trace;
+    if (plan->grid == 0)
+        return;  // nothing to launch (every head skipped)
     DFA2C_CUDA_CHECK(dfa2k::launch_attn(static_cast<int>(d), tq, tk, tv, to, tc, a, plan->grid, stream));
     g_launches.fetch_add(1);
 }
@@ -572,7 +609,7 @@ void plan_jobs(const dfa2c_dims* dims, int64_t block, const int32_t* kinds, cons
     std::map<int64_t, int> ids;  // -1 = full, else window
     for (int64_t h = 0; h < dims->n_heads; ++h) {
         if (kinds[h] == DFA2C_CACHED) {
-            s.jobs.push_back({-1, false});
+            s.jobs.push_back({JOB_COPY, false});
             continue;
         }
         const int64_t key = kinds[h] == DFA2C_FULL ? -1 : windows[h];
@@ -592,9 +629,103 @@ void plan_jobs(const dfa2c_dims* dims, int64_t block, const int32_t* kinds, cons
     put(s.mask_key, dims->order);
 }
 
+// validate_plan_inputs + cached-head checks (src/dispatch.cpp:11-54), all
+// before any device work or cache mutation.
+void validate_forward(int64_t batch, const dfa2c_dims* dims, int64_t block, const int32_t* kinds,
+                      const int64_t* windows, const dfa2c_cache* cache, int64_t layer) {
+    validate_dims(dims);
+    if (block < 1)
+        fail(DFA2C_SHAPE, "block_size must be >= 1");
+    if (batch < 1)
+        fail(DFA2C_SHAPE, "batch must be >= 1");
+    validate_plan(dims, kinds, windows);
+    const int64_t H = dims->n_heads;
+    if (cache) {
+        if (cache->H != H || cache->n != seq_len(dims) || cache->d != dims->head_dim || cache->batch != batch)
+            fail(DFA2C_SHAPE, "cache geometry disagrees with dims/batch");
+        if (layer < 0)
+            fail(DFA2C_SHAPE, "layer index must be >= 0");
+    }
+    for (int64_t h = 0; h < H; ++h)
+        if (kinds[h] == DFA2C_CACHED && (!cache || !cache->has(layer, h)))
+            fail(DFA2C_CACHE_MISS, "plan marks head " + std::to_string(h) + " Cached before it ever computed");
+}
+
+// phase 2 bookkeeping: computed heads now hold output produced at t
+// (src/dispatch.cpp:85-88); cached heads keep their produced_at.
+void commit_produced(const dfa2c_dims* dims, const int32_t* kinds, dfa2c_cache* cache, int64_t layer, int64_t t) {
+    if (!cache)
+        return;
+    const int64_t H = dims->n_heads;
+    for (int64_t h = 0; h < H; ++h)
+        if (kinds[h] != DFA2C_CACHED)
+            cache->produced[static_cast<size_t>(layer * H + h)] = t;
+}
+
+// Per-device copy engine state of dfa2c_mha_forward_host: an upload and a
+// download stream plus two device staging slots used alternately, so one
+// call's uploads overlap the previous call's downloads.
+struct HostPipe {
+    static constexpr int kMaxGroups = 8;
+    struct Slot {
+        void *q = nullptr, *k = nullptr, *v = nullptr, *out = nullptr;
+        size_t cap = 0;
+        cudaEvent_t ev_start{}, ev_done{}, ev_free{};
+        cudaEvent_t ev_in[kMaxGroups]{}, ev_out[kMaxGroups]{};
+    };
+    std::mutex mu;
+    cudaStream_t h2d{}, d2h{};
+    Slot slots[2];
+    int turn = 0;
+
+    void init() {
+        DFA2C_CUDA_CHECK(cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking));
+        DFA2C_CUDA_CHECK(cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking));
+        for (Slot& s : slots) {
+            for (cudaEvent_t* e : {&s.ev_start, &s.ev_done, &s.ev_free})
+                DFA2C_CUDA_CHECK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+            for (int g = 0; g < kMaxGroups; ++g) {
+                DFA2C_CUDA_CHECK(cudaEventCreateWithFlags(&s.ev_in[g], cudaEventDisableTiming));
+                DFA2C_CUDA_CHECK(cudaEventCreateWithFlags(&s.ev_out[g], cudaEventDisableTiming));
+            }
+            DFA2C_CUDA_CHECK(cudaEventRecord(s.ev_free, h2d));  // initially free
+        }
+    }
+    Slot& next(size_t bytes) {
+        Slot& s = slots[turn];
+        turn ^= 1;
+        if (s.cap < bytes) {
+            // the slot's previous user must finish before its buffers go
+            DFA2C_CUDA_CHECK(cudaEventSynchronize(s.ev_free));
+            for (void** p : {&s.q, &s.k, &s.v, &s.out}) {
+                if (*p)
+                    DFA2C_CUDA_CHECK(cudaFree(*p));
+                *p = nullptr;
+                DFA2C_CUDA_CHECK(cudaMalloc(p, bytes));
+            }
+            s.cap = bytes;
+        }
+        return s;
+    }
+};
+
+HostPipe& host_pipe(int device) {
+    static std::mutex mu;
+    static std::map<int, std::unique_ptr<HostPipe>> pipes;
+    std::lock_guard<std::mutex> lk(mu);
+    auto& p = pipes[device];
+    if (!p) {
+        auto fresh = std::make_unique<HostPipe>();
+        fresh->init();
+        p = std::move(fresh);
+    }
+    return *p;
+}
+
 }  // namespace
 
 extern "C" {
+
 
 const char* dfa2c_last_error(void) { return g_err.c_str(); }
 const char* dfa2c_version(void) { return "dfa2c 0.1 (sm_100a tcgen05/TMA fused head-wise attention)"; }
@@ -812,22 +943,7 @@ int dfa2c_mha_forward(const void* q, const void* k, const void* v, int64_t batch
                       int64_t block, const int32_t* kinds, const int64_t* windows, dfa2c_cache* cache,
                       int64_t layer, int64_t t, void* out, void* stream) {
     return guard([&] {
-        // validate_plan_inputs + cached-head checks (src/dispatch.cpp:11-54),
-        // all before any device work or cache mutation.
-        validate_dims(dims);
-        if (block < 1)
-            fail(DFA2C_SHAPE, "block_size must be >= 1");
-        validate_plan(dims, kinds, windows);
-        const int64_t H = dims->n_heads;
-        if (cache) {
-            if (cache->H != H || cache->n != seq_len(dims) || cache->d != dims->head_dim || cache->batch != batch)
-                fail(DFA2C_SHAPE, "cache geometry disagrees with dims/batch");
-            if (layer < 0)
-                fail(DFA2C_SHAPE, "layer index must be >= 0");
-        }
-        for (int64_t h = 0; h < H; ++h)
-            if (kinds[h] == DFA2C_CACHED && (!cache || !cache->has(layer, h)))
-                fail(DFA2C_CACHE_MISS, "plan marks head " + std::to_string(h) + " Cached before it ever computed");
+        validate_forward(batch, dims, block, kinds, windows, cache, layer);
         ForwardSpec s{};
         s.q = q;
         s.k = k;
@@ -840,10 +956,107 @@ int dfa2c_mha_forward(const void* q, const void* k, const void* v, int64_t batch
         s.layer = layer;
         plan_jobs(dims, block, kinds, windows, cache != nullptr, s);
         run_forward(s, as_stream(stream));
-        if (cache)  // phase 2: computed heads now hold output produced at t
+        commit_produced(dims, kinds, cache, layer, t);
+    });
+}
+
+int dfa2c_mha_forward_host(const void* q, const void* k, const void* v, int64_t batch, const dfa2c_dims* dims,
+                           int64_t block, const int32_t* kinds, const int64_t* windows, dfa2c_cache* cache,
+                           int64_t layer, int64_t t, void* out, void* stream) {
+    return guard([&] {
+        validate_forward(batch, dims, block, kinds, windows, cache, layer);
+        if (!q || !k || !v || !out)
+            fail(DFA2C_SHAPE, "q, k, v and out must not be NULL");
+        const int64_t H = dims->n_heads, n = seq_len(dims), d = dims->head_dim;
+        const size_t head_bytes = static_cast<size_t>(n * d) * 2;
+        const size_t row_pitch = static_cast<size_t>(H) * head_bytes;  // one sample
+        const size_t bytes = static_cast<size_t>(batch) * row_pitch;
+        int device = 0;
+        DFA2C_CUDA_CHECK(cudaGetDevice(&device));
+        const cudaStream_t user = as_stream(stream);
+
+        // Computed heads in index order, split into up to kGroups groups of
+        // near-equal head count; each group is copied in as maximal runs of
+        // consecutive heads (one 2-D copy per run and tensor: width = run
+        // bytes, height = batch, pitch = one sample).
+        constexpr int kGroups = 6;
+        static_assert(kGroups <= HostPipe::kMaxGroups, "event slots");
+        std::vector<int64_t> computed;
+        for (int64_t h = 0; h < H; ++h)
+            if (kinds[h] != DFA2C_CACHED)
+                computed.push_back(h);
+        const int G = static_cast<int>(std::min<size_t>(kGroups, computed.size()));
+
+        HostPipe& hp = host_pipe(device);
+        std::lock_guard<std::mutex> lk(hp.mu);
+        HostPipe::Slot& ws = hp.next(bytes);
+        // Uploads wait only for this staging slot to be free (its use two
+        // calls ago), so they overlap the previous call's download tail; the
+        // download stream (which reads cache slots written by earlier work on
+        // `stream`) and every launch stay ordered after `stream`.
+        DFA2C_CUDA_CHECK(cudaEventRecord(ws.ev_start, user));
+        DFA2C_CUDA_CHECK(cudaStreamWaitEvent(hp.h2d, ws.ev_free, 0));
+        DFA2C_CUDA_CHECK(cudaStreamWaitEvent(hp.d2h, ws.ev_start, 0));
+        DFA2C_CUDA_CHECK(cudaStreamWaitEvent(hp.d2h, ws.ev_free, 0));
+        auto copy_runs = [&](const std::vector<int64_t>& heads, const void* src, void* dst, cudaMemcpyKind kind,
+                             cudaStream_t st) {
+            for (size_t i = 0; i < heads.size();) {
+                size_t j = i + 1;
+                while (j < heads.size() && heads[j] == heads[j - 1] + 1)
+                    ++j;
+                const size_t off = static_cast<size_t>(heads[i]) * head_bytes;
+                DFA2C_CUDA_CHECK(cudaMemcpy2DAsync(static_cast<char*>(dst) + off, row_pitch,
+                                                   static_cast<const char*>(src) + off, row_pitch,
+                                                   (j - i) * head_bytes, static_cast<size_t>(batch), kind, st));
+                i = j;
+            }
+        };
+        // Cached heads: their output IS the pre-call slot; it goes straight
+        // from the cache to the host (no q/k/v upload, no kernel work).
+        std::vector<int64_t> cached;
+        for (int64_t h = 0; h < H; ++h)
+            if (kinds[h] == DFA2C_CACHED)
+                cached.push_back(h);
+        if (!cached.empty())
+            copy_runs(cached, cache->layer_ptr(layer), out, cudaMemcpyDeviceToHost, hp.d2h);
+
+        ForwardSpec base{};
+        base.q = ws.q;
+        base.k = ws.k;
+        base.v = ws.v;
+        base.out = ws.out;
+        base.batch = batch;
+        base.dims = dims;
+        base.block = block;
+        base.cache = cache;
+        base.layer = layer;
+        plan_jobs(dims, block, kinds, windows, cache != nullptr, base);
+        for (int g = 0; g < G; ++g) {
+            const size_t lo = computed.size() * g / G, hi = computed.size() * (g + 1) / G;
+            const std::vector<int64_t> heads(computed.begin() + lo, computed.begin() + hi);
+            copy_runs(heads, q, ws.q, cudaMemcpyHostToDevice, hp.h2d);
+            copy_runs(heads, k, ws.k, cudaMemcpyHostToDevice, hp.h2d);
+            copy_runs(heads, v, ws.v, cudaMemcpyHostToDevice, hp.h2d);
+            DFA2C_CUDA_CHECK(cudaEventRecord(ws.ev_in[g], hp.h2d));
+            DFA2C_CUDA_CHECK(cudaStreamWaitEvent(user, ws.ev_in[g], 0));
+            ForwardSpec s = base;
+            std::vector<bool> in_group(static_cast<size_t>(H), false);
+            for (int64_t h : heads)
+                in_group[h] = true;
             for (int64_t h = 0; h < H; ++h)
-                if (kinds[h] != DFA2C_CACHED)
-                    cache->produced[static_cast<size_t>(layer * H + h)] = t;
+                if (!in_group[h])
+                    s.jobs[h].mask_id = JOB_SKIP;
+            run_forward(s, user);
+            DFA2C_CUDA_CHECK(cudaEventRecord(ws.ev_out[g], user));
+            DFA2C_CUDA_CHECK(cudaStreamWaitEvent(hp.d2h, ws.ev_out[g], 0));
+            copy_runs(heads, ws.out, out, cudaMemcpyDeviceToHost, hp.d2h);
+        }
+        // the call completes on the caller's stream: host `out` is final once
+        // `stream` reaches this point
+        DFA2C_CUDA_CHECK(cudaEventRecord(ws.ev_done, hp.d2h));
+        DFA2C_CUDA_CHECK(cudaStreamWaitEvent(user, ws.ev_done, 0));
+        DFA2C_CUDA_CHECK(cudaEventRecord(ws.ev_free, user));
+        commit_produced(dims, kinds, cache, layer, t);
     });
 }
 
@@ -909,11 +1122,12 @@ int dfa2c_rse_async(const void* y_m, const void* y_o, int32_t dtype, int64_t n_h
         const cudaStream_t st = as_stream(stream);
         int device = 0;
         DFA2C_CUDA_CHECK(cudaGetDevice(&device));
-        const int64_t target = std::max<int64_t>(1, 4 * num_sms(device) / n_heads);
+        // one wave: nblk CTAs per head so that nblk * H fills the resident
+        // slots (rse_ctas_per_sm per SM), each CTA streaming >= 8 K elements
+        const int64_t target = std::max<int64_t>(1, dfa2k::rse_ctas_per_sm() * num_sms(device) / n_heads);
         const int nblk = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(target, ceil_div(numel, 8192))));
         double* scratch = nullptr;
-        DFA2C_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&scratch),
-                                         static_cast<size_t>(n_heads * nblk * 5) * sizeof(double), st));
+        scratch_alloc(&scratch, static_cast<size_t>(n_heads * nblk * 5) * sizeof(double), st);
         DFA2C_CUDA_CHECK(dfa2k::launch_rse(y_m, y_o, dtype, n_heads, numel, mode, out_dev, scratch, nblk, st));
         g_launches.fetch_add(2);
         DFA2C_CUDA_CHECK(cudaFreeAsync(scratch, st));
@@ -927,7 +1141,7 @@ int dfa2c_rse(const void* y_m, const void* y_o, int32_t dtype, int64_t n_heads, 
             fail(DFA2C_SHAPE, "rse output must not be NULL");
         const cudaStream_t st = as_stream(stream);
         double* dev = nullptr;
-        DFA2C_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&dev), static_cast<size_t>(n_heads) * sizeof(double), st));
+        scratch_alloc(&dev, static_cast<size_t>(n_heads) * sizeof(double), st);
         const int rc = dfa2c_rse_async(y_m, y_o, dtype, n_heads, numel, mode, dev, stream);
         if (rc != DFA2C_OK) {
             cudaFreeAsync(dev, st);
@@ -972,15 +1186,14 @@ int dfa2c_influence_for_layer(const void* q, const void* k, const void* v, const
         void* orig = original;
         void* scratch_orig = nullptr;
         if (!orig) {
-            DFA2C_CUDA_CHECK(cudaMallocAsync(&scratch_orig, layer_bytes, st));
+            scratch_alloc(&scratch_orig, layer_bytes, st);
             orig = scratch_orig;
         }
         void* scratch_cand = nullptr;
         if (!method_outputs)
-            DFA2C_CUDA_CHECK(cudaMallocAsync(&scratch_cand, layer_bytes, st));
+            scratch_alloc(&scratch_cand, layer_bytes, st);
         double* rse_dev = nullptr;
-        DFA2C_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&rse_dev),
-                                         static_cast<size_t>(M * H) * sizeof(double), st));
+        scratch_alloc(&rse_dev, static_cast<size_t>(M * H) * sizeof(double), st);
         std::vector<uint8_t> eligible(static_cast<size_t>(M * H), 0);
 
         // 1 original evaluation: all heads Full (src/calibrate.cpp:206).
@@ -1008,24 +1221,25 @@ int dfa2c_influence_for_layer(const void* q, const void* k, const void* v, const
                     fail(rc, g_err);
                 for (int64_t h = 0; h < H; ++h)
                     eligible[m * H + h] = 1;
-            } else if (t > 0 && cache) {
-                // Cached: slot vs original for heads with a slot (src/calibrate.cpp:222-235).
-                if (method_outputs)
+            } else if (t > 0 && cache && layer >= 0 && layer < cache->L && cache->layer_buf[layer]) {
+                // Cached: slot vs original for heads with a slot (src/calibrate.cpp:222-235),
+                // one RSE launch over the layer's contiguous [H, N, d] slot array; heads
+                // without a slot stay ineligible (+inf).
+                const void* slots = cache->layer_buf[layer];
+                if (method_outputs) {
                     DFA2C_CUDA_CHECK(cudaMemsetAsync(cand, 0, layer_bytes, st));
-                for (int64_t h = 0; h < H; ++h) {
-                    if (layer < 0 || layer >= cache->L || !cache->has(layer, h))
-                        continue;
-                    const char* slot = static_cast<const char*>(cache->layer_buf[layer]) + h * head_elems * 2;
-                    if (method_outputs)
-                        DFA2C_CUDA_CHECK(cudaMemcpyAsync(static_cast<char*>(cand) + h * head_elems * 2, slot,
-                                                         head_elems * 2, cudaMemcpyDeviceToDevice, st));
-                    const int rc = dfa2c_rse_async(slot, static_cast<const char*>(orig) + h * head_elems * 2,
-                                                   DFA2C_BF16, 1, static_cast<int64_t>(head_elems), mode,
-                                                   rse_dev + m * H + h, stream);
-                    if (rc != DFA2C_OK)
-                        fail(rc, g_err);
-                    eligible[m * H + h] = 1;
+                    for (int64_t h = 0; h < H; ++h)
+                        if (cache->has(layer, h))
+                            DFA2C_CUDA_CHECK(cudaMemcpyAsync(static_cast<char*>(cand) + h * head_elems * 2,
+                                                             static_cast<const char*>(slots) + h * head_elems * 2,
+                                                             head_elems * 2, cudaMemcpyDeviceToDevice, st));
                 }
+                const int rc = dfa2c_rse_async(slots, orig, DFA2C_BF16, H, static_cast<int64_t>(head_elems), mode,
+                                               rse_dev + m * H, stream);
+                if (rc != DFA2C_OK)
+                    fail(rc, g_err);
+                for (int64_t h = 0; h < H; ++h)
+                    eligible[m * H + h] = cache->has(layer, h) ? 1 : 0;
             }
         }
         std::vector<double> host(static_cast<size_t>(M * H));

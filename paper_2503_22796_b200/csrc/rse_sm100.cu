@@ -3,20 +3,26 @@
 // Replaces rse()/mean_of/sum_sq_dev/sum_sq_diff
 // (/root/reference/proj/src/calibrate.cpp:18-87), which makes three
 // sequential double passes over two [N, d] f32 tensors per (head, method),
-// with ONE coalesced, 16-byte-vectorised pass per head:
+// with ONE streaming pass per head. Each CTA owns a contiguous chunk of one
+// head; a producer warp moves it through a 4-stage shared-memory ring with
+// 1-D bulk copies (cp.async.bulk, 8 KB per operand per stage, mbarrier
+// completion), so HBM reads stay in flight while 8 consumer warps convert
+// and accumulate from shared memory:
 //   K     = y_o[0]                       (shift for a cancellation-safe variance)
 //   so1   = sum(y_o - K)     so2 = sum((y_o - K)^2)
 //   sd2   = sum((y_m - y_o)^2)                      (standard numerator)
 //   sm1   = sum(y_m - K)     sm2 = sum((y_m - K)^2) (literal numerator)
 // all in fp64. Partials per CTA are written to a scratch array and a second
-// tiny kernel folds them in a fixed order, so results are bitwise
-// reproducible run to run (no atomics on values).
+// tiny kernel (one warp per head) folds them in a fixed order, so results
+// are bitwise reproducible run to run (no atomics on values).
 //   mean = K + so1/n,  den = so2 - so1^2/n
 //   standard: num = sd2;  literal: num = sm2 - 2 (mean-K) sm1 + n (mean-K)^2
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
+
+#include "sm100_ptx.cuh"
 
 namespace dfa2k {
 
@@ -30,8 +36,7 @@ struct Vec;
 template <>
 struct Vec<__nv_bfloat16> {
     static constexpr int W = 8;  // elements per 16-byte load
-    __device__ static void load(const __nv_bfloat16* p, double (&x)[8]) {
-        const uint4 u = __ldg(reinterpret_cast<const uint4*>(p));
+    __device__ static void unpack(const uint4& u, double (&x)[8]) {
         const uint32_t w[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
@@ -44,8 +49,9 @@ struct Vec<__nv_bfloat16> {
 template <>
 struct Vec<float> {
     static constexpr int W = 4;
-    __device__ static void load(const float* p, double (&x)[4]) {
-        const float4 u = __ldg(reinterpret_cast<const float4*>(p));
+    __device__ static void unpack(const uint4& r, double (&x)[4]) {
+        const float4 u = make_float4(__uint_as_float(r.x), __uint_as_float(r.y), __uint_as_float(r.z),
+                                     __uint_as_float(r.w));
         x[0] = u.x;
         x[1] = u.y;
         x[2] = u.z;
@@ -57,71 +63,125 @@ struct Vec<float> {
 template <>
 struct Vec<double> {
     static constexpr int W = 2;
-    __device__ static void load(const double* p, double (&x)[2]) {
-        const double2 u = __ldg(reinterpret_cast<const double2*>(p));
-        x[0] = u.x;
-        x[1] = u.y;
+    __device__ static void unpack(const uint4& r, double (&x)[2]) {
+        x[0] = __hiloint2double(static_cast<int>(r.y), static_cast<int>(r.x));
+        x[1] = __hiloint2double(static_cast<int>(r.w), static_cast<int>(r.z));
     }
     __device__ static double one(const double* p) { return *p; }
 };
 
+template <bool LIT>
 __device__ __forceinline__ void accum(double m, double o, double K, double (&a)[NACC]) {
     const double dO = o - K;
-    const double dM = m - K;
     const double dd = m - o;
     a[0] += dO;
     a[1] = fma(dO, dO, a[1]);
     a[2] = fma(dd, dd, a[2]);
-    a[3] += dM;
-    a[4] = fma(dM, dM, a[4]);
+    if (LIT) {  // literal numerator only: sum(y_m - K), sum((y_m - K)^2)
+        const double dM = m - K;
+        a[3] += dM;
+        a[4] = fma(dM, dM, a[4]);
+    }
 }
+
+constexpr int RSE_STAGES = 4;
+constexpr uint32_t RSE_STAGE_BYTES = 8192;  // per operand per stage
+constexpr uint32_t RSE_BAR_OFF = RSE_STAGES * 2 * RSE_STAGE_BYTES;
+constexpr uint32_t RSE_SMEM = RSE_BAR_OFF + 2 * RSE_STAGES * 8;
 
 }  // namespace
 
-// grid (nblk, H). Each CTA reduces one contiguous, vector-aligned chunk of one
-// head and writes NACC partials to part[(h * nblk + b) * NACC].
-template <typename T>
-__global__ void __launch_bounds__(RSE_THREADS) rse_partial(const T* __restrict__ ym,
-                                                           const T* __restrict__ yo, int64_t numel,
-                                                           int64_t chunk, int vec_ok,
-                                                           double* __restrict__ part) {
+// grid (nblk, H), RSE_THREADS consumer threads + 1 producer warp. CTA (b, h)
+// reduces elements [b*chunk, min((b+1)*chunk, numel)) of head h and writes
+// NACC partials to part[(h * nblk + b) * NACC]. vec_ok (host-checked): both
+// bases 16-byte aligned, numel % W == 0 and chunk % W == 0; otherwise the
+// whole chunk takes the scalar path. The order every value is folded in is
+// fixed by (stage, thread, vector), so results are run-to-run bitwise stable.
+template <typename T, bool LIT>
+__global__ void __launch_bounds__(RSE_THREADS + 32) rse_partial(const T* __restrict__ ym,
+                                                                const T* __restrict__ yo, int64_t numel,
+                                                                int64_t chunk, int vec_ok,
+                                                                double* __restrict__ part) {
     constexpr int W = Vec<T>::W;
+    constexpr int64_t EPS = RSE_STAGE_BYTES / sizeof(T);  // elements per stage
+    extern __shared__ __align__(128) uint8_t smem[];
+    const uint32_t sbase = smem_u32(smem);
+    const uint32_t full0 = sbase + RSE_BAR_OFF, empty0 = full0 + 8 * RSE_STAGES;
     const int h = blockIdx.y;
     const int b = blockIdx.x;
     const T* m = ym + static_cast<int64_t>(h) * numel;
     const T* o = yo + static_cast<int64_t>(h) * numel;
-    const double K = Vec<T>::one(o);
-    const int64_t lo = static_cast<int64_t>(b) * chunk;
+    const int64_t lo = min(static_cast<int64_t>(b) * chunk, numel);
     const int64_t hi = min(lo + chunk, numel);
-    double a[NACC] = {0, 0, 0, 0, 0};
-    // vec_ok (host-checked): 16-byte aligned bases and numel % W == 0; chunk is
-    // a multiple of W. Otherwise scalar loads.
-    if (vec_ok) {
-        for (int64_t i = lo + static_cast<int64_t>(threadIdx.x) * W; i + W <= hi; i += RSE_THREADS * W) {
-            double xm[W], xo[W];
-            Vec<T>::load(m + i, xm);
-            Vec<T>::load(o + i, xo);
-#pragma unroll
-            for (int e = 0; e < W; ++e)
-                accum(xm[e], xo[e], K, a);
-        }
-    } else {
-        for (int64_t i = lo + threadIdx.x; i < hi; i += RSE_THREADS)
-            accum(Vec<T>::one(m + i), Vec<T>::one(o + i), K, a);
-    }
-    // fixed-pattern warp tree, then warps in index order
-#pragma unroll
-    for (int k = 0; k < NACC; ++k)
-        for (int off = 16; off > 0; off >>= 1)
-            a[k] += __shfl_xor_sync(0xFFFFFFFFu, a[k], off);
-    __shared__ double red[RSE_THREADS / 32][NACC];
+    const int64_t n_vec = vec_ok ? (hi - lo) / W * W : 0;  // staged through smem
+    const int n_stage = static_cast<int>((n_vec + EPS - 1) / EPS);
     const int warp = threadIdx.x >> 5;
-    if ((threadIdx.x & 31) == 0)
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < RSE_STAGES; ++s) {
+            mbar_init(full0 + 8 * s, 1);
+            mbar_init(empty0 + 8 * s, RSE_THREADS / 32);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    double a[NACC] = {0, 0, 0, 0, 0};
+    if (warp == RSE_THREADS / 32) {
+        // ---- producer: one elected lane streams the chunk through the ring
+        if (elect_one()) {
+            for (int s = 0; s < n_stage; ++s) {
+                const int slot = s % RSE_STAGES;
+                if (s >= RSE_STAGES)
+                    mbar_wait(empty0 + 8 * slot, ((s / RSE_STAGES) - 1) & 1);
+                const int64_t e0 = lo + s * EPS;
+                const uint32_t bytes = static_cast<uint32_t>(min(EPS, lo + n_vec - e0) * sizeof(T));
+                const uint32_t dst = sbase + slot * 2 * RSE_STAGE_BYTES;
+                mbar_arrive_expect_tx(full0 + 8 * slot, 2 * bytes);
+                bulk_load_1d(dst, m + e0, bytes, full0 + 8 * slot);
+                bulk_load_1d(dst + RSE_STAGE_BYTES, o + e0, bytes, full0 + 8 * slot);
+            }
+        }
+        __syncwarp();
+    } else {
+        const double K = Vec<T>::one(o);
+        // ---- consumers: W-element vectors, thread-strided within a stage
+        for (int s = 0; s < n_stage; ++s) {
+            const int slot = s % RSE_STAGES;
+            mbar_wait(full0 + 8 * slot, (s / RSE_STAGES) & 1);
+            const int64_t e_stage = min(EPS, n_vec - s * EPS);
+            const uint32_t sm_m = sbase + slot * 2 * RSE_STAGE_BYTES;
+            const uint32_t sm_o = sm_m + RSE_STAGE_BYTES;
+#pragma unroll 2
+            for (int64_t e = static_cast<int64_t>(threadIdx.x) * W; e < e_stage; e += RSE_THREADS * W) {
+                const uint32_t off = static_cast<uint32_t>(e * sizeof(T));
+                double xm[W], xo[W];
+                Vec<T>::unpack(ld_shared_v4(sm_m + off), xm);
+                Vec<T>::unpack(ld_shared_v4(sm_o + off), xo);
+#pragma unroll
+                for (int k = 0; k < W; ++k)
+                    accum<LIT>(xm[k], xo[k], K, a);
+            }
+            __syncwarp();
+            if ((threadIdx.x & 31) == 0)
+                mbar_arrive(empty0 + 8 * slot);
+        }
+        // elements the ring does not cover (unaligned operands, sub-vector tail)
+        for (int64_t i = lo + n_vec + threadIdx.x; i < hi; i += RSE_THREADS)
+            accum<LIT>(Vec<T>::one(m + i), Vec<T>::one(o + i), K, a);
+        // fixed-pattern warp tree
+#pragma unroll
+        for (int k = 0; k < NACC; ++k)
+            for (int off = 16; off > 0; off >>= 1)
+                a[k] += __shfl_xor_sync(0xFFFFFFFFu, a[k], off);
+    }
+    __shared__ double red[RSE_THREADS / 32][NACC];
+    if (warp < RSE_THREADS / 32 && (threadIdx.x & 31) == 0)
 #pragma unroll
         for (int k = 0; k < NACC; ++k)
             red[warp][k] = a[k];
     __syncthreads();
-    if (threadIdx.x < NACC) {
+    if (threadIdx.x < NACC) {  // consumer warps in index order
         double t = 0.0;
         for (int w = 0; w < RSE_THREADS / 32; ++w)
             t += red[w][threadIdx.x];
@@ -129,18 +189,26 @@ __global__ void __launch_bounds__(RSE_THREADS) rse_partial(const T* __restrict__
     }
 }
 
-// One thread per head: fold partials in CTA order, finish the RSE.
+// One warp per head: lane j folds partials j, j+32, ... in order, then a
+// fixed xor tree; lane 0 finishes the RSE.
 template <typename T>
 __global__ void rse_finalize(const T* __restrict__ yo, const double* __restrict__ part, int nblk,
                              int n_heads, int64_t numel, int mode, double* __restrict__ out) {
-    const int h = blockIdx.x * blockDim.x + threadIdx.x;
+    const int h = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
     if (h >= n_heads)
         return;
     double a[NACC] = {0, 0, 0, 0, 0};
-    for (int b = 0; b < nblk; ++b)
+    for (int b = lane; b < nblk; b += 32)
 #pragma unroll
         for (int k = 0; k < NACC; ++k)
             a[k] += part[(static_cast<int64_t>(h) * nblk + b) * NACC + k];
+#pragma unroll
+    for (int k = 0; k < NACC; ++k)
+        for (int off = 16; off > 0; off >>= 1)
+            a[k] += __shfl_xor_sync(0xFFFFFFFFu, a[k], off);
+    if (lane != 0)
+        return;
     const double K = Vec<T>::one(yo + static_cast<int64_t>(h) * numel);
     const double n = static_cast<double>(numel);
     const double dmean = a[0] / n;  // mean - K
@@ -153,32 +221,52 @@ __global__ void rse_finalize(const T* __restrict__ yo, const double* __restrict_
     out[h] = den > 0.0 ? num / den : __longlong_as_double(0x7FF8000000000000ll);
 }
 
+namespace {
+template <typename T, bool LIT>
+void launch_partial(const dim3& grid, const T* m, const T* o, int64_t numel, int64_t chunk, int vec_ok,
+                    double* scratch, cudaStream_t stream) {
+    static uint64_t configured = 0;  // bit per device the smem attribute was set on
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev >= 64 || !((configured >> dev) & 1u)) {
+        cudaFuncSetAttribute(rse_partial<T, LIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, RSE_SMEM);
+        if (dev < 64)
+            configured |= uint64_t{1} << dev;
+    }
+    rse_partial<T, LIT><<<grid, RSE_THREADS + 32, RSE_SMEM, stream>>>(m, o, numel, chunk, vec_ok, scratch);
+}
+
+template <typename T>
+void launch_typed(const void* ym, const void* yo, int64_t n_heads, int64_t numel, int mode, double* out_dev,
+                  double* scratch, int nblk, int64_t chunk, int vec_ok, cudaStream_t stream) {
+    const dim3 grid(nblk, static_cast<unsigned>(n_heads));
+    const T* m = static_cast<const T*>(ym);
+    const T* o = static_cast<const T*>(yo);
+    if (mode == 0)
+        launch_partial<T, false>(grid, m, o, numel, chunk, vec_ok, scratch, stream);
+    else
+        launch_partial<T, true>(grid, m, o, numel, chunk, vec_ok, scratch, stream);
+    const int fin_blocks = static_cast<int>((n_heads + 7) / 8);
+    rse_finalize<T><<<fin_blocks, 256, 0, stream>>>(o, scratch, nblk, static_cast<int>(n_heads), numel, mode,
+                                                   out_dev);
+}
+}  // namespace
+
+int rse_ctas_per_sm() { return 3; }  // 3 x (64 KB ring + bars) per SM
+
 cudaError_t launch_rse(const void* ym, const void* yo, int dtype, int64_t n_heads, int64_t numel,
                        int mode, double* out_dev, double* scratch, int nblk, cudaStream_t stream) {
     const int64_t W = dtype == 0 ? 8 : dtype == 1 ? 4 : 2;
     int64_t chunk = (numel + nblk - 1) / nblk;
     chunk = (chunk + W - 1) / W * W;
-    const dim3 grid(nblk, static_cast<unsigned>(n_heads));
     const int vec_ok = (numel % W) == 0 && (reinterpret_cast<uintptr_t>(ym) % 16) == 0 &&
                        (reinterpret_cast<uintptr_t>(yo) % 16) == 0;
-    const int fin_blocks = static_cast<int>((n_heads + 127) / 128);
-    if (dtype == 0) {
-        rse_partial<__nv_bfloat16><<<grid, RSE_THREADS, 0, stream>>>(
-            static_cast<const __nv_bfloat16*>(ym), static_cast<const __nv_bfloat16*>(yo), numel, chunk, vec_ok, scratch);
-        rse_finalize<__nv_bfloat16><<<fin_blocks, 128, 0, stream>>>(
-            static_cast<const __nv_bfloat16*>(yo), scratch, nblk, static_cast<int>(n_heads), numel, mode, out_dev);
-    } else if (dtype == 2) {
-        rse_partial<double><<<grid, RSE_THREADS, 0, stream>>>(static_cast<const double*>(ym),
-                                                              static_cast<const double*>(yo), numel, chunk, vec_ok,
-                                                              scratch);
-        rse_finalize<double><<<fin_blocks, 128, 0, stream>>>(static_cast<const double*>(yo), scratch, nblk,
-                                                             static_cast<int>(n_heads), numel, mode, out_dev);
-    } else {
-        rse_partial<float><<<grid, RSE_THREADS, 0, stream>>>(static_cast<const float*>(ym),
-                                                             static_cast<const float*>(yo), numel, chunk, vec_ok, scratch);
-        rse_finalize<float><<<fin_blocks, 128, 0, stream>>>(static_cast<const float*>(yo), scratch, nblk,
-                                                            static_cast<int>(n_heads), numel, mode, out_dev);
-    }
+    if (dtype == 0)
+        launch_typed<__nv_bfloat16>(ym, yo, n_heads, numel, mode, out_dev, scratch, nblk, chunk, vec_ok, stream);
+    else if (dtype == 2)
+        launch_typed<double>(ym, yo, n_heads, numel, mode, out_dev, scratch, nblk, chunk, vec_ok, stream);
+    else
+        launch_typed<float>(ym, yo, n_heads, numel, mode, out_dev, scratch, nblk, chunk, vec_ok, stream);
     return cudaGetLastError();
 }
 

@@ -124,6 +124,35 @@ def test_cached_heads_and_cache_commit_semantics():
     assert cache.size() == 4
 
 
+@pytest.mark.parametrize("d,pinned", [(64, True), (128, True), (64, False)])
+def test_host_buffer_path_matches_device_path(d, pinned):
+    """dfa2c_mha_forward_host (head-group upload / compute / download
+    pipeline, cached heads straight from their slots) is bitwise the device
+    path: outputs, cache slots and produced_at, over two timesteps."""
+    t = torch()
+    Bt, H, nv, nt, B = 2, 7, 1024, 77, 128
+    n = nv + nt
+    dims = AttentionDims(H, d, nv, nt)
+    dev_cache, host_cache = HeadCache(1, H, n, d, batch=Bt), HeadCache(1, H, n, d, batch=Bt)
+    for step, plan in enumerate((LayerPlan.all_full(H), LayerPlan.parse("F C A0 A2 C C F"))):
+        q, _ = bf16_inputs((Bt, H, n, d), 300 + 3 * step)
+        k, _ = bf16_inputs((Bt, H, n, d), 301 + 3 * step)
+        v, _ = bf16_inputs((Bt, H, n, d), 302 + 3 * step)
+        od = api.multi_strategy_attention(q, k, v, plan, dev_cache, 0, step, dims, B)
+        hq, hk, hv = (x.cpu() for x in (q, k, v))
+        if pinned:
+            hq, hk, hv = hq.pin_memory(), hk.pin_memory(), hv.pin_memory()
+        oh = api.multi_strategy_attention_host(hq, hk, hv, plan, host_cache, 0, step, dims, B)
+        t.cuda.synchronize()
+        assert not oh.is_cuda and t.equal(oh.cuda(), od)
+        for h in range(H):
+            assert host_cache.produced_at(0, h) == dev_cache.produced_at(0, h)
+            assert t.equal(host_cache.fetch(0, h), dev_cache.fetch(0, h))
+    with pytest.raises(CacheMissError):  # validation before any transfer
+        api.multi_strategy_attention_host(hq, hk, hv, LayerPlan.parse("C F F F F F F"), HeadCache(1, H, n, d, batch=Bt),
+                                          0, 1, dims, B)
+
+
 def test_cache_miss_is_raised_before_any_compute():
     t = torch()
     H, n, d = 3, 300, 64
