@@ -195,6 +195,35 @@ int dfa2c_influence_for_layer(const void* q, const void* k, const void* v,
                               void* original, void* method_outputs, int64_t* evals,
                               void* stream);
 
+/* ---- plan files (JSON version 1) ---------------------------------------
+ * The reference's plan file format (inc/plan.hpp:44-52; src/plan.cpp:109-228):
+ * {version, dims:{T,L,H,d,n_visual,n_text,block}, delta, coeff, window_set,
+ *  plan:[{t, layer, heads:[{kind, window_blocks?}]}], influence_digest},
+ * written with the same text layout as the reference (sorted keys, 2-space
+ * indent, trailing newline). Plans are flat timestep-major arrays
+ * kinds/windows[(t*L + l)*H + h] (CompressionPlan::at, src/plan.cpp:25-31). */
+typedef struct {
+    int64_t n_timesteps, n_layers, n_heads, head_dim, n_visual, n_text, block_size;
+    double delta, coeff;
+    int64_t n_window_set; /* entries of window_set */
+    int64_t digest_len;   /* influence_digest bytes (excl. NUL); set by from_json */
+} dfa2c_plan_header;
+/* plan_to_json: buf may be NULL to query *len (bytes, excl. NUL); otherwise
+ * cap must be >= *len + 1. No validation (as in the reference). */
+int dfa2c_plan_to_json(const dfa2c_plan_header* hdr, const int32_t* kinds, const int64_t* windows,
+                       const int64_t* window_set, const char* influence_digest, char* buf,
+                       int64_t cap, int64_t* len);
+/* plan_from_json: parses and validates (CompressionPlan::validate);
+ * malformed text and schema violations -> DFA2C_PLAN. text_len < 0 means
+ * NUL-terminated. Call with kinds == NULL to learn the header (sizes), then
+ * with kinds/windows [T*L*H], window_set [n_window_set] and digest
+ * [digest_len + 1]. */
+int dfa2c_plan_from_json(const char* text, int64_t text_len, dfa2c_plan_header* hdr,
+                         int32_t* kinds, int64_t* windows, int64_t* window_set, char* digest,
+                         int64_t digest_cap);
+/* fnv1a_hex (inc/plan.hpp:57-58): FNV-1a 64 of n bytes as 16 hex chars + NUL. */
+int dfa2c_fnv1a_hex(const void* bytes, int64_t n, char* out);
+
 /* Kernel launches issued by this library since load (evidence counter). */
 int64_t dfa2c_launch_count(void);
 /* Debug: device buffer (int64 [2][4096][8]) receiving per-tile clock64 stamps

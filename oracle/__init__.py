@@ -30,6 +30,14 @@ def build(ref: bool = True) -> None:
         subprocess.run(["make", "-s", "-C", HERE, "-j8", "ref"], check=True)
 
 
+def build_reftests() -> None:
+    """Compiles the reference's own unit suites against the drop-in headers
+    and the built libdfa2_b200.so (oracle/_ref/tests/; needs /root/reference
+    and the product library)."""
+    if os.path.isdir(REF_SRC):
+        subprocess.run(["make", "-s", "-C", HERE, "-j8", "reftests"], check=True)
+
+
 _P = lambda t: POINTER(t)  # noqa: E731
 _orc = None
 _ref = None
@@ -99,6 +107,9 @@ def ref() -> ctypes.CDLL:
                                                    _P(c_int64), _P(c_int64), _P(c_double)],
             "ref_layer_sample": [_P(c_float)] * 5 + [c_int64] * 4 + [c_int, c_int64, _P(c_int32), _P(c_int64),
                                                                       _P(c_int64), c_int64],
+            "ref_plan_to_json": [c_int64] * 7 + [c_double, c_double, _P(c_int64), c_int64, _P(c_int32), _P(c_int64),
+                                                 c_char_p, c_char_p, c_int64, _P(c_int64)],
+            "ref_plan_from_json": [c_char_p, c_int64, _P(c_int32), _P(c_int64), _P(c_int64)],
         }
         for name, args in sig.items():
             fn = getattr(L, name)

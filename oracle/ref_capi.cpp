@@ -323,3 +323,44 @@ REF_API int ref_layer_sample(const float* q, const float* k, const float* v,
         }
     });
 }
+
+// plan_to_json (src/plan.cpp:109-143) of a plan given as flat timestep-major
+// arrays; *len receives the text size, buf (cap bytes) the NUL-terminated
+// text when large enough.
+REF_API int ref_plan_to_json(int64_t H, int64_t d, int64_t nv, int64_t nt, int64_t T, int64_t L,
+                             int64_t B, double delta, double coeff, const int64_t* window_set,
+                             int64_t n_ws, const int32_t* kinds, const int64_t* windows,
+                             const char* digest, char* buf, int64_t cap, int64_t* len) {
+    return guard([&] {
+        dfa2::CompressionPlan p = dfa2::CompressionPlan::all_full(make_dims(H, d, nv, nt, 0), T, L, B);
+        p.delta = delta;
+        p.coeff = coeff;
+        p.window_set.assign(window_set, window_set + n_ws);
+        for (int64_t i = 0; i < T * L; ++i)
+            p.layers[static_cast<size_t>(i)] = make_plan(H, kinds + i * H, windows + i * H);
+        p.influence_digest = digest ? digest : "";
+        const std::string s = dfa2::plan_to_json(p);
+        *len = static_cast<int64_t>(s.size());
+        if (buf && cap > *len)
+            std::memcpy(buf, s.c_str(), s.size() + 1);
+    });
+}
+
+// plan_from_json (src/plan.cpp:145-209) -> status (PLAN on any schema or
+// validation failure) and, on success, the flat kinds/windows arrays.
+REF_API int ref_plan_from_json(const char* text, int64_t cap_entries, int32_t* kinds, int64_t* windows,
+                               int64_t* n_entries) {
+    return guard([&] {
+        const dfa2::CompressionPlan p = dfa2::plan_from_json(text);
+        const int64_t H = p.dims.n_heads;
+        *n_entries = p.n_timesteps * p.n_layers * H;
+        if (*n_entries > cap_entries)
+            return;
+        for (int64_t i = 0; i < p.n_timesteps * p.n_layers; ++i)
+            for (int64_t h = 0; h < H; ++h) {
+                const dfa2::HeadStrategy& s = p.layers[static_cast<size_t>(i)].strategies[static_cast<size_t>(h)];
+                kinds[i * H + h] = static_cast<int32_t>(s.kind);
+                windows[i * H + h] = s.window_blocks;
+            }
+    });
+}

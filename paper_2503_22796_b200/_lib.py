@@ -85,6 +85,13 @@ class Dims(ctypes.Structure):
 
 
 # name -> (restype, argtypes)
+class PlanHeader(ctypes.Structure):
+    """dfa2c_plan_header."""
+    _fields_ = [("n_timesteps", c_int64), ("n_layers", c_int64), ("n_heads", c_int64), ("head_dim", c_int64),
+                ("n_visual", c_int64), ("n_text", c_int64), ("block_size", c_int64), ("delta", c_double),
+                ("coeff", c_double), ("n_window_set", c_int64), ("digest_len", c_int64)]
+
+
 _SIGS = {
     "dfa2c_last_error": (c_char_p, []),
     "dfa2c_version": (c_char_p, []),
@@ -124,6 +131,11 @@ _SIGS = {
                             c_void_p]),
     "dfa2c_rse_async": (c_int32, [c_void_p, c_void_p, c_int32, c_int64, c_int64, c_int32, c_void_p,
                                   c_void_p]),
+    "dfa2c_plan_to_json": (c_int32, [POINTER(PlanHeader), POINTER(c_int32), POINTER(c_int64), POINTER(c_int64),
+                                     c_char_p, c_char_p, c_int64, POINTER(c_int64)]),
+    "dfa2c_plan_from_json": (c_int32, [c_char_p, c_int64, POINTER(PlanHeader), POINTER(c_int32), POINTER(c_int64),
+                                       POINTER(c_int64), c_char_p, c_int64]),
+    "dfa2c_fnv1a_hex": (c_int32, [c_char_p, c_int64, c_char_p]),
     "dfa2c_influence_for_layer": (c_int32, [c_void_p, c_void_p, c_void_p, POINTER(Dims), c_int64,
                                             POINTER(c_int64), c_int64, c_int32, c_void_p, c_int64, c_int64,
                                             c_int32, POINTER(c_double), c_void_p, c_void_p, POINTER(c_int64),

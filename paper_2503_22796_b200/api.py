@@ -611,6 +611,7 @@ class CompressionPlan:
     coeff: float = 1.5
     window_set: List[int] = field(default_factory=list)
     layers: List[LayerPlan] = field(default_factory=list)
+    influence_digest: str = ""
 
     @staticmethod
     def all_full(dims: AttentionDims, timesteps: int, layers: int, block_size: int) -> "CompressionPlan":
@@ -657,6 +658,81 @@ class CompressionPlan:
 
     def aggregate_sparsity(self) -> float:
         return self._aggregate()[2]
+
+    # ---- plan file (JSON v1, inc/plan.hpp:44-52), via dfa2c_plan_to/from_json
+    def to_json(self) -> str:
+        """plan_to_json (src/plan.cpp:109-143): the reference's file text."""
+        H = self.dims.n_heads
+        kinds, wins = [], []
+        for lp in self.layers:
+            if lp.n_heads() != H:
+                raise ShapeError("head array length must equal H")
+            kinds += [_KIND_CODE[s_.kind] for s_ in lp.strategies]
+            wins += [s_.window_blocks for s_ in lp.strategies]
+        n = max(1, len(kinds))
+        k, w = (c_int32 * n)(*kinds), (c_int64 * n)(*wins)
+        ws = (c_int64 * max(1, len(self.window_set)))(*self.window_set)
+        hdr = _lib.PlanHeader(self.n_timesteps, self.n_layers, H, self.dims.head_dim, self.dims.n_visual,
+                              self.dims.n_text, self.block_size, self.delta, self.coeff, len(self.window_set), 0)
+        ln = c_int64()
+        dig = self.influence_digest.encode()
+        check(lib().dfa2c_plan_to_json(byref(hdr), k, w, ws, dig, None, 0, byref(ln)))
+        buf = ctypes.create_string_buffer(ln.value + 1)
+        check(lib().dfa2c_plan_to_json(byref(hdr), k, w, ws, dig, buf, ln.value + 1, byref(ln)))
+        return buf.raw[:ln.value].decode()
+
+    @staticmethod
+    def from_json(text: str) -> "CompressionPlan":
+        """plan_from_json (src/plan.cpp:145-209): parses and validates;
+        PlanValidationError on malformed text or schema violations."""
+        raw = text.encode()
+        hdr = _lib.PlanHeader()
+        check(lib().dfa2c_plan_from_json(raw, len(raw), byref(hdr), None, None, None, None, 0))
+        T, L, H = hdr.n_timesteps, hdr.n_layers, hdr.n_heads
+        k, w = (c_int32 * (T * L * H))(), (c_int64 * (T * L * H))()
+        ws = (c_int64 * max(1, hdr.n_window_set))()
+        dig = ctypes.create_string_buffer(hdr.digest_len + 1)
+        check(lib().dfa2c_plan_from_json(raw, len(raw), byref(hdr), k, w, ws, dig, hdr.digest_len + 1))
+        inv = {v: k_ for k_, v in _KIND_CODE.items()}
+        layers = [LayerPlan([HeadStrategy(inv[k[i * H + h]], w[i * H + h] if k[i * H + h] == 1 else 0)
+                             for h in range(H)]) for i in range(T * L)]
+        dims = AttentionDims(H, hdr.head_dim, hdr.n_visual, hdr.n_text)
+        return CompressionPlan(dims, T, L, hdr.block_size, hdr.delta, hdr.coeff, list(ws[:hdr.n_window_set]),
+                               layers, dig.raw[:hdr.digest_len].decode())
+
+    def save(self, path: str) -> None:
+        """save_plan (inc/plan.hpp:51)."""
+        try:
+            with open(path, "w") as f:
+                f.write(self.to_json())
+        except OSError as e:
+            raise IoError(f"cannot write {path}: {e}") from None
+
+    @staticmethod
+    def load(path: str) -> "CompressionPlan":
+        """load_plan (inc/plan.hpp:52)."""
+        try:
+            with open(path) as f:
+                text = f.read()
+        except OSError as e:
+            raise IoError(f"cannot open {path}: {e}") from None
+        return CompressionPlan.from_json(text)
+
+
+def plan_to_json(plan: CompressionPlan) -> str:
+    return plan.to_json()
+
+
+def plan_from_json(text: str) -> CompressionPlan:
+    return CompressionPlan.from_json(text)
+
+
+def fnv1a_hex(data) -> str:
+    """fnv1a_hex (inc/plan.hpp:57-58): FNV-1a 64 as 16 hex chars."""
+    raw = data.encode() if isinstance(data, str) else bytes(data)
+    out = ctypes.create_string_buffer(17)
+    check(lib().dfa2c_fnv1a_hex(raw, len(raw), out))
+    return out.value.decode()
 
 
 @dataclass

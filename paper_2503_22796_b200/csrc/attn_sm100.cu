@@ -59,10 +59,14 @@ struct Cfg {
     static constexpr int THREADS = 384;
 };
 
-// Every EMU_EVERY-th column of a 32-column chunk computes exp2 on the FMA
-// pipe instead of MUFU (0 disables).
-#ifndef DFA2_EMU_EVERY
-#define DFA2_EMU_EVERY 0
+// Every EMU-th column pair of a 32-column chunk computes exp2 on the FMA
+// pipe instead of MUFU (0 disables), per head dim: at d=64 the MMAs of a
+// tile take half as long as at d=128 while the exp count is the same.
+#ifndef DFA2_EMU_EVERY64
+#define DFA2_EMU_EVERY64 3
+#endif
+#ifndef DFA2_EMU_EVERY128
+#define DFA2_EMU_EVERY128 8
 #endif
 
 #ifndef DFA2_TRACE
@@ -153,6 +157,7 @@ __device__ __forceinline__ void mask_tile_in_tmem(uint32_t sc, const uint32_t (&
 template <int D>
 __device__ __forceinline__ void softmax_half(const uint32_t* s, float2 scale2, float2 neg_m, float2& sum,
                                              uint32_t dst) {
+    constexpr int EMU = D == 64 ? DFA2_EMU_EVERY64 : DFA2_EMU_EVERY128;
 #pragma unroll
     for (int cc = 0; cc < 2; ++cc) {
         uint32_t pk[16];
@@ -162,7 +167,7 @@ __device__ __forceinline__ void softmax_half(const uint32_t* s, float2 scale2, f
                 make_float2(__uint_as_float(s[32 * cc + 2 * i]), __uint_as_float(s[32 * cc + 2 * i + 1])), scale2,
                 neg_m);
             float2 p;
-            if (DFA2_EMU_EVERY > 0 && (i % (DFA2_EMU_EVERY > 0 ? DFA2_EMU_EVERY : 1)) == DFA2_EMU_EVERY - 1) {
+            if (EMU > 0 && (i % (EMU > 0 ? EMU : 1)) == EMU - 1) {
                 p = ex2_poly2(x);
             } else {
                 p = make_float2(ex2_approx(x.x), ex2_approx(x.y));
@@ -447,6 +452,7 @@ __global__ void __launch_bounds__(384, 1)
                                 mbar_wait(v_full(vst), (vcount / VS) & 1);
                                 v_ready = true;
                             }
+                            if (DFA2_TRACE == 1 && lane == 0) DFA2_STAMP(L, pcnt[L], 7);
                             // keys 64..127 (P in cols [64,96)) as soon as that half is ready,
                             // then keys 0..63 (cols [0,32))
                             const uint64_t vdesc = smem_desc_sw128(v_addr, C::BOX_BYTES, 1024);
@@ -478,6 +484,7 @@ __global__ void __launch_bounds__(384, 1)
                                 mbar_wait(k_full(kst), (kcount / KS) & 1);
                                 k_ready = true;
                             }
+                            if (DFA2_TRACE == 1 && lane == 0) DFA2_STAMP(L, scount[L], 6);
                             tc_fence_after();
                             const uint64_t qdesc = smem_desc_sw128(sbase + C::Q_OFF + L * C::TILE_BYTES, 16, 1024);
                             const uint64_t kdesc = smem_desc_sw128(k_addr, 16, 1024);

@@ -21,6 +21,7 @@
 #include <vector>
 
 #include "attn_types.h"
+#include "json_lite.h"
 
 namespace dfa2k {
 cudaError_t launch_attn(int d, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
@@ -521,12 +522,113 @@ struct ForwardSpec {
     std::string mask_key;                     // identifies the masks in the plan cache
     dfa2c_cache* cache;                       // slots read (copy) / written (commit)
     int64_t layer;
+    int64_t scale_d = 0;                      // head dim of the softmax scale (0: dims->head_dim)
 };
 
-void run_forward(const ForwardSpec& s, cudaStream_t stream) {
+// The kernel instantiations: D = 64 serves head dims 1..64, D = 128 serves 65..128.
+int kernel_dim(int64_t d) { return d <= 64 ? 64 : 128; }
+// TMA maps over the caller's own [.., d] layout need a 16-byte row pitch and
+// a full first 64-column box; other head dims run through zero-padded copies.
+bool direct_layout(int64_t d) { return d == 64 || (d % 8 == 0 && d >= 64 && d <= 128); }
+
+void launch_forward(const ForwardSpec& s, cudaStream_t stream);
+
+// Head dims without a direct TMA layout (d % 8 != 0 or d < 64): q/k/v are
+// copied into zero-padded [rows, D] scratch (zero columns change neither
+// Q K^T nor the first d columns of P V; the softmax scale keeps the true d),
+// the kernel runs with no cache binding, and the outputs, cache commits and
+// cached-head copies are done as strided copies on the same stream.
+void run_padded(const ForwardSpec& s, cudaStream_t st) {
     const int64_t n = seq_len(s.dims), d = s.dims->head_dim, H = s.dims->n_heads;
-    if (d != 64 && d != 128)
-        fail(DFA2C_UNSUPPORTED, "head_dim must be 64 or 128 on the sm_100a path (got " + std::to_string(d) + ")");
+    const int64_t D = kernel_dim(d);
+    if (s.batch < 1)
+        fail(DFA2C_SHAPE, "batch must be >= 1");
+    for (const void* x : {s.q, s.k, s.v, static_cast<const void*>(s.out)})
+        if (!x)
+            fail(DFA2C_SHAPE, "q, k, v and out must not be NULL");
+    const size_t rows = static_cast<size_t>(s.batch * H * n);
+    const size_t pbytes = rows * static_cast<size_t>(D) * 2;
+    void *qp = nullptr, *kp = nullptr, *vp = nullptr, *op = nullptr;
+    scratch_alloc(&qp, pbytes, st);
+    scratch_alloc(&kp, pbytes, st);
+    scratch_alloc(&vp, pbytes, st);
+    scratch_alloc(&op, pbytes, st);
+    const std::pair<const void*, void*> ins[3] = {{s.q, qp}, {s.k, kp}, {s.v, vp}};
+    for (const auto& [src, dst] : ins) {
+        DFA2C_CUDA_CHECK(cudaMemsetAsync(dst, 0, pbytes, st));
+        DFA2C_CUDA_CHECK(cudaMemcpy2DAsync(dst, D * 2, src, d * 2, d * 2, rows, cudaMemcpyDeviceToDevice, st));
+    }
+    dfa2c_dims pd = *s.dims;
+    pd.head_dim = D;
+    ForwardSpec p = s;
+    p.q = qp;
+    p.k = kp;
+    p.v = vp;
+    p.out = op;
+    p.dims = &pd;
+    p.cache = nullptr;
+    p.scale_d = d;
+    bool any = false;
+    for (HeadJob& j : p.jobs) {
+        if (j.mask_id == JOB_COPY)
+            j.mask_id = JOB_SKIP;
+        j.commit = false;
+        any |= j.mask_id >= 0;
+    }
+    if (any) {
+        launch_forward(p, st);
+        // every row back to the caller's layout; rows of heads the kernel
+        // skipped are rewritten below or belong to other launches' heads
+        // (host-path groups), so copy computed heads only
+        const size_t head_rows = static_cast<size_t>(n);
+        for (int64_t b = 0; b < s.batch; ++b)
+            for (int64_t h = 0; h < H; ++h)
+                if (p.jobs[h].mask_id >= 0) {
+                    const size_t r0 = static_cast<size_t>(b * H + h) * head_rows;
+                    DFA2C_CUDA_CHECK(cudaMemcpy2DAsync(static_cast<char*>(s.out) + r0 * d * 2, d * 2,
+                                                       static_cast<const char*>(op) + r0 * D * 2, D * 2, d * 2,
+                                                       head_rows, cudaMemcpyDeviceToDevice, st));
+                }
+    }
+    void* cache_layer = nullptr;
+    for (const HeadJob& j : s.jobs)
+        if ((j.mask_id == JOB_COPY || j.commit) && !cache_layer) {
+            if (!s.cache)
+                fail(DFA2C_CACHE_MISS, "cached heads need a cache");
+            s.cache->ensure(s.layer);
+            cache_layer = s.cache->layer_ptr(s.layer);
+        }
+    const size_t head_bytes = static_cast<size_t>(n * d) * 2;
+    for (int64_t h = 0; h < H; ++h) {
+        const HeadJob& j = s.jobs[h];
+        if (j.mask_id != JOB_COPY && !j.commit)
+            continue;
+        // per head, one strided copy over the samples ([batch, H, n, d] layout on both sides)
+        char* slot = static_cast<char*>(cache_layer) + h * head_bytes;
+        char* o = static_cast<char*>(s.out) + h * head_bytes;
+        if (j.mask_id == JOB_COPY)
+            DFA2C_CUDA_CHECK(cudaMemcpy2DAsync(o, H * head_bytes, slot, H * head_bytes, head_bytes, s.batch,
+                                               cudaMemcpyDeviceToDevice, st));
+        else
+            DFA2C_CUDA_CHECK(cudaMemcpy2DAsync(slot, H * head_bytes, o, H * head_bytes, head_bytes, s.batch,
+                                               cudaMemcpyDeviceToDevice, st));
+    }
+    for (void* x : {qp, kp, vp, op})
+        DFA2C_CUDA_CHECK(cudaFreeAsync(x, st));
+}
+
+void run_forward(const ForwardSpec& s, cudaStream_t stream) {
+    const int64_t d = s.dims->head_dim;
+    if (d < 1 || d > 128)
+        fail(DFA2C_UNSUPPORTED, "head_dim must be in [1, 128] on the sm_100a path (got " + std::to_string(d) + ")");
+    if (direct_layout(d))
+        launch_forward(s, stream);
+    else
+        run_padded(s, stream);
+}
+
+void launch_forward(const ForwardSpec& s, cudaStream_t stream) {
+    const int64_t n = seq_len(s.dims), d = s.dims->head_dim, H = s.dims->n_heads;
     if (s.batch < 1)
         fail(DFA2C_SHAPE, "batch must be >= 1");
     if (s.batch * H > std::numeric_limits<int32_t>::max() / 2 || n > (1 << 24))
@@ -590,11 +692,11 @@ void run_forward(const ForwardSpec& s, cudaStream_t stream) {
     a.n = static_cast<int32_t>(n);
     a.block = static_cast<int32_t>(std::min<int64_t>(s.block, int64_t{1} << 30));
     a.nb = static_cast<int32_t>(ceil_div(n, s.block));
-    a.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(d)));
+    a.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(s.scale_d ? s.scale_d : d)));
     a.trace = g_trace;
     if (plan->grid == 0)
         return;  // nothing to launch (every head skipped)
-    DFA2C_CUDA_CHECK(dfa2k::launch_attn(static_cast<int>(d), tq, tk, tv, to, tc, a, plan->grid, stream));
+    DFA2C_CUDA_CHECK(dfa2k::launch_attn(kernel_dim(d), tq, tk, tv, to, tc, a, plan->grid, stream));
     g_launches.fetch_add(1);
 }
 
@@ -1262,6 +1364,190 @@ int dfa2c_influence_for_layer(const void* q, const void* k, const void* v, const
             }
         if (evals)
             *evals += 1 + M;
+    });
+}
+
+// ------------------------------------------------------------ plan files
+// The reference's plan file (JSON version 1; inc/plan.hpp:44-52,
+// src/plan.cpp:109-228): same schema, same validation, same text.
+
+int dfa2c_fnv1a_hex(const void* bytes, int64_t n, char* out) {
+    return guard([&] {
+        if (!out || n < 0 || (n > 0 && !bytes))
+            fail(DFA2C_SHAPE, "fnv1a_hex needs bytes and a 17-byte output");
+        uint64_t h = 0xcbf29ce484222325ull;  // FNV-1a 64 offset basis / prime
+        const auto* p = static_cast<const unsigned char*>(bytes);
+        for (int64_t i = 0; i < n; ++i) {
+            h ^= p[i];
+            h *= 0x100000001b3ull;
+        }
+        std::snprintf(out, 17, "%016llx", static_cast<unsigned long long>(h));
+    });
+}
+
+int dfa2c_plan_to_json(const dfa2c_plan_header* hdr, const int32_t* kinds, const int64_t* windows,
+                       const int64_t* window_set, const char* influence_digest, char* buf, int64_t cap,
+                       int64_t* len) {
+    return guard([&] {
+        using json_lite::Value;
+        if (!hdr || hdr->n_timesteps < 0 || hdr->n_layers < 0 || hdr->n_heads < 0 || hdr->n_window_set < 0)
+            fail(DFA2C_SHAPE, "bad plan header");
+        const int64_t T = hdr->n_timesteps, L = hdr->n_layers, H = hdr->n_heads;
+        if (T * L * H > 0 && !kinds)
+            fail(DFA2C_SHAPE, "plan arrays must not be NULL");
+        Value j = Value::object();
+        j.set("version", Value::integer(1));
+        Value dims = Value::object();
+        dims.set("T", Value::integer(T));
+        dims.set("L", Value::integer(L));
+        dims.set("H", Value::integer(H));
+        dims.set("d", Value::integer(hdr->head_dim));
+        dims.set("n_visual", Value::integer(hdr->n_visual));
+        dims.set("n_text", Value::integer(hdr->n_text));
+        dims.set("block", Value::integer(hdr->block_size));
+        j.set("dims", std::move(dims));
+        j.set("delta", Value::real(hdr->delta));
+        j.set("coeff", Value::real(hdr->coeff));
+        Value ws = Value::array();
+        for (int64_t i = 0; i < hdr->n_window_set; ++i)
+            ws.push(Value::integer(window_set[i]));
+        j.set("window_set", std::move(ws));
+        Value entries = Value::array();
+        for (int64_t t = 0; t < T; ++t)
+            for (int64_t l = 0; l < L; ++l) {
+                Value heads = Value::array();
+                for (int64_t h = 0; h < H; ++h) {
+                    const int64_t i = (t * L + l) * H + h;
+                    Value e = Value::object();
+                    switch (kinds[i]) {
+                    case DFA2C_FULL: e.set("kind", Value::str("full")); break;
+                    case DFA2C_ARROW:
+                        e.set("kind", Value::str("arrow"));
+                        e.set("window_blocks", Value::integer(windows ? windows[i] : 0));
+                        break;
+                    case DFA2C_CACHED: e.set("kind", Value::str("cached")); break;
+                    default: fail(DFA2C_PLAN, "unknown strategy kind");
+                    }
+                    heads.push(std::move(e));
+                }
+                Value entry = Value::object();
+                entry.set("t", Value::integer(t));
+                entry.set("layer", Value::integer(l));
+                entry.set("heads", std::move(heads));
+                entries.push(std::move(entry));
+            }
+        j.set("plan", std::move(entries));
+        j.set("influence_digest", Value::str(influence_digest ? influence_digest : ""));
+        const std::string text = j.dump(2) + "\n";
+        if (len)
+            *len = static_cast<int64_t>(text.size());
+        if (buf) {
+            if (cap < static_cast<int64_t>(text.size()) + 1)
+                fail(DFA2C_SHAPE, "output buffer too small");
+            std::memcpy(buf, text.c_str(), text.size() + 1);
+        }
+    });
+}
+
+int dfa2c_plan_from_json(const char* text, int64_t text_len, dfa2c_plan_header* hdr, int32_t* kinds,
+                         int64_t* windows, int64_t* window_set, char* digest, int64_t digest_cap) {
+    return guard([&] {
+        using json_lite::Value;
+        if (!text || !hdr)
+            fail(DFA2C_SHAPE, "plan text and header must not be NULL");
+        const std::string src = text_len >= 0 ? std::string(text, static_cast<size_t>(text_len)) : std::string(text);
+        Value j;
+        try {
+            j = json_lite::parse(src);
+        } catch (const json_lite::ParseError& e) {
+            fail(DFA2C_PLAN, std::string("malformed plan JSON: ") + e.what());
+        }
+        try {
+            if (j.at("version").as_int() != 1)
+                fail(DFA2C_PLAN, "unsupported plan version");
+            const Value& d = j.at("dims");
+            dfa2c_plan_header h{};
+            h.n_timesteps = d.at("T").as_int();
+            h.n_layers = d.at("L").as_int();
+            h.n_heads = d.at("H").as_int();
+            h.head_dim = d.at("d").as_int();
+            h.n_visual = d.at("n_visual").as_int();
+            h.n_text = d.at("n_text").as_int();
+            h.block_size = d.at("block").as_int();
+            h.delta = j.at("delta").as_double();
+            h.coeff = j.at("coeff").as_double();
+            const auto& wsv = j.at("window_set").items();
+            h.n_window_set = static_cast<int64_t>(wsv.size());
+            const std::string& dig = j.at("influence_digest").as_string();
+            h.digest_len = static_cast<int64_t>(dig.size());
+            if (h.n_timesteps < 1 || h.n_layers < 1)
+                fail(DFA2C_PLAN, "plan needs T >= 1 and L >= 1");
+            const int64_t T = h.n_timesteps, L = h.n_layers, H = h.n_heads;
+            const dfa2c_dims dims{H, h.head_dim, h.n_visual, h.n_text, DFA2C_VISUAL_FIRST};
+            validate_dims(&dims);  // AttentionDims::validate -> ShapeError
+            std::vector<int32_t> k(static_cast<size_t>(T * L * H), -1);
+            std::vector<int64_t> w(static_cast<size_t>(T * L * H), 0);
+            std::vector<uint8_t> seen(static_cast<size_t>(T * L), 0);
+            for (const Value& e : j.at("plan").items()) {
+                const int64_t t = e.at("t").as_int();
+                const int64_t l = e.at("layer").as_int();
+                if (t < 0 || t >= T || l < 0 || l >= L)
+                    fail(DFA2C_PLAN, "plan entry out of range");
+                const size_t idx = static_cast<size_t>(t * L + l);
+                if (seen[idx])
+                    fail(DFA2C_PLAN, "duplicate plan entry");
+                seen[idx] = 1;
+                const auto& heads = e.at("heads").items();
+                if (static_cast<int64_t>(heads.size()) != H)
+                    fail(DFA2C_PLAN, "head array length must equal H");
+                for (int64_t hh = 0; hh < H; ++hh) {
+                    const Value& hv = heads[static_cast<size_t>(hh)];
+                    const std::string& kind = hv.at("kind").as_string();
+                    const size_t i = idx * static_cast<size_t>(H) + static_cast<size_t>(hh);
+                    if (kind == "full") {
+                        k[i] = DFA2C_FULL;
+                    } else if (kind == "arrow") {
+                        k[i] = DFA2C_ARROW;
+                        w[i] = hv.at("window_blocks").as_int();
+                    } else if (kind == "cached") {
+                        k[i] = DFA2C_CACHED;
+                    } else {
+                        fail(DFA2C_PLAN, "unknown strategy kind: " + kind);
+                    }
+                }
+            }
+            for (uint8_t sflag : seen)
+                if (!sflag)
+                    fail(DFA2C_PLAN, "plan must cover every (t, layer)");
+            // CompressionPlan::validate (src/plan.cpp:33-56): dims (ShapeError),
+            // then T/L/block, delta, coeff, coverage, per-head rules
+            if (h.block_size < 1)
+                fail(DFA2C_PLAN, "plan needs T >= 1, L >= 1, block >= 1");
+            if (!(h.delta >= 0.0))
+                fail(DFA2C_PLAN, "delta must be >= 0");
+            if (!(h.coeff >= 1.0))
+                fail(DFA2C_PLAN, "coeff must be >= 1");
+            const int rc = dfa2c_plan_aggregate(&dims, T, L, h.block_size, k.data(), w.data(), nullptr, nullptr,
+                                                nullptr);
+            if (rc != DFA2C_OK)
+                fail(rc, g_err);
+            *hdr = h;
+            if (kinds) {
+                std::copy(k.begin(), k.end(), kinds);
+                if (windows)
+                    std::copy(w.begin(), w.end(), windows);
+                if (window_set)
+                    for (size_t i = 0; i < wsv.size(); ++i)
+                        window_set[i] = wsv[i].as_int();
+                if (digest) {
+                    if (digest_cap < h.digest_len + 1)
+                        fail(DFA2C_SHAPE, "digest buffer too small");
+                    std::memcpy(digest, dig.c_str(), dig.size() + 1);
+                }
+            }
+        } catch (const json_lite::TypeError& e) {
+            fail(DFA2C_PLAN, std::string("plan schema violation: ") + e.what());
+        }
     });
 }
 

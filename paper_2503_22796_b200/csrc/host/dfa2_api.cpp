@@ -8,7 +8,9 @@
 // (src/dispatch.cpp:11-54, inc/errors.hpp:8-45).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <limits>
 #include <string>
@@ -646,6 +648,8 @@ void plan_flat(const CompressionPlan& p, std::vector<int32_t>& kinds, std::vecto
 
 DFA2_API void CompressionPlan::validate() const {
     dims.validate();
+    if (n_timesteps < 1 || n_layers < 1 || block_size < 1)
+        throw PlanValidationError("plan needs T >= 1, L >= 1, block >= 1");
     if (!(delta >= 0.0))
         throw PlanValidationError("delta must be >= 0");
     if (!(coeff >= 1.0))
@@ -672,6 +676,105 @@ DFA2_API int64_t CompressionPlan::flops_dense_total() const {
 }
 DFA2_API double CompressionPlan::aggregate_sparsity() const {
     return 1.0 - static_cast<double>(flops_total()) / static_cast<double>(flops_dense_total());
+}
+
+DFA2_API bool CompressionPlan::operator==(const CompressionPlan& o) const {
+    return dims.n_heads == o.dims.n_heads && dims.head_dim == o.dims.head_dim && dims.n_visual == o.dims.n_visual &&
+           dims.n_text == o.dims.n_text && dims.order == o.dims.order && n_timesteps == o.n_timesteps &&
+           n_layers == o.n_layers && block_size == o.block_size && delta == o.delta && coeff == o.coeff &&
+           window_set == o.window_set && layers == o.layers && influence_digest == o.influence_digest;
+}
+
+// ---------------------------------------------------------------- plan files
+DFA2_API std::string fnv1a_hex(const std::string& bytes) {
+    char out[17];
+    check(dfa2c_fnv1a_hex(bytes.data(), static_cast<int64_t>(bytes.size()), out));
+    return out;
+}
+
+DFA2_API std::string plan_to_json(const CompressionPlan& plan) {
+    const int64_t T = plan.n_timesteps, L = plan.n_layers, H = plan.dims.n_heads;
+    std::vector<int32_t> kinds(static_cast<size_t>(std::max<int64_t>(T * L * H, 0)), DFA2C_FULL);
+    std::vector<int64_t> wins(kinds.size(), 0);
+    for (int64_t t = 0; t < T; ++t)
+        for (int64_t l = 0; l < L; ++l) {
+            const LayerPlan& lp = plan.at(t, l);
+            if (lp.n_heads() != H)
+                throw ShapeError("head array length must equal H");
+            std::vector<int32_t> k;
+            std::vector<int64_t> w;
+            plan_arrays(lp, k, w);
+            std::copy(k.begin(), k.end(), kinds.begin() + (t * L + l) * H);
+            std::copy(w.begin(), w.end(), wins.begin() + (t * L + l) * H);
+        }
+    dfa2c_plan_header hdr{T, L, H, plan.dims.head_dim, plan.dims.n_visual, plan.dims.n_text, plan.block_size,
+                          plan.delta, plan.coeff, static_cast<int64_t>(plan.window_set.size()), 0};
+    int64_t len = 0;
+    check(dfa2c_plan_to_json(&hdr, kinds.data(), wins.data(), plan.window_set.data(), plan.influence_digest.c_str(),
+                             nullptr, 0, &len));
+    std::string text(static_cast<size_t>(len) + 1, '\0');
+    check(dfa2c_plan_to_json(&hdr, kinds.data(), wins.data(), plan.window_set.data(), plan.influence_digest.c_str(),
+                             text.data(), len + 1, &len));
+    text.resize(static_cast<size_t>(len));
+    return text;
+}
+
+DFA2_API CompressionPlan plan_from_json(const std::string& text) {
+    dfa2c_plan_header hdr{};
+    check(dfa2c_plan_from_json(text.data(), static_cast<int64_t>(text.size()), &hdr, nullptr, nullptr, nullptr,
+                               nullptr, 0));
+    const int64_t T = hdr.n_timesteps, L = hdr.n_layers, H = hdr.n_heads;
+    std::vector<int32_t> kinds(static_cast<size_t>(T * L * H));
+    std::vector<int64_t> wins(kinds.size());
+    std::vector<int64_t> ws(static_cast<size_t>(hdr.n_window_set) + 1);
+    std::string digest(static_cast<size_t>(hdr.digest_len) + 1, '\0');
+    check(dfa2c_plan_from_json(text.data(), static_cast<int64_t>(text.size()), &hdr, kinds.data(), wins.data(),
+                               ws.data(), digest.data(), hdr.digest_len + 1));
+    CompressionPlan p;
+    p.dims.n_heads = H;
+    p.dims.head_dim = hdr.head_dim;
+    p.dims.n_visual = hdr.n_visual;
+    p.dims.n_text = hdr.n_text;
+    p.n_timesteps = T;
+    p.n_layers = L;
+    p.block_size = hdr.block_size;
+    p.delta = hdr.delta;
+    p.coeff = hdr.coeff;
+    p.window_set.assign(ws.begin(), ws.begin() + hdr.n_window_set);
+    digest.resize(static_cast<size_t>(hdr.digest_len));
+    p.influence_digest = digest;
+    p.layers.resize(static_cast<size_t>(T * L));
+    for (int64_t i = 0; i < T * L; ++i)
+        for (int64_t h = 0; h < H; ++h) {
+            const size_t j = static_cast<size_t>(i * H + h);
+            p.layers[static_cast<size_t>(i)].strategies.push_back(
+                kinds[j] == DFA2C_ARROW ? HeadStrategy::Arrow(wins[j])
+                                        : kinds[j] == DFA2C_CACHED ? HeadStrategy::Cached() : HeadStrategy::Full());
+        }
+    return p;
+}
+
+DFA2_API void save_plan(const CompressionPlan& plan, const std::string& path) {
+    const std::string text = plan_to_json(plan);
+    FILE* f = std::fopen(path.c_str(), "wb");
+    if (!f)
+        throw IoError("cannot open " + path + " for writing");
+    const bool ok = std::fwrite(text.data(), 1, text.size(), f) == text.size();
+    if (std::fclose(f) != 0 || !ok)
+        throw IoError("failed writing " + path);
+}
+
+DFA2_API CompressionPlan load_plan(const std::string& path) {
+    FILE* f = std::fopen(path.c_str(), "rb");
+    if (!f)
+        throw IoError("cannot open " + path);
+    std::string text;
+    char buf[1 << 16];
+    size_t got;
+    while ((got = std::fread(buf, 1, sizeof buf, f)) > 0)
+        text.append(buf, got);
+    std::fclose(f);
+    return plan_from_json(text);
 }
 
 }  // namespace dfa2

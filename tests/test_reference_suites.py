@@ -1,0 +1,114 @@
+"""The reference's OWN unit suites, compiled unchanged against this repo's
+drop-in headers (include/dfa2/) and libdfa2_b200.so.
+
+`make -C oracle reftests` (run by __graft_entry__.build() where
+/root/reference exists) compiles /root/reference/proj/tests/test_<suite>.cpp
+with the doctest-subset shim of tests/cpp/shim/ into oracle/_ref/tests/
+(git-ignored binaries that travel to the GPU box). Each binary prints one
+`CASE PASS|FAIL <name>` line per reference TEST_CASE.
+
+Caveat stated plainly: in the drop-in, `attention_reference` is the GPU
+Full-head path (as in the reference, where it is the CPU Full-head path,
+src/dispatch.cpp:68-71). Reference cases whose oracle is
+attention_reference therefore compare the sm_100a kernel with itself; the
+independent numeric parity check is tests/test_gpu_parity.py (f64 oracle,
+stated bf16 tolerance). These suites prove the API drop-in: names,
+signatures, error types, cache semantics and integer results.
+"""
+import os
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+BIN = os.path.join(ROOT, "oracle", "_ref", "tests")
+
+# Reference cases that cannot hold on a bf16 path, with the reason
+# (SURVEY.md §8c "Will fail by design").
+BY_DESIGN = {
+    ("dispatch", "mixed plan matches the per-head oracles"):
+        "checks a Cached head bitwise against an f32 tensor stored by the test that is not "
+        "bf16-representable (test_dispatch.cpp:83); the device cache holds bf16",
+}
+
+# Cases that need no GPU: masks, FLOP accounting, plan validation, cache
+# bookkeeping, error taxonomy.
+HOST_CASES = {
+    "arrow": [
+        "arrow mask: 512 visual + 128 text at block 128, window 0",
+        "window at or past the visual extent densifies the mask",
+        "no text band gives a pure block-diagonal mask",
+        "text-first ordering mirrors the band onto leading blocks",
+        "zero block size is an error",
+        "arrow masks are symmetric",
+        "flops: dense formula",
+        "flops: 13 of 25 uniform blocks is 0.52 of dense",
+        "flops: block-diagonal with four blocks is a quarter of dense",
+        "ragged tail blocks count true token coverage",
+        "flops are monotone in the window and reach dense at the max",
+    ],
+    "cache": None,  # every case
+    "dispatch": [
+        "cached head without an entry is a cache miss",
+        "plan must cover every head",
+        "plan flops: all-full, all-cached, half",
+        "plan flops add up per head",
+    ],
+    "plan_io": None,
+}
+
+
+def suites():
+    if not os.path.isdir(BIN):
+        return []
+    return sorted(f[len("test_"):] for f in os.listdir(BIN)
+                  if f.startswith("test_") and not f.endswith(".log") and os.access(os.path.join(BIN, f), os.X_OK))
+
+
+def run_suite(name):
+    r = subprocess.run([os.path.join(BIN, "test_" + name)], capture_output=True, text=True, timeout=900)
+    results = {}
+    for line in r.stdout.splitlines():
+        if line.startswith("CASE "):
+            _, status, case = line.split(" ", 2)
+            results[case] = status
+    assert results, r.stdout + r.stderr
+    return results, r.stdout
+
+
+def _need_binaries():
+    if not suites():
+        pytest.skip("reference suites not built (needs /root/reference: make -C oracle reftests)")
+
+
+def test_reference_suites_built_against_drop_in():
+    _need_binaries()
+    # at least these compile unchanged against include/dfa2/
+    assert {"arrow", "cache", "dispatch"} <= set(suites())
+
+
+@pytest.mark.parametrize("suite", sorted(HOST_CASES))
+def test_reference_host_cases_pass(suite):
+    _need_binaries()
+    if suite not in suites():
+        pytest.skip(f"test_{suite} not built")
+    results, out = run_suite(suite)
+    want = HOST_CASES[suite] if HOST_CASES[suite] is not None else list(results)
+    bad = [c for c in want if results.get(c) != "PASS"]
+    assert not bad, f"{suite}: {bad}\n{out}"
+
+
+@pytest.mark.gpu
+def test_reference_suites_pass_on_gpu():
+    _need_binaries()
+    failed = {}
+    for s in suites():
+        results, out = run_suite(s)
+        for case, status in results.items():
+            if status != "PASS" and (s, case) not in BY_DESIGN:
+                failed[(s, case)] = out
+    assert not failed, "\n".join(f"{s}: {c}" for s, c in failed)
+    # the by-design failures still fail (if one starts passing, update BY_DESIGN)
+    for (s, case) in BY_DESIGN:
+        if s in suites():
+            assert run_suite(s)[0].get(case) == "FAIL"

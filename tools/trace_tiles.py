@@ -46,13 +46,10 @@ for L in range(2):
         d = lambda a_, b_: med(x[:, b_] - x[:, a_])
         extra = (f"\n   softmax detail: ld+wait {d(1, 3):.0f}  max+decide {d(3, 4):.0f}  P(hi) {d(4, 5):.0f}  "
                  f"st.wait+arrive {d(5, 6):.0f}  reload lo {d(6, 7):.0f}  P(lo)+st+arrive {d(7, 2):.0f}")
-    elif L == 1 and (x[:, 7] > 0).sum() > 3:
-        # MMA warp, union step u: 4 = before K wait, 5 = K ready, 6 = S issued, 7 = PV(u-1)... issued
-        kw = x[:, 5] - x[:, 4]
-        si = x[:, 6] - x[:, 5]
-        pv = x[1:, 7] - x[1:, 6]
-        nxt = x[1:, 4] - x[:-1, 7]
-        extra += (f"\n   MMA warp: K wait {med(kw):.0f}  S issue {med(si):.0f}  S->PV done {med(pv):.0f}  "
-                  f"PV done->next step {med(nxt):.0f}")
+    elif (x[:, 6] > 0).sum() > 3 and (x[:, 7] > 0).sum() > 3:
+        # MMA warp (TRACE=1), per lane tile j: 7 = V(j) ready, 3 = P(j) half seen, 4 = PV(j) issued,
+        # 6 = K(j) ready (before S(j) issue), 5 = S(j) issued
+        extra += (f"\n   MMA warp: V ready->P seen {med(x[:, 3] - x[:, 7]):.0f}  "
+                  f"PV(j-1) issued->K(j) ready {med(x[1:, 6] - x[:-1, 4]):.0f}  K ready->S issued {med(x[:, 5] - x[:, 6]):.0f}")
     print(f"lane {L}: tiles {n}  period {med(period):.0f}  softmax {med(soft):.0f}  wait_S {med(wait):.0f}  "
           f"P->MMA {med(pseen):.0f}" + extra)
