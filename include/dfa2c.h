@@ -195,6 +195,31 @@ int dfa2c_influence_for_layer(const void* q, const void* k, const void* v,
                               void* original, void* method_outputs, int64_t* evals,
                               void* stream);
 
+/* ---- per-layer plan selection (calibration driver) ----------------------
+ * The selection problem of calibrate_model (inc/plansolver.hpp:19-75;
+ * src/calibrate.cpp:314-320): per head pick Full (full_cost, influence 0)
+ * or one method m with finite influence[h*M + m] <= selection_cap, keeping
+ * the summed influence <= delta, minimising the summed cost. Ties: lower
+ * summed influence, then the lexicographically smaller choice vector
+ * (method index, Full after every method). delta == 0 -> all Full.
+ * choice[H] receives -1 (Full) or a method index. exhaustive != 0
+ * enumerates every assignment (test oracle; (M+1)^H <= 1e7). Invalid
+ * problems -> DFA2C_SHAPE (std::invalid_argument in the reference). */
+double dfa2c_selection_cap(double coeff, int64_t n_heads, double delta);
+int dfa2c_plan_solve(int64_t n_heads, int64_t n_methods, const double* influence,
+                     double full_cost, const double* method_cost, double delta, double coeff,
+                     int32_t exhaustive, int64_t* choice, double* objective,
+                     double* total_influence, int64_t* nodes);
+/* LP relaxation optimum (fractional multiple-choice knapsack) of the same problem. */
+int dfa2c_plan_lp_bound(int64_t n_heads, int64_t n_methods, const double* influence,
+                        double full_cost, const double* method_cost, double delta, double coeff,
+                        double* bound);
+/* analytic_costs: full_cost = 1, Arrow(w) = active fraction of its mask,
+ * Cached = 0 (kinds/windows[n_methods] describe the candidates). */
+int dfa2c_analytic_costs(const dfa2c_dims* dims, int64_t block, const int32_t* kinds,
+                         const int64_t* windows, int64_t n_methods, double* full_cost,
+                         double* method_cost);
+
 /* ---- plan files (JSON version 1) ---------------------------------------
  * The reference's plan file format (inc/plan.hpp:44-52; src/plan.cpp:109-228):
  * {version, dims:{T,L,H,d,n_visual,n_text,block}, delta, coeff, window_set,

@@ -110,6 +110,8 @@ def ref() -> ctypes.CDLL:
             "ref_plan_to_json": [c_int64] * 7 + [c_double, c_double, _P(c_int64), c_int64, _P(c_int32), _P(c_int64),
                                                  c_char_p, c_char_p, c_int64, _P(c_int64)],
             "ref_plan_from_json": [c_char_p, c_int64, _P(c_int32), _P(c_int64), _P(c_int64)],
+            "ref_plan_solve": [c_int64, c_int64, _P(c_double), c_double, _P(c_double), c_double, c_double, c_int,
+                               _P(c_int64), _P(c_double), _P(c_double), _P(c_double)],
         }
         for name, args in sig.items():
             fn = getattr(L, name)

@@ -20,6 +20,7 @@
 #include "dfa2/calibrate.hpp"
 #include "dfa2/dispatch.hpp"
 #include "dfa2/plan.hpp"
+#include "dfa2/plansolver.hpp"
 #include "dfa2/tensor.hpp"
 #include "dfa2/workload.hpp"
 
@@ -362,5 +363,30 @@ REF_API int ref_plan_from_json(const char* text, int64_t cap_entries, int32_t* k
                 kinds[i * H + h] = static_cast<int32_t>(s.kind);
                 windows[i * H + h] = s.window_blocks;
             }
+    });
+}
+
+// solve / brute_force / lp_relaxation_bound (src/plansolver.cpp) of one
+// selection problem; choice[H] gets -1 (Full) or a method index.
+REF_API int ref_plan_solve(int64_t H, int64_t M, const double* infl, double full_cost,
+                           const double* method_cost, double delta, double coeff, int brute,
+                           int64_t* choice, double* objective, double* total_influence,
+                           double* lp_bound) {
+    return guard([&] {
+        dfa2::PlanProblem p;
+        p.n_heads = H;
+        p.n_methods = M;
+        p.influence.assign(infl, infl + H * M);
+        p.costs.full_cost = full_cost;
+        p.costs.method_cost.assign(method_cost, method_cost + M);
+        p.delta = delta;
+        p.coeff = coeff;
+        const dfa2::PlanSolution s = brute ? dfa2::brute_force(p) : dfa2::solve(p);
+        for (int64_t h = 0; h < H; ++h)
+            choice[h] = s.choice[static_cast<size_t>(h)];
+        *objective = s.objective;
+        *total_influence = s.total_influence;
+        if (lp_bound)
+            *lp_bound = dfa2::lp_relaxation_bound(p);
     });
 }

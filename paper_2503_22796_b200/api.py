@@ -598,6 +598,100 @@ def influence_for_layer(q, k, v, methods: Sequence[MethodCandidate], cache: Opti
     return LayerInfluence(original, outs, infl)
 
 
+# --------------------------------------------------------------- plan selection
+kFullChoice = -1
+
+
+@dataclass
+class CostModel:
+    """CostModel (inc/plansolver.hpp:12-17)."""
+
+    full_cost: float = 1.0
+    method_cost: List[float] = field(default_factory=list)
+
+
+@dataclass
+class PlanProblem:
+    """PlanProblem (inc/plansolver.hpp:25-37): influence is [n_heads * n_methods], row-major by head."""
+
+    n_heads: int = 0
+    n_methods: int = 0
+    influence: Sequence[float] = field(default_factory=list)
+    costs: CostModel = field(default_factory=CostModel)
+    delta: float = 0.0
+    coeff: float = 1.5
+
+
+@dataclass
+class PlanSolution:
+    """PlanSolution (inc/plansolver.hpp:43-48): choice[h] is kFullChoice or a method index."""
+
+    choice: List[int] = field(default_factory=list)
+    objective: float = 0.0
+    total_influence: float = 0.0
+    nodes: int = 0
+
+
+def selection_cap(coeff: float, n_heads: int, delta: float) -> float:
+    """Per-selection cap (coeff / n_heads) * delta (inc/plansolver.hpp:39-41)."""
+    return float(lib().dfa2c_selection_cap(coeff, n_heads, delta))
+
+
+def _problem_args(p: PlanProblem):
+    infl = np.ascontiguousarray(np.asarray(p.influence, np.float64).reshape(-1))
+    if infl.size != p.n_heads * p.n_methods or len(p.costs.method_cost) != p.n_methods:
+        raise ShapeError("influence grid / cost model do not match H x M")
+    mc = np.ascontiguousarray(np.asarray(p.costs.method_cost if p.n_methods else [0.0], np.float64))
+    return infl, mc
+
+
+def _solve(p: PlanProblem, exhaustive: bool) -> PlanSolution:
+    infl, mc = _problem_args(p)
+    choice = np.zeros(max(1, p.n_heads), np.int64)
+    obj, tot, nodes = c_double(), c_double(), c_int64()
+    check(lib().dfa2c_plan_solve(p.n_heads, p.n_methods, infl.ctypes.data_as(POINTER(c_double)), p.costs.full_cost,
+                                 mc.ctypes.data_as(POINTER(c_double)), p.delta, p.coeff, 1 if exhaustive else 0,
+                                 choice.ctypes.data_as(POINTER(c_int64)), byref(obj), byref(tot), byref(nodes)))
+    return PlanSolution([int(c) for c in choice[:p.n_heads]], obj.value, tot.value, nodes.value)
+
+
+def solve(problem: PlanProblem) -> PlanSolution:
+    """solve (inc/plansolver.hpp:50-61): exact optimum with the reference's tie-break."""
+    return _solve(problem, False)
+
+
+def brute_force(problem: PlanProblem) -> PlanSolution:
+    """brute_force (inc/plansolver.hpp:63-65): exhaustive enumeration, same tie-break."""
+    return _solve(problem, True)
+
+
+def lp_relaxation_bound(problem: PlanProblem) -> float:
+    """lp_relaxation_bound (inc/plansolver.hpp:67-69)."""
+    infl, mc = _problem_args(problem)
+    b = c_double()
+    check(lib().dfa2c_plan_lp_bound(problem.n_heads, problem.n_methods, infl.ctypes.data_as(POINTER(c_double)),
+                                    problem.costs.full_cost, mc.ctypes.data_as(POINTER(c_double)), problem.delta,
+                                    problem.coeff, byref(b)))
+    return b.value
+
+
+def analytic_costs(dims: AttentionDims, block_size: int, methods: Sequence[HeadStrategy]) -> CostModel:
+    """analytic_costs (inc/plansolver.hpp:19-21): Arrow(w) = active fraction of its mask, Cached = 0."""
+    M = len(methods)
+    kinds = (c_int32 * max(1, M))(*[_KIND_CODE[m.kind] for m in methods])
+    wins = (c_int64 * max(1, M))(*[m.window_blocks for m in methods])
+    out = (c_double * max(1, M))()
+    full = c_double()
+    d = dims.c()
+    check(lib().dfa2c_analytic_costs(byref(d), block_size, kinds, wins, M, byref(full), out))
+    return CostModel(full.value, list(out[:M]))
+
+
+def to_layer_plan(solution: PlanSolution, methods: Sequence[HeadStrategy]) -> LayerPlan:
+    """to_layer_plan (inc/plansolver.hpp:74-76)."""
+    return LayerPlan([HeadStrategy.Full() if c == kFullChoice else methods[c] for c in solution.choice])
+
+
 # --------------------------------------------------------------- compression plan
 @dataclass
 class CompressionPlan:

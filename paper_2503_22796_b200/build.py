@@ -21,7 +21,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 CU_SOURCES = ["attn_sm100.cu", "rse_sm100.cu"]
-CPP_SOURCES = ["dfa2c.cpp", "json_lite.cpp"]
+CPP_SOURCES = ["dfa2c.cpp", "json_lite.cpp", "plansolver.cpp"]
 
 
 def _sources():

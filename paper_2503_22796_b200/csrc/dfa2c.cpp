@@ -21,6 +21,7 @@
 #include <vector>
 
 #include "attn_types.h"
+#include "capi_status.h"
 #include "json_lite.h"
 
 namespace dfa2k {
@@ -36,16 +37,11 @@ using dfa2k::WorkItem;
 
 namespace {
 
-thread_local std::string g_err;
+using dfa2c_detail::fail;
+using dfa2c_detail::g_err;
+using dfa2c_detail::guard;
 long long* g_trace = nullptr;  // debug: per-tile timestamps (kernels built with -DDFA2_TRACE=1)
 std::atomic<int64_t> g_launches{0};
-
-struct Failure {
-    int code;
-    std::string msg;
-};
-
-[[noreturn]] void fail(int code, const std::string& msg) { throw Failure{code, msg}; }
 
 #define DFA2C_CUDA_CHECK(expr)                                                             \
     do {                                                                                   \
@@ -53,23 +49,6 @@ struct Failure {
         if (e_ != cudaSuccess)                                                             \
             fail(DFA2C_CUDA, std::string(#expr) + " failed: " + cudaGetErrorString(e_)); \
     } while (0)
-
-template <class F>
-int guard(F&& f) {
-    try {
-        f();
-        return DFA2C_OK;
-    } catch (const Failure& e) {
-        g_err = e.msg;
-        return e.code;
-    } catch (const std::bad_alloc&) {
-        g_err = "host allocation failed";
-        return DFA2C_CUDA;
-    } catch (const std::exception& e) {
-        g_err = e.what();
-        return DFA2C_CUDA;
-    }
-}
 
 int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
@@ -1364,6 +1343,38 @@ int dfa2c_influence_for_layer(const void* q, const void* k, const void* v, const
             }
         if (evals)
             *evals += 1 + M;
+    });
+}
+
+// analytic_costs (reference: src/plansolver.cpp, CostModel in
+// inc/plansolver.hpp:12-23): full_cost = 1; Arrow(w) = flops_count of its
+// mask / dense_flops; Cached = 0; Full = 1.
+int dfa2c_analytic_costs(const dfa2c_dims* dims, int64_t block, const int32_t* kinds, const int64_t* windows,
+                         int64_t n_methods, double* full_cost, double* method_cost) {
+    return guard([&] {
+        validate_dims(dims);
+        if (block < 1)
+            fail(DFA2C_SHAPE, "block_size must be >= 1");
+        if (n_methods < 0 || (n_methods > 0 && (!kinds || !method_cost)))
+            fail(DFA2C_SHAPE, "bad method list");
+        const int64_t n = seq_len(dims), d = dims->head_dim;
+        const double dense = static_cast<double>(4 * d * n * n);
+        for (int64_t m = 0; m < n_methods; ++m) {
+            switch (kinds[m]) {
+            case DFA2C_FULL: method_cost[m] = 1.0; break;
+            case DFA2C_CACHED: method_cost[m] = 0.0; break;
+            case DFA2C_ARROW: {
+                if (!windows || windows[m] < 0)
+                    fail(DFA2C_SHAPE, "window_blocks must be >= 0");
+                const std::vector<uint8_t> mk = arrow_mask(dims, block, windows[m]);
+                method_cost[m] = static_cast<double>(4 * d * active_positions(mk.data(), n, block)) / dense;
+                break;
+            }
+            default: fail(DFA2C_SHAPE, "unknown strategy kind");
+            }
+        }
+        if (full_cost)
+            *full_cost = 1.0;
     });
 }
 
