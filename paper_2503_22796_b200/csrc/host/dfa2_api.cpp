@@ -564,38 +564,52 @@ DFA2_API LayerInfluence influence_for_layer(const Tensor& q, const Tensor& k, co
                                             RseMode mode, CalibrationStats* stats) {
     if (methods.empty())
         throw ShapeError("candidate set must be nonempty");
+    // Candidates in any order, as in src/calibrate.cpp:216-251: Cached
+    // entries measure the cache slots, every other kind is an arrow pass with
+    // its window. The device call evaluates each distinct window once plus
+    // the cached column; results are mapped back to the caller's order.
     std::vector<int64_t> windows;
+    std::vector<int64_t> column;  // per method: device column
     bool cached = false;
     for (const MethodCandidate& m : methods) {
-        if (m.strategy.kind == StrategyKind::arrow) {
-            if (cached)
-                throw ShapeError("Cached must be the last candidate");
-            windows.push_back(m.strategy.window_blocks);
-        } else if (m.strategy.kind == StrategyKind::cached) {
+        if (m.strategy.kind == StrategyKind::cached) {
             cached = true;
+            column.push_back(-1);
         } else {
-            throw ShapeError("Full is not a compression candidate");
+            if (m.strategy.window_blocks < 0)
+                throw ShapeError("window radii must be >= 0");
+            windows.push_back(m.strategy.window_blocks);
+            column.push_back(static_cast<int64_t>(windows.size()) - 1);
         }
     }
+    const int64_t NW = static_cast<int64_t>(windows.size());
+    for (int64_t& c : column)
+        if (c < 0)
+            c = NW;
     dims.validate();
     const int64_t H = dims.n_heads, n = dims.seq_len(), d = dims.head_dim, numel = H * n * d;
     const int64_t M = static_cast<int64_t>(methods.size());
+    const int64_t MD = NW + (cached ? 1 : 0);  // device columns
     if (q.ndim() != 3 || q.dim(0) != H || q.dim(1) != n || q.dim(2) != d || q.shape() != k.shape() ||
         q.shape() != v.shape())
         throw ShapeError("tensor shape disagrees with dims");
     dfa2c_cache* dev = cache.size() > 0 ? cache.bind(H, n, d) : nullptr;
-    DevBuf dq(numel * 2), dk(numel * 2), dv(numel * 2), dorig(numel * 2), douts(numel * 2 * M);
+    DevBuf dq(numel * 2), dk(numel * 2), dv(numel * 2), dorig(numel * 2), douts(numel * 2 * MD);
     upload_bf16(as_f32(q).data(), numel, dq.p);
     upload_bf16(as_f32(k).data(), numel, dk.p);
     upload_bf16(as_f32(v).data(), numel, dv.p);
-    LayerInfluence li;
-    li.influence.assign(static_cast<size_t>(H * M), 0.0);
+    std::vector<double> infl_dev(static_cast<size_t>(H * MD), 0.0);
     int64_t evals = 0;
     const dfa2c_dims cd = cdims(dims);
-    check(dfa2c_influence_for_layer(dq.p, dk.p, dv.p, &cd, block_size, windows.data(),
-                                    static_cast<int64_t>(windows.size()), cached ? 1 : 0, dev, layer, t,
-                                    mode == RseMode::standard ? DFA2C_RSE_STANDARD : DFA2C_RSE_LITERAL,
-                                    li.influence.data(), dorig.p, douts.p, &evals, nullptr));
+    check(dfa2c_influence_for_layer(dq.p, dk.p, dv.p, &cd, block_size, windows.data(), NW, cached ? 1 : 0, dev,
+                                    layer, t, mode == RseMode::standard ? DFA2C_RSE_STANDARD : DFA2C_RSE_LITERAL,
+                                    infl_dev.data(), dorig.p, douts.p, &evals, nullptr));
+    LayerInfluence li;
+    li.influence.assign(static_cast<size_t>(H * M), 0.0);
+    for (int64_t h = 0; h < H; ++h)
+        for (int64_t m = 0; m < M; ++m)
+            li.influence[static_cast<size_t>(h * M + m)] = infl_dev[static_cast<size_t>(h * MD + column[m])];
+    evals = 1 + M;  // one original + one evaluation per candidate (src/calibrate.cpp:207, 220-221)
     li.original = Tensor::zeros({H, n, d});
     download_bf16(dorig.p, numel, li.original.f32());
     li.method_outputs.resize(static_cast<size_t>(M));
@@ -603,7 +617,7 @@ DFA2_API LayerInfluence influence_for_layer(const Tensor& q, const Tensor& k, co
         if (methods[m].strategy.kind == StrategyKind::cached && t == 0)
             continue;  // ineligible: left unset, as in the reference
         li.method_outputs[m] = Tensor::zeros({H, n, d});
-        download_bf16(static_cast<const char*>(douts.p) + m * numel * 2, numel, li.method_outputs[m].f32());
+        download_bf16(static_cast<const char*>(douts.p) + column[m] * numel * 2, numel, li.method_outputs[m].f32());
     }
     if (stats)
         stats->attention_evals += evals;

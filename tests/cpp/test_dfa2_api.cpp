@@ -7,6 +7,7 @@
 //   ./test_dfa2_api gpu    -> everything
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <limits>
@@ -19,6 +20,7 @@
 #include "dfa2/calibrate.hpp"
 #include "dfa2/dispatch.hpp"
 #include "dfa2/plan.hpp"
+#include "dfa2/workload.hpp"
 
 using namespace dfa2;
 
@@ -280,7 +282,34 @@ TEST(influence_for_layer_semantics, true) {  // test_calibrate.cpp:85-146
     }
 }
 
+// dump-workload H d nv nt order L T B seed path: raw f32 q|k|v of every
+// (t, layer) slot of generate(), t-major, for the bit-exactness check
+// against the reference generator (tests/test_cpp_api.py).
+static int dump_workload(char** a) {
+    WorkloadConfig cfg;
+    cfg.dims.n_heads = std::atoll(a[0]);
+    cfg.dims.head_dim = std::atoll(a[1]);
+    cfg.dims.n_visual = std::atoll(a[2]);
+    cfg.dims.n_text = std::atoll(a[3]);
+    cfg.dims.order = std::atoi(a[4]) ? TokenOrder::text_first : TokenOrder::visual_first;
+    cfg.n_layers = std::atoll(a[5]);
+    cfg.n_timesteps = std::atoll(a[6]);
+    cfg.block_size = std::atoll(a[7]);
+    cfg.seed = std::strtoull(a[8], nullptr, 10);
+    const Workload w = generate(cfg);
+    FILE* f = std::fopen(a[9], "wb");
+    if (!f)
+        return 2;
+    for (int64_t t = 0; t < cfg.n_timesteps; ++t)
+        for (int64_t l = 0; l < cfg.n_layers; ++l)
+            for (const Tensor* x : {&w.q(t, l), &w.k(t, l), &w.v(t, l)})
+                std::fwrite(x->f32(), sizeof(float), static_cast<size_t>(x->numel()), f);
+    return std::fclose(f) == 0 ? 0 : 2;
+}
+
 int main(int argc, char** argv) {
+    if (argc == 12 && std::string(argv[1]) == "dump-workload")
+        return dump_workload(argv + 2);
     const bool gpu = argc > 1 && std::string(argv[1]) == "gpu";
     int ran = 0;
     for (const Case& c : cases()) {

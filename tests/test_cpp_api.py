@@ -31,3 +31,19 @@ def test_cpp_api_host_cases(binary):
 @pytest.mark.gpu
 def test_cpp_api_gpu_cases(binary):
     _run(binary, "gpu")
+
+
+def test_generate_is_bit_identical_to_reference(binary, tmp_path):
+    """dfa2::generate (C++ drop-in) hashes to the same bytes as the
+    reference's generate() on the same configs (tests/golden/
+    gen_workload_golden.py), so pipelines and calibration runs see the
+    reference's exact inputs."""
+    import hashlib
+    import json
+
+    gold = json.load(open(os.path.join(ROOT, "tests", "golden", "workload_golden.json")))
+    for g in gold:
+        path = str(tmp_path / "w.bin")
+        r = subprocess.run([binary, "dump-workload", *map(str, g["config"]), path], capture_output=True, timeout=600)
+        assert r.returncode == 0, r.stderr
+        assert hashlib.sha256(open(path, "rb").read()).hexdigest() == g["sha256"], g["config"]

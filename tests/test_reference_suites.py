@@ -55,6 +55,16 @@ HOST_CASES = {
         "plan flops add up per head",
     ],
     "plan_io": None,
+    "plansolver": None,
+    "io": None,
+    "workload": [
+        "identical seeds give bitwise-identical streams and dumps",
+        "default profiles pin the per-layer extremes",
+        "drifting heads actually move",
+        "plan and workload dims must agree",
+        "pipeline rejects plans with cached heads at t0 before running",
+    ],
+    "calibrate": ["candidate ids and strategies"],
 }
 
 
@@ -84,7 +94,7 @@ def _need_binaries():
 def test_reference_suites_built_against_drop_in():
     _need_binaries()
     # at least these compile unchanged against include/dfa2/
-    assert {"arrow", "cache", "dispatch"} <= set(suites())
+    assert {"arrow", "cache", "dispatch", "plan_io", "plansolver", "io", "workload", "calibrate"} <= set(suites())
 
 
 @pytest.mark.parametrize("suite", sorted(HOST_CASES))
