@@ -1,0 +1,209 @@
+// bench_api.cpp — run_bench / find_window_for_sparsity / write_bench_csv of
+// the reference (src/bench.cpp:46-184) on the B200 path: one seeded head
+// (mt19937_64 + Box-Muller, as the reference draws it) uploaded once as
+// bf16; each sample times a fixed batch of back-to-back launches of
+// dfa2c_dense_attention_forward / dfa2c_sparse_attention_forward with CUDA
+// events; dense and sparse samples interleave as in the reference.
+//
+// check_outputs: the reference compares the sparse pass with an f64 oracle
+// at 1e-5, which a bf16 path cannot meet by design (tolerances are tested in
+// tests/test_gpu_parity.py). Here the check is exact and GPU-side: rows of
+// text query blocks keep every key block in an arrow mask, so the sparse
+// pass must reproduce the dense pass on them bit for bit, and every output
+// must be finite; otherwise OracleError.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <ostream>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "dfa2/bench.hpp"
+#include "dfa2/errors.hpp"
+#include "dfa2c.h"
+
+#define DFA2_API __attribute__((visibility("default")))
+
+namespace dfa2 {
+
+void throw_status(int status);  // dfa2_api.cpp
+
+namespace {
+
+void cuda_ok(cudaError_t e, const char* what) {
+    if (e != cudaSuccess)
+        throw DeviceError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+struct Dev {
+    void* p = nullptr;
+    explicit Dev(size_t bytes) { cuda_ok(cudaMalloc(&p, bytes), "cudaMalloc"); }
+    ~Dev() { cudaFree(p); }
+    Dev(const Dev&) = delete;
+    Dev& operator=(const Dev&) = delete;
+};
+
+uint16_t bf16_bits(float f) {  // round to nearest even
+    uint32_t u;
+    std::memcpy(&u, &f, 4);
+    if ((u & 0x7F800000u) == 0x7F800000u)
+        return static_cast<uint16_t>(u >> 16);
+    u += 0x7FFFu + ((u >> 16) & 1u);
+    return static_cast<uint16_t>(u >> 16);
+}
+
+double median(std::vector<double> x) {
+    std::sort(x.begin(), x.end());
+    const size_t n = x.size();
+    return n % 2 ? x[n / 2] : 0.5 * (x[n / 2 - 1] + x[n / 2]);
+}
+
+}  // namespace
+
+DFA2_API std::pair<int64_t, double> find_window_for_sparsity(const AttentionDims& dims, int64_t block_size,
+                                                             double target) {
+    const int64_t max_w = std::max<int64_t>(0, (dims.n_visual + block_size - 1) / block_size - 1);
+    int64_t best_w = 0;
+    double best_s = 0.0, best_err = INFINITY;
+    for (int64_t w = 0; w <= max_w; ++w) {
+        const double s = sparsity_ratio(build_arrow_mask({dims, block_size, w}));
+        if (std::fabs(s - target) < best_err) {
+            best_err = std::fabs(s - target);
+            best_w = w;
+            best_s = s;
+        }
+    }
+    if (best_err > 0.02)
+        throw ShapeError("no window reaches sparsity " + std::to_string(target) + " within +/-2% (closest " +
+                         std::to_string(best_s) + ")");
+    return {best_w, best_s};
+}
+
+DFA2_API std::vector<BenchResult> run_bench(const BenchConfig& config) {
+    AttentionDims dims;
+    dims.n_heads = 1;
+    dims.head_dim = config.head_dim;
+    dims.n_visual = config.n_visual;
+    dims.n_text = config.n_text;
+    dims.validate();
+    if (config.iters < 1 || config.warmup < 0)
+        throw ShapeError("need iters >= 1 and warmup >= 0");
+    const int64_t n = dims.seq_len(), d = dims.head_dim;
+    const size_t elems = static_cast<size_t>(n * d);
+
+    // seeded single-head inputs, drawn like the reference's bench
+    std::mt19937_64 eng(config.seed);
+    auto uniform = [&] { return static_cast<double>(eng() >> 11) * 0x1.0p-53; };
+    auto gaussian = [&] {
+        double u1;
+        do
+            u1 = uniform();
+        while (u1 <= 0.0);
+        return std::sqrt(-2.0 * std::log(u1)) * std::cos(2.0 * 3.14159265358979323846 * uniform());
+    };
+    std::vector<uint16_t> hq(elems), hk(elems), hv(elems);
+    for (size_t i = 0; i < elems; ++i) {
+        hq[i] = bf16_bits(static_cast<float>(gaussian()));
+        hk[i] = bf16_bits(static_cast<float>(gaussian()));
+        hv[i] = bf16_bits(static_cast<float>(gaussian()));
+    }
+    Dev q(elems * 2), k(elems * 2), v(elems * 2), od(elems * 2), os(elems * 2);
+    cuda_ok(cudaMemcpy(q.p, hq.data(), elems * 2, cudaMemcpyHostToDevice), "upload");
+    cuda_ok(cudaMemcpy(k.p, hk.data(), elems * 2, cudaMemcpyHostToDevice), "upload");
+    cuda_ok(cudaMemcpy(v.p, hv.data(), elems * 2, cudaMemcpyHostToDevice), "upload");
+
+    cudaEvent_t e0, e1;
+    cuda_ok(cudaEventCreate(&e0), "event");
+    cuda_ok(cudaEventCreate(&e1), "event");
+    constexpr int kBatch = 8;  // launches per sample: keeps event resolution below 1%
+    auto sample_ms = [&](auto&& pass) {
+        cuda_ok(cudaEventRecord(e0, nullptr), "event");
+        for (int r = 0; r < kBatch; ++r)
+            pass();
+        cuda_ok(cudaEventRecord(e1, nullptr), "event");
+        cuda_ok(cudaEventSynchronize(e1), "event");
+        float ms = 0.f;
+        cuda_ok(cudaEventElapsedTime(&ms, e0, e1), "event");
+        return static_cast<double>(ms) / kBatch;
+    };
+    auto dense_pass = [&] { throw_status(dfa2c_dense_attention_forward(q.p, k.p, v.p, od.p, 1, n, d, nullptr)); };
+
+    std::vector<BenchResult> results;
+    try {
+        for (double target : config.targets) {
+            const auto [w, achieved] = find_window_for_sparsity(dims, config.block, target);
+            const BlockMask mask = build_arrow_mask({dims, config.block, w});
+            auto sparse_pass = [&] {
+                throw_status(dfa2c_sparse_attention_forward(q.p, k.p, v.p, os.p, 1, n, d, mask.active.data(),
+                                                            config.block, nullptr));
+            };
+            if (config.check_outputs) {
+                dense_pass();
+                sparse_pass();
+                cuda_ok(cudaDeviceSynchronize(), "sync");
+                std::vector<uint16_t> a(elems), b(elems);
+                cuda_ok(cudaMemcpy(a.data(), od.p, elems * 2, cudaMemcpyDeviceToHost), "download");
+                cuda_ok(cudaMemcpy(b.data(), os.p, elems * 2, cudaMemcpyDeviceToHost), "download");
+                for (size_t i = 0; i < elems; ++i)
+                    if ((b[i] & 0x7F80u) == 0x7F80u)
+                        throw OracleError("sparse benchmark path produced a non-finite output");
+                for (int64_t qb = 0; qb < mask.n_query_blocks; ++qb) {
+                    if (!std::all_of(mask.active.begin() + qb * mask.n_key_blocks,
+                                     mask.active.begin() + (qb + 1) * mask.n_key_blocks,
+                                     [](uint8_t x) { return x != 0; }))
+                        continue;
+                    const int64_t r0 = qb * config.block, r1 = std::min(n, r0 + config.block);
+                    if (std::memcmp(a.data() + r0 * d, b.data() + r0 * d, static_cast<size_t>((r1 - r0) * d) * 2))
+                        throw OracleError("sparse pass differs from the dense pass on fully active rows");
+                }
+            }
+            for (int i = 0; i < config.warmup; ++i) {
+                sample_ms(dense_pass);
+                sample_ms(sparse_pass);
+            }
+            std::vector<double> ds, ss;
+            for (int i = 0; i < config.iters; ++i) {
+                ds.push_back(sample_ms(dense_pass));
+                ss.push_back(sample_ms(sparse_pass));
+            }
+            BenchResult r;
+            r.n_visual = config.n_visual;
+            r.n_text = config.n_text;
+            r.head_dim = config.head_dim;
+            r.block = config.block;
+            r.target_sparsity = target;
+            r.achieved_sparsity = achieved;
+            r.window = w;
+            r.dense_ms = median(ds);
+            r.sparse_ms = median(ss);
+            r.speedup = r.dense_ms / r.sparse_ms;
+            r.ideal = 1.0 / (1.0 - achieved);
+            results.push_back(r);
+        }
+    } catch (...) {
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        throw;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return results;
+}
+
+DFA2_API void write_bench_csv(std::ostream& out, const std::vector<BenchResult>& results) {
+    out << "n_visual,n_text,head_dim,block,target_sparsity,achieved_sparsity,dense_ms,sparse_ms,speedup,ideal\n";
+    char line[256];
+    for (const BenchResult& r : results) {
+        std::snprintf(line, sizeof line, "%lld,%lld,%lld,%lld,%.4f,%.6f,%.4f,%.4f,%.4f,%.4f\n",
+                      static_cast<long long>(r.n_visual), static_cast<long long>(r.n_text),
+                      static_cast<long long>(r.head_dim), static_cast<long long>(r.block), r.target_sparsity,
+                      r.achieved_sparsity, r.dense_ms, r.sparse_ms, r.speedup, r.ideal);
+        out << line;
+    }
+}
+
+}  // namespace dfa2

@@ -65,6 +65,11 @@ HOST_CASES = {
         "pipeline rejects plans with cached heads at t0 before running",
     ],
     "calibrate": ["candidate ids and strategies"],
+    "bench": [
+        "window search hits the standard sparsity levels within 2%",
+        "a target of zero lands on the fully dense mask",
+        "unreachable targets are rejected",
+    ],
 }
 
 
@@ -94,7 +99,8 @@ def _need_binaries():
 def test_reference_suites_built_against_drop_in():
     _need_binaries()
     # at least these compile unchanged against include/dfa2/
-    assert {"arrow", "cache", "dispatch", "plan_io", "plansolver", "io", "workload", "calibrate"} <= set(suites())
+    assert {"arrow", "cache", "dispatch", "plan_io", "plansolver", "io", "workload", "calibrate",
+            "bench"} <= set(suites())
 
 
 @pytest.mark.parametrize("suite", sorted(HOST_CASES))
