@@ -57,9 +57,31 @@ def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=()
     return out
 
 
+CLI = os.path.join(HERE, "bin", "dfa2")
+CLI_SOURCES = [os.path.join(CSRC, "cli", "dfa2_main.cpp"), os.path.join(CSRC, "json_lite.cpp")]
+
+
+def build_cli(force: bool = False) -> str:
+    """The `dfa2` command-line front end (calibrate | run | verify | bench |
+    workload, the reference CLI's subcommands) linked against libdfa2_b200.so."""
+    deps = CLI_SOURCES + [LIB, os.path.join(CSRC, "json_lite.h")]
+    inc = os.path.join(ROOT, "include", "dfa2")
+    deps += [os.path.join(inc, f) for f in os.listdir(inc)]
+    if not force and not _stale(CLI, deps):
+        return CLI
+    os.makedirs(os.path.dirname(CLI), exist_ok=True)
+    cmd = [os.environ.get("CXX", "g++"), "-std=c++20", "-O2", "-I", os.path.join(ROOT, "include"), "-I", CSRC,
+           *CLI_SOURCES, "-o", CLI + ".tmp", "-L", HERE, "-ldfa2_b200", "-Wl,-rpath,$ORIGIN/.."]
+    subprocess.run(cmd, check=True)
+    os.replace(CLI + ".tmp", CLI)
+    return CLI
+
+
 if __name__ == "__main__":
     # python -m paper_2503_22796_b200.build [--force] [-v] [--out PATH] [-DNAME=VAL ...]
     argv = sys.argv[1:]
     out = argv[argv.index("--out") + 1] if "--out" in argv else LIB
     defs = [a[2:] for a in argv if a.startswith("-D")]
     print(build(force="--force" in argv or bool(defs), verbose="-v" in argv, out=out, defines=defs))
+    if out == LIB:
+        print(build_cli(force="--force" in argv))

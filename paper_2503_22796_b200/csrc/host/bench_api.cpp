@@ -94,6 +94,10 @@ DFA2_API std::vector<BenchResult> run_bench(const BenchConfig& config) {
         throw ShapeError("need iters >= 1 and warmup >= 0");
     const int64_t n = dims.seq_len(), d = dims.head_dim;
     const size_t elems = static_cast<size_t>(n * d);
+    // every target resolves to a window before any device work
+    std::vector<std::pair<int64_t, double>> windows;
+    for (double target : config.targets)
+        windows.push_back(find_window_for_sparsity(dims, config.block, target));
 
     // seeded single-head inputs, drawn like the reference's bench
     std::mt19937_64 eng(config.seed);
@@ -134,8 +138,9 @@ DFA2_API std::vector<BenchResult> run_bench(const BenchConfig& config) {
 
     std::vector<BenchResult> results;
     try {
-        for (double target : config.targets) {
-            const auto [w, achieved] = find_window_for_sparsity(dims, config.block, target);
+        for (size_t ti = 0; ti < config.targets.size(); ++ti) {
+            const double target = config.targets[ti];
+            const auto [w, achieved] = windows[ti];
             const BlockMask mask = build_arrow_mask({dims, config.block, w});
             auto sparse_pass = [&] {
                 throw_status(dfa2c_sparse_attention_forward(q.p, k.p, v.p, os.p, 1, n, d, mask.active.data(),

@@ -70,6 +70,12 @@ HOST_CASES = {
         "a target of zero lands on the fully dense mask",
         "unreachable targets are rejected",
     ],
+    # test_cli drives the repo's `dfa2` front end (paper_2503_22796_b200/bin/dfa2)
+    "cli": [
+        "bench rejects unreachable sparsity targets",
+        "workload export writes DFA2 dumps deterministically",
+        "unknown flags are validation errors",
+    ],
 }
 
 
@@ -100,7 +106,7 @@ def test_reference_suites_built_against_drop_in():
     _need_binaries()
     # at least these compile unchanged against include/dfa2/
     assert {"arrow", "cache", "dispatch", "plan_io", "plansolver", "io", "workload", "calibrate",
-            "bench"} <= set(suites())
+            "bench", "cli"} <= set(suites())
 
 
 @pytest.mark.parametrize("suite", sorted(HOST_CASES))
