@@ -598,6 +598,167 @@ def influence_for_layer(q, k, v, methods: Sequence[MethodCandidate], cache: Opti
     return LayerInfluence(original, outs, infl)
 
 
+# --------------------------------------------------------------- calibration driver
+class InfluenceTable:
+    """InfluenceTable (inc/calibrate.hpp:32-58; src/calibrate.cpp:105-191):
+    measured I(t, layer, head, method), NaN where unmeasured (ineligible)."""
+
+    HEADER = "t,layer,head,method,influence"
+
+    def __init__(self, t: int, layers: int, heads: int, method_ids: Sequence[str]):
+        self.method_ids = list(method_ids)
+        self.values = np.full((t, layers, heads, len(self.method_ids)), np.nan)
+
+    def _check(self, t, layer, head, m):
+        T, L, H, M = self.values.shape
+        if not (0 <= t < T and 0 <= layer < L and 0 <= head < H and 0 <= m < M):
+            raise ShapeError("influence index out of range")
+
+    def get(self, t: int, layer: int, head: int, m: int) -> float:
+        self._check(t, layer, head, m)
+        return float(self.values[t, layer, head, m])
+
+    def set(self, t: int, layer: int, head: int, m: int, v: float) -> None:
+        self._check(t, layer, head, m)
+        self.values[t, layer, head, m] = v
+
+    def measured(self, t: int, layer: int, head: int, m: int) -> bool:
+        return not math.isnan(self.get(t, layer, head, m))
+
+    def to_csv(self) -> str:
+        """17 significant digits, so values round-trip exactly."""
+        rows = [self.HEADER]
+        T, L, H, M = self.values.shape
+        for t in range(T):
+            for l in range(L):
+                for h in range(H):
+                    for m in range(M):
+                        v = self.values[t, l, h, m]
+                        if not math.isnan(v):
+                            rows.append(f"{t},{l},{h},{self.method_ids[m]},{v:.17g}")
+        return "\n".join(rows) + "\n"
+
+    @staticmethod
+    def parse_csv(text: str, t: int, layers: int, heads: int, method_ids: Sequence[str]) -> "InfluenceTable":
+        """parse_influence_csv (inc/calibrate.hpp:61-63); IoError on a bad header or unknown method."""
+        table = InfluenceTable(t, layers, heads, method_ids)
+        col = {m: i for i, m in enumerate(method_ids)}
+        lines = text.split("\n")
+        if not lines or lines[0] != InfluenceTable.HEADER:
+            raise IoError("influence CSV header mismatch")
+        for line in lines[1:]:
+            if not line:
+                continue
+            f = line.split(",")
+            if len(f) != 5 or f[3] not in col:
+                raise IoError(f"bad influence CSV row: {line}")
+            table.set(int(f[0]), int(f[1]), int(f[2]), col[f[3]], float(f[4]))
+        return table
+
+
+@dataclass
+class CalibrationConfig:
+    """CalibrationConfig (inc/calibrate.hpp:88-93)."""
+
+    methods: List["MethodCandidate"] = field(default_factory=list)
+    delta: float = 0.4
+    coeff: float = 1.5
+    rse_mode: int = 0
+
+
+@dataclass
+class CalibrationResult:
+    """CalibrationResult (inc/calibrate.hpp:95-99)."""
+
+    plan: "CompressionPlan"
+    influences: InfluenceTable
+    stats: "CalibrationStats"
+    budget_spent: List[float] = field(default_factory=list)  # [T * L]
+    objective: List[float] = field(default_factory=list)     # [T * L]
+    wall_seconds: float = 0.0
+    outputs: List[object] = field(default_factory=list)      # [T * L] spliced layer outputs (keep_outputs)
+
+
+def calibrate_model(q_stream, k_stream, v_stream, dims: "AttentionDims", n_timesteps: int, n_layers: int,
+                    block_size: int, config: CalibrationConfig, cache: Optional["HeadCache"] = None,
+                    keep_outputs: bool = False) -> CalibrationResult:
+    """calibrate_model (inc/calibrate.hpp:101-105; src/calibrate.cpp:255-348),
+    GPU-resident: for each (t, layer) in forward order, influence_for_layer
+    (1 + |M| fused launches + RSE kernels) on the already-compressed stream,
+    the exact per-layer solve (host, microseconds), and the splice: each
+    computed head commits the output of its chosen measurement pass to the
+    device cache (no extra attention evaluation); Cached heads keep their
+    slot. q_stream(t, l) etc. give the [H, N, d] device inputs. keep_outputs
+    records each layer's spliced output (what the plan's run_pipeline must
+    reproduce bit for bit)."""
+    import time
+
+    torch = _torch()
+    if not config.methods:
+        raise ShapeError("candidate set must be nonempty")
+    if not (config.delta >= 0.0):
+        raise ShapeError("delta must be >= 0")
+    if not (config.coeff >= 1.0):
+        raise ShapeError("coeff must be >= 1")
+    t0 = time.perf_counter()
+    H, M = dims.n_heads, len(config.methods)
+    strategies = [m.strategy for m in config.methods]
+    costs = analytic_costs(dims, block_size, strategies)
+    plan = CompressionPlan(dims, n_timesteps, n_layers, block_size, config.delta, config.coeff,
+                           [s.window_blocks for s in strategies if s.kind == StrategyKind.arrow],
+                           [LayerPlan() for _ in range(n_timesteps * n_layers)])
+    table = InfluenceTable(n_timesteps, n_layers, H, [m.id for m in config.methods])
+    stats = CalibrationStats()
+    res = CalibrationResult(plan, table, stats)
+    if cache is None:
+        cache = HeadCache(n_layers, H, dims.seq_len(), dims.head_dim)
+    for t in range(n_timesteps):
+        for l in range(n_layers):
+            li = influence_for_layer(q_stream(t, l), k_stream(t, l), v_stream(t, l), config.methods, cache, l, t,
+                                     dims, block_size, config.rse_mode, stats, keep_outputs=True)
+            grid = li.influence.reshape(H, M)
+            finite = np.isfinite(grid)
+            table.values[t, l][finite] = grid[finite]
+            sol = solve(PlanProblem(H, M, li.influence, costs, config.delta, config.coeff))
+            res.budget_spent.append(sol.total_influence)
+            res.objective.append(sol.objective)
+            plan.layers[t * n_layers + l] = to_layer_plan(sol, strategies)
+            if keep_outputs:
+                res.outputs.append(torch.stack([li.original[h] if c == kFullChoice else li.method_outputs[c][h]
+                                                for h, c in enumerate(sol.choice)]))
+            for h, c in enumerate(sol.choice):
+                if c == kFullChoice:
+                    cache.store(l, h, li.original[h], t)
+                elif strategies[c].kind == StrategyKind.arrow:
+                    cache.store(l, h, li.method_outputs[c][h], t)
+    res.wall_seconds = time.perf_counter() - t0
+    return res
+
+
+def audit_plan_constraints(plan: "CompressionPlan", influences: InfluenceTable) -> int:
+    """audit_plan_constraints (inc/calibrate.hpp:107-110; src/calibrate.cpp:350-382):
+    number of budget / cap violations (0 for any plan calibrate_model emits)."""
+    plan.validate()
+    col = {m: i for i, m in enumerate(influences.method_ids)}
+    cap = selection_cap(plan.coeff, plan.dims.n_heads, plan.delta)
+    bad = 0
+    for t in range(plan.n_timesteps):
+        for l in range(plan.n_layers):
+            spent = 0.0
+            for h, s_ in enumerate(plan.at(t, l).strategies):
+                if s_.kind == StrategyKind.full:
+                    continue
+                m = col.get(method_id(s_))
+                if m is None or not influences.measured(t, l, h, m):
+                    bad += 1
+                    continue
+                v = influences.get(t, l, h, m)
+                spent += v
+                bad += 1 if v > cap else 0
+            bad += 1 if spent > plan.delta else 0
+    return bad
+
+
 # --------------------------------------------------------------- plan selection
 kFullChoice = -1
 

@@ -7,8 +7,9 @@
   cfg4  FLUX 2K 28-step x 57-layer schedule with one shared device cache
         (5 F, 9 A8, 4 A0, 6 C per layer for t >= 1, rotated per (t, l);
         all Full at t = 0), one sample per GPU (batch 8 over 8 GPUs = 8x this)
-  cfg5  FLUX-shaped calibration sweep: influence_for_layer over 57 layers,
-        candidates Arrow {0, 2, 8, 16, 32} + Cached, plus the RSE kernel alone
+  cfg5  FLUX-shaped progressive calibration (calibrate_model) over 57 layers
+        x 2 timesteps, candidates Arrow {0, 2, 8, 16, 32} + Cached, plus the
+        RSE kernel alone
 All timings: CUDA events, warm-up first; inputs resident in HBM.
 """
 import argparse
@@ -129,28 +130,36 @@ if "4" in only:
     del qs, cache
 
 if "5" in only:
-    L, H, nv, nt, d, B = 57, 24, 16384, 512, 128, 128
+    # the progressive calibration driver at FLUX 2K scale: every layer of a
+    # 57-layer model at t = 0 (Cached ineligible) and t = 1 (Cached measured
+    # against the t = 0 commits), candidates Arrow {0, 2, 8, 16, 32} + Cached;
+    # per layer 1 + 6 fused launches, 6 RSE launches, the exact solve and the
+    # device-side splice into the cache
+    L, H, nv, nt, d, B, T = 57, 24, 16384, 512, 128, 128, 2
     n = nv + nt
     dims = api.AttentionDims(H, d, nv, nt)
     q, k, v = (randn(s, H, n, d) for s in (1, 2, 3))
-    cache = api.HeadCache(L, H, n, d)
-    for l in range(L):  # t = 0: every slot produced
-        api.multi_strategy_attention(q, k, v, api.LayerPlan.all_full(H), cache, l, 0, dims, B)
-    methods = api.make_candidates([0, 2, 8, 16, 32], include_cached=True)
-    stats = api.CalibrationStats()
-    api.influence_for_layer(q, k, v, methods, cache, 0, 1, dims, B, stats=stats, keep_outputs=False)
+    qs = [q, (q.float() + 0.05 * randn(4, H, n, d).float()).to(torch.bfloat16)]
+    cfg = api.CalibrationConfig(api.make_candidates([0, 2, 8, 16, 32], include_cached=True), 0.4, 1.5)
+    warm = api.calibrate_model(lambda t, l: qs[t], lambda t, l: k, lambda t, l: v, dims, 2, 1, B, cfg)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    for l in range(L):
-        li = api.influence_for_layer(q, k, v, methods, cache, l, 1, dims, B, stats=stats, keep_outputs=False)
+    r = api.calibrate_model(lambda t, l: qs[t], lambda t, l: k, lambda t, l: v, dims, T, L, B, cfg)
     torch.cuda.synchronize()
     sweep_s = time.perf_counter() - t0
+    kinds = {}
+    for lp in r.plan.layers[L:]:
+        for s_ in lp.strategies:
+            kinds[api.method_id(s_)] = kinds.get(api.method_id(s_), 0) + 1
     # the RSE kernel alone: 24 heads x [N, d] bf16, 2 operands
     a, b = randn(7, H, n, d), randn(8, H, n, d)
-    ms = time_calls(lambda: api.rse_per_head(a, b), 20)
+    dev = torch.empty(H, device="cuda", dtype=torch.float64)
+    ms = time_calls(lambda: api.rse_per_head_async(a, b, dev), 20)
     bytes_ = 2 * a.numel() * 2
-    out = {"layers": L, "candidates": [m.id for m in methods], "sweep_s": sweep_s, "per_layer_ms": 1e3 * sweep_s / L,
-           "attention_evals": stats.attention_evals, "influence_example": [float(x) for x in li.influence[:6]],
+    out = {"layers": L, "timesteps": T, "candidates": [m.id for m in cfg.methods], "calibration_s": sweep_s,
+           "per_layer_ms": 1e3 * sweep_s / (T * L), "attention_evals": r.stats.attention_evals,
+           "aggregate_sparsity": r.plan.aggregate_sparsity(), "t1_choices": kinds,
+           "audit_violations": api.audit_plan_constraints(r.plan, r.influences),
            "rse_ms": ms, "rse_bytes": bytes_, "rse_gbs": bytes_ / ms / 1e6}
     res["cfg5_calibration"] = out
     print("cfg5", json.dumps(out))
