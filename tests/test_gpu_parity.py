@@ -72,6 +72,13 @@ CASES = [
     (2, 130, 17, 128, 16, 0, "A0 A3"),          # small ragged
     (2, 600, 50, 64, 200, 0, "A0 A1"),          # B > 128
     (2, 17, 3, 64, 8, 0, "A0 F"),               # N < one tile
+    # head dims other than 64 / 128: direct TMA layout for
+    # d % 8 == 0 above 64, zero-padded copies otherwise
+    (2, 300, 20, 96, 64, 0, "F A1"),            # d=96 direct (partial second column box)
+    (2, 200, 10, 100, 32, 1, "A0 F"),           # d=100 padded to 128
+    (3, 256, 32, 32, 32, 0, "A0 A1 F"),         # d=32 padded to 64 (test_arrow.cpp geometry)
+    (2, 130, 7, 8, 16, 0, "F A2"),              # d=8
+    (2, 64, 16, 72, 16, 0, "A0 F"),             # d=72 direct
 ]
 
 
@@ -151,6 +158,27 @@ def test_host_buffer_path_matches_device_path(d, pinned):
     with pytest.raises(CacheMissError):  # validation before any transfer
         api.multi_strategy_attention_host(hq, hk, hv, LayerPlan.parse("C F F F F F F"), HeadCache(1, H, n, d, batch=Bt),
                                           0, 1, dims, B)
+
+
+def test_padded_head_dim_cache_semantics():
+    """The zero-padded path (d % 8 != 0) keeps the fused call's cache rules:
+    cached heads are the stored slot bit for bit, computed heads commit."""
+    t = torch()
+    H, nv, nt, d, B = 4, 200, 20, 40, 32
+    n = nv + nt
+    dims = AttentionDims(H, d, nv, nt)
+    cache = HeadCache(1, H, n, d)
+    q, _ = bf16_inputs((H, n, d), 61)
+    o0 = api.multi_strategy_attention(q, q, q, LayerPlan.all_full(H), cache, 0, 0, dims, B)
+    q1, q1n = bf16_inputs((H, n, d), 62)
+    lp = LayerPlan.parse("C A0 F C")
+    o1 = api.multi_strategy_attention(q1, q1, q1, lp, cache, 0, 1, dims, B)
+    t.cuda.synchronize()
+    assert t.equal(o1[0], o0[0]) and t.equal(o1[3], o0[3])
+    assert [cache.produced_at(0, h) for h in range(H)] == [0, 1, 1, 0]
+    for h in (1, 2):
+        assert t.equal(cache.fetch(0, h), o1[h])
+        check_close(to_np(o1[h]), oracle_head(q1n[h], q1n[h], q1n[h], dims, B, lp.strategies[h]))
 
 
 def test_cache_miss_is_raised_before_any_compute():
