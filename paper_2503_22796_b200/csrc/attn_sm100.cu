@@ -72,6 +72,12 @@ struct Cfg {
 #ifndef DFA2_TRACE
 #define DFA2_TRACE 0
 #endif
+
+// Row max: keys 0..63 are loaded and reduced (8 chains) while keys 64..127
+// are still in flight from TMEM (1), or everything loads first (0).
+#ifndef DFA2_SPLITLD
+#define DFA2_SPLITLD 1
+#endif
 // trace[((lane * 4096) + tile) * 8 + slot] = clock64() for CTA 0 (debug builds)
 #define DFA2_STAMP(L_, j_, k_)                                                          \
     do {                                                                                \
@@ -194,6 +200,32 @@ __device__ __forceinline__ void softmax_tile(uint32_t sc, uint32_t oc, float sl2
     float mx;
     {
         uint32_t lo[64];
+#if DFA2_SPLITLD
+        // keys 0..63 first; their max chains run while keys 64..127 load
+        tmem_ld32(sc, lo);
+        tmem_ld32(sc + 32, lo + 32);
+        tmem_ld_wait();
+        tmem_ld32(sc + 64, hi);
+        tmem_ld32(sc + 96, hi + 32);
+        float mm[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            mm[j] = fmaxf(__uint_as_float(lo[2 * j]), __uint_as_float(lo[2 * j + 1]));
+#pragma unroll
+        for (int c = 16; c < 64; c += 16)
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                mm[j] = fmaxf(mm[j], fmaxf(__uint_as_float(lo[c + 2 * j]), __uint_as_float(lo[c + 2 * j + 1])));
+        tmem_ld_wait();
+        DFA2_SSTAMP(3);
+#pragma unroll
+        for (int c = 0; c < 64; c += 16)
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                mm[j] = fmaxf(mm[j], fmaxf(__uint_as_float(hi[c + 2 * j]), __uint_as_float(hi[c + 2 * j + 1])));
+        mx = fmaxf(fmaxf(fmaxf(mm[0], mm[1]), fmaxf(mm[2], mm[3])), fmaxf(fmaxf(mm[4], mm[5]), fmaxf(mm[6], mm[7]))) *
+             sl2;
+#else
         tmem_ld32(sc, lo);
         tmem_ld32(sc + 32, lo + 32);
         tmem_ld32(sc + 64, hi);
@@ -209,6 +241,7 @@ __device__ __forceinline__ void softmax_tile(uint32_t sc, uint32_t oc, float sl2
             m3 = fmaxf(m3, fmaxf(__uint_as_float(hi[c + 2]), __uint_as_float(hi[c + 3])));
         }
         mx = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3)) * sl2;
+#endif
     }
     // lazy rescale: keep the reference max unless the tile max exceeds it by
     // more than 8 (P <= 2^8 stays exact in fp32 and representable in bf16)
