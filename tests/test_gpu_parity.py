@@ -79,6 +79,8 @@ CASES = [
     (3, 256, 32, 32, 32, 0, "A0 A1 F"),         # d=32 padded to 64 (test_arrow.cpp geometry)
     (2, 130, 7, 8, 16, 0, "F A2"),              # d=8
     (2, 64, 16, 72, 16, 0, "A0 F"),             # d=72 direct
+    (2, 512, 0, 128, 128, 0, "A0 A1"),          # no text band: block-diagonal (test_arrow.cpp:76-81)
+    (1, 4096, 333, 64, 128, 1, "A8"),           # SD3 geometry, text-first, one head
 ]
 
 
