@@ -180,6 +180,12 @@ int dfa2c_rse(const void* y_m, const void* y_o, int32_t dtype, int64_t n_heads,
 int dfa2c_rse_async(const void* y_m, const void* y_o, int32_t dtype, int64_t n_heads,
                     int64_t numel, int32_t mode, double* out_dev, void* stream);
 
+/* Element-type conversion of n device elements (DFA2C_BF16 / F32 / F64;
+ * to bf16: round to nearest even). The C++ drop-in converts the reference's
+ * f32 host tensors on the device with it. Asynchronous on `stream`. */
+int dfa2c_convert(const void* src, int32_t src_dtype, void* dst, int32_t dst_dtype, int64_t n,
+                  void* stream);
+
 /* influence_for_layer (inc/calibrate.hpp:80-86; src/calibrate.cpp:193-253)
  * for one sample (batch 1): 1 original (all Full) + |M| candidate
  * evaluations, M = n_windows Arrow(w) candidates then Cached when

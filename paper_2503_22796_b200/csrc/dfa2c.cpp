@@ -29,6 +29,8 @@ cudaError_t launch_attn(int d, const CUtensorMap& tq, const CUtensorMap& tk, con
                         const CUtensorMap& to, const CUtensorMap& tc, const AttnArgs& args, int grid,
                         cudaStream_t stream);
 int rse_ctas_per_sm();
+cudaError_t launch_convert(const void* src, int src_dtype, void* dst, int dst_dtype, int64_t n, int sms,
+                           cudaStream_t stream);
 cudaError_t launch_rse(const void* ym, const void* yo, int dtype, int64_t n_heads, int64_t numel,
                        int mode, double* out_dev, double* scratch, int nblk, cudaStream_t stream);
 }  // namespace dfa2k
@@ -1343,6 +1345,21 @@ int dfa2c_influence_for_layer(const void* q, const void* k, const void* v, const
             }
         if (evals)
             *evals += 1 + M;
+    });
+}
+
+int dfa2c_convert(const void* src, int32_t src_dtype, void* dst, int32_t dst_dtype, int64_t n, void* stream) {
+    return guard([&] {
+        for (int32_t dt : {src_dtype, dst_dtype})
+            if (dt != DFA2C_BF16 && dt != DFA2C_F32 && dt != DFA2C_F64)
+                fail(DFA2C_SHAPE, "dtype must be DFA2C_BF16, DFA2C_F32 or DFA2C_F64");
+        if (n < 0 || (n > 0 && (!src || !dst)))
+            fail(DFA2C_SHAPE, "convert needs device buffers and n >= 0");
+        int device = 0;
+        DFA2C_CUDA_CHECK(cudaGetDevice(&device));
+        DFA2C_CUDA_CHECK(dfa2k::launch_convert(src, src_dtype, dst, dst_dtype, n, num_sms(device), as_stream(stream)));
+        if (n > 0)
+            g_launches.fetch_add(1);
     });
 }
 

@@ -14,6 +14,7 @@
 #include <cstring>
 #include <limits>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "dfa2/arrow.hpp"
@@ -65,23 +66,6 @@ int64_t shape_numel(const std::vector<int64_t>& shape) {
     return n;
 }
 
-uint16_t to_bf16(float f) {
-    uint32_t u;
-    std::memcpy(&u, &f, 4);
-    if ((u & 0x7f800000u) != 0x7f800000u)
-        u += 0x7fffu + ((u >> 16) & 1u);
-    else if (u & 0x007fffffu)
-        u |= 0x00400000u;  // quiet NaN
-    return static_cast<uint16_t>(u >> 16);
-}
-
-float from_bf16(uint16_t b) {
-    const uint32_t u = static_cast<uint32_t>(b) << 16;
-    float f;
-    std::memcpy(&f, &u, 4);
-    return f;
-}
-
 // Owning device buffer.
 struct DevBuf {
     void* p = nullptr;
@@ -92,19 +76,133 @@ struct DevBuf {
     DevBuf& operator=(const DevBuf&) = delete;
 };
 
-// f32 host values -> bf16 device buffer.
+// Per-thread device staging for f32 transfers (grow-only).
+struct Staging {
+    void* p = nullptr;
+    size_t bytes = 0;
+    ~Staging() {
+        if (p)
+            cudaFree(p);
+    }
+    void* get(size_t n) {
+        if (n > bytes) {
+            if (p)
+                cuda_check(cudaFree(p), "cudaFree");
+            p = nullptr;
+            cuda_check(cudaMalloc(&p, n), "cudaMalloc");
+            bytes = n;
+        }
+        return p;
+    }
+};
+thread_local Staging g_stage;
+
+// Host <-> device mover for the reference's pageable host tensors: 32 MB
+// chunks go through two pinned buffers, filled / drained by all host cores
+// in parallel, while the previous chunk is in flight on a copy stream.
+// Synchronous for the caller, like the reference API.
+class HostMover {
+public:
+    static constexpr size_t kChunk = size_t{32} << 20;
+    ~HostMover() {
+        for (int i = 0; i < 2; ++i) {
+            if (pin_[i])
+                cudaFreeHost(pin_[i]);
+            if (ev_[i])
+                cudaEventDestroy(ev_[i]);
+        }
+        if (st_)
+            cudaStreamDestroy(st_);
+    }
+    void up(const void* src, void* dst_dev, size_t bytes) { move(src, dst_dev, bytes, true); }
+    void down(const void* src_dev, void* dst, size_t bytes) { move(src_dev, dst, bytes, false); }
+
+private:
+    void init() {
+        if (st_)
+            return;
+        cuda_check(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking), "stream");
+        for (int i = 0; i < 2; ++i) {
+            cuda_check(cudaMallocHost(&pin_[i], kChunk), "cudaMallocHost");
+            cuda_check(cudaEventCreateWithFlags(&ev_[i], cudaEventDisableTiming), "event");
+        }
+    }
+    static void par_copy(void* dst, const void* src, size_t bytes) {
+        const size_t workers = std::max<size_t>(1, std::min<size_t>(std::thread::hardware_concurrency(),
+                                                                    bytes / (size_t{1} << 20)));
+        if (workers == 1) {
+            std::memcpy(dst, src, bytes);
+            return;
+        }
+        std::vector<std::thread> pool;
+        const size_t per = (bytes + workers - 1) / workers;
+        for (size_t w = 0; w < workers; ++w) {
+            const size_t lo = w * per, hi = std::min(bytes, lo + per);
+            if (lo < hi)
+                pool.emplace_back([=] {
+                    std::memcpy(static_cast<char*>(dst) + lo, static_cast<const char*>(src) + lo, hi - lo);
+                });
+        }
+        for (std::thread& t : pool)
+            t.join();
+    }
+    void move(const void* src, void* dst, size_t bytes, bool to_device) {
+        init();
+        cuda_check(cudaDeviceSynchronize(), "sync");  // device-side producers of `src` (downloads) are done
+        bool pending[2] = {false, false};
+        size_t pending_off[2] = {0, 0}, pending_len[2] = {0, 0};
+        int b = 0;
+        for (size_t off = 0; off < bytes; off += kChunk, b ^= 1) {
+            const size_t len = std::min(kChunk, bytes - off);
+            if (pending[b]) {  // this pinned buffer's previous transfer must finish first
+                cuda_check(cudaEventSynchronize(ev_[b]), "event");
+                if (!to_device)
+                    par_copy(static_cast<char*>(dst) + pending_off[b], pin_[b], pending_len[b]);
+            }
+            if (to_device) {
+                par_copy(pin_[b], static_cast<const char*>(src) + off, len);
+                cuda_check(cudaMemcpyAsync(static_cast<char*>(dst) + off, pin_[b], len, cudaMemcpyHostToDevice, st_),
+                           "upload");
+            } else {
+                cuda_check(cudaMemcpyAsync(pin_[b], static_cast<const char*>(src) + off, len, cudaMemcpyDeviceToHost,
+                                           st_),
+                           "download");
+            }
+            cuda_check(cudaEventRecord(ev_[b], st_), "event");
+            pending[b] = true;
+            pending_off[b] = off;
+            pending_len[b] = len;
+        }
+        for (int j = 0; j < 2; ++j) {  // drain both buffers
+            if (!pending[j])
+                continue;
+            cuda_check(cudaEventSynchronize(ev_[j]), "event");
+            if (!to_device)
+                par_copy(static_cast<char*>(dst) + pending_off[j], pin_[j], pending_len[j]);
+        }
+    }
+    cudaStream_t st_ = nullptr;
+    void* pin_[2] = {nullptr, nullptr};
+    cudaEvent_t ev_[2] = {nullptr, nullptr};
+};
+thread_local HostMover g_mover;
+
+// f32 host values -> bf16 device buffer: the f32 bytes cross PCIe through
+// pinned chunks and are rounded to bf16 on the device (dfa2c_convert).
 void upload_bf16(const float* src, int64_t n, void* dst) {
-    std::vector<uint16_t> h(static_cast<size_t>(n));
-    for (int64_t i = 0; i < n; ++i)
-        h[i] = to_bf16(src[i]);
-    cuda_check(cudaMemcpy(dst, h.data(), h.size() * 2, cudaMemcpyHostToDevice), "upload");
+    if (n <= 0)
+        return;
+    void* f = g_stage.get(static_cast<size_t>(n) * 4);
+    g_mover.up(src, f, static_cast<size_t>(n) * 4);
+    check(dfa2c_convert(f, DFA2C_F32, dst, DFA2C_BF16, n, nullptr));
 }
 
 void download_bf16(const void* src, int64_t n, float* dst) {
-    std::vector<uint16_t> h(static_cast<size_t>(n));
-    cuda_check(cudaMemcpy(h.data(), src, h.size() * 2, cudaMemcpyDeviceToHost), "download");
-    for (int64_t i = 0; i < n; ++i)
-        dst[i] = from_bf16(h[i]);
+    if (n <= 0)
+        return;
+    void* f = g_stage.get(static_cast<size_t>(n) * 4);
+    check(dfa2c_convert(src, DFA2C_BF16, f, DFA2C_F32, n, nullptr));
+    g_mover.down(f, dst, static_cast<size_t>(n) * 4);
 }
 
 // f32 view of a tensor (f64 narrowed).
@@ -486,18 +584,35 @@ DFA2_API Tensor multi_strategy_attention(const Tensor& q, const Tensor& k, const
             throw CacheMissError("plan marks head " + std::to_string(h) + " Cached before it ever computed");
     const int64_t H = dims.n_heads, n = dims.seq_len(), d = dims.head_dim, numel = H * n * d;
     dfa2c_cache* dev = cache.bind(H, n, d);
-    DevBuf dq(numel * 2), dk(numel * 2), dv(numel * 2), dout(numel * 2);
-    upload_bf16(q.f32(), numel, dq.p);
-    upload_bf16(k.f32(), numel, dk.p);
-    upload_bf16(v.f32(), numel, dv.p);
+    thread_local Staging sq, sk, sv, so;  // grow-only device buffers, reused call to call
+    void* dq = sq.get(static_cast<size_t>(numel) * 2);
+    void* dk = sk.get(static_cast<size_t>(numel) * 2);
+    void* dv = sv.get(static_cast<size_t>(numel) * 2);
+    void* dout = so.get(static_cast<size_t>(numel) * 2);
+    // only computed heads' inputs cross PCIe (a Cached head reads its slot),
+    // one transfer per run of consecutive computed heads
+    const int64_t hs = n * d;
+    for (int64_t h0 = 0; h0 < H;) {
+        if (plan.strategies[h0].kind == StrategyKind::cached) {
+            ++h0;
+            continue;
+        }
+        int64_t h1 = h0 + 1;
+        while (h1 < H && plan.strategies[h1].kind != StrategyKind::cached)
+            ++h1;
+        upload_bf16(q.f32() + h0 * hs, (h1 - h0) * hs, static_cast<char*>(dq) + h0 * hs * 2);
+        upload_bf16(k.f32() + h0 * hs, (h1 - h0) * hs, static_cast<char*>(dk) + h0 * hs * 2);
+        upload_bf16(v.f32() + h0 * hs, (h1 - h0) * hs, static_cast<char*>(dv) + h0 * hs * 2);
+        h0 = h1;
+    }
     std::vector<int32_t> kinds;
     std::vector<int64_t> wins;
     plan_arrays(plan, kinds, wins);
     const dfa2c_dims cd = cdims(dims);
-    check(dfa2c_mha_forward(dq.p, dk.p, dv.p, 1, &cd, block_size, kinds.data(), wins.data(), dev, layer, t, dout.p,
+    check(dfa2c_mha_forward(dq, dk, dv, 1, &cd, block_size, kinds.data(), wins.data(), dev, layer, t, dout,
                             nullptr));
     Tensor out = Tensor::zeros(q.shape(), Dtype::f32);
-    download_bf16(dout.p, numel, out.f32());
+    download_bf16(dout, numel, out.f32());
     for (int64_t h = 0; h < H; ++h)
         if (plan.strategies[h].kind != StrategyKind::cached)
             CacheAccess::committed(cache, layer, h, t);
