@@ -38,19 +38,23 @@ struct Cfg {
 #ifndef DFA2_KSTAGES128
 #define DFA2_KSTAGES128 2
 #endif
-    static constexpr int KSTAGES = D == 128 ? DFA2_KSTAGES128 : 5;
+    // Q pair buffers: at d=64 a second one lets the next item's Q load while
+    // the current item still computes (short arrow items switch often); at
+    // d=128 shared memory has no room for it.
+    static constexpr int QBUF = D == 128 ? 1 : 2;
+    static constexpr int KSTAGES = D == 128 ? DFA2_KSTAGES128 : 4;
     static constexpr int VSTAGES = D == 128 ? 2 : 4;
     static constexpr int BOXES = D / 64;                       // 128-byte column boxes
     static constexpr uint32_t BOX_BYTES = 128u * 128u;         // 128 rows x 128 B
     static constexpr uint32_t TILE_BYTES = BOXES * BOX_BYTES;  // one Q, K or V tile
-    static constexpr uint32_t Q_OFF = 0;                       // Q_A, Q_B
-    static constexpr uint32_t K_OFF = 2 * TILE_BYTES;
+    static constexpr uint32_t Q_OFF = 0;                       // [QBUF] x (Q_A, Q_B)
+    static constexpr uint32_t K_OFF = QBUF * 2 * TILE_BYTES;
     static constexpr uint32_t V_OFF = K_OFF + KSTAGES * TILE_BYTES;
     // two 16 KB staging boxes (128 rows x 64 cols bf16, 128B swizzle), one per
     // lane: O epilogue and cached-head copies go smem -> TMA bulk store
     static constexpr uint32_t STG_OFF = V_OFF + VSTAGES * TILE_BYTES;
     static constexpr uint32_t BAR_OFF = STG_OFF + 2 * BOX_BYTES;
-    static constexpr int NBARS = 2 + 2 * KSTAGES + 2 * VSTAGES + 10;
+    static constexpr int NBARS = 2 * QBUF + 2 * KSTAGES + 2 * VSTAGES + 10;
     // The dynamic window starts 1024-aligned (the 1 KB system reservation
     // precedes it); the kernel traps otherwise, so no alignment slack.
     static constexpr uint32_t SMEM_BYTES = BAR_OFF + NBARS * 8 + 16;
@@ -334,22 +338,25 @@ __global__ void __launch_bounds__(384, 1)
     const int lane = threadIdx.x & 31;
 
     const uint32_t bars = sbase + C::BAR_OFF;
-    const uint32_t q_full = bars;
-    const uint32_t q_empty = bars + 8;
-    auto k_full = [&](int s) { return bars + 8u * (2 + s); };
-    auto k_empty = [&](int s) { return bars + 8u * (2 + KS + s); };
-    auto v_full = [&](int s) { return bars + 8u * (2 + 2 * KS + s); };
-    auto v_empty = [&](int s) { return bars + 8u * (2 + 2 * KS + VS + s); };
-    auto s_full = [&](int l) { return bars + 8u * (2 + 2 * KS + 2 * VS + l); };
-    auto p_full = [&](int l) { return bars + 8u * (4 + 2 * KS + 2 * VS + l); };
-    auto o_full = [&](int l) { return bars + 8u * (6 + 2 * KS + 2 * VS + l); };
-    auto p_half = [&](int l) { return bars + 8u * (8 + 2 * KS + 2 * VS + l); };
-    auto c_full = [&](int l) { return bars + 8u * (10 + 2 * KS + 2 * VS + l); };  // copy-box landed
+    constexpr int QB = 2 * C::QBUF;
+    auto q_full = [&](int s) { return bars + 8u * s; };
+    auto q_empty = [&](int s) { return bars + 8u * (C::QBUF + s); };
+    auto k_full = [&](int s) { return bars + 8u * (QB + s); };
+    auto k_empty = [&](int s) { return bars + 8u * (QB + KS + s); };
+    auto v_full = [&](int s) { return bars + 8u * (QB + 2 * KS + s); };
+    auto v_empty = [&](int s) { return bars + 8u * (QB + 2 * KS + VS + s); };
+    auto s_full = [&](int l) { return bars + 8u * (QB + 2 * KS + 2 * VS + l); };
+    auto p_full = [&](int l) { return bars + 8u * (QB + 2 + 2 * KS + 2 * VS + l); };
+    auto o_full = [&](int l) { return bars + 8u * (QB + 4 + 2 * KS + 2 * VS + l); };
+    auto p_half = [&](int l) { return bars + 8u * (QB + 6 + 2 * KS + 2 * VS + l); };
+    auto c_full = [&](int l) { return bars + 8u * (QB + 8 + 2 * KS + 2 * VS + l); };  // copy-box landed
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::BAR_OFF + C::NBARS * 8);
 
     if (threadIdx.x == 0) {
-        mbar_init(q_full, 1);
-        mbar_init(q_empty, 1);
+        for (int s = 0; s < C::QBUF; ++s) {
+            mbar_init(q_full(s), 1);
+            mbar_init(q_empty(s), 1);
+        }
         for (int s = 0; s < KS; ++s) {
             mbar_init(k_full(s), 1);
             mbar_init(k_empty(s), 1);
@@ -395,25 +402,29 @@ __global__ void __launch_bounds__(384, 1)
             Cursor kc{it0, 0}, vc{it0, 0};
             skip_copies(items, it1, kc);
             skip_copies(items, it1, vc);
-            uint32_t kcount = 0, vcount = 0, qcount = 0;
+            uint32_t kcount = 0, vcount = 0, qcount = 0, vitem = 0;
             while (vc.it < it1) {
-                // K runs up to KS-1 tiles ahead of V, but never into the next
-                // item before every V of the current one is issued (the Q pair
-                // buffer is single and freed by the current item's last S).
-                while (kc.it < it1 && kcount < vcount + (KS - 1) && !(kc.j == 0 && kc.it > vc.it)) {
+                // K runs up to KS-1 tiles ahead of V, and into a later item
+                // only while that item's Q pair buffer is free: at most QBUF
+                // items ahead of V's item (each Q buffer is freed by its item's
+                // last S, which needs that item's V stream)
+                while (kc.it < it1 && kcount < vcount + (KS - 1) &&
+                       !(kc.j == 0 && qcount - vitem >= static_cast<uint32_t>(C::QBUF))) {
                     const WorkItem& w = items[kc.it];
                     if (kc.j == 0) {
-                        mbar_wait(q_empty, (qcount & 1) ^ 1);
+                        const int qs = qcount % C::QBUF;
+                        const uint32_t qaddr = sbase + C::Q_OFF + qs * 2 * C::TILE_BYTES;
+                        mbar_wait(q_empty(qs), ((qcount / C::QBUF) & 1) ^ 1);
                         const int nq = w.qtile_b >= 0 ? 2 : 1;
                         if (elect_one()) {
-                            mbar_arrive_expect_tx(q_full, nq * C::TILE_BYTES);
+                            mbar_arrive_expect_tx(q_full(qs), nq * C::TILE_BYTES);
 #pragma unroll
                             for (int b = 0; b < C::BOXES; ++b) {
-                                tma_load_3d(sbase + C::Q_OFF + b * C::BOX_BYTES, &tmq, q_full, b * 64,
-                                            w.qtile_a * TILE_M, w.bh);
+                                tma_load_3d(qaddr + b * C::BOX_BYTES, &tmq, q_full(qs), b * 64, w.qtile_a * TILE_M,
+                                            w.bh);
                                 if (nq == 2)
-                                    tma_load_3d(sbase + C::Q_OFF + C::TILE_BYTES + b * C::BOX_BYTES, &tmq, q_full,
-                                                b * 64, w.qtile_b * TILE_M, w.bh);
+                                    tma_load_3d(qaddr + C::TILE_BYTES + b * C::BOX_BYTES, &tmq, q_full(qs), b * 64,
+                                                w.qtile_b * TILE_M, w.bh);
                             }
                         }
                         __syncwarp();
@@ -447,6 +458,8 @@ __global__ void __launch_bounds__(384, 1)
                 __syncwarp();
                 ++vcount;
                 advance(items, it1, vc);
+                if (vc.j == 0)
+                    ++vitem;
             }
         }
     } else if (warp == 1) {
@@ -463,7 +476,9 @@ __global__ void __launch_bounds__(384, 1)
                 const WorkItem w = items[it];
                 if ((w.flags & ITEM_COPY) || w.n_tiles == 0)
                     continue;
-                mbar_wait(q_full, qcount & 1);
+                const int qs = qcount % C::QBUF;
+                const uint32_t qbase = sbase + C::Q_OFF + qs * 2 * C::TILE_BYTES;
+                mbar_wait(q_full(qs), (qcount / C::QBUF) & 1);
                 tc_fence_after();
                 bool first_pv[2] = {true, true};
                 uint32_t prev = 0;
@@ -519,7 +534,7 @@ __global__ void __launch_bounds__(384, 1)
                             }
                             if (DFA2_TRACE == 1 && lane == 0) DFA2_STAMP(L, scount[L], 6);
                             tc_fence_after();
-                            const uint64_t qdesc = smem_desc_sw128(sbase + C::Q_OFF + L * C::TILE_BYTES, 16, 1024);
+                            const uint64_t qdesc = smem_desc_sw128(qbase + L * C::TILE_BYTES, 16, 1024);
                             const uint64_t kdesc = smem_desc_sw128(k_addr, 16, 1024);
                             if (elect_one()) {
 #pragma unroll
@@ -540,7 +555,7 @@ __global__ void __launch_bounds__(384, 1)
                         if (u < U) {
                             mma_commit(k_empty(kst));  // K(u) free once its S MMAs complete
                             if (u == U - 1)
-                                mma_commit(q_empty);
+                                mma_commit(q_empty(qs));
                         }
                     }
                     __syncwarp();
