@@ -498,7 +498,8 @@ struct ForwardSpec {
     int64_t batch;
     const dfa2c_dims* dims;
     int64_t block;
-    std::vector<std::vector<uint8_t>> masks;  // distinct masks
+    std::vector<std::vector<uint8_t>> masks;  // distinct masks (explicit, or built from mask_windows on a plan miss)
+    std::vector<int64_t> mask_windows;        // per distinct mask: -1 = all active, else arrow window
     std::vector<HeadJob> jobs;                // per head
     std::string mask_key;                     // identifies the masks in the plan cache
     dfa2c_cache* cache;                       // slots read (copy) / written (commit)
@@ -641,7 +642,17 @@ void launch_forward(const ForwardSpec& s, cudaStream_t stream) {
         if (it == g_plans.end()) {
             if (g_plans.size() >= 256)
                 g_plans.clear();
-            it = g_plans.emplace(key, build_dev_plan(device, s.batch, H, n, s.block, s.masks, s.jobs)).first;
+            // masks are only materialised when the work list has to be built
+            std::vector<std::vector<uint8_t>> built;
+            const std::vector<std::vector<uint8_t>>* masks = &s.masks;
+            if (s.masks.empty() && !s.mask_windows.empty()) {
+                const int64_t nb = ceil_div(n, s.block);
+                for (int64_t w : s.mask_windows)
+                    built.push_back(w < 0 ? std::vector<uint8_t>(static_cast<size_t>(nb * nb), uint8_t{1})
+                                          : arrow_mask(s.dims, s.block, w));
+                masks = &built;
+            }
+            it = g_plans.emplace(key, build_dev_plan(device, s.batch, H, n, s.block, *masks, s.jobs)).first;
         }
         plan = it->second.get();
     }
@@ -685,10 +696,8 @@ cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
 
 // Standard per-call mask bookkeeping for a LayerPlan: one mask per distinct
 // window (src/dispatch.cpp:38-54) plus the all-active mask for Full heads.
-void plan_jobs(const dfa2c_dims* dims, int64_t block, const int32_t* kinds, const int64_t* windows,
+void plan_jobs(const dfa2c_dims* dims, int64_t /*block*/, const int32_t* kinds, const int64_t* windows,
                bool commit, ForwardSpec& s) {
-    const int64_t n = seq_len(dims);
-    const int64_t nb = ceil_div(n, block);
     std::map<int64_t, int> ids;  // -1 = full, else window
     for (int64_t h = 0; h < dims->n_heads; ++h) {
         if (kinds[h] == DFA2C_CACHED) {
@@ -698,11 +707,8 @@ void plan_jobs(const dfa2c_dims* dims, int64_t block, const int32_t* kinds, cons
         const int64_t key = kinds[h] == DFA2C_FULL ? -1 : windows[h];
         auto it = ids.find(key);
         if (it == ids.end()) {
-            it = ids.emplace(key, static_cast<int>(s.masks.size())).first;
-            if (key < 0)
-                s.masks.emplace_back(static_cast<size_t>(nb * nb), uint8_t{1});
-            else
-                s.masks.push_back(arrow_mask(dims, block, key));
+            it = ids.emplace(key, static_cast<int>(s.mask_windows.size())).first;
+            s.mask_windows.push_back(key);  // built lazily, on a plan-cache miss
             put(s.mask_key, key);
         }
         s.jobs.push_back({it->second, commit});

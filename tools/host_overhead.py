@@ -1,4 +1,5 @@
-"""Host-side cost of one fused-layer call vs its GPU time (FLUX68 shape)."""
+"""Host-side cost of one fused-layer call vs its GPU time (FLUX68 shape, or
+the cfg1 layer with --cfg1)."""
 import time
 import sys
 import os
@@ -8,7 +9,7 @@ import torch
 
 from paper_2503_22796_b200 import api
 
-H, NV, NT, D, B = 24, 16384, 512, 128, 128
+H, NV, NT, D, B = (4, 1024, 77, 64, 128) if "--cfg1" in sys.argv else (24, 16384, 512, 128, 128)
 N = NV + NT
 dims = api.AttentionDims(H, D, NV, NT)
 q, k, v = (torch.randn(1, H, N, D, device="cuda").to(torch.bfloat16) for _ in range(3))
@@ -16,7 +17,7 @@ out = torch.empty_like(q)
 cache = api.HeadCache(1, H, N, D)
 for h in range(H):
     cache.store(0, h, torch.randn(N, D, device="cuda").to(torch.bfloat16), 0)
-lp = api.flux68_plan()
+lp = api.LayerPlan.parse("F A0 A2 C") if "--cfg1" in sys.argv else api.flux68_plan()
 for _ in range(5):
     api.multi_strategy_attention(q, k, v, lp, cache, 0, 1, dims, B, out=out)
 torch.cuda.synchronize()
