@@ -206,8 +206,9 @@ def run_reference(args):
 
 def run_head_mode(args, rank, world, barrier, max_over_ranks):
     """One FLUX sample on `world` GPUs: heads LPT-sharded by plan cost, one
-    fused launch per rank over its heads, NCCL all-gather of the bf16 output
-    heads (paper_2503_22796_b200.parallel). Strong scaling."""
+    fused launch per rank over the full plan with the other ranks' heads
+    DFA2C_SKIP, NCCL all-gather of the bf16 output heads
+    (paper_2503_22796_b200.parallel). Strong scaling."""
     import torch
 
     from paper_2503_22796_b200 import api, parallel
@@ -222,25 +223,23 @@ def run_head_mode(args, rank, world, barrier, max_over_ranks):
         return torch.randn(*shape, device="cuda", dtype=torch.float32, generator=gen).to(torch.bfloat16)
 
     q, k, v = (randn(s, H, N, D) for s in (1, 2, 3))  # the same sample on every rank
-    idx = torch.tensor(shard.heads, device="cuda", dtype=torch.long)
-    ql, kl, vl = (x.index_select(0, idx).contiguous() for x in (q, k, v))
     nh = len(shard.heads)
-    ldims = api.AttentionDims(max(nh, 1), D, NV, NT)
-    lplan = parallel.sub_plan(lp, shard.heads)
-    cache = api.HeadCache(1, max(nh, 1), N, D)
-    for i, h in enumerate(shard.heads):
-        cache.store(0, i, randn(100 + h, N, D), 0)
-    local = torch.empty_like(ql)
+    cache = api.HeadCache(1, H, N, D)  # layer-shaped; only this rank's slots are touched
+    for h in shard.heads:
+        cache.store(0, h, randn(100 + h, N, D), 0)
     full = torch.empty_like(q)
+    skip = [h for h in range(H) if h not in set(shard.heads)]
     stream = torch.cuda.current_stream()
 
-    def compute():
+    def compute():  # one fused launch over the full plan, other ranks' heads DFA2C_SKIP
         if nh:
-            api.multi_strategy_attention(ql, kl, vl, lplan, cache, 0, 1, ldims, BLOCK, out=local)
+            api.multi_strategy_attention(q, k, v, lp, cache, 0, 1, dims, BLOCK, out=full, skip_heads=skip)
+
+    idx = torch.tensor(shard.heads, device="cuda", dtype=torch.long)
 
     def step():
         compute()
-        parallel.gather_heads(local, shard, full)
+        parallel.gather_heads(full.index_select(0, idx), shard, full)
 
     def timed(fn, steps):
         for _ in range(args.warmup):

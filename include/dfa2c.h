@@ -51,6 +51,12 @@ typedef enum {
 } dfa2c_status;
 
 enum { DFA2C_FULL = 0, DFA2C_ARROW = 1, DFA2C_CACHED = 2 }; /* StrategyKind */
+/* Flag OR-ed into kinds[h] of dfa2c_mha_forward(_host): head h belongs to
+ * the layer plan (it counts for scheduling decisions) but this call neither
+ * computes, copies nor commits it, and leaves its output rows untouched.
+ * Lets several calls (e.g. one per GPU) split one layer by heads while every
+ * head's result stays bitwise what the single call produces. */
+enum { DFA2C_SKIP = 0x100 };
 enum { DFA2C_VISUAL_FIRST = 0, DFA2C_TEXT_FIRST = 1 };     /* TokenOrder */
 enum { DFA2C_BF16 = 0, DFA2C_F32 = 1, DFA2C_F64 = 2 };    /* element type */
 enum { DFA2C_RSE_STANDARD = 0, DFA2C_RSE_LITERAL = 1 };     /* RseMode */
@@ -154,6 +160,16 @@ int dfa2c_mha_forward_host(const void* q, const void* k, const void* v, int64_t 
                            const dfa2c_dims* dims, int64_t block, const int32_t* kinds,
                            const int64_t* windows, dfa2c_cache* cache, int64_t layer,
                            int64_t t, void* out, void* stream);
+
+/* Split-KV scheduling for latency-bound layers (process-wide; default from
+ * the environment, DFA2_SPLIT_KV=1). When on, a query-tile pair whose key
+ * tiles cost more than the layer's average load per SM (reference 148 SMs)
+ * runs as key chunks combined in a fixed order by the CTA finishing last:
+ * e.g. a late-timestep layer with most heads Cached drops from being bound
+ * by one arrow head's text rows. Results stay deterministic (independent
+ * of batch, launch split and device) but each head then also depends on the
+ * other heads' strategies, so the default is off (bitwise head isolation). */
+int dfa2c_set_split_kv(int32_t on);
 
 /* sparse_attention_forward (inc/arrow.hpp:59-63; src/arrow.cpp:171-208) for
  * `n_heads` independent [N, d] heads sharing one arbitrary block mask

@@ -352,13 +352,33 @@ class HeadCache:
 
 
 # --------------------------------------------------------------- attention
+def _plan_kinds(plan: LayerPlan, skip_heads):
+    kinds, wins = plan.arrays()
+    for h in skip_heads or ():
+        if not 0 <= h < plan.n_heads():
+            raise ShapeError(f"skip head {h} out of range")
+        kinds[h] |= SKIP
+    return kinds, wins
+
+
+SKIP = 0x100  # DFA2C_SKIP
+
+
+def set_split_kv(on: bool) -> None:
+    """dfa2c_set_split_kv: split-KV scheduling for latency-bound layers
+    (process-wide; default off, or DFA2_SPLIT_KV=1)."""
+    check(lib().dfa2c_set_split_kv(1 if on else 0))
+
+
 def multi_strategy_attention(q, k, v, plan: LayerPlan, cache: Optional[HeadCache], layer: int, t: int,
-                             dims: AttentionDims, block_size: int, out=None, stream=None):
+                             dims: AttentionDims, block_size: int, out=None, stream=None, skip_heads=None):
     """multi_strategy_attention (inc/dispatch.hpp:44-47; src/dispatch.cpp:30-91).
 
     q/k/v: [H, N, d] or [batch, H, N, d] CUDA tensors. One fused sm_100a
     launch: Full/Arrow heads computed, Cached heads copied from `cache`,
-    computed heads committed to `cache` (produced_at = t).
+    computed heads committed to `cache` (produced_at = t). skip_heads: heads
+    of the layer this call leaves alone (DFA2C_SKIP; e.g. the heads another
+    GPU owns); their output rows are not written.
     """
     torch = _torch()
     q = _as_bf16_cuda(q, "q")
@@ -376,7 +396,7 @@ def multi_strategy_attention(q, k, v, plan: LayerPlan, cache: Optional[HeadCache
     if out is None:
         out = torch.empty_like(q)
     d = dims.c()
-    kinds, wins = plan.arrays()
+    kinds, wins = _plan_kinds(plan, skip_heads)
     check(lib().dfa2c_mha_forward(c_void_p(q.data_ptr()), c_void_p(k.data_ptr()), c_void_p(v.data_ptr()),
                                   q.shape[0], byref(d), block_size, kinds, wins,
                                   cache.handle if cache is not None else None, layer, t,
@@ -385,7 +405,7 @@ def multi_strategy_attention(q, k, v, plan: LayerPlan, cache: Optional[HeadCache
 
 
 def multi_strategy_attention_host(q, k, v, plan: LayerPlan, cache: Optional[HeadCache], layer: int, t: int,
-                                  dims: AttentionDims, block_size: int, out=None, stream=None):
+                                  dims: AttentionDims, block_size: int, out=None, stream=None, skip_heads=None):
     """multi_strategy_attention with HOST tensors (the reference's calling
     convention, inc/dispatch.hpp:44-47) through dfa2c_mha_forward_host:
     q/k/v are host bf16 [H, N, d] or [batch, H, N, d] (pin them for
@@ -411,7 +431,7 @@ def multi_strategy_attention_host(q, k, v, plan: LayerPlan, cache: Optional[Head
     elif out.is_cuda or out.dtype != torch.bfloat16 or out.shape != q.shape or not out.is_contiguous():
         raise ShapeError("out must be a contiguous host bf16 tensor shaped like q")
     d = dims.c()
-    kinds, wins = plan.arrays()
+    kinds, wins = _plan_kinds(plan, skip_heads)
     check(lib().dfa2c_mha_forward_host(c_void_p(q.data_ptr()), c_void_p(k.data_ptr()), c_void_p(v.data_ptr()),
                                        q.shape[0], byref(d), block_size, kinds, wins,
                                        cache.handle if cache is not None else None, layer, t,

@@ -640,29 +640,23 @@ __global__ void __launch_bounds__(384, 1)
                 ++scnt;
                 first = false;
             }
-            // ---- epilogue: O / l -> bf16 -> staging (128B swizzle) -> TMA
-            // bulk stores to out and, for computed heads, the cache slot
             mbar_wait(o_full(L), icnt & 1);
             ++icnt;
             tc_fence_after();
-            const float inv = 1.f / l;
+            // ---- epilogue: O / l -> bf16 -> staging (128B swizzle) -> TMA
+            // bulk stores to out and, for computed heads, the cache slot
             const bool commit = (w.flags & ITEM_COMMIT) && args.cache;
-#pragma unroll
-            for (int b = 0; b < D / 64; ++b) {
-                uint32_t o[64];
-                tmem_ld32(oc + 64 * b, o);
-                tmem_ld32(oc + 64 * b + 32, o + 32);
+            auto store_box = [&](int b, const float* vals, float inv) {
                 if (issuer)
                     bulk_wait_read0();  // previous store from this buffer has read smem
                 named_bar_sync(1 + L, 128);
-                tmem_ld_wait();
                 const uint32_t rbase = stg + static_cast<uint32_t>(r) * 128u;
 #pragma unroll
                 for (int c = 0; c < 8; ++c) {
-                    const uint32_t p0 = pack_bf16x2(__uint_as_float(o[8 * c + 0]) * inv, __uint_as_float(o[8 * c + 1]) * inv);
-                    const uint32_t p1 = pack_bf16x2(__uint_as_float(o[8 * c + 2]) * inv, __uint_as_float(o[8 * c + 3]) * inv);
-                    const uint32_t p2 = pack_bf16x2(__uint_as_float(o[8 * c + 4]) * inv, __uint_as_float(o[8 * c + 5]) * inv);
-                    const uint32_t p3 = pack_bf16x2(__uint_as_float(o[8 * c + 6]) * inv, __uint_as_float(o[8 * c + 7]) * inv);
+                    const uint32_t p0 = pack_bf16x2(vals[8 * c + 0] * inv, vals[8 * c + 1] * inv);
+                    const uint32_t p1 = pack_bf16x2(vals[8 * c + 2] * inv, vals[8 * c + 3] * inv);
+                    const uint32_t p2 = pack_bf16x2(vals[8 * c + 4] * inv, vals[8 * c + 5] * inv);
+                    const uint32_t p3 = pack_bf16x2(vals[8 * c + 6] * inv, vals[8 * c + 7] * inv);
                     st_shared_v4(rbase + static_cast<uint32_t>((c ^ (r & 7)) * 16), p0, p1, p2, p3);
                 }
                 fence_proxy_async_smem();
@@ -673,8 +667,84 @@ __global__ void __launch_bounds__(384, 1)
                         tma_store_3d(&tmc, stg, b * 64, qt * TILE_M, w.bh);
                     bulk_commit();
                 }
+            };
+            if (!(w.flags & ITEM_SPLIT)) {
+                const float inv = 1.f / l;
+#pragma unroll
+                for (int b = 0; b < D / 64; ++b) {
+                    float o[64];
+                    tmem_ld32(oc + 64 * b, reinterpret_cast<uint32_t*>(o));
+                    tmem_ld32(oc + 64 * b + 32, reinterpret_cast<uint32_t*>(o) + 32);
+                    tmem_ld_wait();
+                    store_box(b, o, inv);
+                }
+                tc_fence_before();
+                continue;
+            }
+            // ---- split item (one key chunk of a heavy query-tile pair):
+            // publish this chunk's unnormalised O, reference max and row sum
+            // ([slot][lane][col][row], coalesced over rows), then the CTA that
+            // completes the group folds all chunks in chunk order (fixed, so
+            // results do not depend on which CTA finishes last) and stores.
+            {
+                const size_t base = (static_cast<size_t>(w.part) * 2 + L);
+                float* po = args.part_o + base * D * TILE_M;
+#pragma unroll
+                for (int b = 0; b < D / 64; ++b) {
+                    uint32_t o[64];
+                    tmem_ld32(oc + 64 * b, o);
+                    tmem_ld32(oc + 64 * b + 32, o + 32);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int c = 0; c < 64; ++c)
+                        po[(64 * b + c) * TILE_M + r] = __uint_as_float(o[c]);
+                }
+                args.part_ml[(base * 2 + 0) * TILE_M + r] = m_ref;
+                args.part_ml[(base * 2 + 1) * TILE_M + r] = l;
             }
             tc_fence_before();
+            __threadfence();
+            named_bar_sync(1 + L, 128);
+            int* flag = reinterpret_cast<int*>(smem + C::BAR_OFF + C::NBARS * 8 + 8) + L;
+            if (r == 0)
+                *flag = atomicAdd(args.counters + 2 * w.group + L, 1) == w.nchunk - 1;
+            named_bar_sync(1 + L, 128);
+            if (!*flag)
+                continue;
+            __threadfence();
+            {
+                const int slot0 = w.part - w.chunk;
+                auto ml = [&](int c, int which) {
+                    return __ldcg(args.part_ml + ((static_cast<size_t>(slot0 + c) * 2 + L) * 2 + which) * TILE_M + r);
+                };
+                float m = -INFINITY;
+                for (int c = 0; c < w.nchunk; ++c)
+                    m = fmaxf(m, ml(c, 0));
+                float lsum = 0.f;
+                for (int c = 0; c < w.nchunk; ++c) {
+                    const float mc = ml(c, 0);
+                    if (mc != -INFINITY)
+                        lsum += exp2f(mc - m) * ml(c, 1);
+                }
+#pragma unroll 1
+                for (int b = 0; b < D / 64; ++b) {
+                    float acc[64];
+#pragma unroll
+                    for (int i = 0; i < 64; ++i)
+                        acc[i] = 0.f;
+                    for (int c = 0; c < w.nchunk; ++c) {
+                        const float mc = ml(c, 0);
+                        if (mc == -INFINITY)
+                            continue;  // this lane folded no tile in chunk c
+                        const float wc = exp2f(mc - m);
+                        const float* po = args.part_o + (static_cast<size_t>(slot0 + c) * 2 + L) * D * TILE_M;
+#pragma unroll
+                        for (int i = 0; i < 64; ++i)
+                            acc[i] = fmaf(wc, __ldcg(po + (64 * b + i) * TILE_M + r), acc[i]);
+                    }
+                    store_box(b, acc, 1.f / lsum);
+                }
+            }
         }
         if (issuer)
             bulk_wait0();  // every bulk store of this lane has completed

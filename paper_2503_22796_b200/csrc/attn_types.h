@@ -17,13 +17,18 @@ struct WorkItem {
     int32_t tile_begin;  // offset into the tile-word list (compute items)
     int32_t n_tiles;     // union length (0 for copy items)
     int32_t mask_off;    // byte offset of this head's nb*nb block mask
-    int32_t flags;       // ITEM_COPY | ITEM_COMMIT
+    int32_t flags;       // ITEM_COPY | ITEM_COMMIT | ITEM_SPLIT
+    int32_t part;        // ITEM_SPLIT: partial-output slot of this chunk
+    int32_t group;       // ITEM_SPLIT: split group (the original pair item)
+    int32_t chunk;       // ITEM_SPLIT: chunk index within the group
+    int32_t nchunk;      // ITEM_SPLIT: chunks in the group
     int32_t pad;
 };
 
 enum : int32_t {
     ITEM_COPY = 1,    // Cached head: out <- cache slot (src/dispatch.cpp:77-81)
     ITEM_COMMIT = 2,  // computed head: also store O into the cache slot (:85-88)
+    ITEM_SPLIT = 4,   // one key chunk of a heavy pair; the group's last chunk combines
 };
 
 // Tile word: KV tile index in bits [0,24); bit 24/25: lane A/B folds this
@@ -50,6 +55,9 @@ struct AttnArgs {
     int32_t nb;
     float scale_log2;          // log2(e) / sqrt(d)
     long long* trace;          // debug builds (-DDFA2_TRACE=1): per-tile clock64 stamps of CTA 0
+    float* part_o;             // split items: [slots][2 lanes][D][128] unnormalised O
+    float* part_ml;            // split items: [slots][2 lanes][2][128] reference max, row sum
+    int* counters;             // split groups: [groups][2 lanes] chunks finished (zeroed per launch)
 };
 
 constexpr int TILE_M = 128;  // query rows per tile (tcgen05 M)

@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <map>
@@ -112,12 +113,16 @@ void validate_plan(const dfa2c_dims* dims, const int32_t* kinds, const int64_t* 
     if (!kinds)
         fail(DFA2C_SHAPE, "plan must assign exactly one strategy per head");
     for (int64_t h = 0; h < dims->n_heads; ++h) {
-        if (kinds[h] < DFA2C_FULL || kinds[h] > DFA2C_CACHED)
+        const int32_t k = kinds[h] & ~DFA2C_SKIP;
+        if ((kinds[h] & ~(DFA2C_SKIP | 3)) != 0 || k < DFA2C_FULL || k > DFA2C_CACHED)
             fail(DFA2C_SHAPE, "unknown strategy kind for head " + std::to_string(h));
-        if (kinds[h] == DFA2C_ARROW && (!windows || windows[h] < 0))
+        if (k == DFA2C_ARROW && (!windows || windows[h] < 0))
             fail(DFA2C_SHAPE, "window_blocks must be >= 0");
     }
 }
+
+int32_t kind_of(int32_t k) { return k & ~DFA2C_SKIP; }
+bool skipped(int32_t k) { return (k & DFA2C_SKIP) != 0; }
 
 // plan_flops (src/dispatch.cpp:93-120).
 int64_t plan_flops(const dfa2c_dims* dims, int64_t B, const int32_t* kinds, const int64_t* windows) {
@@ -127,9 +132,9 @@ int64_t plan_flops(const dfa2c_dims* dims, int64_t B, const int32_t* kinds, cons
     std::map<int64_t, int64_t> arrow;
     int64_t total = 0;
     for (int64_t h = 0; h < dims->n_heads; ++h) {
-        if (kinds[h] == DFA2C_FULL) {
+        if (kind_of(kinds[h]) == DFA2C_FULL) {
             total += 4 * d * n * n;
-        } else if (kinds[h] == DFA2C_ARROW) {
+        } else if (kind_of(kinds[h]) == DFA2C_ARROW) {
             auto it = arrow.find(windows[h]);
             if (it == arrow.end()) {
                 const auto m = arrow_mask(dims, B, windows[h]);
@@ -193,6 +198,8 @@ void check_rows_nonempty(const uint8_t* m, int64_t nb) {
 // ------------------------------------------------------------ device plan
 struct DevPlan {
     int grid = 0;
+    int32_t n_groups = 0;  // split groups (counters per launch)
+    int32_t n_slots = 0;   // partial-output slots (one per split chunk)
     WorkItem* items = nullptr;
     int32_t* cta_begin = nullptr;
     uint32_t* tiles = nullptr;
@@ -213,6 +220,21 @@ struct HeadJob {
     int mask_id;
     bool commit;
 };
+
+// Split-KV scheduling switch: dfa2c_set_split_kv(), default from the
+// environment (DFA2_SPLIT_KV=1), process-wide.
+std::atomic<int> g_split_kv{-1};
+bool split_kv_enabled() {
+    int v = g_split_kv.load();
+    if (v < 0) {
+        const char* e = std::getenv("DFA2_SPLIT_KV");
+        v = (e && e[0] == '1') ? 1 : 0;
+        int expect = -1;
+        g_split_kv.compare_exchange_strong(expect, v);
+        v = g_split_kv.load();
+    }
+    return v == 1;
+}
 
 int num_sms(int device) {
     int v = 0;
@@ -295,7 +317,7 @@ PairSet build_pair_set(const TileSet& ts, int64_t nqt) {
 // outputs are bitwise reproducible.
 std::unique_ptr<DevPlan> build_dev_plan(int device, int64_t batch, int64_t H, int64_t n, int64_t B,
                                         const std::vector<std::vector<uint8_t>>& masks,
-                                        const std::vector<HeadJob>& jobs) {
+                                        const std::vector<HeadJob>& jobs, const std::vector<int>& ref_jobs) {
     const int64_t nqt = ceil_div(n, dfa2k::TILE_M);
     const int64_t np = (nqt + 1) / 2;
     std::vector<uint32_t> tiles;
@@ -316,6 +338,50 @@ std::unique_ptr<DevPlan> build_dev_plan(int device, int64_t batch, int64_t H, in
     if (mask_bytes.size() > static_cast<size_t>(std::numeric_limits<int32_t>::max()) ||
         tiles.size() > static_cast<size_t>(std::numeric_limits<int32_t>::max()) || nqt > (1 << 24))
         fail(DFA2C_UNSUPPORTED, "work list too large");
+
+    // Split-KV (opt-in, DFA2_SPLIT_KV=1): for latency-bound layers, e.g. a
+    // late timestep with most heads Cached, where one text-row pair of an
+    // arrow head (every key tile) outlasts everything else. The per-sample
+    // load of the whole layer plan (ref_jobs: every head, including heads a
+    // launch skips) is spread over a fixed reference of 148 SMs; a pair
+    // costing more than that average becomes ceil(cost / average) key
+    // chunks, combined in chunk order by the CTA that finishes the group's
+    // last chunk. The decision is independent of the batch, of how a call is
+    // split into launches (host-path groups; multi-GPU shards keep the plan
+    // whole through DFA2C_SKIP) and of the device, so results are still
+    // deterministic; but it depends on the other heads' strategies, which is
+    // why it is off by default: with it off every head's result is a
+    // function of its own strategy alone (head isolation, bitwise,
+    // test_dispatch.cpp:98-109).
+    constexpr double kRefSMs = 148.0;
+    std::vector<std::vector<int32_t>> chunks_of(sets.size());
+    for (size_t mi = 0; mi < sets.size(); ++mi)
+        chunks_of[mi].assign(static_cast<size_t>(np), 1);
+    if (split_kv_enabled()) {
+        double per_sample = 0.0;
+        for (int64_t h = 0; h < H; ++h) {
+            const int rj = ref_jobs.empty() ? jobs[h].mask_id : ref_jobs[h];
+            if (rj < 0) {
+                per_sample += static_cast<double>(n) / 128.0;  // a copy: ~1 unit per 128 rows
+                continue;
+            }
+            const PairSet& ps = sets[rj];
+            for (int64_t p = 0; p < np; ++p)
+                per_sample += ps.n_a[p] + ps.n_b[p] + 1.0;
+        }
+        const double avg = std::max(per_sample / kRefSMs, 1.0);
+        for (size_t mi = 0; mi < sets.size(); ++mi) {
+            const PairSet& ps = sets[mi];
+            for (int64_t p = 0; p < np; ++p) {
+                const double cost = ps.n_a[p] + ps.n_b[p] + 1.0;
+                const int64_t len = ps.row_ptr[p + 1] - ps.row_ptr[p];
+                if (cost > avg && len >= 8)
+                    chunks_of[mi][p] = static_cast<int32_t>(
+                        std::min<int64_t>({static_cast<int64_t>(std::ceil(cost / avg)), len / 4, 32}));
+            }
+        }
+    }
+    int32_t n_groups = 0, n_slots = 0;
 
     struct Cand {
         WorkItem w;
@@ -348,7 +414,30 @@ std::unique_ptr<DevPlan> build_dev_plan(int device, int64_t batch, int64_t H, in
                         fail(DFA2C_FULLY_MASKED, "query tile " + std::to_string(2 * p) + " has no active key tiles");
                     if (w.qtile_b >= 0 && ps.n_b[p] < 1)
                         fail(DFA2C_FULLY_MASKED, "query tile " + std::to_string(2 * p + 1) + " has no active key tiles");
-                    cands.push_back({w, (ps.n_a[p] + ps.n_b[p]) * (dfa2k::TILE_N / 128.0) + 1.0});
+                    const int32_t nch = chunks_of[j.mask_id][p];
+                    if (nch <= 1) {
+                        cands.push_back({w, (ps.n_a[p] + ps.n_b[p]) * (dfa2k::TILE_N / 128.0) + 1.0});
+                        continue;
+                    }
+                    const int32_t U = w.n_tiles, begin = w.tile_begin;
+                    for (int32_t c = 0; c < nch; ++c) {
+                        WorkItem cw = w;
+                        const int32_t lo = static_cast<int32_t>(int64_t{c} * U / nch);
+                        const int32_t hi = static_cast<int32_t>(int64_t{c + 1} * U / nch);
+                        cw.tile_begin = begin + lo;
+                        cw.n_tiles = hi - lo;
+                        cw.flags |= dfa2k::ITEM_SPLIT;
+                        cw.group = n_groups;
+                        cw.chunk = c;
+                        cw.nchunk = nch;
+                        cw.part = n_slots + c;
+                        int64_t fold = 0;
+                        for (int32_t u = cw.tile_begin; u < cw.tile_begin + cw.n_tiles; ++u)
+                            fold += ((tiles[u] & dfa2k::TILE_NEED_A) != 0) + ((tiles[u] & dfa2k::TILE_NEED_B) != 0);
+                        cands.push_back({cw, static_cast<double>(fold) + 1.5});
+                    }
+                    ++n_groups;
+                    n_slots += nch;
                 }
             }
         }
@@ -381,6 +470,8 @@ std::unique_ptr<DevPlan> build_dev_plan(int device, int64_t batch, int64_t H, in
 
     auto p = std::make_unique<DevPlan>();
     p->grid = grid;
+    p->n_groups = n_groups;
+    p->n_slots = n_slots;
     DFA2C_CUDA_CHECK(cudaMalloc(&p->items, items.size() * sizeof(WorkItem)));
     DFA2C_CUDA_CHECK(cudaMalloc(&p->cta_begin, cta_begin.size() * sizeof(int32_t)));
     DFA2C_CUDA_CHECK(cudaMalloc(&p->tiles, tiles.size() * sizeof(uint32_t)));
@@ -500,7 +591,8 @@ struct ForwardSpec {
     int64_t block;
     std::vector<std::vector<uint8_t>> masks;  // distinct masks (explicit, or built from mask_windows on a plan miss)
     std::vector<int64_t> mask_windows;        // per distinct mask: -1 = all active, else arrow window
-    std::vector<HeadJob> jobs;                // per head
+    std::vector<HeadJob> jobs;                // per head (JOB_SKIP: not part of this launch)
+    std::vector<int> ref_jobs;                // per head, the layer plan's job before any skipping
     std::string mask_key;                     // identifies the masks in the plan cache
     dfa2c_cache* cache;                       // slots read (copy) / written (commit)
     int64_t layer;
@@ -633,6 +725,10 @@ void launch_forward(const ForwardSpec& s, cudaStream_t stream) {
         put(key, j.mask_id);
         put(key, j.commit);
     }
+    put(key, split_kv_enabled());
+    if (split_kv_enabled())
+        for (int rj : s.ref_jobs)
+            put(key, rj);
     key += s.mask_key;
 
     DevPlan* plan = nullptr;
@@ -652,7 +748,7 @@ void launch_forward(const ForwardSpec& s, cudaStream_t stream) {
                                           : arrow_mask(s.dims, s.block, w));
                 masks = &built;
             }
-            it = g_plans.emplace(key, build_dev_plan(device, s.batch, H, n, s.block, *masks, s.jobs)).first;
+            it = g_plans.emplace(key, build_dev_plan(device, s.batch, H, n, s.block, *masks, s.jobs, s.ref_jobs)).first;
         }
         plan = it->second.get();
     }
@@ -688,7 +784,21 @@ void launch_forward(const ForwardSpec& s, cudaStream_t stream) {
     a.trace = g_trace;
     if (plan->grid == 0)
         return;  // nothing to launch (every head skipped)
+    // split-KV scratch: stream-ordered from the library pool, counters zeroed
+    // per launch, released after the launch on the same stream
+    if (plan->n_groups > 0) {
+        const int D = kernel_dim(d);
+        scratch_alloc(&a.part_o, static_cast<size_t>(plan->n_slots) * 2 * D * dfa2k::TILE_M * sizeof(float), stream);
+        scratch_alloc(&a.part_ml, static_cast<size_t>(plan->n_slots) * 2 * 2 * dfa2k::TILE_M * sizeof(float), stream);
+        scratch_alloc(&a.counters, static_cast<size_t>(plan->n_groups) * 2 * sizeof(int), stream);
+        DFA2C_CUDA_CHECK(cudaMemsetAsync(a.counters, 0, static_cast<size_t>(plan->n_groups) * 2 * sizeof(int), stream));
+    }
     DFA2C_CUDA_CHECK(dfa2k::launch_attn(kernel_dim(d), tq, tk, tv, to, tc, a, plan->grid, stream));
+    if (plan->n_groups > 0) {
+        DFA2C_CUDA_CHECK(cudaFreeAsync(a.part_o, stream));
+        DFA2C_CUDA_CHECK(cudaFreeAsync(a.part_ml, stream));
+        DFA2C_CUDA_CHECK(cudaFreeAsync(a.counters, stream));
+    }
     g_launches.fetch_add(1);
 }
 
@@ -700,18 +810,21 @@ void plan_jobs(const dfa2c_dims* dims, int64_t /*block*/, const int32_t* kinds, 
                bool commit, ForwardSpec& s) {
     std::map<int64_t, int> ids;  // -1 = full, else window
     for (int64_t h = 0; h < dims->n_heads; ++h) {
-        if (kinds[h] == DFA2C_CACHED) {
-            s.jobs.push_back({JOB_COPY, false});
+        const int32_t k = kind_of(kinds[h]);
+        if (k == DFA2C_CACHED) {
+            s.ref_jobs.push_back(JOB_COPY);
+            s.jobs.push_back({skipped(kinds[h]) ? JOB_SKIP : JOB_COPY, false});
             continue;
         }
-        const int64_t key = kinds[h] == DFA2C_FULL ? -1 : windows[h];
+        const int64_t key = k == DFA2C_FULL ? -1 : windows[h];
         auto it = ids.find(key);
         if (it == ids.end()) {
             it = ids.emplace(key, static_cast<int>(s.mask_windows.size())).first;
             s.mask_windows.push_back(key);  // built lazily, on a plan-cache miss
             put(s.mask_key, key);
         }
-        s.jobs.push_back({it->second, commit});
+        s.ref_jobs.push_back(it->second);
+        s.jobs.push_back({skipped(kinds[h]) ? JOB_SKIP : it->second, commit});
     }
     put(s.mask_key, dims->n_visual);
     put(s.mask_key, dims->n_text);
@@ -736,7 +849,7 @@ void validate_forward(int64_t batch, const dfa2c_dims* dims, int64_t block, cons
             fail(DFA2C_SHAPE, "layer index must be >= 0");
     }
     for (int64_t h = 0; h < H; ++h)
-        if (kinds[h] == DFA2C_CACHED && (!cache || !cache->has(layer, h)))
+        if (kinds[h] == DFA2C_CACHED && (!cache || !cache->has(layer, h)))  // skipped heads are not read
             fail(DFA2C_CACHE_MISS, "plan marks head " + std::to_string(h) + " Cached before it ever computed");
 }
 
@@ -747,7 +860,7 @@ void commit_produced(const dfa2c_dims* dims, const int32_t* kinds, dfa2c_cache* 
         return;
     const int64_t H = dims->n_heads;
     for (int64_t h = 0; h < H; ++h)
-        if (kinds[h] != DFA2C_CACHED)
+        if (!skipped(kinds[h]) && kinds[h] != DFA2C_CACHED)
             cache->produced[static_cast<size_t>(layer * H + h)] = t;
 }
 
@@ -1072,7 +1185,7 @@ int dfa2c_mha_forward_host(const void* q, const void* k, const void* v, int64_t 
         static_assert(kGroups <= HostPipe::kMaxGroups, "event slots");
         std::vector<int64_t> computed;
         for (int64_t h = 0; h < H; ++h)
-            if (kinds[h] != DFA2C_CACHED)
+            if (!skipped(kinds[h]) && kinds[h] != DFA2C_CACHED)
                 computed.push_back(h);
         const int G = static_cast<int>(std::min<size_t>(kGroups, computed.size()));
 
@@ -1104,7 +1217,7 @@ int dfa2c_mha_forward_host(const void* q, const void* k, const void* v, int64_t 
         // from the cache to the host (no q/k/v upload, no kernel work).
         std::vector<int64_t> cached;
         for (int64_t h = 0; h < H; ++h)
-            if (kinds[h] == DFA2C_CACHED)
+            if (kinds[h] == DFA2C_CACHED)  // a skipped cached head is neither read nor written
                 cached.push_back(h);
         if (!cached.empty())
             copy_runs(cached, cache->layer_ptr(layer), out, cudaMemcpyDeviceToHost, hp.d2h);
@@ -1352,6 +1465,11 @@ int dfa2c_influence_for_layer(const void* q, const void* k, const void* v, const
         if (evals)
             *evals += 1 + M;
     });
+}
+
+int dfa2c_set_split_kv(int32_t on) {
+    g_split_kv.store(on ? 1 : 0);
+    return DFA2C_OK;
 }
 
 int dfa2c_convert(const void* src, int32_t src_dtype, void* dst, int32_t dst_dtype, int64_t n, void* stream) {

@@ -9,12 +9,14 @@ so no data-path collective is needed inside the layer:
 * head sharding (configs 2/3, one sample on W GPUs, strong scaling): heads
   are assigned to ranks longest-processing-time-first on their plan cost
   (Full and Arrow heads carry very different FLOPs, Cached heads are copies),
-  each rank runs ONE fused launch over its heads, and the per-rank outputs
-  are assembled with an all-gather over NVLink (all_gather_into_tensor on
-  equal-size padded shards). Each rank owns the cache slots of its heads.
+  each rank runs ONE fused launch over the full layer plan with the heads it
+  does not own marked DFA2C_SKIP, and the per-rank outputs are assembled
+  with an all-gather over NVLink (all_gather_into_tensor on equal-size padded
+  shards). Each rank owns the cache slots of its heads.
 
 Outputs are bitwise identical for any W: a head's result depends only on
-its own tile sequence, which the static schedule fixes.
+its own tile sequence and on scheduling decisions taken from the full layer
+plan (DFA2C_SKIP keeps the plan whole), both fixed by the static schedule.
 """
 from __future__ import annotations
 
@@ -107,19 +109,23 @@ def gather_heads(local_out, shard: HeadShard, full_out, group=None):
 def sharded_multi_strategy_attention(q, k, v, plan: api.LayerPlan, cache: Optional[api.HeadCache], layer: int,
                                      t: int, dims: api.AttentionDims, block_size: int, shard: HeadShard,
                                      gather: bool = True, out=None):
-    """One sample on W GPUs: this rank runs ONE fused launch over its heads
-    (cache holds only this rank's heads, indexed locally), then the output
-    heads are all-gathered. q/k/v: the full [H, N, d] sample (replicated)."""
+    """One sample on W GPUs: this rank runs ONE fused launch over the whole
+    layer plan with every head it does not own marked DFA2C_SKIP, so the
+    kernel's scheduling decisions (split-KV) follow the full plan and each
+    head's result is bitwise what a single-GPU call gives. The rank's cache
+    is the layer-shaped cache; only its own heads' slots are ever touched.
+    Then the owned heads are all-gathered. q/k/v: the full [H, N, d] sample
+    (replicated)."""
     import torch
 
     heads = shard.heads
-    local_dims = api.AttentionDims(len(heads), dims.head_dim, dims.n_visual, dims.n_text, dims.order)
+    owned = set(heads)
+    full = out if out is not None else torch.empty_like(q)
+    if heads:
+        api.multi_strategy_attention(q, k, v, plan, cache, layer, t, dims, block_size, out=full,
+                                     skip_heads=[h for h in range(dims.n_heads) if h not in owned])
     idx = torch.tensor(heads, device=q.device, dtype=torch.long)
-    ql, kl, vl = (x.index_select(0, idx).contiguous() for x in (q, k, v))
-    local = api.multi_strategy_attention(ql, kl, vl, sub_plan(plan, heads), cache, layer, t, local_dims,
-                                         block_size) if heads else q.new_empty((0,) + tuple(q.shape[1:]))
+    local = full.index_select(0, idx) if heads else q.new_empty((0,) + tuple(q.shape[1:]))
     if not gather:
         return local
-    if out is None:
-        out = torch.empty_like(q)
-    return gather_heads(local, shard, out)
+    return gather_heads(local, shard, full)

@@ -313,6 +313,83 @@ def test_flux_2k_sampled_rows(plan_kind):
         check_close(o[h][rows], want, f"head {h} {s}")
 
 
+@pytest.mark.parametrize("d,order", [(64, 0), (128, 1)])
+def test_split_kv_text_rows(d, order):
+    """Split-KV (opt-in): the text-row pairs of arrow heads
+    run as key chunks combined in chunk order by the CTA that finishes last.
+    Their rows match the f64 oracle, the committed cache slot equals the
+    output, batched and repeated calls are bitwise identical."""
+    t = torch()
+    api.set_split_kv(True)
+    try:
+        _split_kv_text_rows(t, d, order)
+    finally:
+        api.set_split_kv(False)
+
+
+def _split_kv_text_rows(t, d, order):
+    Bt, H, nv, nt, B = 2, 3, 4096, 333, 128
+    n = nv + nt
+    dims = AttentionDims(H, d, nv, nt, api.TEXT_FIRST if order else api.VISUAL_FIRST)
+    q, qn = bf16_inputs((Bt, H, n, d), 71)
+    k, kn = bf16_inputs((Bt, H, n, d), 72)
+    v, vn = bf16_inputs((Bt, H, n, d), 73)
+    lp = LayerPlan.parse("A0 A2 A40")
+    cache = HeadCache(1, H, n, d, batch=Bt)
+    out = api.multi_strategy_attention(q, k, v, lp, cache, 0, 0, dims, B)
+    again = api.multi_strategy_attention(q, k, v, lp, None, 0, 0, dims, B)
+    single = api.multi_strategy_attention(q[1], k[1], v[1], lp, None, 0, 0, dims, B)
+    t.cuda.synchronize()
+    assert t.equal(out, again) and t.equal(out[1], single)
+    lo, hi = dims.text_begin(), dims.text_end()
+    rows = np.concatenate([np.arange(lo, hi, 7), np.arange(0, n, 503)]).astype(np.int64)
+    o = to_np(out)
+    for b in range(Bt):
+        for h in range(2):
+            want = oracle_head(qn[b, h], kn[b, h], vn[b, h], dims, B, lp.strategies[h], rows)
+            check_close(o[b, h][rows], want, f"sample {b} head {h}")
+            assert t.equal(cache.fetch(0, h)[b], out[b, h])
+
+
+@pytest.mark.parametrize("split", [False, True])
+def test_skip_heads_split_one_layer_bitwise(split):
+    """DFA2C_SKIP: two calls over complementary head sets (as two GPUs would
+    run) reproduce the single call bit for bit, leave skipped rows and
+    skipped heads' cache bookkeeping untouched, and a skipped Cached head
+    needs no slot."""
+    t = torch()
+    api.set_split_kv(split)
+    try:
+        _skip_heads(t)
+    finally:
+        api.set_split_kv(False)
+
+
+def _skip_heads(t):
+    H, nv, nt, d, B = 4, 4096, 333, 64, 128
+    n = nv + nt
+    dims = AttentionDims(H, d, nv, nt)
+    q, _ = bf16_inputs((H, n, d), 81)
+    k, _ = bf16_inputs((H, n, d), 82)
+    v, _ = bf16_inputs((H, n, d), 83)
+    ref_cache, a_cache = HeadCache(1, H, n, d), HeadCache(1, H, n, d)
+    api.multi_strategy_attention(q, k, v, LayerPlan.all_full(H), ref_cache, 0, 0, dims, B)
+    api.multi_strategy_attention(q, k, v, LayerPlan.all_full(H), a_cache, 0, 0, dims, B, skip_heads=[0, 3])
+    plan = LayerPlan.parse("A0 C A2 F")
+    ref = api.multi_strategy_attention(q, k, v, plan, ref_cache, 0, 1, dims, B)
+    out = t.full_like(q, 7.0)
+    api.multi_strategy_attention(q, k, v, plan, a_cache, 0, 1, dims, B, out=out, skip_heads=[0, 3])
+    t.cuda.synchronize()
+    assert bool((out[0] == 7.0).all()) and bool((out[3] == 7.0).all())  # skipped rows untouched
+    assert not a_cache.has(0, 0) and not a_cache.has(0, 3)            # skipped heads never committed
+    assert a_cache.produced_at(0, 2) == 1 and a_cache.produced_at(0, 1) == 0
+    assert t.equal(out[1], ref[1]) and t.equal(out[2], ref[2])
+    b_cache = HeadCache(1, H, n, d)
+    api.multi_strategy_attention(q, k, v, plan, b_cache, 0, 0, dims, B, out=out, skip_heads=[1, 2])  # no slots
+    t.cuda.synchronize()
+    assert t.equal(out, ref)  # head 0 (split text rows) and head 3 from the other "GPU"
+
+
 def test_rse_kernel_against_oracle_and_reference_semantics():
     t = torch()
     # f32 operands: fp64 accumulation, within 1e-9 of the reference's sequential rse
