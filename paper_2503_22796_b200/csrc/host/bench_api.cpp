@@ -5,6 +5,9 @@
 // dfa2c_dense_attention_forward / dfa2c_sparse_attention_forward with CUDA
 // events; dense and sparse samples interleave as in the reference.
 //
+// Both passes run with split-KV scheduling on: a single head is
+// latency-bound by its text-row pairs otherwise.
+//
 // check_outputs: the reference compares the sparse pass with an f64 oracle
 // at 1e-5, which a bf16 path cannot meet by design (tolerances are tested in
 // tests/test_gpu_parity.py). Here the check is exact and GPU-side: rows of
@@ -16,6 +19,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <ostream>
 #include <random>
@@ -136,6 +140,15 @@ DFA2_API std::vector<BenchResult> run_bench(const BenchConfig& config) {
     };
     auto dense_pass = [&] { throw_status(dfa2c_dense_attention_forward(q.p, k.p, v.p, od.p, 1, n, d, nullptr)); };
 
+    // One head is a latency-bound launch: time both paths with split-KV
+    // scheduling (dfa2c_set_split_kv), restoring the caller's setting after.
+    struct SplitScope {
+        bool prev;
+        SplitScope() : prev(std::getenv("DFA2_SPLIT_KV") && std::getenv("DFA2_SPLIT_KV")[0] == '1') {
+            dfa2c_set_split_kv(1);
+        }
+        ~SplitScope() { dfa2c_set_split_kv(prev ? 1 : 0); }
+    } split_scope;
     std::vector<BenchResult> results;
     try {
         for (size_t ti = 0; ti < config.targets.size(); ++ti) {
