@@ -84,8 +84,17 @@ __device__ __forceinline__ void accum(double m, double o, double K, double (&a)[
     }
 }
 
-constexpr int RSE_STAGES = 4;
-constexpr uint32_t RSE_STAGE_BYTES = 8192;  // per operand per stage
+#ifndef DFA2_RSE_STAGES
+#define DFA2_RSE_STAGES 4
+#endif
+#ifndef DFA2_RSE_STAGE_KB
+#define DFA2_RSE_STAGE_KB 8
+#endif
+#ifndef DFA2_RSE_CTAS
+#define DFA2_RSE_CTAS 3
+#endif
+constexpr int RSE_STAGES = DFA2_RSE_STAGES;
+constexpr uint32_t RSE_STAGE_BYTES = DFA2_RSE_STAGE_KB * 1024;  // per operand per stage
 constexpr uint32_t RSE_BAR_OFF = RSE_STAGES * 2 * RSE_STAGE_BYTES;
 constexpr uint32_t RSE_SMEM = RSE_BAR_OFF + 2 * RSE_STAGES * 8;
 
@@ -252,7 +261,7 @@ void launch_typed(const void* ym, const void* yo, int64_t n_heads, int64_t numel
 }
 }  // namespace
 
-int rse_ctas_per_sm() { return 3; }  // 3 x (64 KB ring + bars) per SM
+int rse_ctas_per_sm() { return DFA2_RSE_CTAS; }  // 3 x (64 KB ring + bars) per SM by default
 
 cudaError_t launch_rse(const void* ym, const void* yo, int dtype, int64_t n_heads, int64_t numel,
                        int mode, double* out_dev, double* scratch, int nblk, cudaStream_t stream) {
