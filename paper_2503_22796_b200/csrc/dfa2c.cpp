@@ -544,10 +544,23 @@ struct dfa2c_cache {
     std::vector<void*> layer_buf;    // [L] -> [batch, H, n, d] bf16, lazily allocated
     std::vector<int64_t> produced;   // [L*H], INT64_MIN = empty slot
 
+    // Layer buffers come from the library's device pool (release threshold
+    // max): a cache of 57 FLUX layers (5.9 GB) is created and destroyed in
+    // microseconds instead of paying cudaMalloc / cudaFree (unmap) per layer.
     ~dfa2c_cache() {
+        bool any = false;
+        for (void* p : layer_buf)
+            any |= p != nullptr;
+        if (!any)
+            return;
+        int cur = 0;
+        cudaGetDevice(&cur);
+        cudaSetDevice(device);
+        cudaDeviceSynchronize();  // no launch may still read or write a slot
         for (void* p : layer_buf)
             if (p)
-                cudaFree(p);
+                cudaFreeAsync(p, nullptr);
+        cudaSetDevice(cur);
     }
     size_t slot_elems() const { return static_cast<size_t>(n * d); }
     size_t layer_bytes() const { return static_cast<size_t>(batch * H * n * d) * 2; }
@@ -574,8 +587,11 @@ struct dfa2c_cache {
     }
     void* layer_ptr(int64_t layer) {
         if (!layer_buf[layer]) {
-            DFA2C_CUDA_CHECK(cudaMalloc(&layer_buf[layer], layer_bytes()));
-            DFA2C_CUDA_CHECK(cudaMemset(layer_buf[layer], 0, layer_bytes()));
+            // stream-ordered on the legacy default stream, which orders with
+            // every blocking stream the caller launches on
+            DFA2C_CUDA_CHECK(
+                cudaMallocFromPoolAsync(&layer_buf[layer], layer_bytes(), scratch_pool(device), nullptr));
+            DFA2C_CUDA_CHECK(cudaMemsetAsync(layer_buf[layer], 0, layer_bytes(), nullptr));
         }
         return layer_buf[layer];
     }
