@@ -603,7 +603,12 @@ def influence_for_layer(q, k, v, methods: Sequence[MethodCandidate], cache: Opti
     M = len(methods)
     H, n, dd = dims.n_heads, dims.seq_len(), dims.head_dim
     original = torch.empty(H, n, dd, dtype=torch.bfloat16, device="cuda")
-    outs = torch.zeros(M, H, n, dd, dtype=torch.bfloat16, device="cuda") if keep_outputs else None
+    # every Arrow candidate's output and (t > 0) the Cached candidate's are
+    # fully written by the call; only an ineligible Cached slot (t == 0,
+    # "unset" in the reference) needs clearing
+    outs = torch.empty(M, H, n, dd, dtype=torch.bfloat16, device="cuda") if keep_outputs else None
+    if outs is not None and include_cached and t == 0:
+        outs[M - 1].zero_()
     infl = np.zeros(H * M, np.float64)
     evals = c_int64(0)
     d = dims.c()
