@@ -208,7 +208,15 @@ int dfa2c_convert(const void* src, int32_t src_dtype, void* dst, int32_t dst_dty
  * include_cached != 0 (make_candidates, src/calibrate.cpp:89-103).
  * influence[H*M] host (h*M + m), +inf where ineligible (Cached at t == 0 or
  * empty slot). original / method_outputs are optional device outputs
- * ([H,N,d] and [M,H,N,d] bf16); evals (optional) += 1 + M. Synchronous. */
+ * ([H,N,d] and [M,H,N,d] bf16); evals (optional) += 1 + M (the
+ * reference's count of layer-level evaluations, whatever the launch count).
+ * Synchronous.
+ * When block == 128, the head dim is read in place (64, or 72..128 step 8)
+ * and 1 <= n_windows <= 15, the original and every Arrow candidate come from
+ * ONE fused launch: arrow masks are nested in w, so each
+ * query tile folds its key tiles band by band and a snapshot of O / l after
+ * band i is candidate i's output. Those outputs equal the per-candidate
+ * passes' up to the key-tile fold order (bf16 rounding). */
 int dfa2c_influence_for_layer(const void* q, const void* k, const void* v,
                               const dfa2c_dims* dims, int64_t block,
                               const int64_t* windows, int64_t n_windows,
@@ -216,6 +224,12 @@ int dfa2c_influence_for_layer(const void* q, const void* k, const void* v,
                               int64_t layer, int64_t t, int32_t mode, double* influence,
                               void* original, void* method_outputs, int64_t* evals,
                               void* stream);
+
+/* Fused calibration pass switch (process-wide; default on, environment
+ * DFA2_INFLUENCE_FUSED=0 turns it off): 0 = one launch per candidate, whose
+ * outputs are bitwise dfa2c_mha_forward's for the same strategy. */
+int dfa2c_set_influence_fused(int32_t on);
+int32_t dfa2c_influence_fused_enabled(void);
 
 /* ---- per-layer plan selection (calibration driver) ----------------------
  * The selection problem of calibrate_model (inc/plansolver.hpp:19-75;

@@ -370,6 +370,18 @@ def set_split_kv(on: bool) -> None:
     check(lib().dfa2c_set_split_kv(1 if on else 0))
 
 
+def set_influence_fused(on: bool) -> None:
+    """dfa2c_set_influence_fused: influence_for_layer evaluates the original and
+    every Arrow candidate in one fused launch (window-band snapshots; default
+    on, or DFA2_INFLUENCE_FUSED=0). Off: one pass per candidate, outputs bitwise
+    those of multi_strategy_attention."""
+    check(lib().dfa2c_set_influence_fused(1 if on else 0))
+
+
+def influence_fused_enabled() -> bool:
+    return bool(lib().dfa2c_influence_fused_enabled())
+
+
 def multi_strategy_attention(q, k, v, plan: LayerPlan, cache: Optional[HeadCache], layer: int, t: int,
                              dims: AttentionDims, block_size: int, out=None, stream=None, skip_heads=None):
     """multi_strategy_attention (inc/dispatch.hpp:44-47; src/dispatch.cpp:30-91).

@@ -521,6 +521,10 @@ __global__ void __launch_bounds__(384, 1)
                                 for (int kk = 0; kk < 4; ++kk)
                                     mma_bf16_ts(tmem + o_col(L), tmem + s_col(L) + kk * 8, vdesc + (kk * 2048 >> 4),
                                                 IDESC_O, 1u);
+                                // calibration snapshot: O_L is final for this band once
+                                // these PVs complete (the lane's next PV waits for it)
+                                if (prev & (L ? TILE_SNAP_B : TILE_SNAP_A))
+                                    mma_commit(o_full(L));
                             }
                             __syncwarp();
                             if (lane == 0) DFA2_STAMP(L, pcnt[L], 4);
@@ -584,7 +588,6 @@ __global__ void __launch_bounds__(384, 1)
         const uint32_t need_bit = L ? TILE_NEED_B : TILE_NEED_A;
         const uint32_t part_bit = L ? TILE_PART_B : TILE_PART_A;
         const float sl2 = args.scale_log2;
-        const int N = args.n;
         const uint32_t sc = tmem + lrow + s_col(L);
         const uint32_t oc = tmem + lrow + o_col(L);
         const uint32_t stg = sbase + C::STG_OFF + L * C::BOX_BYTES;  // this lane's staging box
@@ -618,6 +621,53 @@ __global__ void __launch_bounds__(384, 1)
             float m_ref = -INFINITY;
             float l = 0.f;
             bool first = true;
+            // ---- epilogue: O / l -> bf16 -> staging (128B swizzle) -> TMA
+            // bulk stores to out and, for computed heads, the cache slot; for
+            // calibration items (ITEM_MULTI) to every output in `dst`
+            const bool commit = (w.flags & ITEM_COMMIT) && args.cache;
+            const bool multi = (w.flags & ITEM_MULTI) != 0;
+            auto store_box = [&](int b, const float* vals, float inv, uint32_t dst) {
+                if (issuer)
+                    bulk_wait_read0();  // previous store from this buffer has read smem
+                named_bar_sync(1 + L, 128);
+                const uint32_t rbase = stg + static_cast<uint32_t>(r) * 128u;
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                    const uint32_t p0 = pack_bf16x2(vals[8 * c + 0] * inv, vals[8 * c + 1] * inv);
+                    const uint32_t p1 = pack_bf16x2(vals[8 * c + 2] * inv, vals[8 * c + 3] * inv);
+                    const uint32_t p2 = pack_bf16x2(vals[8 * c + 4] * inv, vals[8 * c + 5] * inv);
+                    const uint32_t p3 = pack_bf16x2(vals[8 * c + 6] * inv, vals[8 * c + 7] * inv);
+                    st_shared_v4(rbase + static_cast<uint32_t>((c ^ (r & 7)) * 16), p0, p1, p2, p3);
+                }
+                fence_proxy_async_smem();
+                named_bar_sync(1 + L, 128);
+                if (issuer) {
+                    if (!multi) {
+                        tma_store_3d(&tmo, stg, b * 64, qt * TILE_M, w.bh);  // rows >= N are clipped
+                        if (commit)
+                            tma_store_3d(&tmc, stg, b * 64, qt * TILE_M, w.bh);
+                    } else {
+                        if (dst & SNAP_ORIGINAL)
+                            tma_store_3d(&tmc, stg, b * 64, qt * TILE_M, w.bh);
+                        for (uint32_t m = dst & (SNAP_ORIGINAL - 1u); m; m &= m - 1u)
+                            tma_store_3d(&tmo, stg, b * 64, qt * TILE_M, w.bh + (__ffs(m) - 1) * args.snap_stride);
+                    }
+                    bulk_commit();
+                }
+            };
+            auto store_tile = [&](uint32_t dst) {
+                const float inv = 1.f / l;
+#pragma unroll
+                for (int b = 0; b < D / 64; ++b) {
+                    float o[64];
+                    tmem_ld32(oc + 64 * b, reinterpret_cast<uint32_t*>(o));
+                    tmem_ld32(oc + 64 * b + 32, reinterpret_cast<uint32_t*>(o) + 32);
+                    tmem_ld_wait();
+                    store_box(b, o, inv, dst);
+                }
+            };
+            const uint32_t snap_bit = L ? TILE_SNAP_B : TILE_SNAP_A;
+            int sidx = 0;
             for (int u = 0; u < w.n_tiles; ++u) {
                 const uint32_t word = args.tiles[w.tile_begin + u];
                 if (!(word & need_bit))
@@ -639,45 +689,26 @@ __global__ void __launch_bounds__(384, 1)
                 if (r == 0) DFA2_STAMP(L, scnt, 2);
                 ++scnt;
                 first = false;
+                if (word & snap_bit) {
+                    // the narrower candidate's window is complete: its output
+                    // is this state, O / l (the reference's sparse pass over
+                    // exactly these key blocks, src/arrow.cpp:24-72)
+                    mbar_wait(o_full(L), icnt & 1);
+                    ++icnt;
+                    tc_fence_after();
+                    store_tile(args.snap_slots[sidx++]);
+                    tc_fence_before();
+                }
             }
             mbar_wait(o_full(L), icnt & 1);
             ++icnt;
             tc_fence_after();
-            // ---- epilogue: O / l -> bf16 -> staging (128B swizzle) -> TMA
-            // bulk stores to out and, for computed heads, the cache slot
-            const bool commit = (w.flags & ITEM_COMMIT) && args.cache;
-            auto store_box = [&](int b, const float* vals, float inv) {
-                if (issuer)
-                    bulk_wait_read0();  // previous store from this buffer has read smem
-                named_bar_sync(1 + L, 128);
-                const uint32_t rbase = stg + static_cast<uint32_t>(r) * 128u;
-#pragma unroll
-                for (int c = 0; c < 8; ++c) {
-                    const uint32_t p0 = pack_bf16x2(vals[8 * c + 0] * inv, vals[8 * c + 1] * inv);
-                    const uint32_t p1 = pack_bf16x2(vals[8 * c + 2] * inv, vals[8 * c + 3] * inv);
-                    const uint32_t p2 = pack_bf16x2(vals[8 * c + 4] * inv, vals[8 * c + 5] * inv);
-                    const uint32_t p3 = pack_bf16x2(vals[8 * c + 6] * inv, vals[8 * c + 7] * inv);
-                    st_shared_v4(rbase + static_cast<uint32_t>((c ^ (r & 7)) * 16), p0, p1, p2, p3);
-                }
-                fence_proxy_async_smem();
-                named_bar_sync(1 + L, 128);
-                if (issuer) {
-                    tma_store_3d(&tmo, stg, b * 64, qt * TILE_M, w.bh);  // rows >= N are clipped
-                    if (commit)
-                        tma_store_3d(&tmc, stg, b * 64, qt * TILE_M, w.bh);
-                    bulk_commit();
-                }
-            };
             if (!(w.flags & ITEM_SPLIT)) {
-                const float inv = 1.f / l;
-#pragma unroll
-                for (int b = 0; b < D / 64; ++b) {
-                    float o[64];
-                    tmem_ld32(oc + 64 * b, reinterpret_cast<uint32_t*>(o));
-                    tmem_ld32(oc + 64 * b + 32, reinterpret_cast<uint32_t*>(o) + 32);
-                    tmem_ld_wait();
-                    store_box(b, o, inv);
-                }
+                uint32_t dst = 0;
+                if (multi)  // every snapshot not yet emitted: the full row covers them
+                    for (int i = sidx; i < args.n_snap; ++i)
+                        dst |= args.snap_slots[i];
+                store_tile(dst);
                 tc_fence_before();
                 continue;
             }
@@ -742,7 +773,7 @@ __global__ void __launch_bounds__(384, 1)
                         for (int i = 0; i < 64; ++i)
                             acc[i] = fmaf(wc, __ldcg(po + (64 * b + i) * TILE_M + r), acc[i]);
                     }
-                    store_box(b, acc, 1.f / lsum);
+                    store_box(b, acc, 1.f / lsum, 0u);
                 }
             }
         }

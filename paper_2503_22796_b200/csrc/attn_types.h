@@ -29,6 +29,8 @@ enum : int32_t {
     ITEM_COPY = 1,    // Cached head: out <- cache slot (src/dispatch.cpp:77-81)
     ITEM_COMMIT = 2,  // computed head: also store O into the cache slot (:85-88)
     ITEM_SPLIT = 4,   // one key chunk of a heavy pair; the group's last chunk combines
+    ITEM_MULTI = 8,   // calibration pass: every key tile in window-band order, with
+                      // snapshots of O/l written to the candidates' outputs (see below)
 };
 
 // Tile word: KV tile index in bits [0,24); bit 24/25: lane A/B folds this
@@ -39,6 +41,15 @@ constexpr uint32_t TILE_NEED_A = 1u << 24;
 constexpr uint32_t TILE_NEED_B = 1u << 25;
 constexpr uint32_t TILE_PART_A = 1u << 26;
 constexpr uint32_t TILE_PART_B = 1u << 27;
+// ITEM_MULTI: after folding this tile lane A/B emits its next snapshot
+// (args.snap_slots[i], i = the lane's snapshot count); at the item end the
+// lane emits every remaining snapshot from its final state.
+constexpr uint32_t TILE_SNAP_A = 1u << 28;
+constexpr uint32_t TILE_SNAP_B = 1u << 29;
+// snap_slots bit m < 15: candidate output m (map `to`, row bh + m * snap_stride);
+// SNAP_ORIGINAL: the original (all-Full) output (map `tc`).
+constexpr uint32_t SNAP_ORIGINAL = 1u << 15;
+constexpr int MAX_SNAPS = 16;
 // Per-query-tile tile-set word (dfa2c_tile_set): bit 31 = needs element masking.
 constexpr uint32_t TILE_SET_PARTIAL = 0x80000000u;
 
@@ -58,6 +69,9 @@ struct AttnArgs {
     float* part_o;             // split items: [slots][2 lanes][D][128] unnormalised O
     float* part_ml;            // split items: [slots][2 lanes][2][128] reference max, row sum
     int* counters;             // split groups: [groups][2 lanes] chunks finished (zeroed per launch)
+    int32_t snap_stride;       // ITEM_MULTI: rows of `to` between candidate outputs (= batch*H)
+    int32_t n_snap;            // ITEM_MULTI: snapshots per query tile (window bands + the full row)
+    uint16_t snap_slots[MAX_SNAPS];
 };
 
 constexpr int TILE_M = 128;  // query rows per tile (tcgen05 M)

@@ -204,6 +204,8 @@ struct DevPlan {
     int32_t* cta_begin = nullptr;
     uint32_t* tiles = nullptr;
     uint8_t* masks = nullptr;
+    int32_t n_snap = 0;                                   // calibration plans: snapshots per query tile
+    uint16_t snap_slots[dfa2k::MAX_SNAPS] = {};
     ~DevPlan() {
         cudaFree(items);
         cudaFree(cta_begin);
@@ -308,6 +310,13 @@ PairSet build_pair_set(const TileSet& ts, int64_t nqt) {
     return ps;
 }
 
+struct Cand {
+    WorkItem w;
+    double cost;
+};
+std::unique_ptr<DevPlan> schedule_items(int device, std::vector<Cand>& cands, const std::vector<uint32_t>& tiles,
+                                        const std::vector<uint8_t>& mask_bytes, int32_t n_groups, int32_t n_slots);
+
 // Builds the LPT-scheduled work list: each (sample, head, query-tile pair)
 // is one item costing (#lane-A tiles + #lane-B tiles + 1) tile-units
 // (compute) or #rows/128 (copy); items are sorted by cost (desc), then
@@ -383,10 +392,6 @@ std::unique_ptr<DevPlan> build_dev_plan(int device, int64_t batch, int64_t H, in
     }
     int32_t n_groups = 0, n_slots = 0;
 
-    struct Cand {
-        WorkItem w;
-        double cost;
-    };
     std::vector<Cand> cands;
     cands.reserve(static_cast<size_t>(batch * H * np));
     for (int64_t b = 0; b < batch; ++b)
@@ -441,6 +446,14 @@ std::unique_ptr<DevPlan> build_dev_plan(int device, int64_t batch, int64_t H, in
                 }
             }
         }
+    return schedule_items(device, cands, tiles, mask_bytes, n_groups, n_slots);
+}
+
+// LPT assignment of the work items to one persistent CTA per SM (cost desc,
+// then (bh, pair) so concurrently running CTAs share a head's K/V in L2) and
+// upload of the device plan.
+std::unique_ptr<DevPlan> schedule_items(int device, std::vector<Cand>& cands, const std::vector<uint32_t>& tiles,
+                                        const std::vector<uint8_t>& mask_bytes, int32_t n_groups, int32_t n_slots) {
     std::stable_sort(cands.begin(), cands.end(), [](const Cand& a, const Cand& b) {
         if (a.cost != b.cost)
             return a.cost > b.cost;
@@ -819,6 +832,215 @@ void launch_forward(const ForwardSpec& s, cudaStream_t stream) {
 }
 
 cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+// ------------------------------------------------- fused calibration pass
+// influence_for_layer (src/calibrate.cpp:193-253) evaluates the original
+// (all heads Full) and one all-heads Arrow(w) output per candidate window:
+// 1 + |windows| attention passes. Arrow masks are nested in w, so one pass
+// that folds every query tile's key tiles band by band — band 0 = the
+// narrowest candidate's keys, band i = the keys the i-th window adds, the
+// last band = the rest of the row — holds each candidate's exact key set
+// after its band, and a snapshot of O / l there IS that candidate's output
+// (SURVEY.md §8f-1). The kernel writes it to the candidate's output and
+// carries on; one launch computes the original plus every Arrow candidate
+// for the cost of the original. Results agree with the per-candidate passes
+// up to the fold order of the key tiles (bf16 rounding of the outputs);
+// dfa2c_set_influence_fused(0) selects the per-candidate passes, whose
+// outputs are bitwise those of dfa2c_mha_forward.
+std::atomic<int> g_influence_fused{-1};
+bool influence_fused_enabled() {
+    int v = g_influence_fused.load();
+    if (v < 0) {
+        const char* e = std::getenv("DFA2_INFLUENCE_FUSED");
+        v = (e && e[0] == '0') ? 0 : 1;
+        int expect = -1;
+        g_influence_fused.compare_exchange_strong(expect, v);
+        v = g_influence_fused.load();
+    }
+    return v == 1;
+}
+
+// Mask blocks must be the kernel's 128-key tiles (bands are whole tiles) and
+// the head dim one the kernel reads in place.
+bool influence_fused_eligible(const dfa2c_dims* dims, int64_t block, int64_t n_windows) {
+    return influence_fused_enabled() && block == dfa2k::TILE_N && direct_layout(dims->head_dim) &&
+           n_windows >= 1 && n_windows < dfa2k::MAX_SNAPS;
+}
+
+// One item per pair of query tiles (2p, 2p+1). Each lane folds every key
+// tile of its row, band by band; a tile both lanes take in the same band is
+// one shared K/V load, a tile in different bands of the two lanes is loaded
+// once per lane. A lane's last tile of band i (i < last band) carries its
+// SNAP bit unless it is the lane's last tile overall (the item end emits
+// every remaining snapshot from the final state).
+std::unique_ptr<DevPlan> build_multi_plan(int device, int64_t H, int64_t n,
+                                          const std::vector<std::vector<uint8_t>>& bands) {
+    const int64_t nt = ceil_div(n, dfa2k::TILE_N);  // key tiles == mask blocks (block == 128)
+    const int64_t np = (nt + 1) / 2;
+    const int S = static_cast<int>(bands.size());
+    const bool ragged = n % dfa2k::TILE_N != 0;
+    std::vector<uint32_t> tiles;
+    struct PairWords {
+        int64_t begin, len;
+    };
+    std::vector<PairWords> pw(static_cast<size_t>(np));
+    std::vector<int> ba(static_cast<size_t>(nt)), bb(static_cast<size_t>(nt));
+    auto band_of = [&](int64_t q, int64_t t) {
+        for (int s = 0; s < S; ++s)
+            if (bands[s][q * nt + t])
+                return s;
+        return S;
+    };
+    for (int64_t p = 0; p < np; ++p) {
+        const int64_t qa = 2 * p, qb = 2 * p + 1;
+        const bool has_b = qb < nt;
+        for (int64_t t = 0; t < nt; ++t) {
+            ba[t] = band_of(qa, t);
+            bb[t] = has_b ? band_of(qb, t) : -1;
+        }
+        const int64_t begin = static_cast<int64_t>(tiles.size());
+        std::vector<int64_t> snap_a, snap_b;  // per band: index of the lane's last tile in it
+        int64_t last_a = -1, last_b = -1;
+        for (int s = 0; s <= S; ++s) {
+            int64_t ra = -1, rb = -1;
+            auto push = [&](int64_t t, bool a, bool b) {
+                uint32_t wd = static_cast<uint32_t>(t);
+                const bool part = ragged && t == nt - 1;
+                if (a)
+                    wd |= dfa2k::TILE_NEED_A | (part ? dfa2k::TILE_PART_A : 0u);
+                if (b)
+                    wd |= dfa2k::TILE_NEED_B | (part ? dfa2k::TILE_PART_B : 0u);
+                tiles.push_back(wd);
+                const int64_t idx = static_cast<int64_t>(tiles.size()) - 1;
+                if (a)
+                    ra = last_a = idx;
+                if (b)
+                    rb = last_b = idx;
+            };
+            for (int64_t t = 0; t < nt; ++t)  // shared loads first
+                if (ba[t] == s && bb[t] == s)
+                    push(t, true, true);
+            for (int64_t t = 0; t < nt; ++t)
+                if (ba[t] == s && bb[t] != s)
+                    push(t, true, false);
+            for (int64_t t = 0; t < nt; ++t)
+                if (bb[t] == s && ba[t] != s)
+                    push(t, false, true);
+            if (s < S) {
+                snap_a.push_back(ra);
+                snap_b.push_back(rb);
+            }
+        }
+        for (int64_t i : snap_a)
+            if (i >= 0 && i != last_a)
+                tiles[i] |= dfa2k::TILE_SNAP_A;
+        for (int64_t i : snap_b)
+            if (i >= 0 && i != last_b)
+                tiles[i] |= dfa2k::TILE_SNAP_B;
+        pw[p] = {begin, static_cast<int64_t>(tiles.size()) - begin};
+    }
+    if (tiles.size() > static_cast<size_t>(std::numeric_limits<int32_t>::max()) || nt > (1 << 24))
+        fail(DFA2C_UNSUPPORTED, "work list too large");
+    // element masking of the ragged last key tile reads an all-active mask
+    const std::vector<uint8_t> mask_bytes(static_cast<size_t>(nt * nt), uint8_t{1});
+    std::vector<Cand> cands;
+    for (int64_t h = 0; h < H; ++h)
+        for (int64_t p = 0; p < np; ++p) {
+            WorkItem w{};
+            w.bh = static_cast<int32_t>(h);
+            w.qtile_a = static_cast<int32_t>(2 * p);
+            w.qtile_b = 2 * p + 1 < nt ? static_cast<int32_t>(2 * p + 1) : -1;
+            w.tile_begin = static_cast<int32_t>(pw[p].begin);
+            w.n_tiles = static_cast<int32_t>(pw[p].len);
+            w.mask_off = 0;
+            w.flags = dfa2k::ITEM_MULTI;
+            cands.push_back({w, static_cast<double>(nt * (w.qtile_b >= 0 ? 2 : 1)) + 1.0 + 0.25 * S});
+        }
+    return schedule_items(device, cands, tiles, mask_bytes, 0, 0);
+}
+
+// The fused pass: `orig` <- all-Full output, `cand` + m * layer <- Arrow(windows[m])
+// output, every head, batch 1.
+void run_influence_fused(const void* q, const void* k, const void* v, const dfa2c_dims* dims,
+                         const int64_t* windows, int64_t n_windows, void* orig, void* cand, cudaStream_t stream) {
+    const int64_t n = seq_len(dims), d = dims->head_dim, H = dims->n_heads;
+    const int64_t B = dfa2k::TILE_N;
+    if (H * n_windows > std::numeric_limits<int32_t>::max() / 2 || n > (1 << 24))
+        fail(DFA2C_UNSUPPORTED, "problem too large for the 32-bit tile coordinates");
+    check_ptr(q, "q");
+    check_ptr(k, "k");
+    check_ptr(v, "v");
+    check_ptr(orig, "original");
+    check_ptr(cand, "method outputs");
+    int device = 0;
+    DFA2C_CUDA_CHECK(cudaGetDevice(&device));
+    std::string key = "influence";
+    put(key, device);
+    put(key, H);
+    put(key, n);
+    put(key, d);
+    put(key, dims->n_visual);
+    put(key, dims->order);
+    for (int64_t m = 0; m < n_windows; ++m)
+        put(key, windows[m]);
+    DevPlan* plan = nullptr;
+    {
+        std::lock_guard<std::mutex> lk(g_plan_mu);
+        auto it = g_plans.find(key);
+        if (it == g_plans.end()) {
+            if (g_plans.size() >= 256)
+                g_plans.clear();
+            // distinct effective windows (the clamp of src/arrow.cpp:135-137),
+            // narrowest first: their masks are nested; a window whose mask is
+            // all-active is the original's full row
+            const int64_t nvb = ceil_div(dims->n_visual, B);
+            std::map<int64_t, uint32_t> by_window;
+            for (int64_t m = 0; m < n_windows; ++m)
+                by_window[std::min(windows[m], std::max<int64_t>(0, nvb - 1))] |= 1u << m;
+            uint32_t full_slots = dfa2k::SNAP_ORIGINAL;
+            std::vector<std::vector<uint8_t>> bands;
+            std::vector<uint32_t> band_slots;
+            for (const auto& [w, bits] : by_window) {
+                std::vector<uint8_t> mk = arrow_mask(dims, B, w);
+                if (std::all_of(mk.begin(), mk.end(), [](uint8_t x) { return x != 0; })) {
+                    full_slots |= bits;
+                } else {
+                    bands.push_back(std::move(mk));
+                    band_slots.push_back(bits);
+                }
+            }
+            auto p = build_multi_plan(device, H, n, bands);
+            p->n_snap = static_cast<int32_t>(bands.size()) + 1;
+            for (size_t i = 0; i < bands.size(); ++i)
+                p->snap_slots[i] = static_cast<uint16_t>(band_slots[i]);
+            p->snap_slots[bands.size()] = static_cast<uint16_t>(full_slots);
+            it = g_plans.emplace(key, std::move(p)).first;
+        }
+        plan = it->second.get();
+    }
+    const CUtensorMap tq = make_map(q, H, n, d, dfa2k::TILE_M);
+    const CUtensorMap tk = make_map(k, H, n, d, dfa2k::TILE_N);
+    const CUtensorMap tv = make_map(v, H, n, d, dfa2k::TILE_N);
+    const CUtensorMap to = make_map(cand, H * n_windows, n, d, dfa2k::TILE_M);
+    const CUtensorMap tc = make_map(orig, H, n, d, dfa2k::TILE_M);
+    dfa2k::AttnArgs a{};
+    a.items = plan->items;
+    a.cta_begin = plan->cta_begin;
+    a.tiles = plan->tiles;
+    a.masks = plan->masks;
+    a.out = static_cast<__nv_bfloat16*>(cand);
+    a.cache = nullptr;
+    a.n = static_cast<int32_t>(n);
+    a.block = static_cast<int32_t>(B);
+    a.nb = static_cast<int32_t>(ceil_div(n, B));
+    a.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(d)));
+    a.trace = g_trace;
+    a.snap_stride = static_cast<int32_t>(H);
+    a.n_snap = plan->n_snap;
+    std::copy(plan->snap_slots, plan->snap_slots + dfa2k::MAX_SNAPS, a.snap_slots);
+    DFA2C_CUDA_CHECK(dfa2k::launch_attn(kernel_dim(d), tq, tk, tv, to, tc, a, plan->grid, stream));
+    g_launches.fetch_add(1);
+}
 
 // Standard per-call mask bookkeeping for a LayerPlan: one mask per distinct
 // window (src/dispatch.cpp:38-54) plus the all-active mask for Full heads.
@@ -1407,32 +1629,41 @@ int dfa2c_influence_for_layer(const void* q, const void* k, const void* v, const
             scratch_alloc(&scratch_orig, layer_bytes, st);
             orig = scratch_orig;
         }
+        // fused: one launch writes the original and every Arrow candidate
+        // (all candidates resident at once); otherwise one pass per candidate
+        const bool fused = influence_fused_eligible(dims, block, n_windows);
         void* scratch_cand = nullptr;
         if (!method_outputs)
-            scratch_alloc(&scratch_cand, layer_bytes, st);
+            scratch_alloc(&scratch_cand, layer_bytes * static_cast<size_t>(fused ? n_windows : 1), st);
         double* rse_dev = nullptr;
         scratch_alloc(&rse_dev, static_cast<size_t>(M * H) * sizeof(double), st);
         std::vector<uint8_t> eligible(static_cast<size_t>(M * H), 0);
 
-        // 1 original evaluation: all heads Full (src/calibrate.cpp:206).
         std::vector<int32_t> kinds(static_cast<size_t>(H), DFA2C_FULL);
         std::vector<int64_t> wins(static_cast<size_t>(H), 0);
-        {
+        if (fused) {
+            run_influence_fused(q, k, v, dims, windows, n_windows, orig,
+                                method_outputs ? method_outputs : scratch_cand, st);
+        } else {
+            // 1 original evaluation: all heads Full (src/calibrate.cpp:206).
             ForwardSpec s{};
             s.q = q; s.k = k; s.v = v; s.out = orig; s.batch = 1; s.dims = dims; s.block = block;
             plan_jobs(dims, block, kinds.data(), wins.data(), false, s);
             run_forward(s, st);
         }
         for (int64_t m = 0; m < M; ++m) {
-            void* cand = method_outputs ? static_cast<char*>(method_outputs) + m * layer_bytes : scratch_cand;
+            void* cand = method_outputs ? static_cast<char*>(method_outputs) + m * layer_bytes
+                                        : static_cast<char*>(scratch_cand) + (fused ? m * layer_bytes : 0);
             if (m < n_windows) {
                 // Arrow(w) over every head, then per-head RSE (src/calibrate.cpp:238-250).
-                std::fill(kinds.begin(), kinds.end(), DFA2C_ARROW);
-                std::fill(wins.begin(), wins.end(), windows[m]);
-                ForwardSpec s{};
-                s.q = q; s.k = k; s.v = v; s.out = cand; s.batch = 1; s.dims = dims; s.block = block;
-                plan_jobs(dims, block, kinds.data(), wins.data(), false, s);
-                run_forward(s, st);
+                if (!fused) {
+                    std::fill(kinds.begin(), kinds.end(), DFA2C_ARROW);
+                    std::fill(wins.begin(), wins.end(), windows[m]);
+                    ForwardSpec s{};
+                    s.q = q; s.k = k; s.v = v; s.out = cand; s.batch = 1; s.dims = dims; s.block = block;
+                    plan_jobs(dims, block, kinds.data(), wins.data(), false, s);
+                    run_forward(s, st);
+                }
                 const int rc = dfa2c_rse_async(cand, orig, DFA2C_BF16, H, static_cast<int64_t>(head_elems), mode,
                                                rse_dev + m * H, stream);
                 if (rc != DFA2C_OK)
@@ -1482,6 +1713,13 @@ int dfa2c_influence_for_layer(const void* q, const void* k, const void* v, const
             *evals += 1 + M;
     });
 }
+
+int dfa2c_set_influence_fused(int32_t on) {
+    g_influence_fused.store(on ? 1 : 0);
+    return DFA2C_OK;
+}
+
+int32_t dfa2c_influence_fused_enabled(void) { return influence_fused_enabled() ? 1 : 0; }
 
 int dfa2c_set_split_kv(int32_t on) {
     g_split_kv.store(on ? 1 : 0);

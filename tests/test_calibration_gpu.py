@@ -1,8 +1,10 @@
 """The GPU-resident calibration driver (api.calibrate_model, contract of
 /root/reference/proj/src/calibrate.cpp:255-382) on a drifting multi-layer
 stream: the properties the reference's test_calibrate.cpp / test_workload.cpp
-assert, at d=128 and a ragged text block, plus the bitwise replay of the
-calibration stream by run_pipeline."""
+assert, at d=128 and a ragged text block, plus the replay of the
+calibration stream by run_pipeline: bitwise with the per-candidate
+influence passes (dfa2c_set_influence_fused(0)), within the bf16 output
+tolerance with the fused band-snapshot pass (the default at block 128)."""
 import math
 
 import numpy as np
@@ -37,6 +39,26 @@ def streams():
     return (lambda t, l: get(t, l, 0)), (lambda t, l: get(t, l, 1)), (lambda t, l: get(t, l, 2))
 
 
+@pytest.fixture(params=[False, True], ids=["exact", "fused"])
+def fused(request):
+    before = api.influence_fused_enabled()
+    api.set_influence_fused(request.param)
+    yield request.param
+    api.set_influence_fused(before)
+
+
+def same_stream(a, b, fused):
+    """Bitwise for the per-candidate passes; the fused pass folds key tiles
+    in window-band order, so its spliced outputs differ from the executed
+    plan's by bf16 rounding only (tests/test_gpu_parity.py tolerance)."""
+    import torch
+
+    if not fused:
+        return torch.equal(a, b)
+    x, y = a.double(), b.double()
+    return bool((x - y).abs().max() <= 1e-2 * y.abs().max())
+
+
 def calibrate(delta, keep=True):
     q, k, v = streams()
     cfg = api.CalibrationConfig(api.make_candidates([0, 2], include_cached=True), delta, 1.5)
@@ -44,7 +66,7 @@ def calibrate(delta, keep=True):
     return api.calibrate_model(q, k, v, dims, T, L, B, cfg, keep_outputs=keep), (q, k, v), cfg, dims
 
 
-def test_zero_budget_is_all_full_and_replays_the_baseline():
+def test_zero_budget_is_all_full_and_replays_the_baseline(fused):
     import torch
 
     r, (q, k, v), cfg, dims = calibrate(0.0)
@@ -52,7 +74,7 @@ def test_zero_budget_is_all_full_and_replays_the_baseline():
     assert r.stats.attention_evals == T * L * (1 + len(cfg.methods))
     base = api.run_pipeline(q, k, v, api.CompressionPlan.all_full(dims, T, L, B))
     torch.cuda.synchronize()
-    assert all(torch.equal(a, b) for a, b in zip(r.outputs, base.outputs))
+    assert all(same_stream(a, b, fused) for a, b in zip(r.outputs, base.outputs))
 
 
 def test_calibrated_plan_constraints_and_csv():
@@ -69,7 +91,7 @@ def test_calibrated_plan_constraints_and_csv():
     assert not any(r.influences.measured(0, l, h, len(cfg.methods) - 1) for l in range(L) for h in range(H))
 
 
-def test_executing_the_plan_reproduces_the_calibration_stream_bitwise():
+def test_executing_the_plan_reproduces_the_calibration_stream(fused):
     import torch
 
     r, (q, k, v), _, _ = calibrate(0.4)
@@ -77,10 +99,10 @@ def test_executing_the_plan_reproduces_the_calibration_stream_bitwise():
     torch.cuda.synchronize()
     assert run.sparsity == pytest.approx(r.plan.aggregate_sparsity(), abs=0)
     for i, (a, b) in enumerate(zip(r.outputs, run.outputs)):
-        assert torch.equal(a, b), f"layer slot {i}"
+        assert same_stream(a, b, fused), f"layer slot {i}"
 
 
-def test_remeasuring_under_the_plan_reproduces_the_influences():
+def test_remeasuring_under_the_plan_reproduces_the_influences(fused):
     r, (q, k, v), cfg, dims = calibrate(0.4, keep=False)
     cache = api.HeadCache(L, H, NV + NT, D)
     M = len(cfg.methods)

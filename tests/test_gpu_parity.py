@@ -419,8 +419,19 @@ def test_rse_kernel_against_oracle_and_reference_semantics():
         api.rse(t.tensor([5.0, 6.0], device="cuda"), t.tensor([5.0, 5.0], device="cuda"))
 
 
-def test_influence_for_layer_semantics():
-    """calibrate.cpp:193-253 + test_calibrate.cpp:85-146."""
+@pytest.mark.parametrize("fused", [False, True], ids=["exact", "fused"])
+def test_influence_for_layer_semantics(fused):
+    """calibrate.cpp:193-253 + test_calibrate.cpp:85-146, with the
+    per-candidate passes and with the fused band-snapshot pass."""
+    before = api.influence_fused_enabled()
+    api.set_influence_fused(fused)
+    try:
+        _influence_for_layer_semantics(fused)
+    finally:
+        api.set_influence_fused(before)
+
+
+def _influence_for_layer_semantics(fused):
     t = torch()
     H, nv, nt, d, B = 4, 1024, 77, 64, 128
     dims = AttentionDims(H, d, nv, nt)
@@ -443,12 +454,21 @@ def test_influence_for_layer_semantics():
         assert infl[h, 0] == pytest.approx(want, rel=1e-12)
     full = api.multi_strategy_attention(q, k, v, LayerPlan.all_full(H), None, 0, 0, dims, B)
     t.cuda.synchronize()
-    assert t.equal(full, li.original)
-    # Cached candidate against identical entries measures 0 (test_calibrate.cpp:97-109)
+    if fused:  # key tiles folded in window-band order: equal up to bf16 rounding
+        for h in range(H):
+            check_close(to_np(li.original[h]), to_np(full[h]).astype(np.float64), f"original head {h}")
+    else:
+        assert t.equal(full, li.original)
+    # Cached candidate against identical entries measures 0 (test_calibrate.cpp:97-109):
+    # the slots hold the original of the same candidate set (in fused mode the
+    # original is the band-order fold of that set's pass)
     for h in range(H):
         cache.store(0, h, li.original[h], 0)
-    li2 = api.influence_for_layer(q, k, v, api.make_candidates([], True), cache, 0, 1, dims, B)
-    assert (li2.influence == 0.0).all()
+    li2 = api.influence_for_layer(q, k, v, methods, cache, 0, 1, dims, B)
+    assert (li2.influence.reshape(H, M)[:, 3] == 0.0).all()
+    if not fused:
+        li3 = api.influence_for_layer(q, k, v, api.make_candidates([], True), cache, 0, 1, dims, B)
+        assert (li3.influence == 0.0).all()
 
 
 def test_influence_matches_reference_values():
@@ -556,3 +576,102 @@ def test_head_sharded_layer_is_bitwise_the_single_gpu_layer():
                 assembled[h] = local[i]
         t.cuda.synchronize()
         assert t.equal(assembled, ref), f"W={W}"
+
+
+# ---- fused calibration pass (dfa2c_influence_for_layer at block 128):
+# the original and every Arrow candidate from one launch, each candidate the
+# snapshot of its query tiles after the candidate's window band.
+FUSED_CASES = [
+    # (H, nv, nt, d, order, windows)
+    (2, 1024, 77, 64, 0, [0, 2, 5, 100]),                  # cfg1 geometry, ragged tail; 100 clamps to Full
+    (2, 1024, 77, 128, 1, [3, 1, 1, 0]),                   # text-first; unsorted and duplicate windows
+    (2, 768, 0, 128, 0, [0, 1]),                           # no text band (block diagonal)
+    (1, 2048, 256, 128, 0, [0, 2, 4, 6, 8, 10, 12, 14]),   # eight bands, 15 (= Full) left to the original
+    (3, 300, 20, 96, 0, [0, 1]),                           # d=96 in place; 3 query tiles (single-lane item)
+]
+
+
+@pytest.mark.parametrize("H,nv,nt,d,order,windows", FUSED_CASES)
+def test_fused_influence_outputs_match_oracle(H, nv, nt, d, order, windows):
+    t = torch()
+    B = 128
+    assert api.influence_fused_enabled()  # the default
+    dims = AttentionDims(H, d, nv, nt, api.TEXT_FIRST if order else api.VISUAL_FIRST)
+    n = nv + nt
+    q, qn = bf16_inputs((H, n, d), 91)
+    k, kn = bf16_inputs((H, n, d), 92)
+    v, vn = bf16_inputs((H, n, d), 93)
+    methods = api.make_candidates(windows, include_cached=False)
+    launches = api.launch_count()
+    li = api.influence_for_layer(q, k, v, methods, None, 0, 0, dims, B)
+    t.cuda.synchronize()
+    assert api.launch_count() - launches == 1 + 2 * len(windows)  # one attention launch; RSE = 2 per window
+    rows = None if n <= 1200 else np.arange(0, n, 5)
+    for h in range(H):
+        want = oracle_head(qn[h], kn[h], vn[h], dims, B, HeadStrategy.Full(), rows)
+        got = to_np(li.original[h]) if rows is None else to_np(li.original[h])[rows]
+        check_close(got, want, f"original head {h}")
+        for m, w in enumerate(windows):
+            want = oracle_head(qn[h], kn[h], vn[h], dims, B, HeadStrategy.Arrow(w), rows)
+            got = to_np(li.method_outputs[m][h])
+            check_close(got if rows is None else got[rows], want, f"Arrow({w}) head {h}")
+    # equal effective windows share one snapshot; a window covering the row is the original
+    nvb = (nv + B - 1) // B
+    for m, w in enumerate(windows):
+        weff = min(w, max(0, nvb - 1))
+        for m2, w2 in enumerate(windows):
+            if min(w2, max(0, nvb - 1)) == weff:
+                assert t.equal(li.method_outputs[m], li.method_outputs[m2])
+        if (head_mask(dims, B, HeadStrategy.Arrow(w)) == 1).all():
+            assert t.equal(li.method_outputs[m], li.original)
+            assert (li.influence.reshape(H, -1)[:, m] == 0.0).all()
+    # deterministic: a second call is bitwise identical
+    li2 = api.influence_for_layer(q, k, v, methods, None, 0, 0, dims, B)
+    assert t.equal(li2.original, li.original) and t.equal(li2.method_outputs, li.method_outputs)
+    assert np.array_equal(li2.influence, li.influence)
+
+
+def test_fused_influence_agrees_with_per_candidate_passes():
+    """Same influences as the per-candidate passes (the outputs differ only by
+    the key-tile fold order); the per-candidate passes are bitwise the
+    dispatcher's outputs."""
+    t = torch()
+    H, nv, nt, d, B = 4, 2048, 77, 128, 128
+    dims = AttentionDims(H, d, nv, nt)
+    n = nv + nt
+    q, _ = bf16_inputs((H, n, d), 94)
+    k, _ = bf16_inputs((H, n, d), 95)
+    v, _ = bf16_inputs((H, n, d), 96)
+    # sharpen the logits of two heads so the windows matter unequally
+    q[:2] *= 3
+    methods = api.make_candidates([0, 2, 8], include_cached=False)
+    fused = api.influence_for_layer(q, k, v, methods, None, 0, 0, dims, B)
+    api.set_influence_fused(False)
+    try:
+        exact = api.influence_for_layer(q, k, v, methods, None, 0, 0, dims, B)
+    finally:
+        api.set_influence_fused(True)
+    np.testing.assert_allclose(fused.influence, exact.influence, rtol=2e-2, atol=1e-6)
+    for m, w in enumerate([0, 2, 8]):
+        lp = LayerPlan([HeadStrategy.Arrow(w)] * H)
+        ref = api.multi_strategy_attention(q, k, v, lp, None, 0, 0, dims, B)
+        t.cuda.synchronize()
+        assert t.equal(exact.method_outputs[m], ref)
+        for h in range(H):
+            check_close(to_np(fused.method_outputs[m][h]), to_np(ref[h]).astype(np.float64), f"Arrow({w}) head {h}")
+
+
+def test_fused_influence_falls_back_off_tile_blocks():
+    """Mask blocks other than the 128-key tile take the per-candidate passes
+    (outputs bitwise the dispatcher's)."""
+    t = torch()
+    H, nv, nt, d, B = 2, 512, 64, 64, 64
+    dims = AttentionDims(H, d, nv, nt)
+    n = nv + nt
+    q, _ = bf16_inputs((H, n, d), 97)
+    k, _ = bf16_inputs((H, n, d), 98)
+    v, _ = bf16_inputs((H, n, d), 99)
+    li = api.influence_for_layer(q, k, v, api.make_candidates([1], False), None, 0, 0, dims, B)
+    full = api.multi_strategy_attention(q, k, v, LayerPlan.all_full(H), None, 0, 0, dims, B)
+    t.cuda.synchronize()
+    assert t.equal(full, li.original)

@@ -141,6 +141,17 @@ if "5" in only:
     q, k, v = (randn(s, H, n, d) for s in (1, 2, 3))
     qs = [q, (q.float() + 0.05 * randn(4, H, n, d).float()).to(torch.bfloat16)]
     cfg = api.CalibrationConfig(api.make_candidates([0, 2, 8, 16, 32], include_cached=True), 0.4, 1.5)
+    # the per-candidate passes first (1 + 5 attention launches per layer),
+    # then the default fused band-snapshot pass (1 launch per layer)
+    api.set_influence_fused(False)
+    warm = api.calibrate_model(lambda t, l: qs[t], lambda t, l: k, lambda t, l: v, dims, 2, 1, B, cfg)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    r = api.calibrate_model(lambda t, l: qs[t], lambda t, l: k, lambda t, l: v, dims, T, L, B, cfg)
+    torch.cuda.synchronize()
+    per_candidate_s = time.perf_counter() - t0
+    per_candidate_sparsity = r.plan.aggregate_sparsity()
+    api.set_influence_fused(True)
     warm = api.calibrate_model(lambda t, l: qs[t], lambda t, l: k, lambda t, l: v, dims, 2, 1, B, cfg)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
@@ -158,6 +169,10 @@ if "5" in only:
     bytes_ = 2 * a.numel() * 2
     out = {"layers": L, "timesteps": T, "candidates": [m.id for m in cfg.methods], "calibration_s": sweep_s,
            "per_layer_ms": 1e3 * sweep_s / (T * L), "attention_evals": r.stats.attention_evals,
+           "influence_pass": "fused (original + 5 arrow candidates in one launch)",
+           "per_candidate_calibration_s": per_candidate_s,
+           "per_candidate_per_layer_ms": 1e3 * per_candidate_s / (T * L),
+           "per_candidate_aggregate_sparsity": per_candidate_sparsity,
            "aggregate_sparsity": r.plan.aggregate_sparsity(), "t1_choices": kinds,
            "audit_violations": api.audit_plan_constraints(r.plan, r.influences),
            "rse_ms": ms, "rse_bytes": bytes_, "rse_gbs": bytes_ / ms / 1e6}
