@@ -920,12 +920,21 @@ std::unique_ptr<DevPlan> build_multi_plan(int device, int64_t H, int64_t n,
             for (int64_t t = 0; t < nt; ++t)  // shared loads first
                 if (ba[t] == s && bb[t] == s)
                     push(t, true, true);
-            for (int64_t t = 0; t < nt; ++t)
+            // single-lane loads alternate lanes, so one lane's MMAs still
+            // overlap the other lane's softmax
+            std::vector<int64_t> only_a, only_b;
+            for (int64_t t = 0; t < nt; ++t) {
                 if (ba[t] == s && bb[t] != s)
-                    push(t, true, false);
-            for (int64_t t = 0; t < nt; ++t)
+                    only_a.push_back(t);
                 if (bb[t] == s && ba[t] != s)
-                    push(t, false, true);
+                    only_b.push_back(t);
+            }
+            for (size_t i = 0; i < std::max(only_a.size(), only_b.size()); ++i) {
+                if (i < only_a.size())
+                    push(only_a[i], true, false);
+                if (i < only_b.size())
+                    push(only_b[i], false, true);
+            }
             if (s < S) {
                 snap_a.push_back(ra);
                 snap_b.push_back(rb);
