@@ -16,6 +16,9 @@
 //                 [wait P_L(u-1)] O_L += P_L V(u-1)   (TS: P from TMEM)
 //                 S_L = Q_L K(u)^T                      (SS, into TMEM)
 //               so one lane's MMAs overlap the other lane's softmax.
+//               d = 64: P has its own TMEM columns, S_L(u) is issued first
+//               (it waits only for the softmax to have read S_L(u-1)), and
+//               warp 1 issues lane A's MMAs, warp 3 lane B's.
 //   warp 2      TMEM allocator
 //   warps 4-7   softmax lane A, warps 8-11 softmax lane B: one query row per
 //               thread; S read from TMEM twice (row max, then exp2 -> bf16 P
@@ -23,7 +26,8 @@
 //               TMEM, part of the exp2s on the FMA pipe (Cody-Waite +
 //               degree-3 polynomial) to unload MUFU; epilogue O/l -> bf16 ->
 //               out (+ cache slot); Cached heads' copy items.
-// TMEM (512 cols): S_A [0,128) S_B [128,256) O_A [256,256+D) O_B [384,384+D)
+// TMEM (512 cols), d=128: S_A [0,128) S_B [128,256) O_A [256,384) O_B [384,512), P over S;
+//   d=64: S_A, S_B as above, O_A [256,320) O_B [320,384) P_A [384,448) P_B [448,512)
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -32,6 +36,13 @@
 #include "sm100_ptx.cuh"
 
 namespace dfa2k {
+
+#ifndef DFA2_SEP_P64
+#define DFA2_SEP_P64 1
+#endif
+#ifndef DFA2_SPLIT_MMA64
+#define DFA2_SPLIT_MMA64 1
+#endif
 
 template <int D>
 struct Cfg {
@@ -54,7 +65,15 @@ struct Cfg {
     // lane: O epilogue and cached-head copies go smem -> TMA bulk store
     static constexpr uint32_t STG_OFF = V_OFF + VSTAGES * TILE_BYTES;
     static constexpr uint32_t BAR_OFF = STG_OFF + 2 * BOX_BYTES;
-    static constexpr int NBARS = 2 * QBUF + 2 * KSTAGES + 2 * VSTAGES + 10;
+    // d = 64: S 2x128 + O 2x64 columns leave 128 TMEM columns, so P gets
+    // its own 64 columns per lane and a lane's next S no longer waits for
+    // the PV that reads the current P (S_L(u+1) is issued as soon as the
+    // softmax has read S_L(u)). At d = 128 P overwrites S in place.
+    static constexpr bool SEP_P = D == 64 && DFA2_SEP_P64;
+    // With P separate, each lane gets its own MMA-issuing warp (warp 1 lane
+    // A, warp 3 lane B): a lane's S and PV then wait only on that lane.
+    static constexpr bool SPLIT_MMA = SEP_P && DFA2_SPLIT_MMA64;
+    static constexpr int NBARS = 2 * QBUF + 2 * KSTAGES + 2 * VSTAGES + 14;
     // The dynamic window starts 1024-aligned (the 1 KB system reservation
     // precedes it); the kernel traps otherwise, so no alignment slack.
     static constexpr uint32_t SMEM_BYTES = BAR_OFF + NBARS * 8 + 16;
@@ -93,7 +112,18 @@ struct Cfg {
 namespace {
 
 __device__ __forceinline__ uint32_t s_col(int lane) { return lane ? 128u : 0u; }
-__device__ __forceinline__ uint32_t o_col(int lane) { return lane ? 384u : 256u; }
+template <int D>
+__device__ __forceinline__ uint32_t o_col(int lane) {
+    return D == 64 ? 256u + 64u * lane : (lane ? 384u : 256u);
+}
+// P (bf16 pairs, 64 columns): its own columns at d = 64, else over S
+template <int D>
+__device__ __forceinline__ uint32_t p_col(int lane) {
+    return D == 64 ? 384u + 64u * lane : s_col(lane);
+}
+// column offset of the P of keys 64..127 within the lane's P columns
+template <int D>
+constexpr uint32_t P_HI = D == 64 ? 32u : 64u;
 
 // Two exp2s on the FMA/ALU pipes with packed fp32x2 arithmetic: x = j + f,
 // j = floor(x) by the round-down magic-number add, 2^f by a degree-3
@@ -196,10 +226,24 @@ __device__ __forceinline__ void softmax_half(const uint32_t* s, float2 scale2, f
             stamp[k_] = clock64();                             \
     } while (0)
 
+// SEP_P (d = 64): P goes to the lane's own columns `pc`; bar_sfree is
+// signalled once S is fully in registers (the lane's next S may overwrite
+// it), and before the first P store / O rescale the lane waits for the PV
+// of its previous tile (bar_pfree, parity pf_parity; < 0: no earlier tile).
 template <int D>
 __device__ __forceinline__ void softmax_tile(uint32_t sc, uint32_t oc, float sl2, float& m_ref, float& l,
-                                             bool first, uint32_t bar_half, uint32_t bar_full,
+                                             bool first, uint32_t bar_half, uint32_t bar_full, uint32_t pc,
+                                             uint32_t bar_sfree, uint32_t bar_pfree, int pf_parity,
                                              long long* stamp = nullptr) {
+    constexpr bool SEP = Cfg<D>::SEP_P;
+    bool pfree_done = !SEP || pf_parity < 0;
+    auto wait_pfree = [&] {
+        if (!pfree_done) {
+            mbar_wait(bar_pfree, static_cast<uint32_t>(pf_parity));
+            tc_fence_after();
+            pfree_done = true;
+        }
+    };
     uint32_t hi[64];
     float mx;
     {
@@ -262,7 +306,9 @@ __device__ __forceinline__ void softmax_tile(uint32_t sc, uint32_t oc, float sl2
     DFA2_SSTAMP(4);
     if (__any_sync(0xFFFFFFFFu, need)) {
         // O holds every earlier PV of this lane: this S was issued after them,
-        // so they completed before s_full fired.
+        // so they completed before s_full fired (SEP_P: S is issued before
+        // the previous PV, so wait for that PV explicitly).
+        wait_pfree();
 #pragma unroll
         for (int c = 0; c < D / 32; ++c) {
             uint32_t o[32];
@@ -278,8 +324,10 @@ __device__ __forceinline__ void softmax_tile(uint32_t sc, uint32_t oc, float sl2
     const float2 scale2 = make_float2(sl2, sl2);
     const float2 neg_m = make_float2(-msub, -msub);
     float2 sum = make_float2(0.f, 0.f);
-    // keys 64..127 from registers -> cols [64,96): the MMA warp starts on them
-    softmax_half<D>(hi, scale2, neg_m, sum, sc + 64);
+    // keys 64..127 from registers -> P cols [64,96) (SEP_P: [32,64) of P): the
+    // MMA warp starts on them
+    wait_pfree();
+    softmax_half<D>(hi, scale2, neg_m, sum, (SEP ? pc : sc) + P_HI<D>);
     DFA2_SSTAMP(5);
     tmem_st_wait();
     tc_fence_before();
@@ -290,8 +338,12 @@ __device__ __forceinline__ void softmax_tile(uint32_t sc, uint32_t oc, float sl2
     tmem_ld32(sc, lo);
     tmem_ld32(sc + 32, lo + 32);
     tmem_ld_wait();
+    if (SEP) {  // S fully read: the lane's next S may overwrite it
+        tc_fence_before();
+        mbar_arrive(bar_sfree);
+    }
     DFA2_SSTAMP(7);
-    softmax_half<D>(lo, scale2, neg_m, sum, sc);
+    softmax_half<D>(lo, scale2, neg_m, sum, SEP ? pc : sc);
     tmem_st_wait();
     tc_fence_before();
     mbar_arrive(bar_full);
@@ -350,20 +402,22 @@ __global__ void __launch_bounds__(384, 1)
     auto o_full = [&](int l) { return bars + 8u * (QB + 4 + 2 * KS + 2 * VS + l); };
     auto p_half = [&](int l) { return bars + 8u * (QB + 6 + 2 * KS + 2 * VS + l); };
     auto c_full = [&](int l) { return bars + 8u * (QB + 8 + 2 * KS + 2 * VS + l); };  // copy-box landed
+    auto s_free = [&](int l) { return bars + 8u * (QB + 10 + 2 * KS + 2 * VS + l); };  // SEP_P: S read
+    auto p_free = [&](int l) { return bars + 8u * (QB + 12 + 2 * KS + 2 * VS + l); };  // SEP_P: PV done
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::BAR_OFF + C::NBARS * 8);
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < C::QBUF; ++s) {
             mbar_init(q_full(s), 1);
-            mbar_init(q_empty(s), 1);
+            mbar_init(q_empty(s), C::SPLIT_MMA ? 2 : 1);
         }
         for (int s = 0; s < KS; ++s) {
             mbar_init(k_full(s), 1);
-            mbar_init(k_empty(s), 1);
+            mbar_init(k_empty(s), C::SPLIT_MMA ? 2 : 1);
         }
         for (int s = 0; s < VS; ++s) {
             mbar_init(v_full(s), 1);
-            mbar_init(v_empty(s), 1);
+            mbar_init(v_empty(s), C::SPLIT_MMA ? 2 : 1);
         }
         for (int l = 0; l < 2; ++l) {
             mbar_init(s_full(l), 1);
@@ -371,6 +425,8 @@ __global__ void __launch_bounds__(384, 1)
             mbar_init(p_half(l), 128);
             mbar_init(c_full(l), 1);
             mbar_init(o_full(l), 1);
+            mbar_init(s_free(l), 128);
+            mbar_init(p_free(l), 1);
         }
         fence_mbar_init();
     }
@@ -462,6 +518,120 @@ __global__ void __launch_bounds__(384, 1)
                     ++vitem;
             }
         }
+    } else if (C::SPLIT_MMA && (warp == 1 || warp == 3)) {
+        // ------------------------------------------------ per-lane tcgen05 issuer
+        // Both warps walk every union tile; a warp arrives on the K / V / Q
+        // "empty" barriers (count 2) with a commit after its MMAs, or a plain
+        // arrive, once the tile has landed, for tiles its lane does not fold.
+        const int L = warp == 1 ? 0 : 1;
+        const uint32_t need = L ? TILE_NEED_B : TILE_NEED_A;
+        const uint32_t snapb = L ? TILE_SNAP_B : TILE_SNAP_A;
+        constexpr uint32_t IDESC_S = idesc_bf16_f32(128, 128, false);
+        constexpr uint32_t IDESC_O = idesc_bf16_f32(128, D, true);
+        uint32_t kcount = 0, vcount = 0, qcount = 0, pcnt = 0, scount = 0;
+        for (int it = it0; it < it1; ++it) {
+            const WorkItem w = items[it];
+            if ((w.flags & ITEM_COPY) || w.n_tiles == 0)
+                continue;
+            const int qs = qcount % C::QBUF;
+            const uint32_t qbase = sbase + C::Q_OFF + qs * 2 * C::TILE_BYTES;
+            mbar_wait(q_full(qs), (qcount / C::QBUF) & 1);
+            tc_fence_after();
+            const bool has_lane = L == 0 || w.qtile_b >= 0;
+            bool first_pv = true, any_s = false;
+            uint32_t prev = 0;
+            const int U = w.n_tiles;
+            for (int u = 0; u <= U; ++u) {
+                const uint32_t word = u < U ? args.tiles[w.tile_begin + u] : 0u;
+                const int vst = vcount % VS;
+                const int kst = kcount % KS;
+                if (u < U) {
+                    if (word & need) {
+                        if (scount >= 1) {  // the lane's softmax has read its previous S
+                            mbar_wait(s_free(L), (scount - 1) & 1);
+                        }
+                        mbar_wait(k_full(kst), (kcount / KS) & 1);
+                        tc_fence_after();
+                        const uint64_t qdesc = smem_desc_sw128(qbase + L * C::TILE_BYTES, 16, 1024);
+                        const uint64_t kdesc = smem_desc_sw128(sbase + C::K_OFF + kst * C::TILE_BYTES, 16, 1024);
+                        if (elect_one()) {
+#pragma unroll
+                            for (int kk = 0; kk < D / 16; ++kk) {
+                                const uint32_t off = ((kk >> 2) * C::BOX_BYTES + (kk & 3) * 32) >> 4;
+                                mma_bf16_ss(tmem + s_col(L), qdesc + off, kdesc + off, IDESC_S, kk > 0 ? 1u : 0u);
+                            }
+                            mma_commit(s_full(L));
+                            mma_commit(k_empty(kst));
+                            if (u == U - 1)
+                                mma_commit(q_empty(qs));
+                        }
+                        __syncwarp();
+                        ++scount;
+                        any_s = true;
+                    } else {
+                        // the tile must be loaded before this use's arrival, or the
+                        // arrival could complete the slot's previous phase
+                        mbar_wait(k_full(kst), (kcount / KS) & 1);
+                        if (elect_one()) {
+                            mbar_arrive(k_empty(kst));
+                            if (u == U - 1) {
+                                if (any_s)
+                                    mma_commit(q_empty(qs));
+                                else
+                                    mbar_arrive(q_empty(qs));
+                            }
+                        }
+                        __syncwarp();
+                    }
+                }
+                if (u >= 1) {
+                    if (prev & need) {
+                        mbar_wait(v_full(vst), (vcount / VS) & 1);
+                        const uint64_t vdesc = smem_desc_sw128(sbase + C::V_OFF + vst * C::TILE_BYTES, C::BOX_BYTES, 1024);
+                        mbar_wait(p_half(L), pcnt & 1);
+                        tc_fence_after();
+                        if (elect_one()) {
+#pragma unroll
+                            for (int kk = 4; kk < 8; ++kk)
+                                mma_bf16_ts(tmem + o_col<D>(L), tmem + p_col<D>(L) + P_HI<D> + (kk - 4) * 8,
+                                            vdesc + (kk * 2048 >> 4), IDESC_O, (!first_pv || kk > 4) ? 1u : 0u);
+                        }
+                        __syncwarp();
+                        mbar_wait(p_full(L), pcnt & 1);
+                        tc_fence_after();
+                        if (elect_one()) {
+#pragma unroll
+                            for (int kk = 0; kk < 4; ++kk)
+                                mma_bf16_ts(tmem + o_col<D>(L), tmem + p_col<D>(L) + kk * 8, vdesc + (kk * 2048 >> 4),
+                                            IDESC_O, 1u);
+                            if (prev & snapb)
+                                mma_commit(o_full(L));
+                            mma_commit(p_free(L));
+                            mma_commit(v_empty(vst));
+                        }
+                        __syncwarp();
+                        first_pv = false;
+                        ++pcnt;
+                    } else {
+                        mbar_wait(v_full(vst), (vcount / VS) & 1);
+                        if (elect_one())
+                            mbar_arrive(v_empty(vst));
+                        __syncwarp();
+                    }
+                }
+                if (u >= 1)
+                    ++vcount;
+                if (u < U)
+                    ++kcount;
+                prev = word;
+            }
+            if (has_lane) {
+                if (elect_one())
+                    mma_commit(o_full(L));
+                __syncwarp();
+            }
+            ++qcount;
+        }
     } else if (warp == 1) {
         // ------------------------------------------------ tcgen05 issuer
         // Whole warp walks the schedule and waits; one elected lane (the same
@@ -495,7 +665,7 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
                     for (int L = 0; L < 2; ++L) {
                         const uint32_t need = L ? TILE_NEED_B : TILE_NEED_A;
-                        if (u >= 1 && (prev & need)) {
+                        auto issue_pv = [&] {
                             if (!v_ready) {
                                 mbar_wait(v_full(vst), (vcount / VS) & 1);
                                 v_ready = true;
@@ -510,7 +680,7 @@ __global__ void __launch_bounds__(384, 1)
                             if (elect_one()) {
 #pragma unroll
                                 for (int kk = 4; kk < 8; ++kk)
-                                    mma_bf16_ts(tmem + o_col(L), tmem + s_col(L) + 64 + (kk - 4) * 8,
+                                    mma_bf16_ts(tmem + o_col<D>(L), tmem + p_col<D>(L) + P_HI<D> + (kk - 4) * 8,
                                                 vdesc + (kk * 2048 >> 4), IDESC_O, (!first_pv[L] || kk > 4) ? 1u : 0u);
                             }
                             __syncwarp();
@@ -519,19 +689,25 @@ __global__ void __launch_bounds__(384, 1)
                             if (elect_one()) {
 #pragma unroll
                                 for (int kk = 0; kk < 4; ++kk)
-                                    mma_bf16_ts(tmem + o_col(L), tmem + s_col(L) + kk * 8, vdesc + (kk * 2048 >> 4),
+                                    mma_bf16_ts(tmem + o_col<D>(L), tmem + p_col<D>(L) + kk * 8, vdesc + (kk * 2048 >> 4),
                                                 IDESC_O, 1u);
                                 // calibration snapshot: O_L is final for this band once
                                 // these PVs complete (the lane's next PV waits for it)
                                 if (prev & (L ? TILE_SNAP_B : TILE_SNAP_A))
                                     mma_commit(o_full(L));
+                                if (C::SEP_P)
+                                    mma_commit(p_free(L));  // P_L may be overwritten
                             }
                             __syncwarp();
                             if (lane == 0) DFA2_STAMP(L, pcnt[L], 4);
                             first_pv[L] = false;
                             ++pcnt[L];
-                        }
-                        if (u < U && (word & need)) {
+                        };
+                        auto issue_s = [&] {
+                            if (C::SEP_P && scount[L] >= 1) {  // the lane's softmax has read its last S
+                                mbar_wait(s_free(L), (scount[L] - 1) & 1);
+                                tc_fence_after();
+                            }
                             if (!k_ready) {
                                 mbar_wait(k_full(kst), (kcount / KS) & 1);
                                 k_ready = true;
@@ -551,6 +727,19 @@ __global__ void __launch_bounds__(384, 1)
                             __syncwarp();
                             if (lane == 0) DFA2_STAMP(L, scount[L], 5);
                             ++scount[L];
+                        };
+                        const bool do_pv = u >= 1 && (prev & need);
+                        const bool do_s = u < U && (word & need);
+                        if (C::SEP_P) {  // S_L(u) first: it only waits for the softmax to read S_L(u-1)
+                            if (do_s)
+                                issue_s();
+                            if (do_pv)
+                                issue_pv();
+                        } else {
+                            if (do_pv)
+                                issue_pv();
+                            if (do_s)
+                                issue_s();
                         }
                     }
                     if (elect_one()) {
@@ -589,7 +778,8 @@ __global__ void __launch_bounds__(384, 1)
         const uint32_t part_bit = L ? TILE_PART_B : TILE_PART_A;
         const float sl2 = args.scale_log2;
         const uint32_t sc = tmem + lrow + s_col(L);
-        const uint32_t oc = tmem + lrow + o_col(L);
+        const uint32_t oc = tmem + lrow + o_col<D>(L);
+        const uint32_t pc = tmem + lrow + p_col<D>(L);
         const uint32_t stg = sbase + C::STG_OFF + L * C::BOX_BYTES;  // this lane's staging box
         const bool issuer = r == 0;  // issues this lane's bulk copies / stores
         uint32_t scnt = 0, icnt = 0, ccnt = 0;
@@ -685,7 +875,8 @@ __global__ void __launch_bounds__(384, 1)
                 long long* stamp = nullptr;
                 if (DFA2_TRACE == 2 && args.trace && blockIdx.x == 0 && r == 0 && scnt < 4096)
                     stamp = args.trace + ((L * 4096) + scnt) * 8;
-                softmax_tile<D>(sc, oc, sl2, m_ref, l, first, p_half(L), p_full(L), stamp);
+                softmax_tile<D>(sc, oc, sl2, m_ref, l, first, p_half(L), p_full(L), pc, s_free(L), p_free(L),
+                                scnt == 0 ? -1 : static_cast<int>((scnt - 1) & 1), stamp);
                 if (r == 0) DFA2_STAMP(L, scnt, 2);
                 ++scnt;
                 first = false;
