@@ -225,6 +225,23 @@ int dfa2c_influence_for_layer(const void* q, const void* k, const void* v,
                               void* original, void* method_outputs, int64_t* evals,
                               void* stream);
 
+/* Asynchronous influence_for_layer: the same launches, nothing synchronised.
+ * rse_host (HOST double[M*H], pinned for true asynchrony) receives the raw
+ * per-(m, h) RSE at index m*H + h when the stream reaches it; eligible (HOST
+ * uint8[M*H], written before return) marks the measured entries.
+ * dfa2c_influence_finalize turns both into influence[h*M + m] (+inf where
+ * ineligible; DFA2C_DEGENERATE on a zero-variance reference). Lets a
+ * calibration driver solve layer l while the GPU measures layer l+1. */
+int dfa2c_influence_for_layer_async(const void* q, const void* k, const void* v,
+                                    const dfa2c_dims* dims, int64_t block,
+                                    const int64_t* windows, int64_t n_windows,
+                                    int32_t include_cached, const dfa2c_cache* cache,
+                                    int64_t layer, int64_t t, int32_t mode, double* rse_host,
+                                    uint8_t* eligible, void* original, void* method_outputs,
+                                    int64_t* evals, void* stream);
+int dfa2c_influence_finalize(const double* rse_host, const uint8_t* eligible, int64_t n_heads,
+                             int64_t n_methods, double* influence);
+
 /* Fused calibration pass switch (process-wide; default on, environment
  * DFA2_INFLUENCE_FUSED=0 turns it off): 0 = one launch per candidate, whose
  * outputs are bitwise dfa2c_mha_forward's for the same strategy. */

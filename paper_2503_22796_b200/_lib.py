@@ -152,6 +152,12 @@ _SIGS = {
                                             POINTER(c_int64), c_int64, c_int32, c_void_p, c_int64, c_int64,
                                             c_int32, POINTER(c_double), c_void_p, c_void_p, POINTER(c_int64),
                                             c_void_p]),
+    "dfa2c_influence_for_layer_async": (c_int32, [c_void_p, c_void_p, c_void_p, POINTER(Dims), c_int64,
+                                                  POINTER(c_int64), c_int64, c_int32, c_void_p, c_int64, c_int64,
+                                                  c_int32, POINTER(c_double), POINTER(c_uint8), c_void_p, c_void_p,
+                                                  POINTER(c_int64), c_void_p]),
+    "dfa2c_influence_finalize": (c_int32, [POINTER(c_double), POINTER(c_uint8), c_int64, c_int64,
+                                           POINTER(c_double)]),
 }
 
 _lib = None

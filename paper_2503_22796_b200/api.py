@@ -599,16 +599,7 @@ def influence_for_layer(q, k, v, methods: Sequence[MethodCandidate], cache: Opti
     torch = _torch()
     if not methods:
         raise ShapeError("candidate set must be nonempty")
-    windows, include_cached = [], False
-    for i, m in enumerate(methods):
-        if m.strategy.kind == StrategyKind.arrow:
-            if include_cached:
-                raise ShapeError("Cached must be the last candidate")
-            windows.append(m.strategy.window_blocks)
-        elif m.strategy.kind == StrategyKind.cached:
-            include_cached = True
-        else:
-            raise ShapeError("Full is not a compression candidate")
+    windows, include_cached = _candidate_windows(methods)
     q = _as_bf16_cuda(q, "q")
     k = _as_bf16_cuda(k, "k")
     v = _as_bf16_cuda(v, "v")
@@ -633,6 +624,74 @@ def influence_for_layer(q, k, v, methods: Sequence[MethodCandidate], cache: Opti
     if stats is not None:
         stats.attention_evals += evals.value
     return LayerInfluence(original, outs, infl)
+
+
+def _candidate_windows(methods: Sequence[MethodCandidate]):
+    windows, include_cached = [], False
+    for m in methods:
+        if m.strategy.kind == StrategyKind.arrow:
+            if include_cached:
+                raise ShapeError("Cached must be the last candidate")
+            windows.append(m.strategy.window_blocks)
+        elif m.strategy.kind == StrategyKind.cached:
+            include_cached = True
+        else:
+            raise ShapeError("Full is not a compression candidate")
+    return windows, include_cached
+
+
+@dataclass
+class _PendingInfluence:
+    """An influence_for_layer launched with dfa2c_influence_for_layer_async and
+    not yet synchronised (the calibration driver's pipeline)."""
+
+    original: object
+    outs: object
+    rse_host: object      # pinned float64 [M * H], m * H + h
+    eligible: np.ndarray  # uint8 [M * H]
+    event: object
+    H: int
+    M: int
+
+    def finish(self) -> LayerInfluence:
+        self.event.synchronize()
+        infl = np.zeros(self.H * self.M, np.float64)
+        check(lib().dfa2c_influence_finalize(
+            ctypes.cast(self.rse_host.data_ptr(), POINTER(c_double)), self.eligible.ctypes.data_as(POINTER(c_uint8)),
+            self.H, self.M, infl.ctypes.data_as(POINTER(c_double))))
+        return LayerInfluence(self.original, self.outs, infl)
+
+
+def _influence_launch(q, k, v, methods, cache, layer, t, dims, block_size, mode, stats, bufs) -> _PendingInfluence:
+    torch = _torch()
+    windows, include_cached = _candidate_windows(methods)
+    q = _as_bf16_cuda(q, "q")
+    k = _as_bf16_cuda(k, "k")
+    v = _as_bf16_cuda(v, "v")
+    M = len(methods)
+    H, n, dd = dims.n_heads, dims.seq_len(), dims.head_dim
+    if not bufs:
+        bufs.extend([torch.empty(H, n, dd, dtype=torch.bfloat16, device="cuda"),
+                     torch.empty(M, H, n, dd, dtype=torch.bfloat16, device="cuda"),
+                     torch.empty(M * H, dtype=torch.float64, pin_memory=True)])
+    original, outs, rse_host = bufs
+    if include_cached and t == 0:
+        outs[M - 1].zero_()
+    eligible = np.zeros(M * H, np.uint8)
+    evals = c_int64(0)
+    d = dims.c()
+    w_arr = (c_int64 * max(1, len(windows)))(*windows)
+    check(lib().dfa2c_influence_for_layer_async(
+        c_void_p(q.data_ptr()), c_void_p(k.data_ptr()), c_void_p(v.data_ptr()), byref(d), block_size,
+        w_arr, len(windows), 1 if include_cached else 0, cache.handle if cache is not None else None,
+        layer, t, mode, ctypes.cast(rse_host.data_ptr(), POINTER(c_double)),
+        eligible.ctypes.data_as(POINTER(c_uint8)), c_void_p(original.data_ptr()), c_void_p(outs.data_ptr()),
+        byref(evals), c_void_p(_stream_ptr(None))))
+    if stats is not None:
+        stats.attention_evals += evals.value
+    ev = torch.cuda.Event()
+    ev.record()
+    return _PendingInfluence(original, outs, rse_host, eligible, ev, H, M)
 
 
 # --------------------------------------------------------------- calibration driver
@@ -721,7 +780,8 @@ def calibrate_model(q_stream, k_stream, v_stream, dims: "AttentionDims", n_times
                     keep_outputs: bool = False) -> CalibrationResult:
     """calibrate_model (inc/calibrate.hpp:101-105; src/calibrate.cpp:255-348),
     GPU-resident: for each (t, layer) in forward order, influence_for_layer
-    (1 + |M| fused launches + RSE kernels) on the already-compressed stream,
+    (one fused launch at block 128, else 1 + |M|, plus RSE kernels) on the
+    already-compressed stream, enqueued before the previous layer's solve,
     the exact per-layer solve (host, microseconds), and the splice: each
     computed head commits the output of its chosen measurement pass to the
     device cache (no extra attention evaluation); Cached heads keep their
@@ -749,25 +809,47 @@ def calibrate_model(q_stream, k_stream, v_stream, dims: "AttentionDims", n_times
     res = CalibrationResult(plan, table, stats)
     if cache is None:
         cache = HeadCache(n_layers, H, dims.seq_len(), dims.head_dim)
+
+    def finish(t, l, pending):
+        li = pending.finish()
+        grid = li.influence.reshape(H, M)
+        finite = np.isfinite(grid)
+        table.values[t, l][finite] = grid[finite]
+        sol = solve(PlanProblem(H, M, li.influence, costs, config.delta, config.coeff))
+        res.budget_spent.append(sol.total_influence)
+        res.objective.append(sol.objective)
+        plan.layers[t * n_layers + l] = to_layer_plan(sol, strategies)
+        if keep_outputs:
+            res.outputs.append(torch.stack([li.original[h] if c == kFullChoice else li.method_outputs[c][h]
+                                            for h, c in enumerate(sol.choice)]))
+        for h, c in enumerate(sol.choice):
+            if c == kFullChoice:
+                cache.store(l, h, li.original[h], t)
+            elif strategies[c].kind == StrategyKind.arrow:
+                cache.store(l, h, li.method_outputs[c][h], t)
+
+    # Pipelined: (t, l)'s measurement passes are enqueued before (t, l-1)'s
+    # solve and splice, so the GPU measures while the host solves. Only the
+    # Cached candidate of (t, l) reads the cache, and only slot l (written at
+    # t-1 or earlier); a splice into the same slot is finished first (L = 1).
+    # Two output buffer sets alternate; the stream orders each splice before
+    # the launch that reuses its buffers.
+    bufs = ([], [])
+    pending = None
+    idx = 0
     for t in range(n_timesteps):
         for l in range(n_layers):
-            li = influence_for_layer(q_stream(t, l), k_stream(t, l), v_stream(t, l), config.methods, cache, l, t,
-                                     dims, block_size, config.rse_mode, stats, keep_outputs=True)
-            grid = li.influence.reshape(H, M)
-            finite = np.isfinite(grid)
-            table.values[t, l][finite] = grid[finite]
-            sol = solve(PlanProblem(H, M, li.influence, costs, config.delta, config.coeff))
-            res.budget_spent.append(sol.total_influence)
-            res.objective.append(sol.objective)
-            plan.layers[t * n_layers + l] = to_layer_plan(sol, strategies)
-            if keep_outputs:
-                res.outputs.append(torch.stack([li.original[h] if c == kFullChoice else li.method_outputs[c][h]
-                                                for h, c in enumerate(sol.choice)]))
-            for h, c in enumerate(sol.choice):
-                if c == kFullChoice:
-                    cache.store(l, h, li.original[h], t)
-                elif strategies[c].kind == StrategyKind.arrow:
-                    cache.store(l, h, li.method_outputs[c][h], t)
+            if pending is not None and pending[1] == l:
+                finish(*pending)
+                pending = None
+            cur = _influence_launch(q_stream(t, l), k_stream(t, l), v_stream(t, l), config.methods, cache, l, t,
+                                    dims, block_size, config.rse_mode, stats, bufs[idx % 2])
+            idx += 1
+            if pending is not None:
+                finish(*pending)
+            pending = (t, l, cur)
+    if pending is not None:
+        finish(*pending)
     res.wall_seconds = time.perf_counter() - t0
     return res
 

@@ -1606,120 +1606,173 @@ int dfa2c_rse(const void* y_m, const void* y_o, int32_t dtype, int64_t n_heads, 
     });
 }
 
+namespace {
+// influence_for_layer up to the RSE results: every launch enqueued on
+// `stream`, the per-(m, h) RSE values copied (asynchronously) to
+// influence_host[m * H + h] and the eligibility of each entry returned;
+// nothing is synchronised.
+std::vector<uint8_t> influence_enqueue(const void* q, const void* k, const void* v, const dfa2c_dims* dims,
+                                       int64_t block, const int64_t* windows, int64_t n_windows,
+                                       int32_t include_cached, const dfa2c_cache* cache, int64_t layer, int64_t t,
+                                       int32_t mode, double* influence_host, void* original, void* method_outputs,
+                                       void* stream) {
+    validate_dims(dims);
+    if (block < 1)
+        fail(DFA2C_SHAPE, "block_size must be >= 1");
+    if (n_windows < 0 || (n_windows > 0 && !windows))
+        fail(DFA2C_SHAPE, "bad candidate windows");
+    for (int64_t i = 0; i < n_windows; ++i)
+        if (windows[i] < 0)
+            fail(DFA2C_SHAPE, "window radii must be >= 0");
+    const int64_t M = n_windows + (include_cached ? 1 : 0);
+    if (M == 0)
+        fail(DFA2C_SHAPE, "candidate set must be nonempty");
+    if (!influence_host)
+        fail(DFA2C_SHAPE, "influence output must not be NULL");
+    const int64_t H = dims->n_heads, n = seq_len(dims), d = dims->head_dim;
+    const size_t head_elems = static_cast<size_t>(n * d);
+    const size_t layer_bytes = static_cast<size_t>(H) * head_elems * 2;
+    if (include_cached && cache &&
+        (cache->H != H || cache->n != n || cache->d != d || cache->batch != 1))
+        fail(DFA2C_SHAPE, "cache geometry disagrees with dims");
+    const cudaStream_t st = as_stream(stream);
+
+    void* orig = original;
+    void* scratch_orig = nullptr;
+    if (!orig) {
+        scratch_alloc(&scratch_orig, layer_bytes, st);
+        orig = scratch_orig;
+    }
+    // fused: one launch writes the original and every Arrow candidate
+    // (all candidates resident at once); otherwise one pass per candidate
+    const bool fused = influence_fused_eligible(dims, block, n_windows);
+    void* scratch_cand = nullptr;
+    if (!method_outputs)
+        scratch_alloc(&scratch_cand, layer_bytes * static_cast<size_t>(fused ? n_windows : 1), st);
+    double* rse_dev = nullptr;
+    scratch_alloc(&rse_dev, static_cast<size_t>(M * H) * sizeof(double), st);
+    std::vector<uint8_t> eligible(static_cast<size_t>(M * H), 0);
+
+    std::vector<int32_t> kinds(static_cast<size_t>(H), DFA2C_FULL);
+    std::vector<int64_t> wins(static_cast<size_t>(H), 0);
+    if (fused) {
+        run_influence_fused(q, k, v, dims, windows, n_windows, orig,
+                            method_outputs ? method_outputs : scratch_cand, st);
+    } else {
+        // 1 original evaluation: all heads Full (src/calibrate.cpp:206).
+        ForwardSpec s{};
+        s.q = q; s.k = k; s.v = v; s.out = orig; s.batch = 1; s.dims = dims; s.block = block;
+        plan_jobs(dims, block, kinds.data(), wins.data(), false, s);
+        run_forward(s, st);
+    }
+    for (int64_t m = 0; m < M; ++m) {
+        void* cand = method_outputs ? static_cast<char*>(method_outputs) + m * layer_bytes
+                                    : static_cast<char*>(scratch_cand) + (fused ? m * layer_bytes : 0);
+        if (m < n_windows) {
+            // Arrow(w) over every head, then per-head RSE (src/calibrate.cpp:238-250).
+            if (!fused) {
+                std::fill(kinds.begin(), kinds.end(), DFA2C_ARROW);
+                std::fill(wins.begin(), wins.end(), windows[m]);
+                ForwardSpec s{};
+                s.q = q; s.k = k; s.v = v; s.out = cand; s.batch = 1; s.dims = dims; s.block = block;
+                plan_jobs(dims, block, kinds.data(), wins.data(), false, s);
+                run_forward(s, st);
+            }
+            const int rc = dfa2c_rse_async(cand, orig, DFA2C_BF16, H, static_cast<int64_t>(head_elems), mode,
+                                           rse_dev + m * H, stream);
+            if (rc != DFA2C_OK)
+                fail(rc, g_err);
+            for (int64_t h = 0; h < H; ++h)
+                eligible[m * H + h] = 1;
+        } else if (t > 0 && cache && layer >= 0 && layer < cache->L && cache->layer_buf[layer]) {
+            // Cached: slot vs original for heads with a slot (src/calibrate.cpp:222-235),
+            // one RSE launch over the layer's contiguous [H, N, d] slot array; heads
+            // without a slot stay ineligible (+inf).
+            const void* slots = cache->layer_buf[layer];
+            if (method_outputs) {
+                DFA2C_CUDA_CHECK(cudaMemsetAsync(cand, 0, layer_bytes, st));
+                for (int64_t h = 0; h < H; ++h)
+                    if (cache->has(layer, h))
+                        DFA2C_CUDA_CHECK(cudaMemcpyAsync(static_cast<char*>(cand) + h * head_elems * 2,
+                                                         static_cast<const char*>(slots) + h * head_elems * 2,
+                                                         head_elems * 2, cudaMemcpyDeviceToDevice, st));
+            }
+            const int rc = dfa2c_rse_async(slots, orig, DFA2C_BF16, H, static_cast<int64_t>(head_elems), mode,
+                                           rse_dev + m * H, stream);
+            if (rc != DFA2C_OK)
+                fail(rc, g_err);
+            for (int64_t h = 0; h < H; ++h)
+                eligible[m * H + h] = cache->has(layer, h) ? 1 : 0;
+        }
+    }
+    DFA2C_CUDA_CHECK(cudaMemcpyAsync(influence_host, rse_dev, static_cast<size_t>(M * H) * sizeof(double),
+                                     cudaMemcpyDeviceToHost, st));
+    DFA2C_CUDA_CHECK(cudaFreeAsync(rse_dev, st));
+    if (scratch_orig)
+        DFA2C_CUDA_CHECK(cudaFreeAsync(scratch_orig, st));
+    if (scratch_cand)
+        DFA2C_CUDA_CHECK(cudaFreeAsync(scratch_cand, st));
+    return eligible;
+}
+
+// host[m * H + h] (RSE, NaN = degenerate) + eligibility -> influence[h * M + m]
+void influence_finalize(const double* host, const uint8_t* eligible, int64_t H, int64_t M, double* influence) {
+    for (int64_t h = 0; h < H; ++h)
+        for (int64_t m = 0; m < M; ++m) {
+            double val = std::numeric_limits<double>::infinity();
+            if (eligible[m * H + h]) {
+                val = host[m * H + h];
+                if (std::isnan(val))
+                    fail(DFA2C_DEGENERATE, "reference output has zero variance (head " + std::to_string(h) + ")");
+            }
+            influence[h * M + m] = val;
+        }
+}
+}  // namespace
+
 int dfa2c_influence_for_layer(const void* q, const void* k, const void* v, const dfa2c_dims* dims, int64_t block,
                               const int64_t* windows, int64_t n_windows, int32_t include_cached,
                               const dfa2c_cache* cache, int64_t layer, int64_t t, int32_t mode, double* influence,
                               void* original, void* method_outputs, int64_t* evals, void* stream) {
     return guard([&] {
-        validate_dims(dims);
-        if (block < 1)
-            fail(DFA2C_SHAPE, "block_size must be >= 1");
-        if (n_windows < 0 || (n_windows > 0 && !windows))
-            fail(DFA2C_SHAPE, "bad candidate windows");
-        for (int64_t i = 0; i < n_windows; ++i)
-            if (windows[i] < 0)
-                fail(DFA2C_SHAPE, "window radii must be >= 0");
-        const int64_t M = n_windows + (include_cached ? 1 : 0);
-        if (M == 0)
-            fail(DFA2C_SHAPE, "candidate set must be nonempty");
         if (!influence)
             fail(DFA2C_SHAPE, "influence output must not be NULL");
-        const int64_t H = dims->n_heads, n = seq_len(dims), d = dims->head_dim;
-        const size_t head_elems = static_cast<size_t>(n * d);
-        const size_t layer_bytes = static_cast<size_t>(H) * head_elems * 2;
-        if (include_cached && cache &&
-            (cache->H != H || cache->n != n || cache->d != d || cache->batch != 1))
-            fail(DFA2C_SHAPE, "cache geometry disagrees with dims");
-        const cudaStream_t st = as_stream(stream);
-
-        void* orig = original;
-        void* scratch_orig = nullptr;
-        if (!orig) {
-            scratch_alloc(&scratch_orig, layer_bytes, st);
-            orig = scratch_orig;
-        }
-        // fused: one launch writes the original and every Arrow candidate
-        // (all candidates resident at once); otherwise one pass per candidate
-        const bool fused = influence_fused_eligible(dims, block, n_windows);
-        void* scratch_cand = nullptr;
-        if (!method_outputs)
-            scratch_alloc(&scratch_cand, layer_bytes * static_cast<size_t>(fused ? n_windows : 1), st);
-        double* rse_dev = nullptr;
-        scratch_alloc(&rse_dev, static_cast<size_t>(M * H) * sizeof(double), st);
-        std::vector<uint8_t> eligible(static_cast<size_t>(M * H), 0);
-
-        std::vector<int32_t> kinds(static_cast<size_t>(H), DFA2C_FULL);
-        std::vector<int64_t> wins(static_cast<size_t>(H), 0);
-        if (fused) {
-            run_influence_fused(q, k, v, dims, windows, n_windows, orig,
-                                method_outputs ? method_outputs : scratch_cand, st);
-        } else {
-            // 1 original evaluation: all heads Full (src/calibrate.cpp:206).
-            ForwardSpec s{};
-            s.q = q; s.k = k; s.v = v; s.out = orig; s.batch = 1; s.dims = dims; s.block = block;
-            plan_jobs(dims, block, kinds.data(), wins.data(), false, s);
-            run_forward(s, st);
-        }
-        for (int64_t m = 0; m < M; ++m) {
-            void* cand = method_outputs ? static_cast<char*>(method_outputs) + m * layer_bytes
-                                        : static_cast<char*>(scratch_cand) + (fused ? m * layer_bytes : 0);
-            if (m < n_windows) {
-                // Arrow(w) over every head, then per-head RSE (src/calibrate.cpp:238-250).
-                if (!fused) {
-                    std::fill(kinds.begin(), kinds.end(), DFA2C_ARROW);
-                    std::fill(wins.begin(), wins.end(), windows[m]);
-                    ForwardSpec s{};
-                    s.q = q; s.k = k; s.v = v; s.out = cand; s.batch = 1; s.dims = dims; s.block = block;
-                    plan_jobs(dims, block, kinds.data(), wins.data(), false, s);
-                    run_forward(s, st);
-                }
-                const int rc = dfa2c_rse_async(cand, orig, DFA2C_BF16, H, static_cast<int64_t>(head_elems), mode,
-                                               rse_dev + m * H, stream);
-                if (rc != DFA2C_OK)
-                    fail(rc, g_err);
-                for (int64_t h = 0; h < H; ++h)
-                    eligible[m * H + h] = 1;
-            } else if (t > 0 && cache && layer >= 0 && layer < cache->L && cache->layer_buf[layer]) {
-                // Cached: slot vs original for heads with a slot (src/calibrate.cpp:222-235),
-                // one RSE launch over the layer's contiguous [H, N, d] slot array; heads
-                // without a slot stay ineligible (+inf).
-                const void* slots = cache->layer_buf[layer];
-                if (method_outputs) {
-                    DFA2C_CUDA_CHECK(cudaMemsetAsync(cand, 0, layer_bytes, st));
-                    for (int64_t h = 0; h < H; ++h)
-                        if (cache->has(layer, h))
-                            DFA2C_CUDA_CHECK(cudaMemcpyAsync(static_cast<char*>(cand) + h * head_elems * 2,
-                                                             static_cast<const char*>(slots) + h * head_elems * 2,
-                                                             head_elems * 2, cudaMemcpyDeviceToDevice, st));
-                }
-                const int rc = dfa2c_rse_async(slots, orig, DFA2C_BF16, H, static_cast<int64_t>(head_elems), mode,
-                                               rse_dev + m * H, stream);
-                if (rc != DFA2C_OK)
-                    fail(rc, g_err);
-                for (int64_t h = 0; h < H; ++h)
-                    eligible[m * H + h] = cache->has(layer, h) ? 1 : 0;
-            }
-        }
-        std::vector<double> host(static_cast<size_t>(M * H));
-        DFA2C_CUDA_CHECK(cudaMemcpyAsync(host.data(), rse_dev, host.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
-        DFA2C_CUDA_CHECK(cudaFreeAsync(rse_dev, st));
-        if (scratch_orig)
-            DFA2C_CUDA_CHECK(cudaFreeAsync(scratch_orig, st));
-        if (scratch_cand)
-            DFA2C_CUDA_CHECK(cudaFreeAsync(scratch_cand, st));
-        DFA2C_CUDA_CHECK(cudaStreamSynchronize(st));
-        for (int64_t h = 0; h < H; ++h)
-            for (int64_t m = 0; m < M; ++m) {
-                double val = std::numeric_limits<double>::infinity();
-                if (eligible[m * H + h]) {
-                    val = host[m * H + h];
-                    if (std::isnan(val))
-                        fail(DFA2C_DEGENERATE, "reference output has zero variance (head " + std::to_string(h) + ")");
-                }
-                influence[h * M + m] = val;
-            }
+        validate_dims(dims);
+        const int64_t M = n_windows + (include_cached ? 1 : 0);
+        std::vector<double> host(static_cast<size_t>(std::max<int64_t>(M, 1) * dims->n_heads));
+        const std::vector<uint8_t> eligible =
+            influence_enqueue(q, k, v, dims, block, windows, n_windows, include_cached, cache, layer, t, mode,
+                              host.data(), original, method_outputs, stream);
+        DFA2C_CUDA_CHECK(cudaStreamSynchronize(as_stream(stream)));
+        influence_finalize(host.data(), eligible.data(), dims->n_heads, M, influence);
         if (evals)
             *evals += 1 + M;
+    });
+}
+
+int dfa2c_influence_for_layer_async(const void* q, const void* k, const void* v, const dfa2c_dims* dims,
+                                    int64_t block, const int64_t* windows, int64_t n_windows,
+                                    int32_t include_cached, const dfa2c_cache* cache, int64_t layer, int64_t t,
+                                    int32_t mode, double* rse_host, uint8_t* eligible, void* original,
+                                    void* method_outputs, int64_t* evals, void* stream) {
+    return guard([&] {
+        if (!rse_host || !eligible)
+            fail(DFA2C_SHAPE, "rse_host and eligible must not be NULL");
+        const std::vector<uint8_t> el =
+            influence_enqueue(q, k, v, dims, block, windows, n_windows, include_cached, cache, layer, t, mode,
+                              rse_host, original, method_outputs, stream);
+        std::copy(el.begin(), el.end(), eligible);
+        if (evals)
+            *evals += 1 + n_windows + (include_cached ? 1 : 0);
+    });
+}
+
+int dfa2c_influence_finalize(const double* rse_host, const uint8_t* eligible, int64_t n_heads, int64_t n_methods,
+                             double* influence) {
+    return guard([&] {
+        if (!rse_host || !eligible || !influence || n_heads < 1 || n_methods < 1)
+            fail(DFA2C_SHAPE, "bad influence_finalize arguments");
+        influence_finalize(rse_host, eligible, n_heads, n_methods, influence);
     });
 }
 
