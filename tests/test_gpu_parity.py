@@ -675,3 +675,32 @@ def test_fused_influence_falls_back_off_tile_blocks():
     full = api.multi_strategy_attention(q, k, v, LayerPlan.all_full(H), None, 0, 0, dims, B)
     t.cuda.synchronize()
     assert t.equal(full, li.original)
+
+
+def test_async_influence_matches_sync_and_window_limit_falls_back():
+    """dfa2c_influence_for_layer_async + dfa2c_influence_finalize give the
+    synchronous call's influences bitwise; 16 windows (over the fused pass's
+    15-candidate limit) take the per-candidate passes."""
+    t = torch()
+    H, nv, nt, d, B = 2, 1024, 77, 64, 128
+    dims = AttentionDims(H, d, nv, nt)
+    n = nv + nt
+    q, _ = bf16_inputs((H, n, d), 101)
+    k, _ = bf16_inputs((H, n, d), 102)
+    v, _ = bf16_inputs((H, n, d), 103)
+    cache = HeadCache(1, H, n, d)
+    api.multi_strategy_attention(q, k, v, LayerPlan.all_full(H), cache, 0, 0, dims, B)
+    methods = api.make_candidates([0, 1, 3], include_cached=True)
+    sync = api.influence_for_layer(q, k, v, methods, cache, 0, 1, dims, B)
+    bufs = []
+    pend = api._influence_launch(q, k, v, methods, cache, 0, 1, dims, B, api.RseMode.standard, None, bufs)
+    got = pend.finish()
+    assert np.array_equal(got.influence, sync.influence)
+    assert t.equal(got.original, sync.original) and t.equal(got.method_outputs, sync.method_outputs)
+    # 16 windows: per-candidate passes, whose original is bitwise the dispatcher's Full output
+    many = api.make_candidates(list(range(16)), include_cached=False)
+    li = api.influence_for_layer(q, k, v, many, None, 0, 0, dims, B)
+    full = api.multi_strategy_attention(q, k, v, LayerPlan.all_full(H), None, 0, 0, dims, B)
+    t.cuda.synchronize()
+    assert t.equal(li.original, full)
+    assert np.isfinite(li.influence).all()
