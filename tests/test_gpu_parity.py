@@ -704,3 +704,58 @@ def test_async_influence_matches_sync_and_window_limit_falls_back():
     t.cuda.synchronize()
     assert t.equal(li.original, full)
     assert np.isfinite(li.influence).all()
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_random_plans_and_geometries_against_oracle(seed):
+    """Seeded random layers: geometry (visual/text tokens, token order, mask
+    block, head dim), a random F / A(w) / C plan with slots filled at t = 0,
+    split-KV on or off. Sampled rows of every head against the f64 oracle;
+    Cached heads bitwise their slot; every computed head's committed slot
+    bitwise its output."""
+    t = torch()
+    rng = np.random.default_rng(1000 + seed)
+    H = int(rng.integers(2, 6))
+    d = int(rng.choice([64, 128, 96]))
+    nv = int(rng.integers(200, 3000))
+    nt = int(rng.choice([0, int(rng.integers(1, 400))]))
+    order = int(rng.integers(0, 2))
+    B = int(rng.choice([32, 64, 128, 128, 200]))
+    split = bool(rng.integers(0, 2))
+    dims = AttentionDims(H, d, nv, nt, api.TEXT_FIRST if order else api.VISUAL_FIRST)
+    n = nv + nt
+    nvb = (nv + B - 1) // B
+    strategies = []
+    for _ in range(H):
+        r = rng.random()
+        if r < 0.3:
+            strategies.append(HeadStrategy.Full())
+        elif r < 0.8:
+            strategies.append(HeadStrategy.Arrow(int(rng.integers(0, max(1, nvb + 2)))))
+        else:
+            strategies.append(HeadStrategy.Cached())
+    lp = LayerPlan(strategies)
+    q, qn = bf16_inputs((H, n, d), 2000 + seed)
+    k, kn = bf16_inputs((H, n, d), 3000 + seed)
+    v, vn = bf16_inputs((H, n, d), 4000 + seed)
+    cache = HeadCache(1, H, n, d)
+    slots, _ = bf16_inputs((H, n, d), 5000 + seed)
+    for h in range(H):
+        cache.store(0, h, slots[h], 0)
+    api.set_split_kv(split)
+    try:
+        out = api.multi_strategy_attention(q, k, v, lp, cache, 0, 1, dims, B)
+        t.cuda.synchronize()
+    finally:
+        api.set_split_kv(False)
+    rows = np.unique(np.concatenate([np.arange(0, n, max(1, n // 97)), [n - 1],
+                                     np.arange(dims.text_begin(), dims.text_end(), 11)])).astype(np.int64)
+    o = to_np(out)
+    for h, s_ in enumerate(strategies):
+        if s_.kind == "cached":
+            assert t.equal(out[h], slots[h]), f"head {h} cached copy"
+            assert cache.produced_at(0, h) == 0
+            continue
+        want = oracle_head(qn[h], kn[h], vn[h], dims, B, s_, rows)
+        check_close(o[h][rows], want, f"seed {seed} head {h} {s_} (d={d}, B={B}, order={order}, split={split})")
+        assert t.equal(cache.fetch(0, h), out[h]) and cache.produced_at(0, h) == 1
