@@ -759,3 +759,40 @@ def test_random_plans_and_geometries_against_oracle(seed):
         want = oracle_head(qn[h], kn[h], vn[h], dims, B, s_, rows)
         check_close(o[h][rows], want, f"seed {seed} head {h} {s_} (d={d}, B={B}, order={order}, split={split})")
         assert t.equal(cache.fetch(0, h), out[h]) and cache.produced_at(0, h) == 1
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_random_fused_influence_against_oracle(seed):
+    """Seeded random geometries through the fused calibration pass (block
+    128): every candidate's sampled rows against the f64 oracle, influences
+    against the per-candidate passes."""
+    t = torch()
+    rng = np.random.default_rng(7000 + seed)
+    H = int(rng.integers(1, 4))
+    d = int(rng.choice([64, 128, 96]))
+    nv = int(rng.integers(300, 3000))
+    nt = int(rng.choice([0, int(rng.integers(1, 400))]))
+    order = int(rng.integers(0, 2))
+    B = 128
+    dims = AttentionDims(H, d, nv, nt, api.TEXT_FIRST if order else api.VISUAL_FIRST)
+    n = nv + nt
+    windows = [int(w) for w in rng.integers(0, (nv + B - 1) // B + 3, size=int(rng.integers(1, 7)))]
+    q, qn = bf16_inputs((H, n, d), 8000 + seed)
+    k, kn = bf16_inputs((H, n, d), 9000 + seed)
+    v, vn = bf16_inputs((H, n, d), 10000 + seed)
+    methods = api.make_candidates(windows, include_cached=False)
+    li = api.influence_for_layer(q, k, v, methods, None, 0, 0, dims, B)
+    api.set_influence_fused(False)
+    try:
+        exact = api.influence_for_layer(q, k, v, methods, None, 0, 0, dims, B)
+    finally:
+        api.set_influence_fused(True)
+    t.cuda.synchronize()
+    rows = np.unique(np.concatenate([np.arange(0, n, max(1, n // 61)), [n - 1]])).astype(np.int64)
+    for h in range(H):
+        check_close(to_np(li.original[h])[rows], oracle_head(qn[h], kn[h], vn[h], dims, B, HeadStrategy.Full(), rows),
+                    f"seed {seed} original head {h}")
+        for m, w in enumerate(windows):
+            want = oracle_head(qn[h], kn[h], vn[h], dims, B, HeadStrategy.Arrow(w), rows)
+            check_close(to_np(li.method_outputs[m][h])[rows], want, f"seed {seed} Arrow({w}) head {h}")
+    np.testing.assert_allclose(li.influence, exact.influence, rtol=2e-2, atol=1e-6)
