@@ -133,7 +133,7 @@ if "5" in only:
     # the progressive calibration driver at FLUX 2K scale: every layer of a
     # 57-layer model at t = 0 (Cached ineligible) and t = 1 (Cached measured
     # against the t = 0 commits), candidates Arrow {0, 2, 8, 16, 32} + Cached;
-    # per layer 1 + 6 fused launches, 6 RSE launches, the exact solve and the
+    # per layer one fused launch (original + 5 Arrow candidates), 6 RSE launches, the exact solve and the
     # device-side splice into the cache
     L, H, nv, nt, d, B, T = 57, 24, 16384, 512, 128, 128, 2
     n = nv + nt
