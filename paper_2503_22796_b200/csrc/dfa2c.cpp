@@ -1689,14 +1689,15 @@ std::vector<uint8_t> influence_enqueue(const void* q, const void* k, const void*
             // one RSE launch over the layer's contiguous [H, N, d] slot array; heads
             // without a slot stay ineligible (+inf).
             const void* slots = cache->layer_buf[layer];
-            if (method_outputs) {
-                DFA2C_CUDA_CHECK(cudaMemsetAsync(cand, 0, layer_bytes, st));
-                for (int64_t h = 0; h < H; ++h)
+            if (method_outputs)  // the slot where there is one, zeros (unset) elsewhere
+                for (int64_t h = 0; h < H; ++h) {
+                    char* dst = static_cast<char*>(cand) + h * head_elems * 2;
                     if (cache->has(layer, h))
-                        DFA2C_CUDA_CHECK(cudaMemcpyAsync(static_cast<char*>(cand) + h * head_elems * 2,
-                                                         static_cast<const char*>(slots) + h * head_elems * 2,
+                        DFA2C_CUDA_CHECK(cudaMemcpyAsync(dst, static_cast<const char*>(slots) + h * head_elems * 2,
                                                          head_elems * 2, cudaMemcpyDeviceToDevice, st));
-            }
+                    else
+                        DFA2C_CUDA_CHECK(cudaMemsetAsync(dst, 0, head_elems * 2, st));
+                }
             const int rc = dfa2c_rse_async(slots, orig, DFA2C_BF16, H, static_cast<int64_t>(head_elems), mode,
                                            rse_dev + m * H, stream);
             if (rc != DFA2C_OK)

@@ -17,6 +17,11 @@ so no data-path collective is needed inside the layer:
 Outputs are bitwise identical for any W: a head's result depends only on
 its own tile sequence and on scheduling decisions taken from the full layer
 plan (DFA2C_SKIP keeps the plan whole), both fixed by the static schedule.
+
+The gather can overlap the compute per head group
+(pipelined_sharded_attention): each rank splits its heads into G groups,
+launches group g (every other head DFA2C_SKIP), and all-gathers group g's
+padded shard on a communication stream while group g+1 computes.
 """
 from __future__ import annotations
 
@@ -129,3 +134,74 @@ def sharded_multi_strategy_attention(q, k, v, plan: api.LayerPlan, cache: Option
     if not gather:
         return local
     return gather_heads(local, shard, full)
+
+
+@dataclass
+class HeadGroups:
+    """Per rank, its heads split into G consecutive groups; sizes[g] = the
+    largest group g over the ranks (the padded all-gather shard)."""
+
+    per_rank: List[List[List[int]]]
+    sizes: List[int]
+
+
+def head_groups(shard: HeadShard, n_groups: int) -> HeadGroups:
+    n_groups = max(1, n_groups)
+    per_rank = []
+    for hs in shard.all_heads:
+        q, r = divmod(len(hs), n_groups)
+        out, i = [], 0
+        for g in range(n_groups):
+            c = q + (1 if g < r else 0)
+            out.append(list(hs[i:i + c]))
+            i += c
+        per_rank.append(out)
+    sizes = [max(len(per_rank[r][g]) for r in range(shard.world)) for g in range(n_groups)]
+    return HeadGroups(per_rank, sizes)
+
+
+def pipelined_sharded_attention(compute_group, full_out, shard: HeadShard, n_groups: int, group=None,
+                                comm_stream=None):
+    """Compute + gather per head group. compute_group(heads) writes those
+    heads of full_out (on the current stream); after each group its padded
+    shard is all-gathered — on NCCL from `comm_stream` (which waits for the
+    group's compute), so the transfer overlaps the next group's compute; on
+    gloo (CPU tests) synchronously. Returns full_out with every rank's heads."""
+    import torch
+    import torch.distributed as dist
+
+    hg = head_groups(shard, n_groups)
+    mine = hg.per_rank[shard.rank]
+    n, d = full_out.shape[-2], full_out.shape[-1]
+    nccl = shard.world > 1 and dist.get_backend(group) == "nccl"
+    pending = []
+    for g in range(len(mine)):
+        hs = mine[g]
+        if hs:
+            compute_group(hs)
+        if shard.world == 1:
+            continue
+        padded = full_out.new_zeros((hg.sizes[g], n, d))
+        if hs:
+            padded[: len(hs)] = full_out[hs]
+        gathered = full_out.new_empty((shard.world * hg.sizes[g], n, d))
+        if nccl:
+            ev = torch.cuda.current_stream().record_event()
+            cs = comm_stream or torch.cuda.Stream()
+            with torch.cuda.stream(cs):
+                cs.wait_event(ev)
+                work = dist.all_gather_into_tensor(gathered, padded, group=group, async_op=True)
+            pending.append((g, gathered, padded, work))
+        else:
+            parts = list(gathered.chunk(shard.world))
+            dist.all_gather(parts, padded, group=group)
+            pending.append((g, torch.cat(parts), padded, None))
+    for g, gathered, _padded, work in pending:
+        if work is not None:
+            work.wait()  # the current stream waits for the collective
+        for r in range(shard.world):
+            if r == shard.rank:
+                continue
+            for i, h in enumerate(hg.per_rank[r][g]):
+                full_out[h].copy_(gathered[r * hg.sizes[g] + i])
+    return full_out

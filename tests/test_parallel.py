@@ -50,6 +50,19 @@ def _worker(rank, world, port, q):
         full = torch.empty(H, N, D)
         parallel.gather_heads(local, shard, full)
         ok = all(bool((full[h] == h).all()) for h in range(H))
+        # compute + gather pipelined per head group (2 and 3 groups)
+        for groups in (2, 3):
+            piped = torch.full((H, N, D), -1.0)
+            calls = []
+
+            def compute_group(hs):
+                calls.append(list(hs))
+                for h in hs:
+                    piped[h].fill_(float(h))
+
+            parallel.pipelined_sharded_attention(compute_group, piped, shard, groups)
+            ok = ok and all(bool((piped[h] == h).all()) for h in range(H))
+            ok = ok and sorted(h for c in calls for h in c) == shard.heads
         q.put((rank, ok, shard.all_heads))
     finally:
         dist.destroy_process_group()
