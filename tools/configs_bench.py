@@ -1,4 +1,5 @@
-"""BASELINE.json configs 1, 2, 4, 5 on one B200 (config 3 is bench.py).
+"""BASELINE.json configs 1-5 on one B200 (config 3, the headline, is bench.py;
+here it is repeated in both token orders).
 
     python tools/configs_bench.py [--out gpurun_out/configs.json]
 
@@ -25,7 +26,7 @@ from paper_2503_22796_b200 import api
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--out", default="gpurun_out/configs.json")
-ap.add_argument("--only", default="1,2,4,5")
+ap.add_argument("--only", default="1,2,3,4,5")
 args = ap.parse_args()
 only = set(args.only.split(","))
 res = {}
@@ -89,6 +90,33 @@ if "2" in only:
     res["cfg2_sd3_window_sweep"] = rows
     for r in rows:
         print("cfg2", json.dumps(r))
+
+if "3" in only:
+    # config 3 in both token orders (bench.py measures visual-first; FLUX
+    # concatenates text first): FLUX68 and all-Full, layer time per order
+    H, nv, nt, d, B = 24, 16384, 512, 128, 128
+    n = nv + nt
+    q, k, v = (randn(s, 1, H, n, d) for s in (11, 12, 13))
+    out3 = {}
+    orders = ((api.VISUAL_FIRST, "visual_first"), (api.TEXT_FIRST, "text_first"))
+    caches = {}
+    for order, name in orders:
+        dims = api.AttentionDims(H, d, nv, nt, order)
+        caches[name] = api.HeadCache(1, H, n, d)
+        api.multi_strategy_attention(q, k, v, api.LayerPlan.all_full(H), caches[name], 0, 0, dims, B)
+        out3[name] = {}
+    # orders alternate over 3 rounds (the clock drifts as the GPU heats); best of 3
+    for _ in range(3):
+        for pname, lp in (("FLUX68", api.flux68_plan()), ("all Full", api.LayerPlan.all_full(H))):
+            for order, name in orders:
+                dims = api.AttentionDims(H, d, nv, nt, order)
+                ms = time_calls(lambda: api.multi_strategy_attention(q, k, v, lp, caches[name], 0, 1, dims, B))
+                best = out3[name].get(pname)
+                if best is None or ms < best["ms"]:
+                    out3[name][pname] = {"ms": ms, "computed_tflops": api.plan_flops(lp, dims, B) / ms / 1e9}
+    res["cfg3_token_orders"] = out3
+    print("cfg3", json.dumps(out3))
+    del q, k, v
 
 if "4" in only:
     T, L, H, nv, nt, d, B = 28, 57, 24, 16384, 512, 128, 128
