@@ -34,6 +34,10 @@ cudaError_t launch_convert(const void* src, int src_dtype, void* dst, int dst_dt
                            cudaStream_t stream);
 cudaError_t launch_rse(const void* ym, const void* yo, int dtype, int64_t n_heads, int64_t numel,
                        int mode, double* out_dev, double* scratch, int nblk, cudaStream_t stream);
+cudaError_t launch_rse_multi(const void* const* ym, int M, const void* yo, int dtype, int64_t n_heads,
+                             int64_t numel, int mode, double* out_dev, double* scratch, int nblk,
+                             cudaStream_t stream);
+int rse_multi_max();
 }  // namespace dfa2k
 
 using dfa2k::WorkItem;
@@ -1652,6 +1656,9 @@ std::vector<uint8_t> influence_enqueue(const void* q, const void* k, const void*
     double* rse_dev = nullptr;
     scratch_alloc(&rse_dev, static_cast<size_t>(M * H) * sizeof(double), st);
     std::vector<uint8_t> eligible(static_cast<size_t>(M * H), 0);
+    std::vector<const void*> rse_ym(static_cast<size_t>(M), nullptr);  // measured candidates' outputs
+    if (mode != DFA2C_RSE_STANDARD && mode != DFA2C_RSE_LITERAL)
+        fail(DFA2C_SHAPE, "unknown rse mode");
 
     std::vector<int32_t> kinds(static_cast<size_t>(H), DFA2C_FULL);
     std::vector<int64_t> wins(static_cast<size_t>(H), 0);
@@ -1678,10 +1685,7 @@ std::vector<uint8_t> influence_enqueue(const void* q, const void* k, const void*
                 plan_jobs(dims, block, kinds.data(), wins.data(), false, s);
                 run_forward(s, st);
             }
-            const int rc = dfa2c_rse_async(cand, orig, DFA2C_BF16, H, static_cast<int64_t>(head_elems), mode,
-                                           rse_dev + m * H, stream);
-            if (rc != DFA2C_OK)
-                fail(rc, g_err);
+            rse_ym[m] = cand;
             for (int64_t h = 0; h < H; ++h)
                 eligible[m * H + h] = 1;
         } else if (t > 0 && cache && layer >= 0 && layer < cache->L && cache->layer_buf[layer]) {
@@ -1698,13 +1702,39 @@ std::vector<uint8_t> influence_enqueue(const void* q, const void* k, const void*
                     else
                         DFA2C_CUDA_CHECK(cudaMemsetAsync(dst, 0, head_elems * 2, st));
                 }
-            const int rc = dfa2c_rse_async(slots, orig, DFA2C_BF16, H, static_cast<int64_t>(head_elems), mode,
-                                           rse_dev + m * H, stream);
-            if (rc != DFA2C_OK)
-                fail(rc, g_err);
+            rse_ym[m] = slots;
             for (int64_t h = 0; h < H; ++h)
                 eligible[m * H + h] = cache->has(layer, h) ? 1 : 0;
         }
+    }
+    // the layer's RSE grid: runs of consecutive measured candidates share one
+    // launch that streams the original once (rse_multi_partial)
+    if (H > 65535)
+        fail(DFA2C_UNSUPPORTED, "too many heads for one rse launch");
+    int device = 0;
+    DFA2C_CUDA_CHECK(cudaGetDevice(&device));
+    for (int64_t m0 = 0; m0 < M;) {
+        if (!rse_ym[m0]) {
+            ++m0;
+            continue;
+        }
+        int64_t m1 = m0;
+        while (m1 < M && rse_ym[m1] && m1 - m0 < dfa2k::rse_multi_max())
+            ++m1;
+        const int g = static_cast<int>(m1 - m0);
+        // one wave of (2 stages x (g + 1) operands x 8 KB)-smem CTAs
+        const int64_t per_sm = std::max<int64_t>(1, (227 * 1024) / (2 * (g + 1) * 8 * 1024 + 64));
+        const int64_t target = std::max<int64_t>(1, per_sm * num_sms(device) / H);
+        const int nblk =
+            static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(target, ceil_div(static_cast<int64_t>(head_elems), 8192))));
+        double* scratch = nullptr;
+        scratch_alloc(&scratch, static_cast<size_t>(g * H * nblk * 5) * sizeof(double), st);
+        DFA2C_CUDA_CHECK(dfa2k::launch_rse_multi(rse_ym.data() + m0, g, orig, DFA2C_BF16, H,
+                                                 static_cast<int64_t>(head_elems), mode, rse_dev + m0 * H, scratch,
+                                                 nblk, st));
+        g_launches.fetch_add(2);
+        DFA2C_CUDA_CHECK(cudaFreeAsync(scratch, st));
+        m0 = m1;
     }
     DFA2C_CUDA_CHECK(cudaMemcpyAsync(influence_host, rse_dev, static_cast<size_t>(M * H) * sizeof(double),
                                      cudaMemcpyDeviceToHost, st));

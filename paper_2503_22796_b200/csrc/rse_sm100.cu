@@ -198,11 +198,167 @@ __global__ void __launch_bounds__(RSE_THREADS + 32) rse_partial(const T* __restr
     }
 }
 
+// ---- several candidates against one reference (influence_for_layer's
+// per-layer RSE grid): y_o is streamed once per CTA and shared by up to
+// RSE_MAXM candidate streams, so a layer's M RSEs read (M + 1) instead of
+// 2M tensors. Same per-(candidate, head) partials as rse_partial, written as
+// set m * H + h for rse_finalize.
+constexpr int RSE_MAXM = 8;
+constexpr int RSE_MULTI_STAGES = 2;
+template <typename T>
+struct CandPtrs {
+    const T* p[RSE_MAXM];
+};
+constexpr uint32_t rse_multi_smem(int M) {
+    return RSE_MULTI_STAGES * (M + 1) * RSE_STAGE_BYTES + 2 * RSE_MULTI_STAGES * 8;
+}
+
+template <typename T, bool LIT>
+__global__ void __launch_bounds__(RSE_THREADS + 32) rse_multi_partial(CandPtrs<T> cands, int M,
+                                                                      const T* __restrict__ yo, int64_t numel,
+                                                                      int64_t chunk, int vec_ok,
+                                                                      double* __restrict__ part) {
+    constexpr int W = Vec<T>::W;
+    constexpr int64_t EPS = RSE_STAGE_BYTES / sizeof(T);
+    extern __shared__ __align__(128) uint8_t smem[];
+    const uint32_t sbase = smem_u32(smem);
+    const uint32_t stage_bytes = static_cast<uint32_t>(M + 1) * RSE_STAGE_BYTES;
+    const uint32_t full0 = sbase + RSE_MULTI_STAGES * stage_bytes, empty0 = full0 + 8 * RSE_MULTI_STAGES;
+    const int h = blockIdx.y, H = gridDim.y;
+    const int b = blockIdx.x;
+    const T* o = yo + static_cast<int64_t>(h) * numel;
+    const int64_t lo = min(static_cast<int64_t>(b) * chunk, numel);
+    const int64_t hi = min(lo + chunk, numel);
+    const int64_t n_vec = vec_ok ? (hi - lo) / W * W : 0;
+    const int n_stage = static_cast<int>((n_vec + EPS - 1) / EPS);
+    const int warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < RSE_MULTI_STAGES; ++s) {
+            mbar_init(full0 + 8 * s, 1);
+            mbar_init(empty0 + 8 * s, RSE_THREADS / 32);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    double ao[2] = {0, 0};
+    double am[RSE_MAXM][3];
+#pragma unroll
+    for (int c = 0; c < RSE_MAXM; ++c)
+        am[c][0] = am[c][1] = am[c][2] = 0.0;
+    if (warp == RSE_THREADS / 32) {
+        if (elect_one()) {
+            for (int s = 0; s < n_stage; ++s) {
+                const int slot = s % RSE_MULTI_STAGES;
+                if (s >= RSE_MULTI_STAGES)
+                    mbar_wait(empty0 + 8 * slot, ((s / RSE_MULTI_STAGES) - 1) & 1);
+                const int64_t e0 = lo + s * EPS;
+                const uint32_t bytes = static_cast<uint32_t>(min(EPS, lo + n_vec - e0) * sizeof(T));
+                const uint32_t dst = sbase + slot * stage_bytes;
+                mbar_arrive_expect_tx(full0 + 8 * slot, (M + 1) * bytes);
+                bulk_load_1d(dst, o + e0, bytes, full0 + 8 * slot);
+                for (int c = 0; c < M; ++c)
+                    bulk_load_1d(dst + (c + 1) * RSE_STAGE_BYTES, cands.p[c] + static_cast<int64_t>(h) * numel + e0,
+                                 bytes, full0 + 8 * slot);
+            }
+        }
+        __syncwarp();
+    } else {
+        const double K = Vec<T>::one(o);
+        for (int s = 0; s < n_stage; ++s) {
+            const int slot = s % RSE_MULTI_STAGES;
+            mbar_wait(full0 + 8 * slot, (s / RSE_MULTI_STAGES) & 1);
+            const int64_t e_stage = min(EPS, n_vec - s * EPS);
+            const uint32_t sm_o = sbase + slot * stage_bytes;
+            for (int64_t e = static_cast<int64_t>(threadIdx.x) * W; e < e_stage; e += RSE_THREADS * W) {
+                const uint32_t off = static_cast<uint32_t>(e * sizeof(T));
+                double xo[W];
+                Vec<T>::unpack(ld_shared_v4(sm_o + off), xo);
+#pragma unroll
+                for (int k = 0; k < W; ++k) {
+                    const double dO = xo[k] - K;
+                    ao[0] += dO;
+                    ao[1] = fma(dO, dO, ao[1]);
+                }
+#pragma unroll
+                for (int c = 0; c < RSE_MAXM; ++c) {
+                    if (c >= M)
+                        break;
+                    double xm[W];
+                    Vec<T>::unpack(ld_shared_v4(sm_o + (c + 1) * RSE_STAGE_BYTES + off), xm);
+#pragma unroll
+                    for (int k = 0; k < W; ++k) {
+                        const double dd = xm[k] - xo[k];
+                        am[c][0] = fma(dd, dd, am[c][0]);
+                        if (LIT) {
+                            const double dM = xm[k] - K;
+                            am[c][1] += dM;
+                            am[c][2] = fma(dM, dM, am[c][2]);
+                        }
+                    }
+                }
+            }
+            __syncwarp();
+            if ((threadIdx.x & 31) == 0)
+                mbar_arrive(empty0 + 8 * slot);
+        }
+        for (int64_t i = lo + n_vec + threadIdx.x; i < hi; i += RSE_THREADS) {
+            const double xo = Vec<T>::one(o + i);
+            const double dO = xo - K;
+            ao[0] += dO;
+            ao[1] = fma(dO, dO, ao[1]);
+#pragma unroll
+            for (int c = 0; c < RSE_MAXM; ++c) {
+                if (c >= M)
+                    break;
+                const double xm = Vec<T>::one(cands.p[c] + static_cast<int64_t>(h) * numel + i);
+                const double dd = xm - xo;
+                am[c][0] = fma(dd, dd, am[c][0]);
+                if (LIT) {
+                    am[c][1] += xm - K;
+                    am[c][2] = fma(xm - K, xm - K, am[c][2]);
+                }
+            }
+        }
+        for (int off = 16; off > 0; off >>= 1) {
+            ao[0] += __shfl_xor_sync(0xFFFFFFFFu, ao[0], off);
+            ao[1] += __shfl_xor_sync(0xFFFFFFFFu, ao[1], off);
+        }
+#pragma unroll
+        for (int c = 0; c < RSE_MAXM; ++c)
+#pragma unroll
+            for (int k = 0; k < 3; ++k)
+                for (int off = 16; off > 0; off >>= 1)
+                    am[c][k] += __shfl_xor_sync(0xFFFFFFFFu, am[c][k], off);
+    }
+    __shared__ double red[RSE_THREADS / 32][2 + 3 * RSE_MAXM];
+    if (warp < RSE_THREADS / 32 && (threadIdx.x & 31) == 0) {
+        red[warp][0] = ao[0];
+        red[warp][1] = ao[1];
+#pragma unroll
+        for (int c = 0; c < RSE_MAXM; ++c)
+#pragma unroll
+            for (int k = 0; k < 3; ++k)
+                red[warp][2 + 3 * c + k] = am[c][k];
+    }
+    __syncthreads();
+    // thread j < 5M: candidate j / 5, slot j % 5 of the rse_finalize layout
+    if (threadIdx.x < 5 * M) {
+        const int c = threadIdx.x / 5, k = threadIdx.x % 5;
+        const int src = k < 2 ? k : 2 + 3 * c + (k - 2);
+        double t = 0.0;
+        for (int w = 0; w < RSE_THREADS / 32; ++w)
+            t += red[w][src];
+        part[((static_cast<int64_t>(c) * H + h) * gridDim.x + b) * NACC + k] = t;
+    }
+}
+
 // One warp per head: lane j folds partials j, j+32, ... in order, then a
 // fixed xor tree; lane 0 finishes the RSE.
+// n_heads partial sets; set i takes its reference shift from head i % ref_heads of yo
+// (the multi-candidate kernel writes set m * H + h for candidate m, head h).
 template <typename T>
 __global__ void rse_finalize(const T* __restrict__ yo, const double* __restrict__ part, int nblk,
-                             int n_heads, int64_t numel, int mode, double* __restrict__ out) {
+                             int n_heads, int ref_heads, int64_t numel, int mode, double* __restrict__ out) {
     const int h = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
     if (h >= n_heads)
@@ -218,7 +374,7 @@ __global__ void rse_finalize(const T* __restrict__ yo, const double* __restrict_
             a[k] += __shfl_xor_sync(0xFFFFFFFFu, a[k], off);
     if (lane != 0)
         return;
-    const double K = Vec<T>::one(yo + static_cast<int64_t>(h) * numel);
+    const double K = Vec<T>::one(yo + static_cast<int64_t>(h % ref_heads) * numel);
     const double n = static_cast<double>(numel);
     const double dmean = a[0] / n;  // mean - K
     const double den = a[1] - a[0] * dmean;
@@ -256,12 +412,52 @@ void launch_typed(const void* ym, const void* yo, int64_t n_heads, int64_t numel
     else
         launch_partial<T, true>(grid, m, o, numel, chunk, vec_ok, scratch, stream);
     const int fin_blocks = static_cast<int>((n_heads + 7) / 8);
-    rse_finalize<T><<<fin_blocks, 256, 0, stream>>>(o, scratch, nblk, static_cast<int>(n_heads), numel, mode,
-                                                   out_dev);
+    rse_finalize<T><<<fin_blocks, 256, 0, stream>>>(o, scratch, nblk, static_cast<int>(n_heads),
+                                                   static_cast<int>(n_heads), numel, mode, out_dev);
 }
 }  // namespace
 
 int rse_ctas_per_sm() { return DFA2_RSE_CTAS; }  // 3 x (64 KB ring + bars) per SM by default
+int rse_multi_max() { return RSE_MAXM; }
+
+namespace {
+template <typename T>
+void launch_multi_typed(const void* const* ym, int M, const void* yo, int64_t n_heads, int64_t numel, int mode,
+                        double* out_dev, double* scratch, int nblk, int64_t chunk, int vec_ok, cudaStream_t stream) {
+    CandPtrs<T> c{};
+    for (int i = 0; i < M; ++i)
+        c.p[i] = static_cast<const T*>(ym[i]);
+    const dim3 grid(nblk, static_cast<unsigned>(n_heads));
+    const uint32_t smem = rse_multi_smem(M);
+    auto kern = mode == 0 ? rse_multi_partial<T, false> : rse_multi_partial<T, true>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, rse_multi_smem(RSE_MAXM));
+    kern<<<grid, RSE_THREADS + 32, smem, stream>>>(c, M, static_cast<const T*>(yo), numel, chunk, vec_ok, scratch);
+    const int sets = static_cast<int>(M * n_heads);
+    rse_finalize<T><<<(sets + 7) / 8, 256, 0, stream>>>(static_cast<const T*>(yo), scratch, nblk, sets,
+                                                       static_cast<int>(n_heads), numel, mode, out_dev);
+}
+}  // namespace
+
+// out_dev[m * n_heads + h] = RSE(ym[m] head h, yo head h) for m < M <= rse_multi_max();
+// scratch holds M * n_heads * nblk * 5 doubles.
+cudaError_t launch_rse_multi(const void* const* ym, int M, const void* yo, int dtype, int64_t n_heads,
+                             int64_t numel, int mode, double* out_dev, double* scratch, int nblk,
+                             cudaStream_t stream) {
+    const int64_t W = dtype == 0 ? 8 : dtype == 1 ? 4 : 2;
+    int64_t chunk = (numel + nblk - 1) / nblk;
+    chunk = (chunk + W - 1) / W * W;
+    int vec_ok = (numel % W) == 0 && (reinterpret_cast<uintptr_t>(yo) % 16) == 0;
+    for (int i = 0; i < M; ++i)
+        vec_ok = vec_ok && (reinterpret_cast<uintptr_t>(ym[i]) % 16) == 0;
+    if (dtype == 0)
+        launch_multi_typed<__nv_bfloat16>(ym, M, yo, n_heads, numel, mode, out_dev, scratch, nblk, chunk, vec_ok,
+                                          stream);
+    else if (dtype == 2)
+        launch_multi_typed<double>(ym, M, yo, n_heads, numel, mode, out_dev, scratch, nblk, chunk, vec_ok, stream);
+    else
+        launch_multi_typed<float>(ym, M, yo, n_heads, numel, mode, out_dev, scratch, nblk, chunk, vec_ok, stream);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_rse(const void* ym, const void* yo, int dtype, int64_t n_heads, int64_t numel,
                        int mode, double* out_dev, double* scratch, int nblk, cudaStream_t stream) {
