@@ -797,3 +797,35 @@ def test_random_fused_influence_against_oracle(seed):
             want = oracle_head(qn[h], kn[h], vn[h], dims, B, HeadStrategy.Arrow(w), rows)
             check_close(to_np(li.method_outputs[m][h])[rows], want, f"seed {seed} Arrow({w}) head {h}")
     np.testing.assert_allclose(li.influence, exact.influence, rtol=2e-2, atol=1e-6)
+
+
+@pytest.mark.parametrize("mode", [0, 1], ids=["standard", "literal"])
+def test_influence_rse_grid_matches_oracle_rse(mode):
+    """The layer's RSE grid (one multi-candidate launch, original streamed
+    once) against the oracle's rse on the same bf16 outputs, both numerator
+    modes (src/calibrate.cpp:84-85), including more than 8 candidates (two
+    launches) and the Cached candidate."""
+    t = torch()
+    H, nv, nt, d, B = 3, 1024, 77, 64, 128
+    dims = AttentionDims(H, d, nv, nt)
+    n = nv + nt
+    q, _ = bf16_inputs((H, n, d), 111)
+    k, _ = bf16_inputs((H, n, d), 112)
+    v, _ = bf16_inputs((H, n, d), 113)
+    cache = HeadCache(1, H, n, d)
+    slots, _ = bf16_inputs((H, n, d), 114)
+    for h in range(H - 1):  # the last head has no slot: Cached ineligible there
+        cache.store(0, h, slots[h], 0)
+    methods = api.make_candidates(list(range(9)), include_cached=True)
+    li = api.influence_for_layer(q, k, v, methods, cache, 0, 1, dims, B, mode=mode)
+    t.cuda.synchronize()
+    M = len(methods)
+    grid = li.influence.reshape(H, M)
+    for h in range(H):
+        o = to_np(li.original[h])
+        for m in range(M):
+            if m == M - 1 and h == H - 1:
+                assert np.isinf(grid[h, m])
+                continue
+            ym = to_np(li.method_outputs[m][h])
+            assert grid[h, m] == pytest.approx(oracle.rse_f32(ym, o, mode), rel=1e-10, abs=1e-15)
