@@ -9,6 +9,12 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <sys/mman.h>
+#include <chrono>
+#include <cstdlib>
+#include <condition_variable>
+#include <functional>
+#include <mutex>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -29,6 +35,25 @@
 #define DFA2_API __attribute__((visibility("default")))
 
 namespace dfa2 {
+
+namespace detail {
+DFA2_API void* host_alloc(std::size_t bytes) {
+    constexpr std::size_t kHuge = std::size_t{2} << 20;
+    if (bytes < kHuge) {
+        void* p = std::malloc(bytes ? bytes : 1);
+        if (!p)
+            throw std::bad_alloc();
+        return p;
+    }
+    const std::size_t rounded = (bytes + kHuge - 1) / kHuge * kHuge;
+    void* p = std::aligned_alloc(kHuge, rounded);
+    if (!p)
+        throw std::bad_alloc();
+    madvise(p, rounded, MADV_HUGEPAGE);  // advisory: transparent huge pages where enabled
+    return p;
+}
+DFA2_API void host_free(void* p, std::size_t) noexcept { std::free(p); }
+}  // namespace detail
 
 DFA2_API void throw_status(int status) {
     if (status == DFA2C_OK)
@@ -97,15 +122,126 @@ struct Staging {
 };
 thread_local Staging g_stage;
 
-// Host <-> device mover for the reference's pageable host tensors: 32 MB
-// chunks go through two pinned buffers, filled / drained by all host cores
-// in parallel, while the previous chunk is in flight on a copy stream.
-// Synchronous for the caller, like the reference API.
+// Persistent host worker pool: parallel_for(n, fn) runs fn(0..n-1) on
+// up to hardware_concurrency threads (the caller included) and returns when
+// all are done. Used to fill / drain pinned staging buffers.
+class HostPool {
+public:
+    static HostPool& get() {
+        static HostPool pool;
+        return pool;
+    }
+    size_t size() const { return workers_.size() + 1; }
+    template <class F>
+    void parallel_for(size_t n, F&& fn) {
+        if (n <= 1 || workers_.empty()) {
+            for (size_t i = 0; i < n; ++i)
+                fn(i);
+            return;
+        }
+        std::function<void(size_t)> job(std::forward<F>(fn));
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            job_ = &job;
+            n_ = n;
+            next_ = 0;
+            done_ = 0;
+            ++gen_;
+        }
+        cv_.notify_all();
+        run_tasks();
+        std::unique_lock<std::mutex> lk(mu_);
+        done_cv_.wait(lk, [&] { return done_ == n_; });
+        job_ = nullptr;
+    }
+
+private:
+    HostPool() {
+        const size_t hw = std::max<size_t>(1, std::min<size_t>(std::thread::hardware_concurrency(), 32));
+        for (size_t i = 0; i + 1 < hw; ++i)
+            workers_.emplace_back([this] { loop(); });
+    }
+    ~HostPool() {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        for (std::thread& t : workers_)
+            t.join();
+    }
+    void run_tasks() {
+        for (;;) {
+            size_t i;
+            const std::function<void(size_t)>* job;
+            {
+                std::lock_guard<std::mutex> lk(mu_);
+                if (!job_ || next_ >= n_)
+                    return;
+                i = next_++;
+                job = job_;
+            }
+            (*job)(i);
+            std::lock_guard<std::mutex> lk(mu_);
+            if (++done_ == n_)
+                done_cv_.notify_all();
+        }
+    }
+    void loop() {
+        uint64_t seen = 0;
+        for (;;) {
+            {
+                std::unique_lock<std::mutex> lk(mu_);
+                cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+                if (stop_)
+                    return;
+                seen = gen_;
+            }
+            run_tasks();
+        }
+    }
+    std::vector<std::thread> workers_;
+    std::mutex mu_;
+    std::condition_variable cv_, done_cv_;
+    const std::function<void(size_t)>* job_ = nullptr;
+    size_t n_ = 0, next_ = 0, done_ = 0;
+    uint64_t gen_ = 0;
+    bool stop_ = false;
+};
+
+// Parallel host memcpy / zero fill over the worker pool (1 MB tasks).
+void par_memcpy(void* dst, const void* src, size_t bytes) {
+    const size_t task = size_t{1} << 20, n = (bytes + task - 1) / task;
+    HostPool::get().parallel_for(n, [&](size_t t) {
+        const size_t a = t * task, b = std::min(bytes, a + task);
+        std::memcpy(static_cast<char*>(dst) + a, static_cast<const char*>(src) + a, b - a);
+    });
+}
+void par_memset0(void* dst, size_t bytes) {
+    const size_t task = size_t{1} << 20, n = (bytes + task - 1) / task;
+    HostPool::get().parallel_for(n, [&](size_t t) {
+        const size_t a = t * task, b = std::min(bytes, a + task);
+        std::memset(static_cast<char*>(dst) + a, 0, b - a);
+    });
+}
+
+// One contiguous host <-> device piece of a transfer.
+struct Seg {
+    const void* src;
+    void* dst;
+    size_t bytes;
+};
+
+// Host <-> device mover for the reference's pageable host tensors: the
+// segments are streamed in 32 MB chunks through three pinned buffers, each
+// filled / drained by the worker pool while the neighbouring chunks are in
+// flight on a copy stream. Synchronous for the caller, like the reference.
 class HostMover {
 public:
     static constexpr size_t kChunk = size_t{32} << 20;
+    static constexpr int kBufs = 3;
     ~HostMover() {
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < kBufs; ++i) {
             if (pin_[i])
                 cudaFreeHost(pin_[i]);
             if (ev_[i])
@@ -114,76 +250,96 @@ public:
         if (st_)
             cudaStreamDestroy(st_);
     }
-    void up(const void* src, void* dst_dev, size_t bytes) { move(src, dst_dev, bytes, true); }
-    void down(const void* src_dev, void* dst, size_t bytes) { move(src_dev, dst, bytes, false); }
+    void up(const void* src, void* dst_dev, size_t bytes) { move({Seg{src, dst_dev, bytes}}, true); }
+    void down(const void* src_dev, void* dst, size_t bytes) { move({Seg{src_dev, dst, bytes}}, false); }
+    void move(const std::vector<Seg>& segs, bool to_device) {
+        init();
+        cuda_check(cudaDeviceSynchronize(), "sync");  // device-side producers of the sources are done
+        // the transfer as a flat byte range [0, total) over the segments
+        std::vector<size_t> start(segs.size() + 1, 0);
+        for (size_t i = 0; i < segs.size(); ++i)
+            start[i + 1] = start[i] + segs[i].bytes;
+        const size_t total = start.back();
+        // pieces of [lo, hi): (segment, offset in segment, length)
+        auto pieces = [&](size_t lo, size_t hi, auto&& f) {
+            size_t i = static_cast<size_t>(std::upper_bound(start.begin(), start.end(), lo) - start.begin()) - 1;
+            for (size_t pos = lo; pos < hi && i < segs.size(); ++i) {
+                const size_t a = std::max(pos, start[i]), b = std::min(hi, start[i + 1]);
+                if (b > a)
+                    f(segs[i], a - start[i], b - a, a - lo);
+                pos = b;
+            }
+        };
+        HostPool& pool = HostPool::get();
+        auto host_copy = [&](char* pinned, size_t lo, size_t hi, bool into_pinned) {
+            // split the chunk into ~1 MB tasks over the pool
+            const size_t len = hi - lo, task = size_t{1} << 20;
+            const size_t ntask = (len + task - 1) / task;
+            pool.parallel_for(ntask, [&](size_t t) {
+                const size_t a = lo + t * task, b = std::min(hi, a + task);
+                pieces(a, b, [&](const Seg& sg, size_t off, size_t n, size_t at) {
+                    char* pin = pinned + (a - lo) + at;
+                    if (into_pinned)
+                        std::memcpy(pin, static_cast<const char*>(sg.src) + off, n);
+                    else
+                        std::memcpy(static_cast<char*>(sg.dst) + off, pin, n);
+                });
+            });
+        };
+        bool pending[kBufs] = {};
+        size_t plo[kBufs] = {}, phi[kBufs] = {};
+        int b = 0;
+        for (size_t lo = 0; lo < total; lo += kChunk, b = (b + 1) % kBufs) {
+            const size_t hi = std::min(total, lo + kChunk);
+            if (pending[b]) {  // this pinned buffer's previous transfer must finish first
+                cuda_check(cudaEventSynchronize(ev_[b]), "event");
+                if (!to_device)
+                    host_copy(pin_[b], plo[b], phi[b], false);
+            }
+            if (to_device) {
+                host_copy(pin_[b], lo, hi, true);
+                pieces(lo, hi, [&](const Seg& sg, size_t off, size_t n, size_t at) {
+                    cuda_check(cudaMemcpyAsync(static_cast<char*>(sg.dst) + off, pin_[b] + at, n,
+                                               cudaMemcpyHostToDevice, st_),
+                               "upload");
+                });
+            } else {
+                pieces(lo, hi, [&](const Seg& sg, size_t off, size_t n, size_t at) {
+                    cuda_check(cudaMemcpyAsync(pin_[b] + at, static_cast<const char*>(sg.src) + off, n,
+                                               cudaMemcpyDeviceToHost, st_),
+                               "download");
+                });
+            }
+            cuda_check(cudaEventRecord(ev_[b], st_), "event");
+            pending[b] = true;
+            plo[b] = lo;
+            phi[b] = hi;
+        }
+        for (int j = 0; j < kBufs; ++j) {  // drain, oldest first
+            const int i = (b + j) % kBufs;
+            if (!pending[i])
+                continue;
+            cuda_check(cudaEventSynchronize(ev_[i]), "event");
+            if (!to_device)
+                host_copy(pin_[i], plo[i], phi[i], false);
+        }
+    }
 
 private:
     void init() {
         if (st_)
             return;
         cuda_check(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking), "stream");
-        for (int i = 0; i < 2; ++i) {
-            cuda_check(cudaMallocHost(&pin_[i], kChunk), "cudaMallocHost");
+        for (int i = 0; i < kBufs; ++i) {
+            void* p = nullptr;
+            cuda_check(cudaMallocHost(&p, kChunk), "cudaMallocHost");
+            pin_[i] = static_cast<char*>(p);
             cuda_check(cudaEventCreateWithFlags(&ev_[i], cudaEventDisableTiming), "event");
         }
     }
-    static void par_copy(void* dst, const void* src, size_t bytes) {
-        const size_t workers = std::max<size_t>(1, std::min<size_t>(std::thread::hardware_concurrency(),
-                                                                    bytes / (size_t{1} << 20)));
-        if (workers == 1) {
-            std::memcpy(dst, src, bytes);
-            return;
-        }
-        std::vector<std::thread> pool;
-        const size_t per = (bytes + workers - 1) / workers;
-        for (size_t w = 0; w < workers; ++w) {
-            const size_t lo = w * per, hi = std::min(bytes, lo + per);
-            if (lo < hi)
-                pool.emplace_back([=] {
-                    std::memcpy(static_cast<char*>(dst) + lo, static_cast<const char*>(src) + lo, hi - lo);
-                });
-        }
-        for (std::thread& t : pool)
-            t.join();
-    }
-    void move(const void* src, void* dst, size_t bytes, bool to_device) {
-        init();
-        cuda_check(cudaDeviceSynchronize(), "sync");  // device-side producers of `src` (downloads) are done
-        bool pending[2] = {false, false};
-        size_t pending_off[2] = {0, 0}, pending_len[2] = {0, 0};
-        int b = 0;
-        for (size_t off = 0; off < bytes; off += kChunk, b ^= 1) {
-            const size_t len = std::min(kChunk, bytes - off);
-            if (pending[b]) {  // this pinned buffer's previous transfer must finish first
-                cuda_check(cudaEventSynchronize(ev_[b]), "event");
-                if (!to_device)
-                    par_copy(static_cast<char*>(dst) + pending_off[b], pin_[b], pending_len[b]);
-            }
-            if (to_device) {
-                par_copy(pin_[b], static_cast<const char*>(src) + off, len);
-                cuda_check(cudaMemcpyAsync(static_cast<char*>(dst) + off, pin_[b], len, cudaMemcpyHostToDevice, st_),
-                           "upload");
-            } else {
-                cuda_check(cudaMemcpyAsync(pin_[b], static_cast<const char*>(src) + off, len, cudaMemcpyDeviceToHost,
-                                           st_),
-                           "download");
-            }
-            cuda_check(cudaEventRecord(ev_[b], st_), "event");
-            pending[b] = true;
-            pending_off[b] = off;
-            pending_len[b] = len;
-        }
-        for (int j = 0; j < 2; ++j) {  // drain both buffers
-            if (!pending[j])
-                continue;
-            cuda_check(cudaEventSynchronize(ev_[j]), "event");
-            if (!to_device)
-                par_copy(static_cast<char*>(dst) + pending_off[j], pin_[j], pending_len[j]);
-        }
-    }
     cudaStream_t st_ = nullptr;
-    void* pin_[2] = {nullptr, nullptr};
-    cudaEvent_t ev_[2] = {nullptr, nullptr};
+    char* pin_[kBufs] = {};
+    cudaEvent_t ev_[kBufs] = {};
 };
 thread_local HostMover g_mover;
 
@@ -195,6 +351,34 @@ void upload_bf16(const float* src, int64_t n, void* dst) {
     void* f = g_stage.get(static_cast<size_t>(n) * 4);
     g_mover.up(src, f, static_cast<size_t>(n) * 4);
     check(dfa2c_convert(f, DFA2C_F32, dst, DFA2C_BF16, n, nullptr));
+}
+
+// Several (f32 host source, element count, bf16 device destination) pieces
+// in ONE pipelined transfer, then one conversion per piece.
+struct UpPiece {
+    const float* src;
+    int64_t n;
+    void* dst;
+};
+void upload_bf16_many(const std::vector<UpPiece>& ps) {
+    size_t total = 0;
+    for (const UpPiece& p : ps)
+        total += static_cast<size_t>(p.n) * 4;
+    if (total == 0)
+        return;
+    char* f = static_cast<char*>(g_stage.get(total));
+    std::vector<Seg> segs;
+    size_t off = 0;
+    for (const UpPiece& p : ps) {
+        segs.push_back(Seg{p.src, f + off, static_cast<size_t>(p.n) * 4});
+        off += static_cast<size_t>(p.n) * 4;
+    }
+    g_mover.move(segs, true);
+    off = 0;
+    for (const UpPiece& p : ps) {
+        check(dfa2c_convert(f + off, DFA2C_F32, p.dst, DFA2C_BF16, p.n, nullptr));
+        off += static_cast<size_t>(p.n) * 4;
+    }
 }
 
 void download_bf16(const void* src, int64_t n, float* dst) {
@@ -239,10 +423,13 @@ DFA2_API Tensor Tensor::zeros(std::vector<int64_t> shape, Dtype dt) {
     const int64_t n = shape_numel(shape);
     t.shape_ = std::move(shape);
     t.dtype_ = dt;
-    if (dt == Dtype::f32)
-        t.f32_.assign(static_cast<size_t>(n), 0.0f);
-    else
-        t.f64_.assign(static_cast<size_t>(n), 0.0);
+    if (dt == Dtype::f32) {
+        t.f32_.resize(static_cast<size_t>(n));
+        par_memset0(t.f32_.data(), static_cast<size_t>(n) * sizeof(float));
+    } else {
+        t.f64_.resize(static_cast<size_t>(n));
+        par_memset0(t.f64_.data(), static_cast<size_t>(n) * sizeof(double));
+    }
     return t;
 }
 DFA2_API Tensor Tensor::from_f32(std::vector<int64_t> shape, std::vector<float> data) {
@@ -250,7 +437,8 @@ DFA2_API Tensor Tensor::from_f32(std::vector<int64_t> shape, std::vector<float> 
         throw ShapeError("data length does not match shape");
     Tensor t;
     t.shape_ = std::move(shape);
-    t.f32_ = std::move(data);
+    t.f32_.resize(data.size());
+    par_memcpy(t.f32_.data(), data.data(), data.size() * sizeof(float));
     return t;
 }
 DFA2_API Tensor Tensor::from_f64(std::vector<int64_t> shape, std::vector<double> data) {
@@ -259,7 +447,15 @@ DFA2_API Tensor Tensor::from_f64(std::vector<int64_t> shape, std::vector<double>
     Tensor t;
     t.shape_ = std::move(shape);
     t.dtype_ = Dtype::f64;
-    t.f64_ = std::move(data);
+    t.f64_.resize(data.size());
+    par_memcpy(t.f64_.data(), data.data(), data.size() * sizeof(double));
+    return t;
+}
+DFA2_API Tensor Tensor::uninitialized_f32(std::vector<int64_t> shape) {
+    Tensor t;
+    const int64_t n = shape_numel(shape);
+    t.shape_ = std::move(shape);
+    t.f32_.resize(static_cast<size_t>(n));
     return t;
 }
 DFA2_API int64_t Tensor::dim(int64_t i) const {
@@ -592,6 +788,7 @@ DFA2_API Tensor multi_strategy_attention(const Tensor& q, const Tensor& k, const
     // only computed heads' inputs cross PCIe (a Cached head reads its slot),
     // one transfer per run of consecutive computed heads
     const int64_t hs = n * d;
+    std::vector<UpPiece> ups;
     for (int64_t h0 = 0; h0 < H;) {
         if (plan.strategies[h0].kind == StrategyKind::cached) {
             ++h0;
@@ -600,19 +797,33 @@ DFA2_API Tensor multi_strategy_attention(const Tensor& q, const Tensor& k, const
         int64_t h1 = h0 + 1;
         while (h1 < H && plan.strategies[h1].kind != StrategyKind::cached)
             ++h1;
-        upload_bf16(q.f32() + h0 * hs, (h1 - h0) * hs, static_cast<char*>(dq) + h0 * hs * 2);
-        upload_bf16(k.f32() + h0 * hs, (h1 - h0) * hs, static_cast<char*>(dk) + h0 * hs * 2);
-        upload_bf16(v.f32() + h0 * hs, (h1 - h0) * hs, static_cast<char*>(dv) + h0 * hs * 2);
+        ups.push_back({q.f32() + h0 * hs, (h1 - h0) * hs, static_cast<char*>(dq) + h0 * hs * 2});
+        ups.push_back({k.f32() + h0 * hs, (h1 - h0) * hs, static_cast<char*>(dk) + h0 * hs * 2});
+        ups.push_back({v.f32() + h0 * hs, (h1 - h0) * hs, static_cast<char*>(dv) + h0 * hs * 2});
         h0 = h1;
     }
+    const bool prof = std::getenv("DFA2_HOST_PROFILE") != nullptr;
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+    const auto t0 = now();
+    upload_bf16_many(ups);
+    if (prof) cudaDeviceSynchronize();
+    const auto t1 = now();
     std::vector<int32_t> kinds;
     std::vector<int64_t> wins;
     plan_arrays(plan, kinds, wins);
     const dfa2c_dims cd = cdims(dims);
     check(dfa2c_mha_forward(dq, dk, dv, 1, &cd, block_size, kinds.data(), wins.data(), dev, layer, t, dout,
                             nullptr));
-    Tensor out = Tensor::zeros(q.shape(), Dtype::f32);
+    if (prof) cudaDeviceSynchronize();
+    const auto t2 = now();
+    Tensor out = Tensor::uninitialized_f32(q.shape());  // the download writes every element
+    const auto t3 = now();
     download_bf16(dout, numel, out.f32());
+    const auto t4 = now();
+    if (prof)
+        std::fprintf(stderr, "[dfa2 host] upload %.2f ms, kernel %.2f ms, out alloc %.2f ms, download %.2f ms\n",
+                     ms(t0, t1), ms(t1, t2), ms(t2, t3), ms(t3, t4));
     for (int64_t h = 0; h < H; ++h)
         if (plan.strategies[h].kind != StrategyKind::cached)
             CacheAccess::committed(cache, layer, h, t);
