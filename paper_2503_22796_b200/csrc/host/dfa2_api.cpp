@@ -120,7 +120,6 @@ struct Staging {
         return p;
     }
 };
-thread_local Staging g_stage;
 
 // Persistent host worker pool: parallel_for(n, fn) runs fn(0..n-1) on
 // up to hardware_concurrency threads (the caller included) and returns when
@@ -232,6 +231,24 @@ struct Seg {
     size_t bytes;
 };
 
+// f32 -> bf16, round to nearest even (NaN -> 0x7FFF), bitwise what the
+// device conversion (__float2bfloat16_rn, dfa2c_convert) gives.
+void round_f32_to_bf16(const float* src, uint16_t* dst, size_t n) {
+    for (size_t i = 0; i < n; ++i) {
+        uint32_t u;
+        std::memcpy(&u, src + i, 4);
+        const bool nan = (u & 0x7FFFFFFFu) > 0x7F800000u;
+        const uint32_t r = (u + 0x7FFFu + ((u >> 16) & 1u)) >> 16;
+        dst[i] = nan ? uint16_t{0x7FFF} : static_cast<uint16_t>(r);
+    }
+}
+void widen_bf16_to_f32(const uint16_t* src, float* dst, size_t n) {
+    for (size_t i = 0; i < n; ++i) {
+        const uint32_t u = static_cast<uint32_t>(src[i]) << 16;
+        std::memcpy(dst + i, &u, 4);
+    }
+}
+
 // Host <-> device mover for the reference's pageable host tensors: the
 // segments are streamed in 32 MB chunks through three pinned buffers, each
 // filled / drained by the worker pool while the neighbouring chunks are in
@@ -250,9 +267,13 @@ public:
         if (st_)
             cudaStreamDestroy(st_);
     }
+    // kRound: host f32 -> bf16 (round to nearest even) on the way up, bf16 ->
+    // f32 on the way down, done by the pool while filling / draining the
+    // pinned chunks; Seg::bytes then counts the bf16 (device-side) bytes.
+    enum Mode { kCopy, kRound };
     void up(const void* src, void* dst_dev, size_t bytes) { move({Seg{src, dst_dev, bytes}}, true); }
     void down(const void* src_dev, void* dst, size_t bytes) { move({Seg{src_dev, dst, bytes}}, false); }
-    void move(const std::vector<Seg>& segs, bool to_device) {
+    void move(const std::vector<Seg>& segs, bool to_device, Mode mode = kCopy) {
         init();
         cuda_check(cudaDeviceSynchronize(), "sync");  // device-side producers of the sources are done
         // the transfer as a flat byte range [0, total) over the segments
@@ -279,10 +300,18 @@ public:
                 const size_t a = lo + t * task, b = std::min(hi, a + task);
                 pieces(a, b, [&](const Seg& sg, size_t off, size_t n, size_t at) {
                     char* pin = pinned + (a - lo) + at;
-                    if (into_pinned)
+                    if (mode == kRound) {
+                        if (into_pinned)
+                            round_f32_to_bf16(static_cast<const float*>(sg.src) + off / 2,
+                                              reinterpret_cast<uint16_t*>(pin), n / 2);
+                        else
+                            widen_bf16_to_f32(reinterpret_cast<const uint16_t*>(pin),
+                                              static_cast<float*>(sg.dst) + off / 2, n / 2);
+                    } else if (into_pinned) {
                         std::memcpy(pin, static_cast<const char*>(sg.src) + off, n);
-                    else
+                    } else {
                         std::memcpy(static_cast<char*>(sg.dst) + off, pin, n);
+                    }
                 });
             });
         };
@@ -348,45 +377,32 @@ thread_local HostMover g_mover;
 void upload_bf16(const float* src, int64_t n, void* dst) {
     if (n <= 0)
         return;
-    void* f = g_stage.get(static_cast<size_t>(n) * 4);
-    g_mover.up(src, f, static_cast<size_t>(n) * 4);
-    check(dfa2c_convert(f, DFA2C_F32, dst, DFA2C_BF16, n, nullptr));
+    g_mover.move({Seg{src, dst, static_cast<size_t>(n) * 2}}, true, HostMover::kRound);
 }
 
 // Several (f32 host source, element count, bf16 device destination) pieces
-// in ONE pipelined transfer, then one conversion per piece.
+// in ONE pipelined transfer.
 struct UpPiece {
     const float* src;
     int64_t n;
     void* dst;
 };
 void upload_bf16_many(const std::vector<UpPiece>& ps) {
-    size_t total = 0;
-    for (const UpPiece& p : ps)
-        total += static_cast<size_t>(p.n) * 4;
-    if (total == 0)
-        return;
-    char* f = static_cast<char*>(g_stage.get(total));
+    // rounded to bf16 by the pool while it fills the pinned chunks: half the
+    // PCIe bytes of an f32 upload, and no device-side conversion
     std::vector<Seg> segs;
-    size_t off = 0;
-    for (const UpPiece& p : ps) {
-        segs.push_back(Seg{p.src, f + off, static_cast<size_t>(p.n) * 4});
-        off += static_cast<size_t>(p.n) * 4;
-    }
-    g_mover.move(segs, true);
-    off = 0;
-    for (const UpPiece& p : ps) {
-        check(dfa2c_convert(f + off, DFA2C_F32, p.dst, DFA2C_BF16, p.n, nullptr));
-        off += static_cast<size_t>(p.n) * 4;
-    }
+    for (const UpPiece& p : ps)
+        if (p.n > 0)
+            segs.push_back(Seg{p.src, p.dst, static_cast<size_t>(p.n) * 2});
+    if (!segs.empty())
+        g_mover.move(segs, true, HostMover::kRound);
 }
 
 void download_bf16(const void* src, int64_t n, float* dst) {
     if (n <= 0)
         return;
-    void* f = g_stage.get(static_cast<size_t>(n) * 4);
-    check(dfa2c_convert(src, DFA2C_BF16, f, DFA2C_F32, n, nullptr));
-    g_mover.down(f, dst, static_cast<size_t>(n) * 4);
+    // bf16 crosses PCIe; the pool widens it to f32 while draining the chunks
+    g_mover.move({Seg{src, dst, static_cast<size_t>(n) * 2}}, false, HostMover::kRound);
 }
 
 // f32 view of a tensor (f64 narrowed).
