@@ -139,6 +139,7 @@ public:
             return;
         }
         std::function<void(size_t)> job(std::forward<F>(fn));
+        std::lock_guard<std::mutex> one_job(call_mu_);  // callers on several threads take turns
         {
             std::lock_guard<std::mutex> lk(mu_);
             job_ = &job;
@@ -200,7 +201,7 @@ private:
         }
     }
     std::vector<std::thread> workers_;
-    std::mutex mu_;
+    std::mutex call_mu_, mu_;
     std::condition_variable cv_, done_cv_;
     const std::function<void(size_t)>* job_ = nullptr;
     size_t n_ = 0, next_ = 0, done_ = 0;
