@@ -13,6 +13,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <deque>
 #include <limits>
 #include <map>
 #include <memory>
@@ -200,6 +201,12 @@ void check_rows_nonempty(const uint8_t* m, int64_t nb) {
 }
 
 // ------------------------------------------------------------ device plan
+// A work list on the device: one stream-ordered block from the library pool
+// holding the items, CTA ranges, tile words and masks. `used` is recorded
+// after every launch that reads it; on eviction the block is released on an
+// internal stream once that event has fired, so building or dropping a plan
+// never synchronises the device.
+void plan_release(int device, void* dev, cudaEvent_t used);
 struct DevPlan {
     int grid = 0;
     int32_t n_groups = 0;  // split groups (counters per launch)
@@ -210,12 +217,11 @@ struct DevPlan {
     uint8_t* masks = nullptr;
     int32_t n_snap = 0;                                   // calibration plans: snapshots per query tile
     uint16_t snap_slots[dfa2k::MAX_SNAPS] = {};
-    ~DevPlan() {
-        cudaFree(items);
-        cudaFree(cta_begin);
-        cudaFree(tiles);
-        cudaFree(masks);
-    }
+    int device = 0;
+    void* dev = nullptr;
+    size_t bytes = 0;
+    cudaEvent_t used = nullptr;
+    ~DevPlan() { plan_release(device, dev, used); }
 };
 
 // Head strategy for the scheduler: mask_id >= 0 => computed over that mask;
@@ -277,6 +283,73 @@ void scratch_alloc(T** p, size_t bytes, cudaStream_t st) {
     DFA2C_CUDA_CHECK(cudaMallocFromPoolAsync(reinterpret_cast<void**>(p), bytes, scratch_pool(device), st));
 }
 
+// Host staging for plan uploads: per device, a ring of pinned buffers, each
+// reused once the copy that last read it has completed (its event), so a
+// plan-cache miss costs host work and an asynchronous copy, not a device
+// synchronisation.
+struct PlanStaging {
+    static constexpr int kSlots = 8;
+    static constexpr size_t kBytes = size_t{8} << 20;
+    char* buf[kSlots] = {};
+    cudaEvent_t ev[kSlots] = {};
+    int next = 0;
+};
+std::mutex g_staging_mu;
+std::map<int, PlanStaging> g_staging;
+std::map<int, cudaStream_t> g_free_streams;
+
+template <class Fill>
+void plan_upload(int device, cudaStream_t stream, void* dst, size_t bytes, Fill&& fill) {
+    std::lock_guard<std::mutex> lk(g_staging_mu);
+    PlanStaging& ps = g_staging[device];
+    if (bytes > PlanStaging::kBytes) {  // oversized plan: pageable copy, in stream order
+        std::vector<char> h(bytes);
+        fill(h.data());
+        DFA2C_CUDA_CHECK(cudaMemcpyAsync(dst, h.data(), bytes, cudaMemcpyHostToDevice, stream));
+        DFA2C_CUDA_CHECK(cudaStreamSynchronize(stream));  // h goes out of scope
+        return;
+    }
+    const int i = ps.next;
+    ps.next = (ps.next + 1) % PlanStaging::kSlots;
+    if (!ps.buf[i]) {
+        DFA2C_CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&ps.buf[i]), PlanStaging::kBytes,
+                                       cudaHostAllocPortable));
+        DFA2C_CUDA_CHECK(cudaEventCreateWithFlags(&ps.ev[i], cudaEventDisableTiming));
+    } else {
+        DFA2C_CUDA_CHECK(cudaEventSynchronize(ps.ev[i]));  // its previous upload has been read
+    }
+    fill(ps.buf[i]);
+    DFA2C_CUDA_CHECK(cudaMemcpyAsync(dst, ps.buf[i], bytes, cudaMemcpyHostToDevice, stream));
+    DFA2C_CUDA_CHECK(cudaEventRecord(ps.ev[i], stream));
+}
+
+void plan_release(int device, void* dev, cudaEvent_t used) {
+    if (!dev && !used)
+        return;
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(device);
+    cudaStream_t fs;
+    {
+        std::lock_guard<std::mutex> lk(g_staging_mu);
+        auto it = g_free_streams.find(device);
+        if (it == g_free_streams.end()) {
+            cudaStream_t s_ = nullptr;
+            cudaStreamCreateWithFlags(&s_, cudaStreamNonBlocking);
+            it = g_free_streams.emplace(device, s_).first;
+        }
+        fs = it->second;
+    }
+    if (dev) {
+        if (used)
+            cudaStreamWaitEvent(fs, used, 0);  // every launch that read the plan
+        cudaFreeAsync(dev, fs);
+    }
+    if (used)
+        cudaEventDestroy(used);
+    cudaSetDevice(cur);
+}
+
 // Pair lists: for every pair of query tiles (2p, 2p+1) the union of their
 // KV tile rows (ascending), each word tagged with the lanes that fold it.
 struct PairSet {
@@ -289,24 +362,34 @@ PairSet build_pair_set(const TileSet& ts, int64_t nqt) {
     PairSet ps;
     const int64_t np = (nqt + 1) / 2;
     ps.row_ptr.assign(static_cast<size_t>(np + 1), 0);
+    ps.words.reserve(ts.cols.size());
     for (int64_t p = 0; p < np; ++p) {
         const int64_t qa = 2 * p, qb = 2 * p + 1;
-        std::map<uint32_t, uint32_t> u;  // kv tile -> flags
-        for (int64_t i = ts.row_ptr[qa]; i < ts.row_ptr[qa + 1]; ++i) {
-            const uint32_t c = ts.cols[i];
-            u[c & ~dfa2k::TILE_SET_PARTIAL] |=
-                dfa2k::TILE_NEED_A | ((c & dfa2k::TILE_SET_PARTIAL) ? dfa2k::TILE_PART_A : 0u);
-        }
-        int32_t nb_ = 0;
-        if (qb < nqt)
-            for (int64_t i = ts.row_ptr[qb]; i < ts.row_ptr[qb + 1]; ++i) {
-                const uint32_t c = ts.cols[i];
-                u[c & ~dfa2k::TILE_SET_PARTIAL] |=
-                    dfa2k::TILE_NEED_B | ((c & dfa2k::TILE_SET_PARTIAL) ? dfa2k::TILE_PART_B : 0u);
-                ++nb_;
+        // both rows are ascending: merge them (each tile once, tagged with its lanes)
+        int64_t i = ts.row_ptr[qa], ie = ts.row_ptr[qa + 1];
+        int64_t j = qb < nqt ? ts.row_ptr[qb] : 0, je = qb < nqt ? ts.row_ptr[qb + 1] : 0;
+        const int32_t nb_ = static_cast<int32_t>(je - j);
+        auto tag_a = [](uint32_t c) {
+            return dfa2k::TILE_NEED_A | ((c & dfa2k::TILE_SET_PARTIAL) ? dfa2k::TILE_PART_A : 0u);
+        };
+        auto tag_b = [](uint32_t c) {
+            return dfa2k::TILE_NEED_B | ((c & dfa2k::TILE_SET_PARTIAL) ? dfa2k::TILE_PART_B : 0u);
+        };
+        while (i < ie || j < je) {
+            const uint32_t ca = i < ie ? ts.cols[i] : 0u, cb = j < je ? ts.cols[j] : 0u;
+            const uint32_t ta = ca & ~dfa2k::TILE_SET_PARTIAL, tb = cb & ~dfa2k::TILE_SET_PARTIAL;
+            if (j >= je || (i < ie && ta < tb)) {
+                ps.words.push_back(ta | tag_a(ca));
+                ++i;
+            } else if (i >= ie || tb < ta) {
+                ps.words.push_back(tb | tag_b(cb));
+                ++j;
+            } else {
+                ps.words.push_back(ta | tag_a(ca) | tag_b(cb));
+                ++i;
+                ++j;
             }
-        for (const auto& kv : u)
-            ps.words.push_back(kv.first | kv.second);
+        }
         ps.row_ptr[p + 1] = static_cast<int64_t>(ps.words.size());
         ps.n_a.push_back(static_cast<int32_t>(ts.row_ptr[qa + 1] - ts.row_ptr[qa]));
         ps.n_b.push_back(nb_);
@@ -319,7 +402,8 @@ struct Cand {
     double cost;
 };
 std::unique_ptr<DevPlan> schedule_items(int device, std::vector<Cand>& cands, const std::vector<uint32_t>& tiles,
-                                        const std::vector<uint8_t>& mask_bytes, int32_t n_groups, int32_t n_slots);
+                                        const std::vector<uint8_t>& mask_bytes, int32_t n_groups, int32_t n_slots,
+                                        cudaStream_t stream);
 
 // Builds the LPT-scheduled work list: each (sample, head, query-tile pair)
 // is one item costing (#lane-A tiles + #lane-B tiles + 1) tile-units
@@ -330,7 +414,8 @@ std::unique_ptr<DevPlan> schedule_items(int device, std::vector<Cand>& cands, co
 // outputs are bitwise reproducible.
 std::unique_ptr<DevPlan> build_dev_plan(int device, int64_t batch, int64_t H, int64_t n, int64_t B,
                                         const std::vector<std::vector<uint8_t>>& masks,
-                                        const std::vector<HeadJob>& jobs, const std::vector<int>& ref_jobs) {
+                                        const std::vector<HeadJob>& jobs, const std::vector<int>& ref_jobs,
+                                        cudaStream_t stream) {
     const int64_t nqt = ceil_div(n, dfa2k::TILE_M);
     const int64_t np = (nqt + 1) / 2;
     std::vector<uint32_t> tiles;
@@ -450,14 +535,15 @@ std::unique_ptr<DevPlan> build_dev_plan(int device, int64_t batch, int64_t H, in
                 }
             }
         }
-    return schedule_items(device, cands, tiles, mask_bytes, n_groups, n_slots);
+    return schedule_items(device, cands, tiles, mask_bytes, n_groups, n_slots, stream);
 }
 
 // LPT assignment of the work items to one persistent CTA per SM (cost desc,
 // then (bh, pair) so concurrently running CTAs share a head's K/V in L2) and
 // upload of the device plan.
 std::unique_ptr<DevPlan> schedule_items(int device, std::vector<Cand>& cands, const std::vector<uint32_t>& tiles,
-                                        const std::vector<uint8_t>& mask_bytes, int32_t n_groups, int32_t n_slots) {
+                                        const std::vector<uint8_t>& mask_bytes, int32_t n_groups, int32_t n_slots,
+                                        cudaStream_t stream) {
     std::stable_sort(cands.begin(), cands.end(), [](const Cand& a, const Cand& b) {
         if (a.cost != b.cost)
             return a.cost > b.cost;
@@ -489,22 +575,56 @@ std::unique_ptr<DevPlan> schedule_items(int device, std::vector<Cand>& cands, co
     p->grid = grid;
     p->n_groups = n_groups;
     p->n_slots = n_slots;
-    DFA2C_CUDA_CHECK(cudaMalloc(&p->items, items.size() * sizeof(WorkItem)));
-    DFA2C_CUDA_CHECK(cudaMalloc(&p->cta_begin, cta_begin.size() * sizeof(int32_t)));
-    DFA2C_CUDA_CHECK(cudaMalloc(&p->tiles, tiles.size() * sizeof(uint32_t)));
-    DFA2C_CUDA_CHECK(cudaMalloc(&p->masks, mask_bytes.size()));
-    DFA2C_CUDA_CHECK(cudaMemcpy(p->items, items.data(), items.size() * sizeof(WorkItem), cudaMemcpyHostToDevice));
-    DFA2C_CUDA_CHECK(cudaMemcpy(p->cta_begin, cta_begin.data(), cta_begin.size() * sizeof(int32_t),
-                                cudaMemcpyHostToDevice));
-    DFA2C_CUDA_CHECK(cudaMemcpy(p->tiles, tiles.data(), tiles.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
-    DFA2C_CUDA_CHECK(cudaMemcpy(p->masks, mask_bytes.data(), mask_bytes.size(), cudaMemcpyHostToDevice));
+    p->device = device;
+    // one block: [items | cta_begin | tiles | masks], 256-byte aligned parts
+    auto up = [](size_t x) { return (x + 255) / 256 * 256; };
+    const size_t o_items = 0, n_items = items.size() * sizeof(WorkItem);
+    const size_t o_cta = up(o_items + n_items), n_cta = cta_begin.size() * sizeof(int32_t);
+    const size_t o_tiles = up(o_cta + n_cta), n_tiles = tiles.size() * sizeof(uint32_t);
+    const size_t o_masks = up(o_tiles + n_tiles), n_masks = mask_bytes.size();
+    p->bytes = up(o_masks + n_masks);
+    DFA2C_CUDA_CHECK(cudaEventCreateWithFlags(&p->used, cudaEventDisableTiming));
+    scratch_alloc(&p->dev, p->bytes, stream);
+    char* d = static_cast<char*>(p->dev);
+    p->items = reinterpret_cast<WorkItem*>(d + o_items);
+    p->cta_begin = reinterpret_cast<int32_t*>(d + o_cta);
+    p->tiles = reinterpret_cast<uint32_t*>(d + o_tiles);
+    p->masks = reinterpret_cast<uint8_t*>(d + o_masks);
+    plan_upload(device, stream, p->dev, p->bytes, [&](char* h) {
+        std::memcpy(h + o_items, items.data(), n_items);
+        std::memcpy(h + o_cta, cta_begin.data(), n_cta);
+        std::memcpy(h + o_tiles, tiles.data(), n_tiles);
+        std::memcpy(h + o_masks, mask_bytes.data(), n_masks);
+    });
     return p;
 }
 
 // Plans are cached per (device, geometry, plan) so steady-state calls only
 // encode three tensor maps and launch.
 std::mutex g_plan_mu;
-std::map<std::string, std::unique_ptr<DevPlan>> g_plans;
+std::map<std::string, std::shared_ptr<DevPlan>> g_plans;
+std::deque<std::string> g_plan_order;  // insertion order, for eviction
+size_t g_plan_bytes = 0;
+// A calibrated FLUX schedule has one plan per (timestep, layer): 28 x 57 =
+// 1,596 work lists of ~0.4 MB. Keep up to 8,192 plans / 4 GB.
+constexpr size_t kMaxPlans = 8192;
+constexpr size_t kMaxPlanBytes = size_t{4} << 30;
+
+std::shared_ptr<DevPlan> plan_insert(const std::string& key, std::unique_ptr<DevPlan> p) {
+    while (!g_plan_order.empty() && (g_plans.size() >= kMaxPlans || g_plan_bytes + p->bytes > kMaxPlanBytes)) {
+        auto it = g_plans.find(g_plan_order.front());
+        if (it != g_plans.end()) {
+            g_plan_bytes -= it->second->bytes;
+            g_plans.erase(it);
+        }
+        g_plan_order.pop_front();
+    }
+    g_plan_bytes += p->bytes;
+    g_plan_order.push_back(key);
+    std::shared_ptr<DevPlan> sp(std::move(p));
+    g_plans.emplace(key, sp);
+    return sp;
+}
 
 template <class T>
 void put(std::string& key, const T& v) {
@@ -764,13 +884,13 @@ void launch_forward(const ForwardSpec& s, cudaStream_t stream) {
             put(key, rj);
     key += s.mask_key;
 
-    DevPlan* plan = nullptr;
+    std::shared_ptr<DevPlan> plan;
     {
         std::lock_guard<std::mutex> lk(g_plan_mu);
         auto it = g_plans.find(key);
-        if (it == g_plans.end()) {
-            if (g_plans.size() >= 256)
-                g_plans.clear();
+        if (it != g_plans.end()) {
+            plan = it->second;
+        } else {
             // masks are only materialised when the work list has to be built
             std::vector<std::vector<uint8_t>> built;
             const std::vector<std::vector<uint8_t>>* masks = &s.masks;
@@ -781,9 +901,9 @@ void launch_forward(const ForwardSpec& s, cudaStream_t stream) {
                                           : arrow_mask(s.dims, s.block, w));
                 masks = &built;
             }
-            it = g_plans.emplace(key, build_dev_plan(device, s.batch, H, n, s.block, *masks, s.jobs, s.ref_jobs)).first;
+            plan = plan_insert(key, build_dev_plan(device, s.batch, H, n, s.block, *masks, s.jobs, s.ref_jobs,
+                                                   stream));
         }
-        plan = it->second.get();
     }
 
     void* cache_layer = nullptr;
@@ -827,6 +947,7 @@ void launch_forward(const ForwardSpec& s, cudaStream_t stream) {
         DFA2C_CUDA_CHECK(cudaMemsetAsync(a.counters, 0, static_cast<size_t>(plan->n_groups) * 2 * sizeof(int), stream));
     }
     DFA2C_CUDA_CHECK(dfa2k::launch_attn(kernel_dim(d), tq, tk, tv, to, tc, a, plan->grid, stream));
+    DFA2C_CUDA_CHECK(cudaEventRecord(plan->used, stream));
     if (plan->n_groups > 0) {
         DFA2C_CUDA_CHECK(cudaFreeAsync(a.part_o, stream));
         DFA2C_CUDA_CHECK(cudaFreeAsync(a.part_ml, stream));
@@ -878,7 +999,7 @@ bool influence_fused_eligible(const dfa2c_dims* dims, int64_t block, int64_t n_w
 // SNAP bit unless it is the lane's last tile overall (the item end emits
 // every remaining snapshot from the final state).
 std::unique_ptr<DevPlan> build_multi_plan(int device, int64_t H, int64_t n,
-                                          const std::vector<std::vector<uint8_t>>& bands) {
+                                          const std::vector<std::vector<uint8_t>>& bands, cudaStream_t stream) {
     const int64_t nt = ceil_div(n, dfa2k::TILE_N);  // key tiles == mask blocks (block == 128)
     const int64_t np = (nt + 1) / 2;
     const int S = static_cast<int>(bands.size());
@@ -969,7 +1090,7 @@ std::unique_ptr<DevPlan> build_multi_plan(int device, int64_t H, int64_t n,
             w.flags = dfa2k::ITEM_MULTI;
             cands.push_back({w, static_cast<double>(nt * (w.qtile_b >= 0 ? 2 : 1)) + 1.0 + 0.25 * S});
         }
-    return schedule_items(device, cands, tiles, mask_bytes, 0, 0);
+    return schedule_items(device, cands, tiles, mask_bytes, 0, 0, stream);
 }
 
 // The fused pass: `orig` <- all-Full output, `cand` + m * layer <- Arrow(windows[m])
@@ -996,13 +1117,13 @@ void run_influence_fused(const void* q, const void* k, const void* v, const dfa2
     put(key, dims->order);
     for (int64_t m = 0; m < n_windows; ++m)
         put(key, windows[m]);
-    DevPlan* plan = nullptr;
+    std::shared_ptr<DevPlan> plan;
     {
         std::lock_guard<std::mutex> lk(g_plan_mu);
         auto it = g_plans.find(key);
-        if (it == g_plans.end()) {
-            if (g_plans.size() >= 256)
-                g_plans.clear();
+        if (it != g_plans.end()) {
+            plan = it->second;
+        } else {
             // distinct effective windows (the clamp of src/arrow.cpp:135-137),
             // narrowest first: their masks are nested; a window whose mask is
             // all-active is the original's full row
@@ -1022,14 +1143,13 @@ void run_influence_fused(const void* q, const void* k, const void* v, const dfa2
                     band_slots.push_back(bits);
                 }
             }
-            auto p = build_multi_plan(device, H, n, bands);
+            auto p = build_multi_plan(device, H, n, bands, stream);
             p->n_snap = static_cast<int32_t>(bands.size()) + 1;
             for (size_t i = 0; i < bands.size(); ++i)
                 p->snap_slots[i] = static_cast<uint16_t>(band_slots[i]);
             p->snap_slots[bands.size()] = static_cast<uint16_t>(full_slots);
-            it = g_plans.emplace(key, std::move(p)).first;
+            plan = plan_insert(key, std::move(p));
         }
-        plan = it->second.get();
     }
     const CUtensorMap tq = make_map(q, H, n, d, dfa2k::TILE_M);
     const CUtensorMap tk = make_map(k, H, n, d, dfa2k::TILE_N);
@@ -1052,6 +1172,7 @@ void run_influence_fused(const void* q, const void* k, const void* v, const dfa2
     a.n_snap = plan->n_snap;
     std::copy(plan->snap_slots, plan->snap_slots + dfa2k::MAX_SNAPS, a.snap_slots);
     DFA2C_CUDA_CHECK(dfa2k::launch_attn(kernel_dim(d), tq, tk, tv, to, tc, a, plan->grid, stream));
+    DFA2C_CUDA_CHECK(cudaEventRecord(plan->used, stream));
     g_launches.fetch_add(1);
 }
 
