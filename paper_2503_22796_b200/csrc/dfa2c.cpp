@@ -221,7 +221,15 @@ struct DevPlan {
     void* dev = nullptr;
     size_t bytes = 0;
     cudaEvent_t used = nullptr;
-    ~DevPlan() { plan_release(device, dev, used); }
+    cudaEvent_t ready = nullptr;  // the upload (on the building call's stream) has landed
+    ~DevPlan() {
+        plan_release(device, dev, used);
+        if (ready)
+            cudaEventDestroy(ready);
+    }
+    // a launch on any stream first orders itself after the upload
+    void acquire(cudaStream_t stream) const { DFA2C_CUDA_CHECK(cudaStreamWaitEvent(stream, ready, 0)); }
+    void release(cudaStream_t stream) const { DFA2C_CUDA_CHECK(cudaEventRecord(used, stream)); }
 };
 
 // Head strategy for the scheduler: mask_id >= 0 => computed over that mask;
@@ -596,6 +604,8 @@ std::unique_ptr<DevPlan> schedule_items(int device, std::vector<Cand>& cands, co
         std::memcpy(h + o_tiles, tiles.data(), n_tiles);
         std::memcpy(h + o_masks, mask_bytes.data(), n_masks);
     });
+    DFA2C_CUDA_CHECK(cudaEventCreateWithFlags(&p->ready, cudaEventDisableTiming));
+    DFA2C_CUDA_CHECK(cudaEventRecord(p->ready, stream));
     return p;
 }
 
@@ -946,8 +956,9 @@ void launch_forward(const ForwardSpec& s, cudaStream_t stream) {
         scratch_alloc(&a.counters, static_cast<size_t>(plan->n_groups) * 2 * sizeof(int), stream);
         DFA2C_CUDA_CHECK(cudaMemsetAsync(a.counters, 0, static_cast<size_t>(plan->n_groups) * 2 * sizeof(int), stream));
     }
+    plan->acquire(stream);
     DFA2C_CUDA_CHECK(dfa2k::launch_attn(kernel_dim(d), tq, tk, tv, to, tc, a, plan->grid, stream));
-    DFA2C_CUDA_CHECK(cudaEventRecord(plan->used, stream));
+    plan->release(stream);
     if (plan->n_groups > 0) {
         DFA2C_CUDA_CHECK(cudaFreeAsync(a.part_o, stream));
         DFA2C_CUDA_CHECK(cudaFreeAsync(a.part_ml, stream));
@@ -1171,8 +1182,9 @@ void run_influence_fused(const void* q, const void* k, const void* v, const dfa2
     a.snap_stride = static_cast<int32_t>(H);
     a.n_snap = plan->n_snap;
     std::copy(plan->snap_slots, plan->snap_slots + dfa2k::MAX_SNAPS, a.snap_slots);
+    plan->acquire(stream);
     DFA2C_CUDA_CHECK(dfa2k::launch_attn(kernel_dim(d), tq, tk, tv, to, tc, a, plan->grid, stream));
-    DFA2C_CUDA_CHECK(cudaEventRecord(plan->used, stream));
+    plan->release(stream);
     g_launches.fetch_add(1);
 }
 
