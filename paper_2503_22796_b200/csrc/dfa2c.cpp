@@ -317,15 +317,18 @@ void plan_upload(int device, cudaStream_t stream, void* dst, size_t bytes, Fill&
         DFA2C_CUDA_CHECK(cudaStreamSynchronize(stream));  // h goes out of scope
         return;
     }
+    if (!ps.buf[0]) {  // one pinned allocation carved into the slots
+        char* base = nullptr;
+        DFA2C_CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&base), PlanStaging::kSlots * PlanStaging::kBytes,
+                                       cudaHostAllocPortable));
+        for (int j = 0; j < PlanStaging::kSlots; ++j) {
+            ps.buf[j] = base + j * PlanStaging::kBytes;
+            DFA2C_CUDA_CHECK(cudaEventCreateWithFlags(&ps.ev[j], cudaEventDisableTiming));
+        }
+    }
     const int i = ps.next;
     ps.next = (ps.next + 1) % PlanStaging::kSlots;
-    if (!ps.buf[i]) {
-        DFA2C_CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&ps.buf[i]), PlanStaging::kBytes,
-                                       cudaHostAllocPortable));
-        DFA2C_CUDA_CHECK(cudaEventCreateWithFlags(&ps.ev[i], cudaEventDisableTiming));
-    } else {
-        DFA2C_CUDA_CHECK(cudaEventSynchronize(ps.ev[i]));  // its previous upload has been read
-    }
+    DFA2C_CUDA_CHECK(cudaEventSynchronize(ps.ev[i]));  // its previous upload has been read (no-op if unused)
     fill(ps.buf[i]);
     DFA2C_CUDA_CHECK(cudaMemcpyAsync(dst, ps.buf[i], bytes, cudaMemcpyHostToDevice, stream));
     DFA2C_CUDA_CHECK(cudaEventRecord(ps.ev[i], stream));
