@@ -622,9 +622,17 @@ size_t g_plan_bytes = 0;
 // 1,596 work lists of ~0.4 MB. Keep up to 8,192 plans / 4 GB.
 constexpr size_t kMaxPlans = 8192;
 constexpr size_t kMaxPlanBytes = size_t{4} << 30;
+size_t max_plans() {  // DFA2_PLAN_CACHE_MAX overrides the count (tests exercise eviction with it)
+    static const size_t v = [] {
+        const char* e = std::getenv("DFA2_PLAN_CACHE_MAX");
+        const long long x = e ? std::atoll(e) : 0;
+        return x > 0 ? static_cast<size_t>(x) : kMaxPlans;
+    }();
+    return v;
+}
 
 std::shared_ptr<DevPlan> plan_insert(const std::string& key, std::unique_ptr<DevPlan> p) {
-    while (!g_plan_order.empty() && (g_plans.size() >= kMaxPlans || g_plan_bytes + p->bytes > kMaxPlanBytes)) {
+    while (!g_plan_order.empty() && (g_plans.size() >= max_plans() || g_plan_bytes + p->bytes > kMaxPlanBytes)) {
         auto it = g_plans.find(g_plan_order.front());
         if (it != g_plans.end()) {
             g_plan_bytes -= it->second->bytes;

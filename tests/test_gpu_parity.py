@@ -9,6 +9,7 @@ Bit-exact: cached-head copies, cache commits, Full == Arrow(max window),
 run-to-run determinism, head isolation, CacheMiss-before-compute.
 """
 import ctypes
+import os
 
 import numpy as np
 import pytest
@@ -19,6 +20,7 @@ from paper_2503_22796_b200.api import (AttentionDims, ArrowSpec, BlockMask, Cach
                                        HeadCache, HeadStrategy, LayerPlan, ShapeError)
 
 pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 MAX_REL = 1e-2
 MAX_RSE = 5e-5
@@ -829,3 +831,41 @@ def test_influence_rse_grid_matches_oracle_rse(mode):
                 continue
             ym = to_np(li.method_outputs[m][h])
             assert grid[h, m] == pytest.approx(oracle.rse_f32(ym, o, mode), rel=1e-10, abs=1e-15)
+
+
+def test_plan_cache_eviction_keeps_results_bitwise(tmp_path):
+    """Work lists are evicted (FIFO) and rebuilt while earlier launches that
+    read them may still be in flight: with a 3-plan cache, 8 distinct plans
+    cycled twice give bitwise the outputs of a fresh process's first pass."""
+    import subprocess
+    import sys as _sys
+
+    script = tmp_path / "evict.py"
+    script.write_text(r'''
+import sys, hashlib
+sys.path.insert(0, %r)
+import torch
+from paper_2503_22796_b200 import api
+H, nv, nt, d, B = 6, 2048, 77, 128, 128
+n = nv + nt
+dims = api.AttentionDims(H, d, nv, nt)
+g = torch.Generator(device="cuda").manual_seed(3)
+q, k, v = (torch.randn(H, n, d, device="cuda", generator=g).to(torch.bfloat16) for _ in range(3))
+plans = ["F A0 A2 F A8 A1", "A0 F F A3 A1 A2", "A2 A2 F A0 F A5", "F F F A0 A0 A0",
+         "A1 A2 A3 A4 A5 A6", "A0 A0 A0 A0 A0 F", "F A4 A0 A1 F A9", "A7 F A0 F A2 F"]
+outs = []
+for rnd in range(2):
+    for p in plans:
+        outs.append(api.multi_strategy_attention(q, k, v, api.LayerPlan.parse(p), None, 0, 0, dims, B))
+torch.cuda.synchronize()
+h = [hashlib.sha256(o.view(torch.int16).cpu().numpy().tobytes()).hexdigest() for o in outs]
+print(" ".join(h))
+''' % ROOT)
+    env = dict(os.environ)
+    big = subprocess.run([_sys.executable, str(script)], capture_output=True, text=True, env=env, timeout=600)
+    env["DFA2_PLAN_CACHE_MAX"] = "3"
+    small = subprocess.run([_sys.executable, str(script)], capture_output=True, text=True, env=env, timeout=600)
+    assert big.returncode == 0 and small.returncode == 0, big.stderr[-2000:] + small.stderr[-2000:]
+    hb, hs = big.stdout.split(), small.stdout.split()
+    assert len(hb) == 16 and hb == hs
+    assert hb[:8] == hb[8:]  # second cycle (rebuilt plans) bitwise the first
