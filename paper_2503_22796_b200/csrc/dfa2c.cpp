@@ -700,6 +700,7 @@ struct dfa2c_cache {
     int64_t L = 0, H = 0, batch = 0, n = 0, d = 0;
     int device = 0;
     std::vector<void*> layer_buf;    // [L] -> [batch, H, n, d] bf16, lazily allocated
+    std::vector<cudaEvent_t> layer_ready;  // [L] the buffer's allocation + zero fill has landed
     std::vector<int64_t> produced;   // [L*H], INT64_MIN = empty slot
 
     // Layer buffers come from the library's device pool (release threshold
@@ -718,6 +719,9 @@ struct dfa2c_cache {
         for (void* p : layer_buf)
             if (p)
                 cudaFreeAsync(p, nullptr);
+        for (cudaEvent_t e : layer_ready)
+            if (e)
+                cudaEventDestroy(e);
         cudaSetDevice(cur);
     }
     size_t slot_elems() const { return static_cast<size_t>(n * d); }
@@ -727,6 +731,7 @@ struct dfa2c_cache {
     void ensure(int64_t layer) {
         if (layer >= L) {
             layer_buf.resize(static_cast<size_t>(layer + 1), nullptr);
+            layer_ready.resize(static_cast<size_t>(layer + 1), nullptr);
             std::vector<int64_t> p(static_cast<size_t>((layer + 1) * H), std::numeric_limits<int64_t>::min());
             std::copy(produced.begin(), produced.end(), p.begin());
             produced.swap(p);
@@ -743,15 +748,23 @@ struct dfa2c_cache {
         return layer >= 0 && layer < L && head >= 0 && head < H &&
                produced[static_cast<size_t>(layer * H + head)] != std::numeric_limits<int64_t>::min();
     }
-    void* layer_ptr(int64_t layer) {
+    // The layer's slot buffer, ordered on `st`: created (pool allocation +
+    // zero fill) on the first caller's stream; a caller on any other stream
+    // first waits for that to have landed.
+    void* layer_ptr(int64_t layer, cudaStream_t st) {
         if (!layer_buf[layer]) {
-            // stream-ordered on the legacy default stream, which orders with
-            // every blocking stream the caller launches on
-            DFA2C_CUDA_CHECK(
-                cudaMallocFromPoolAsync(&layer_buf[layer], layer_bytes(), scratch_pool(device), nullptr));
-            DFA2C_CUDA_CHECK(cudaMemsetAsync(layer_buf[layer], 0, layer_bytes(), nullptr));
+            DFA2C_CUDA_CHECK(cudaMallocFromPoolAsync(&layer_buf[layer], layer_bytes(), scratch_pool(device), st));
+            DFA2C_CUDA_CHECK(cudaMemsetAsync(layer_buf[layer], 0, layer_bytes(), st));
+            DFA2C_CUDA_CHECK(cudaEventCreateWithFlags(&layer_ready[layer], cudaEventDisableTiming));
+            DFA2C_CUDA_CHECK(cudaEventRecord(layer_ready[layer], st));
+        } else {
+            order_after_ready(layer, st);
         }
         return layer_buf[layer];
+    }
+    void order_after_ready(int64_t layer, cudaStream_t st) const {
+        if (layer >= 0 && layer < L && layer_ready[layer])
+            DFA2C_CUDA_CHECK(cudaStreamWaitEvent(st, layer_ready[layer], 0));
     }
 };
 
@@ -844,7 +857,7 @@ void run_padded(const ForwardSpec& s, cudaStream_t st) {
             if (!s.cache)
                 fail(DFA2C_CACHE_MISS, "cached heads need a cache");
             s.cache->ensure(s.layer);
-            cache_layer = s.cache->layer_ptr(s.layer);
+            cache_layer = s.cache->layer_ptr(s.layer, st);
         }
     const size_t head_bytes = static_cast<size_t>(n * d) * 2;
     for (int64_t h = 0; h < H; ++h) {
@@ -935,7 +948,7 @@ void launch_forward(const ForwardSpec& s, cudaStream_t stream) {
         if (!s.cache)
             fail(DFA2C_CACHE_MISS, "cached heads need a cache");
         s.cache->ensure(s.layer);
-        cache_layer = s.cache->layer_ptr(s.layer);
+        cache_layer = s.cache->layer_ptr(s.layer, stream);
     }
 
     const int64_t bh = s.batch * H;
@@ -1442,6 +1455,7 @@ int dfa2c_cache_create(int64_t L, int64_t H, int64_t batch, int64_t n, int64_t d
         c->d = d;
         DFA2C_CUDA_CHECK(cudaGetDevice(&c->device));
         c->layer_buf.assign(static_cast<size_t>(L), nullptr);
+        c->layer_ready.assign(static_cast<size_t>(L), nullptr);
         c->produced.assign(static_cast<size_t>(L * H), std::numeric_limits<int64_t>::min());
         *out = c.release();
     });
@@ -1483,7 +1497,8 @@ int dfa2c_cache_store(dfa2c_cache* c, int64_t layer, int64_t head, const void* s
         if (!c || !src)
             fail(DFA2C_SHAPE, "NULL cache or source");
         c->check(layer, head);
-        char* dst = static_cast<char*>(c->layer_ptr(layer)) + static_cast<size_t>(head) * c->slot_elems() * 2;
+        char* dst = static_cast<char*>(c->layer_ptr(layer, as_stream(stream))) +
+                    static_cast<size_t>(head) * c->slot_elems() * 2;
         const size_t row = c->slot_elems() * 2;
         DFA2C_CUDA_CHECK(cudaMemcpy2DAsync(dst, row * c->H, src, row, row, static_cast<size_t>(c->batch),
                                            cudaMemcpyDeviceToDevice, as_stream(stream)));
@@ -1498,6 +1513,7 @@ int dfa2c_cache_fetch(const dfa2c_cache* c, int64_t layer, int64_t head, void* d
         if (!c->has(layer, head))
             fail(DFA2C_CACHE_MISS, "no cached output for layer " + std::to_string(layer) + ", head " +
                                        std::to_string(head));
+        c->order_after_ready(layer, as_stream(stream));
         const char* src =
             static_cast<const char*>(c->layer_buf[layer]) + static_cast<size_t>(head) * c->slot_elems() * 2;
         const size_t row = c->slot_elems() * 2;
@@ -1615,7 +1631,7 @@ int dfa2c_mha_forward_host(const void* q, const void* k, const void* v, int64_t 
             if (kinds[h] == DFA2C_CACHED)  // a skipped cached head is neither read nor written
                 cached.push_back(h);
         if (!cached.empty())
-            copy_runs(cached, cache->layer_ptr(layer), out, cudaMemcpyDeviceToHost, hp.d2h);
+            copy_runs(cached, cache->layer_ptr(layer, hp.d2h), out, cudaMemcpyDeviceToHost, hp.d2h);
 
         ForwardSpec base{};
         base.q = ws.q;
@@ -1836,6 +1852,7 @@ std::vector<uint8_t> influence_enqueue(const void* q, const void* k, const void*
             // Cached: slot vs original for heads with a slot (src/calibrate.cpp:222-235),
             // one RSE launch over the layer's contiguous [H, N, d] slot array; heads
             // without a slot stay ineligible (+inf).
+            cache->order_after_ready(layer, st);
             const void* slots = cache->layer_buf[layer];
             if (method_outputs)  // the slot where there is one, zeros (unset) elsewhere
                 for (int64_t h = 0; h < H; ++h) {

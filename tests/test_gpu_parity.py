@@ -869,3 +869,29 @@ print(" ".join(h))
     hb, hs = big.stdout.split(), small.stdout.split()
     assert len(hb) == 16 and hb == hs
     assert hb[:8] == hb[8:]  # second cycle (rebuilt plans) bitwise the first
+
+
+def test_cache_layers_first_touched_on_a_side_stream():
+    """A layer's slot buffer is created (pool allocation + zero fill) on the
+    stream of the call that first touches it; calls on other streams order
+    themselves after it. Fresh layers written from a non-default stream and
+    read back from the default stream hold exactly the committed outputs."""
+    t = torch()
+    H, nv, nt, d, B = 4, 1024, 77, 64, 128
+    dims = AttentionDims(H, d, nv, nt)
+    n = nv + nt
+    q, _ = bf16_inputs((H, n, d), 121)
+    k, _ = bf16_inputs((H, n, d), 122)
+    v, _ = bf16_inputs((H, n, d), 123)
+    cache = HeadCache(8, H, n, d)
+    side = t.cuda.Stream()
+    outs = []
+    with t.cuda.stream(side):
+        for layer in range(8):
+            outs.append(api.multi_strategy_attention(q, k, v, LayerPlan.parse("F A0 A2 F"), cache, layer, 0, dims, B,
+                                                     stream=side))
+    # default stream: fetch every committed slot (ordered after the side stream's creation + commits)
+    t.cuda.current_stream().wait_stream(side)
+    for layer in range(8):
+        for h in range(H):
+            assert t.equal(cache.fetch(layer, h), outs[layer][h])
