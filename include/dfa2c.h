@@ -242,6 +242,13 @@ int dfa2c_influence_for_layer_async(const void* q, const void* k, const void* v,
 int dfa2c_influence_finalize(const double* rse_host, const uint8_t* eligible, int64_t n_heads,
                              int64_t n_methods, double* influence);
 
+/* Drops every cached work list (plans are rebuilt on their next use) and
+ * returns the library pool's unused device memory to the driver on the
+ * current device (head-cache layers and in-flight scratch stay). The pool
+ * otherwise keeps its memory for fast stream-ordered reuse. Synchronises
+ * the device. */
+int dfa2c_release_cached_memory(void);
+
 /* Fused calibration pass switch (process-wide; default on, environment
  * DFA2_INFLUENCE_FUSED=0 turns it off): 0 = one launch per candidate, whose
  * outputs are bitwise dfa2c_mha_forward's for the same strategy. */

@@ -138,6 +138,7 @@ _SIGS = {
     "dfa2c_fnv1a_hex": (c_int32, [c_char_p, c_int64, c_char_p]),
     "dfa2c_set_split_kv": (c_int32, [c_int32]),
     "dfa2c_set_influence_fused": (c_int32, [c_int32]),
+    "dfa2c_release_cached_memory": (c_int32, []),
     "dfa2c_influence_fused_enabled": (c_int32, []),
     "dfa2c_convert": (c_int32, [c_void_p, c_int32, c_void_p, c_int32, c_int64, c_void_p]),
     "dfa2c_selection_cap": (c_double, [c_double, c_int64, c_double]),

@@ -378,6 +378,12 @@ def set_influence_fused(on: bool) -> None:
     check(lib().dfa2c_set_influence_fused(1 if on else 0))
 
 
+def release_cached_memory() -> None:
+    """dfa2c_release_cached_memory: drop cached work lists and trim the
+    library's device memory pool (synchronises the device)."""
+    check(lib().dfa2c_release_cached_memory())
+
+
 def influence_fused_enabled() -> bool:
     return bool(lib().dfa2c_influence_fused_enabled())
 

@@ -1968,6 +1968,21 @@ int dfa2c_influence_finalize(const double* rse_host, const uint8_t* eligible, in
     });
 }
 
+int dfa2c_release_cached_memory(void) {
+    return guard([&] {
+        {
+            std::lock_guard<std::mutex> lk(g_plan_mu);
+            g_plans.clear();  // blocks are released after their last launch (event-ordered)
+            g_plan_order.clear();
+            g_plan_bytes = 0;
+        }
+        int cur = 0;
+        DFA2C_CUDA_CHECK(cudaGetDevice(&cur));
+        DFA2C_CUDA_CHECK(cudaDeviceSynchronize());  // the releases above have run
+        DFA2C_CUDA_CHECK(cudaMemPoolTrimTo(scratch_pool(cur), 0));
+    });
+}
+
 int dfa2c_set_influence_fused(int32_t on) {
     g_influence_fused.store(on ? 1 : 0);
     return DFA2C_OK;

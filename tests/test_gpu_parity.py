@@ -895,3 +895,21 @@ def test_cache_layers_first_touched_on_a_side_stream():
     for layer in range(8):
         for h in range(H):
             assert t.equal(cache.fetch(layer, h), outs[layer][h])
+
+
+def test_release_cached_memory_then_rebuild():
+    """dfa2c_release_cached_memory drops the work lists and trims the pool;
+    the next call rebuilds its plan and gives bitwise the same output."""
+    t = torch()
+    H, nv, nt, d, B = 4, 1024, 77, 128, 128
+    dims = AttentionDims(H, d, nv, nt)
+    n = nv + nt
+    q, _ = bf16_inputs((H, n, d), 131)
+    k, _ = bf16_inputs((H, n, d), 132)
+    v, _ = bf16_inputs((H, n, d), 133)
+    lp = LayerPlan.parse("F A0 A2 A5")
+    a = api.multi_strategy_attention(q, k, v, lp, None, 0, 0, dims, B)
+    api.release_cached_memory()
+    b = api.multi_strategy_attention(q, k, v, lp, None, 0, 0, dims, B)
+    t.cuda.synchronize()
+    assert t.equal(a, b)
