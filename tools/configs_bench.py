@@ -63,8 +63,12 @@ if "1" in only:
         lp = api.LayerPlan.parse("F A0 A2 C")
         o = torch.empty_like(q)
         ms = time_calls(lambda: api.multi_strategy_attention(q, k, v, lp, cache, 0, 1, dims, B, out=o), 50)
+        # the layer is one pair's 9-tile chain long: split-KV (opt-in) spreads it
+        api.set_split_kv(True)
+        ms_split = time_calls(lambda: api.multi_strategy_attention(q, k, v, lp, cache, 0, 1, dims, B, out=o), 50)
+        api.set_split_kv(False)
         fl = api.plan_flops(lp, dims, B)
-        out[f"B{B}"] = {"ms": ms, "plan_gflop": fl / 1e9, "computed_tflops": fl / ms / 1e9,
+        out[f"B{B}"] = {"ms": ms, "ms_split_kv": ms_split, "plan_gflop": fl / 1e9, "computed_tflops": fl / ms / 1e9,
                         "reduction": 1 - fl / (H * api.dense_flops(n, d))}
     res["cfg1"] = out
     print("cfg1", json.dumps(out))
