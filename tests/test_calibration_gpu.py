@@ -122,3 +122,32 @@ def test_remeasuring_under_the_plan_reproduces_the_influences(fused):
                 elif s_.kind == "arrow":
                     m = [c.strategy for c in cfg.methods].index(s_)
                     cache.store(l, h, li.method_outputs[m][h], t)
+
+
+def test_single_layer_schedule_orders_splice_before_next_measurement():
+    """L = 1: every (t, 0) measurement reads the slot the previous timestep's
+    splice wrote, so the pipelined driver must finish that splice first.
+    Re-measuring under the plan (splicing as the driver does) reproduces
+    every influence bitwise."""
+    import torch
+
+    q, k, v = streams()
+    cfg = api.CalibrationConfig(api.make_candidates([0, 2], include_cached=True), 0.4, 1.5)
+    dims = api.AttentionDims(H, D, NV, NT)
+    r = api.calibrate_model(q, k, v, dims, T, 1, B, cfg)
+    assert api.audit_plan_constraints(r.plan, r.influences) == 0
+    cache = api.HeadCache(1, H, NV + NT, D)
+    M = len(cfg.methods)
+    for t in range(T):
+        li = api.influence_for_layer(q(t, 0), k(t, 0), v(t, 0), cfg.methods, cache, 0, t, dims, B)
+        for h in range(H):
+            for m in range(M):
+                val = li.influence[h * M + m]
+                if math.isfinite(val):
+                    assert val == r.influences.get(t, 0, h, m)
+        for h, s_ in enumerate(r.plan.at(t, 0).strategies):
+            if s_.kind == "full":
+                cache.store(0, h, li.original[h], t)
+            elif s_.kind == "arrow":
+                cache.store(0, h, li.method_outputs[[c.strategy for c in cfg.methods].index(s_)][h], t)
+    torch.cuda.synchronize()
