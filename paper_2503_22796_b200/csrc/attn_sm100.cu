@@ -76,7 +76,10 @@ struct Cfg {
     static constexpr int NBARS = 2 * QBUF + 2 * KSTAGES + 2 * VSTAGES + 14;
     // The dynamic window starts 1024-aligned (the 1 KB system reservation
     // precedes it); the kernel traps otherwise, so no alignment slack.
-    static constexpr uint32_t SMEM_BYTES = BAR_OFF + NBARS * 8 + 16;
+    // HALVES items: per lane and row, the (reference max, row sum) exchanged
+    // between the two lanes in the epilogue
+    static constexpr uint32_t XCHG_OFF = BAR_OFF + NBARS * 8 + 16;
+    static constexpr uint32_t SMEM_BYTES = XCHG_OFF + 2 * 2 * TILE_M * 4;
     static_assert(SMEM_BYTES <= 232448, "shared memory budget");
     static constexpr uint32_t TMEM_COLS = 512;
     static constexpr int THREADS = 384;
@@ -894,6 +897,36 @@ __global__ void __launch_bounds__(384, 1)
             mbar_wait(o_full(L), icnt & 1);
             ++icnt;
             tc_fence_after();
+            if (w.flags & ITEM_HALVES) {
+                // both lanes folded halves of this tile's keys: merge
+                // O = (O_A 2^(m_A-M) + O_B 2^(m_B-M)) / (l_A 2^(m_A-M) + l_B 2^(m_B-M)),
+                // lane L storing the 64-column boxes b = L, L + 2, ...
+                float* xch = reinterpret_cast<float*>(smem + C::XCHG_OFF);
+                xch[(L * 2 + 0) * TILE_M + r] = m_ref;
+                xch[(L * 2 + 1) * TILE_M + r] = l;
+                named_bar_sync(3, 256);
+                const float mo = xch[((1 - L) * 2 + 0) * TILE_M + r], lo_ = xch[((1 - L) * 2 + 1) * TILE_M + r];
+                const float mA = L ? mo : m_ref, lA = L ? lo_ : l, mB = L ? m_ref : mo, lB = L ? l : lo_;
+                const float M = fmaxf(mA, mB);
+                const float fA = exp2f(mA - M), fB = exp2f(mB - M);
+                const float inv = 1.f / (lA * fA + lB * fB);
+                for (int b = L; b < D / 64; b += 2) {
+                    float oa[64], ob[64];
+                    const uint32_t ca = tmem + lrow + o_col<D>(0) + 64 * b, cb = tmem + lrow + o_col<D>(1) + 64 * b;
+                    tmem_ld32(ca, reinterpret_cast<uint32_t*>(oa));
+                    tmem_ld32(ca + 32, reinterpret_cast<uint32_t*>(oa) + 32);
+                    tmem_ld32(cb, reinterpret_cast<uint32_t*>(ob));
+                    tmem_ld32(cb + 32, reinterpret_cast<uint32_t*>(ob) + 32);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int i = 0; i < 64; ++i)
+                        oa[i] = fmaf(oa[i], fA, ob[i] * fB);
+                    store_box(b, oa, inv, 0u);
+                }
+                tc_fence_before();
+                named_bar_sync(3, 256);  // both lanes have read O_A and O_B
+                continue;
+            }
             if (!(w.flags & ITEM_SPLIT)) {
                 uint32_t dst = 0;
                 if (multi)  // every snapshot not yet emitted: the full row covers them

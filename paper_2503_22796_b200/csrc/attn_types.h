@@ -31,6 +31,8 @@ enum : int32_t {
     ITEM_SPLIT = 4,   // one key chunk of a heavy pair; the group's last chunk combines
     ITEM_MULTI = 8,   // calibration pass: every key tile in window-band order, with
                       // snapshots of O/l written to the candidates' outputs (see below)
+    ITEM_HALVES = 16, // one query tile on both lanes, each folding half of its key
+                      // tiles; the lanes merge (max, sum, O) in the epilogue (d = 64)
 };
 
 // Tile word: KV tile index in bits [0,24); bit 24/25: lane A/B folds this

@@ -361,50 +361,111 @@ void plan_release(int device, void* dev, cudaEvent_t used) {
     cudaSetDevice(cur);
 }
 
-// Pair lists: for every pair of query tiles (2p, 2p+1) the union of their
-// KV tile rows (ascending), each word tagged with the lanes that fold it.
+// Work entries of one mask: each is a pair of query tiles (lanes A, B)
+// sharing the ascending union of their KV tile rows, every word tagged with
+// the lanes that fold it; or, at d = 64, for a text query tile (every key
+// tile for an arrow head: the longest chain of the layer), a HALVES entry:
+// the tile on both lanes, lane A folding the first half of its key tiles
+// and lane B the second, interleaved, merged in the epilogue. A lane folds
+// its own tiles in ascending order either way, so pairing never changes a
+// row's result; the halving is a fixed property of the geometry (text rows
+// at d = 64, for every head and strategy), so each head's result is still
+// a function of its own strategy alone.
 struct PairSet {
-    std::vector<int64_t> row_ptr;  // [n_pairs + 1]
+    std::vector<int64_t> row_ptr;  // [entries + 1]
     std::vector<uint32_t> words;
-    std::vector<int32_t> n_a, n_b;  // per pair: tiles lane A / lane B fold
+    std::vector<int32_t> n_a, n_b;  // per entry: tiles lane A / lane B fold
+    std::vector<int32_t> qa, qb;    // query tiles of lanes A / B (qb -1: single lane)
+    std::vector<uint8_t> halves;    // HALVES entry
 };
 
-PairSet build_pair_set(const TileSet& ts, int64_t nqt) {
+inline uint32_t tag_lane(uint32_t c, int lane) {
+    const bool part = (c & dfa2k::TILE_SET_PARTIAL) != 0;
+    return lane ? dfa2k::TILE_NEED_B | (part ? dfa2k::TILE_PART_B : 0u)
+                : dfa2k::TILE_NEED_A | (part ? dfa2k::TILE_PART_A : 0u);
+}
+
+// text_tile[q]: query tile q runs as a HALVES entry candidate (empty: none)
+PairSet build_pair_set(const TileSet& ts, int64_t nqt, const std::vector<uint8_t>& text_tile) {
     PairSet ps;
-    const int64_t np = (nqt + 1) / 2;
-    ps.row_ptr.assign(static_cast<size_t>(np + 1), 0);
+    ps.row_ptr.push_back(0);
     ps.words.reserve(ts.cols.size());
-    for (int64_t p = 0; p < np; ++p) {
-        const int64_t qa = 2 * p, qb = 2 * p + 1;
+    auto add_pair = [&](int64_t qa, int64_t qb) {
         // both rows are ascending: merge them (each tile once, tagged with its lanes)
         int64_t i = ts.row_ptr[qa], ie = ts.row_ptr[qa + 1];
-        int64_t j = qb < nqt ? ts.row_ptr[qb] : 0, je = qb < nqt ? ts.row_ptr[qb + 1] : 0;
-        const int32_t nb_ = static_cast<int32_t>(je - j);
-        auto tag_a = [](uint32_t c) {
-            return dfa2k::TILE_NEED_A | ((c & dfa2k::TILE_SET_PARTIAL) ? dfa2k::TILE_PART_A : 0u);
-        };
-        auto tag_b = [](uint32_t c) {
-            return dfa2k::TILE_NEED_B | ((c & dfa2k::TILE_SET_PARTIAL) ? dfa2k::TILE_PART_B : 0u);
-        };
+        int64_t j = qb >= 0 ? ts.row_ptr[qb] : 0, je = qb >= 0 ? ts.row_ptr[qb + 1] : 0;
+        ps.n_a.push_back(static_cast<int32_t>(ie - i));
+        ps.n_b.push_back(static_cast<int32_t>(je - j));
         while (i < ie || j < je) {
             const uint32_t ca = i < ie ? ts.cols[i] : 0u, cb = j < je ? ts.cols[j] : 0u;
             const uint32_t ta = ca & ~dfa2k::TILE_SET_PARTIAL, tb = cb & ~dfa2k::TILE_SET_PARTIAL;
             if (j >= je || (i < ie && ta < tb)) {
-                ps.words.push_back(ta | tag_a(ca));
+                ps.words.push_back(ta | tag_lane(ca, 0));
                 ++i;
             } else if (i >= ie || tb < ta) {
-                ps.words.push_back(tb | tag_b(cb));
+                ps.words.push_back(tb | tag_lane(cb, 1));
                 ++j;
             } else {
-                ps.words.push_back(ta | tag_a(ca) | tag_b(cb));
+                ps.words.push_back(ta | tag_lane(ca, 0) | tag_lane(cb, 1));
                 ++i;
                 ++j;
             }
         }
-        ps.row_ptr[p + 1] = static_cast<int64_t>(ps.words.size());
-        ps.n_a.push_back(static_cast<int32_t>(ts.row_ptr[qa + 1] - ts.row_ptr[qa]));
-        ps.n_b.push_back(nb_);
+        ps.qa.push_back(static_cast<int32_t>(qa));
+        ps.qb.push_back(static_cast<int32_t>(qb));
+        ps.halves.push_back(0);
+        ps.row_ptr.push_back(static_cast<int64_t>(ps.words.size()));
+    };
+    auto add_halves = [&](int64_t q) {
+        const int64_t lo = ts.row_ptr[q], n = ts.row_ptr[q + 1] - lo, h = (n + 1) / 2;
+        for (int64_t i = 0; i < h; ++i) {
+            const uint32_t ca = ts.cols[lo + i];
+            ps.words.push_back((ca & ~dfa2k::TILE_SET_PARTIAL) | tag_lane(ca, 0));
+            if (i < n - h) {
+                const uint32_t cb = ts.cols[lo + h + i];
+                ps.words.push_back((cb & ~dfa2k::TILE_SET_PARTIAL) | tag_lane(cb, 1));
+            }
+        }
+        ps.n_a.push_back(static_cast<int32_t>(h));
+        ps.n_b.push_back(static_cast<int32_t>(n - h));
+        ps.qa.push_back(static_cast<int32_t>(q));
+        ps.qb.push_back(static_cast<int32_t>(q));
+        ps.halves.push_back(1);
+        ps.row_ptr.push_back(static_cast<int64_t>(ps.words.size()));
+    };
+    if (text_tile.empty()) {
+        for (int64_t q = 0; q < nqt; q += 2)
+            add_pair(q, q + 1 < nqt ? q + 1 : -1);
+        return ps;
     }
+    // Halve only when the text rows are the mask's long pole: their key
+    // chains are more than 5x the average chain of the other query tiles
+    // (narrow arrow windows). A property of the mask alone, so heads with
+    // the same strategy are treated alike and Full == Arrow(max) holds.
+    int64_t other_len = 0, n_other = 0, text_len = 0;
+    for (int64_t q = 0; q < nqt; ++q) {
+        const int64_t len = ts.row_ptr[q + 1] - ts.row_ptr[q];
+        if (text_tile[q])
+            text_len = std::max(text_len, len);
+        else {
+            other_len += len;
+            ++n_other;
+        }
+    }
+    const bool halve = n_other > 0 && text_len * n_other > 5 * other_len;
+    int64_t pending = -1;  // the other tiles pair up in order
+    for (int64_t q = 0; q < nqt; ++q) {
+        if (halve && text_tile[q] && ts.row_ptr[q + 1] - ts.row_ptr[q] >= 2) {
+            add_halves(q);
+        } else if (pending < 0) {
+            pending = q;
+        } else {
+            add_pair(pending, q);
+            pending = -1;
+        }
+    }
+    if (pending >= 0)
+        add_pair(pending, -1);
     return ps;
 }
 
@@ -426,15 +487,25 @@ std::unique_ptr<DevPlan> schedule_items(int device, std::vector<Cand>& cands, co
 std::unique_ptr<DevPlan> build_dev_plan(int device, int64_t batch, int64_t H, int64_t n, int64_t B,
                                         const std::vector<std::vector<uint8_t>>& masks,
                                         const std::vector<HeadJob>& jobs, const std::vector<int>& ref_jobs,
-                                        cudaStream_t stream) {
+                                        int64_t text_lo, int64_t text_hi, bool halves, cudaStream_t stream) {
     const int64_t nqt = ceil_div(n, dfa2k::TILE_M);
-    const int64_t np = (nqt + 1) / 2;
+    const int64_t np = (nqt + 1) / 2;  // copy items: pairs (2p, 2p+1)
+    // text query tiles as HALVES entries (d = 64; not under split-KV, which
+    // chunks the long rows its own way)
+    std::vector<uint8_t> text_tile;
+    if (halves && !split_kv_enabled() && text_hi > text_lo) {
+        text_tile.assign(static_cast<size_t>(nqt), 0);
+        for (int64_t q = 0; q < nqt; ++q) {
+            const int64_t r0 = q * dfa2k::TILE_M, r1 = std::min(r0 + dfa2k::TILE_M, n);
+            text_tile[q] = (r0 < text_hi && r1 > text_lo) ? 1 : 0;
+        }
+    }
     std::vector<uint32_t> tiles;
     std::vector<uint8_t> mask_bytes;
     std::vector<int64_t> mask_tile_base, mask_off;
     std::vector<PairSet> sets;
     for (const auto& m : masks) {
-        sets.push_back(build_pair_set(build_tile_set(m.data(), n, B), nqt));
+        sets.push_back(build_pair_set(build_tile_set(m.data(), n, B), nqt, text_tile));
         mask_tile_base.push_back(static_cast<int64_t>(tiles.size()));
         tiles.insert(tiles.end(), sets.back().words.begin(), sets.back().words.end());
         mask_off.push_back(static_cast<int64_t>(mask_bytes.size()));
@@ -465,7 +536,7 @@ std::unique_ptr<DevPlan> build_dev_plan(int device, int64_t batch, int64_t H, in
     constexpr double kRefSMs = 148.0;
     std::vector<std::vector<int32_t>> chunks_of(sets.size());
     for (size_t mi = 0; mi < sets.size(); ++mi)
-        chunks_of[mi].assign(static_cast<size_t>(np), 1);
+        chunks_of[mi].assign(sets[mi].qa.size(), 1);
     if (split_kv_enabled()) {
         double per_sample = 0.0;
         for (int64_t h = 0; h < H; ++h) {
@@ -475,13 +546,13 @@ std::unique_ptr<DevPlan> build_dev_plan(int device, int64_t batch, int64_t H, in
                 continue;
             }
             const PairSet& ps = sets[rj];
-            for (int64_t p = 0; p < np; ++p)
+            for (size_t p = 0; p < ps.qa.size(); ++p)
                 per_sample += ps.n_a[p] + ps.n_b[p] + 1.0;
         }
         const double avg = std::max(per_sample / kRefSMs, 1.0);
         for (size_t mi = 0; mi < sets.size(); ++mi) {
             const PairSet& ps = sets[mi];
-            for (int64_t p = 0; p < np; ++p) {
+            for (size_t p = 0; p < ps.qa.size(); ++p) {
                 const double cost = ps.n_a[p] + ps.n_b[p] + 1.0;
                 const int64_t len = ps.row_ptr[p + 1] - ps.row_ptr[p];
                 if (cost > avg && len >= 8)
@@ -499,26 +570,30 @@ std::unique_ptr<DevPlan> build_dev_plan(int device, int64_t batch, int64_t H, in
             const HeadJob& j = jobs[h];
             if (j.mask_id == JOB_SKIP)
                 continue;
-            for (int64_t p = 0; p < np; ++p) {
+            const int64_t n_entries =
+                j.mask_id == JOB_COPY ? np : static_cast<int64_t>(sets[j.mask_id].qa.size());
+            for (int64_t p = 0; p < n_entries; ++p) {
                 WorkItem w{};
                 w.bh = static_cast<int32_t>(b * H + h);
-                w.qtile_a = static_cast<int32_t>(2 * p);
-                w.qtile_b = 2 * p + 1 < nqt ? static_cast<int32_t>(2 * p + 1) : -1;
                 if (j.mask_id == JOB_COPY) {
+                    w.qtile_a = static_cast<int32_t>(2 * p);
+                    w.qtile_b = 2 * p + 1 < nqt ? static_cast<int32_t>(2 * p + 1) : -1;
                     w.flags = dfa2k::ITEM_COPY;
                     const int64_t rows = std::min<int64_t>(n, (w.qtile_b >= 0 ? w.qtile_b : w.qtile_a) * 128 + 128) -
                                          w.qtile_a * 128;
                     cands.push_back({w, static_cast<double>(rows) / 128.0});
                 } else {
                     const PairSet& ps = sets[j.mask_id];
+                    w.qtile_a = ps.qa[p];
+                    w.qtile_b = ps.qb[p];
                     w.tile_begin = static_cast<int32_t>(mask_tile_base[j.mask_id] + ps.row_ptr[p]);
                     w.n_tiles = static_cast<int32_t>(ps.row_ptr[p + 1] - ps.row_ptr[p]);
                     w.mask_off = static_cast<int32_t>(mask_off[j.mask_id]);
-                    w.flags = j.commit ? dfa2k::ITEM_COMMIT : 0;
+                    w.flags = (j.commit ? dfa2k::ITEM_COMMIT : 0) | (ps.halves[p] ? dfa2k::ITEM_HALVES : 0);
                     if (ps.n_a[p] < 1)
-                        fail(DFA2C_FULLY_MASKED, "query tile " + std::to_string(2 * p) + " has no active key tiles");
+                        fail(DFA2C_FULLY_MASKED, "query tile " + std::to_string(w.qtile_a) + " has no active key tiles");
                     if (w.qtile_b >= 0 && ps.n_b[p] < 1)
-                        fail(DFA2C_FULLY_MASKED, "query tile " + std::to_string(2 * p + 1) + " has no active key tiles");
+                        fail(DFA2C_FULLY_MASKED, "query tile " + std::to_string(w.qtile_b) + " has no active key tiles");
                     const int32_t nch = chunks_of[j.mask_id][p];
                     if (nch <= 1) {
                         cands.push_back({w, (ps.n_a[p] + ps.n_b[p]) * (dfa2k::TILE_N / 128.0) + 1.0});
@@ -936,6 +1011,7 @@ void launch_forward(const ForwardSpec& s, cudaStream_t stream) {
                 masks = &built;
             }
             plan = plan_insert(key, build_dev_plan(device, s.batch, H, n, s.block, *masks, s.jobs, s.ref_jobs,
+                                                   text_begin(s.dims), text_end(s.dims), kernel_dim(d) == 64,
                                                    stream));
         }
     }

@@ -913,3 +913,29 @@ def test_release_cached_memory_then_rebuild():
     b = api.multi_strategy_attention(q, k, v, lp, None, 0, 0, dims, B)
     t.cuda.synchronize()
     assert t.equal(a, b)
+
+
+@pytest.mark.parametrize("order", [0, 1], ids=["visual_first", "text_first"])
+def test_d64_text_rows_halved_across_lanes(order):
+    """d = 64, narrow arrow windows: the text query tiles run on both lanes,
+    each folding half of the key tiles, merged in the epilogue (HALVES).
+    Rows against the f64 oracle; the rule depends on the head's own mask
+    only, so a head's output does not change when another head's strategy
+    does (test_dispatch.cpp:98-109), and it is deterministic."""
+    t = torch()
+    H, nv, nt, d, B = 3, 4096, 333, 64, 128
+    dims = AttentionDims(H, d, nv, nt, api.TEXT_FIRST if order else api.VISUAL_FIRST)
+    n = nv + nt
+    q, qn = bf16_inputs((H, n, d), 141)
+    k, kn = bf16_inputs((H, n, d), 142)
+    v, vn = bf16_inputs((H, n, d), 143)
+    a = api.multi_strategy_attention(q, k, v, LayerPlan.parse("A0 A0 F"), None, 0, 0, dims, B)
+    b = api.multi_strategy_attention(q, k, v, LayerPlan.parse("A0 A8 A1"), None, 0, 0, dims, B)
+    c = api.multi_strategy_attention(q, k, v, LayerPlan.parse("A0 A0 F"), None, 0, 0, dims, B)
+    t.cuda.synchronize()
+    assert t.equal(a[0], b[0]) and t.equal(a, c)
+    lo, hi = dims.text_begin(), dims.text_end()
+    rows = np.concatenate([np.arange(lo, hi, 5), np.arange(0, n, 97)]).astype(np.int64)
+    o = to_np(a)
+    for h, s_ in enumerate(LayerPlan.parse("A0 A0 F").strategies):
+        check_close(o[h][rows], oracle_head(qn[h], kn[h], vn[h], dims, B, s_, rows), f"head {h} {s_}")

@@ -1,7 +1,8 @@
 """compute-sanitizer (memcheck, racecheck, synccheck) over small layers of
 every kernel path: d = 64 and 128, Full / Arrow / Cached items with cache
-commits, split-KV chunks and their combine, the fused calibration pass, and
-a mask block other than the tile (element masking)."""
+commits, split-KV chunks and their combine, the fused calibration pass, a
+mask block other than the tile (element masking), and text rows halved
+across the two lanes."""
 import os
 import shutil
 import subprocess
@@ -29,6 +30,10 @@ for d in (64, 128):
     api.set_split_kv(False)
     api.influence_for_layer(q, k, v, api.make_candidates([0, 2], True), cache, 0, 3, dims, B)
     api.multi_strategy_attention(q, k, v, api.LayerPlan.parse("F A0 A2 C"), cache, 0, 4, dims, 64)
+# text rows halved across the lanes (d = 64, narrow windows)
+dims = api.AttentionDims(2, 64, 4096, 333)
+q, k, v = (torch.randn(2, 4429, 64, device="cuda").to(torch.bfloat16) for _ in range(3))
+api.multi_strategy_attention(q, k, v, api.LayerPlan.parse("A0 A1"), None, 0, 0, dims, 128)
 torch.cuda.synchronize()
 print("case ok")
 ''' % ROOT
