@@ -386,7 +386,7 @@ inline uint32_t tag_lane(uint32_t c, int lane) {
 }
 
 // text_tile[q]: query tile q runs as a HALVES entry candidate (empty: none)
-PairSet build_pair_set(const TileSet& ts, int64_t nqt, const std::vector<uint8_t>& text_tile) {
+PairSet build_pair_set(const TileSet& ts, int64_t nqt, const std::vector<uint8_t>& text_tile, int64_t ratio) {
     PairSet ps;
     ps.row_ptr.push_back(0);
     ps.words.reserve(ts.cols.size());
@@ -452,7 +452,7 @@ PairSet build_pair_set(const TileSet& ts, int64_t nqt, const std::vector<uint8_t
             ++n_other;
         }
     }
-    const bool halve = n_other > 0 && text_len * n_other > 5 * other_len;
+    const bool halve = n_other > 0 && text_len * n_other > ratio * other_len;
     int64_t pending = -1;  // the other tiles pair up in order
     for (int64_t q = 0; q < nqt; ++q) {
         if (halve && text_tile[q] && ts.row_ptr[q + 1] - ts.row_ptr[q] >= 2) {
@@ -487,13 +487,13 @@ std::unique_ptr<DevPlan> schedule_items(int device, std::vector<Cand>& cands, co
 std::unique_ptr<DevPlan> build_dev_plan(int device, int64_t batch, int64_t H, int64_t n, int64_t B,
                                         const std::vector<std::vector<uint8_t>>& masks,
                                         const std::vector<HeadJob>& jobs, const std::vector<int>& ref_jobs,
-                                        int64_t text_lo, int64_t text_hi, bool halves, cudaStream_t stream) {
+                                        int64_t text_lo, int64_t text_hi, int64_t halve_ratio, cudaStream_t stream) {
     const int64_t nqt = ceil_div(n, dfa2k::TILE_M);
     const int64_t np = (nqt + 1) / 2;  // copy items: pairs (2p, 2p+1)
     // text query tiles as HALVES entries (d = 64; not under split-KV, which
     // chunks the long rows its own way)
     std::vector<uint8_t> text_tile;
-    if (halves && !split_kv_enabled() && text_hi > text_lo) {
+    if (halve_ratio > 0 && !split_kv_enabled() && text_hi > text_lo) {
         text_tile.assign(static_cast<size_t>(nqt), 0);
         for (int64_t q = 0; q < nqt; ++q) {
             const int64_t r0 = q * dfa2k::TILE_M, r1 = std::min(r0 + dfa2k::TILE_M, n);
@@ -505,7 +505,7 @@ std::unique_ptr<DevPlan> build_dev_plan(int device, int64_t batch, int64_t H, in
     std::vector<int64_t> mask_tile_base, mask_off;
     std::vector<PairSet> sets;
     for (const auto& m : masks) {
-        sets.push_back(build_pair_set(build_tile_set(m.data(), n, B), nqt, text_tile));
+        sets.push_back(build_pair_set(build_tile_set(m.data(), n, B), nqt, text_tile, halve_ratio));
         mask_tile_base.push_back(static_cast<int64_t>(tiles.size()));
         tiles.insert(tiles.end(), sets.back().words.begin(), sets.back().words.end());
         mask_off.push_back(static_cast<int64_t>(mask_bytes.size()));
@@ -963,6 +963,16 @@ void run_forward(const ForwardSpec& s, cudaStream_t stream) {
         run_padded(s, stream);
 }
 
+// Text rows run on both lanes when their key chains exceed this many times
+// the mask's average chain (0: never): d = 64 from 5x.
+int64_t halve_ratio(int64_t d) {
+    static const int64_t r128 = [] {
+        const char* e = std::getenv("DFA2_HALVES128");
+        return e ? std::atoll(e) : 0;
+    }();
+    return kernel_dim(d) == 64 ? 5 : r128;
+}
+
 void launch_forward(const ForwardSpec& s, cudaStream_t stream) {
     const int64_t n = seq_len(s.dims), d = s.dims->head_dim, H = s.dims->n_heads;
     if (s.batch < 1)
@@ -1011,7 +1021,7 @@ void launch_forward(const ForwardSpec& s, cudaStream_t stream) {
                 masks = &built;
             }
             plan = plan_insert(key, build_dev_plan(device, s.batch, H, n, s.block, *masks, s.jobs, s.ref_jobs,
-                                                   text_begin(s.dims), text_end(s.dims), kernel_dim(d) == 64,
+                                                   text_begin(s.dims), text_end(s.dims), halve_ratio(d),
                                                    stream));
         }
     }
