@@ -709,7 +709,7 @@ def test_async_influence_matches_sync_and_window_limit_falls_back():
     assert np.isfinite(li.influence).all()
 
 
-@pytest.mark.parametrize("seed", range(24))
+@pytest.mark.parametrize("seed", range(48))
 def test_random_plans_and_geometries_against_oracle(seed):
     """Seeded random layers: geometry (visual/text tokens, token order, mask
     block, head dim), a random F / A(w) / C plan with slots filled at t = 0,
