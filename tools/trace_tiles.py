@@ -51,5 +51,8 @@ for L in range(2):
         # 6 = K(j) ready (before S(j) issue), 5 = S(j) issued
         extra += (f"\n   MMA warp: V ready->P seen {med(x[:, 3] - x[:, 7]):.0f}  "
                   f"PV(j-1) issued->K(j) ready {med(x[1:, 6] - x[:-1, 4]):.0f}  K ready->S issued {med(x[:, 5] - x[:, 6]):.0f}")
+    if os.environ.get("DFA2_TRACE_PCT"):
+        pct = lambda a: "/".join(f"{np.percentile(a, p_):.0f}" for p_ in (50, 90, 99))
+        extra += f"\n   p50/p90/p99: wait_S {pct(wait)}  softmax {pct(soft)}  period {pct(period)}  total {x[-1, 2] - x[0, 0]:.0f} clk"
     print(f"lane {L}: tiles {n}  period {med(period):.0f}  softmax {med(soft):.0f}  wait_S {med(wait):.0f}  "
           f"P->MMA {med(pseen):.0f}" + extra)
