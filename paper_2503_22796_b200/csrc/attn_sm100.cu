@@ -43,6 +43,9 @@ namespace dfa2k {
 #ifndef DFA2_SPLIT_MMA64
 #define DFA2_SPLIT_MMA64 1
 #endif
+#ifndef DFA2_SPLIT_MMA128
+#define DFA2_SPLIT_MMA128 0
+#endif
 
 template <int D>
 struct Cfg {
@@ -72,7 +75,7 @@ struct Cfg {
     static constexpr bool SEP_P = D == 64 && DFA2_SEP_P64;
     // With P separate, each lane gets its own MMA-issuing warp (warp 1 lane
     // A, warp 3 lane B): a lane's S and PV then wait only on that lane.
-    static constexpr bool SPLIT_MMA = SEP_P && DFA2_SPLIT_MMA64;
+    static constexpr bool SPLIT_MMA = (SEP_P && DFA2_SPLIT_MMA64) || (D == 128 && DFA2_SPLIT_MMA128);
     static constexpr int NBARS = 2 * QBUF + 2 * KSTAGES + 2 * VSTAGES + 14;
     // The dynamic window starts 1024-aligned (the 1 KB system reservation
     // precedes it); the kernel traps otherwise, so no alignment slack.
@@ -548,9 +551,10 @@ __global__ void __launch_bounds__(384, 1)
                 const uint32_t word = u < U ? args.tiles[w.tile_begin + u] : 0u;
                 const int vst = vcount % VS;
                 const int kst = kcount % KS;
+                auto do_s = [&] {
                 if (u < U) {
                     if (word & need) {
-                        if (scount >= 1) {  // the lane's softmax has read its previous S
+                        if (C::SEP_P && scount >= 1) {  // the lane's softmax has read its previous S
                             mbar_wait(s_free(L), (scount - 1) & 1);
                         }
                         mbar_wait(k_full(kst), (kcount / KS) & 1);
@@ -587,6 +591,8 @@ __global__ void __launch_bounds__(384, 1)
                         __syncwarp();
                     }
                 }
+                };
+                auto do_pv = [&] {
                 if (u >= 1) {
                     if (prev & need) {
                         mbar_wait(v_full(vst), (vcount / VS) & 1);
@@ -609,7 +615,8 @@ __global__ void __launch_bounds__(384, 1)
                                             IDESC_O, 1u);
                             if (prev & snapb)
                                 mma_commit(o_full(L));
-                            mma_commit(p_free(L));
+                            if (C::SEP_P)
+                                mma_commit(p_free(L));
                             mma_commit(v_empty(vst));
                         }
                         __syncwarp();
@@ -621,6 +628,14 @@ __global__ void __launch_bounds__(384, 1)
                             mbar_arrive(v_empty(vst));
                         __syncwarp();
                     }
+                }
+                };
+                if (C::SEP_P) {  // S_L(u) first: it waits only for the softmax to have read S_L(u-1)
+                    do_s();
+                    do_pv();
+                } else {  // P over S: the PV that reads P_L(u-1) goes first
+                    do_pv();
+                    do_s();
                 }
                 if (u >= 1)
                     ++vcount;
