@@ -12,6 +12,7 @@ from paper_2503_22796_b200 import api
 ap = argparse.ArgumentParser()
 ap.add_argument("--sd3", action="store_true")
 ap.add_argument("--steps", type=int, default=20)
+ap.add_argument("--out", default="")
 a = ap.parse_args()
 H, NV, NT, D, B = (24, 4096, 333, 64, 128) if a.sd3 else (24, 16384, 512, 128, 128)
 N = NV + NT
@@ -32,6 +33,7 @@ plans = {
     "all_C": " ".join(["C"] * H),
 }
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+rows = []
 for name, p in plans.items():
     lp = api.LayerPlan.parse(p)
     fl = api.plan_flops(lp, dims, B)
@@ -50,3 +52,9 @@ for name, p in plans.items():
         ms = e0.elapsed_time(e1) / a.steps
         print(f"{name:11s} commit={int(use_cache)} {ms:8.4f} ms  computed {fl / ms / 1e9:7.1f} TF  "
               f"(plan {fl / 1e9:7.1f} GFLOP)")
+        rows.append({"plan": name, "commit": use_cache, "ms": ms, "plan_gflop": fl / 1e9,
+                     "computed_tflops": fl / ms / 1e9})
+if a.out:
+    import json
+
+    json.dump({"shape": "SD3" if a.sd3 else "FLUX 2K", "rows": rows}, open(a.out, "w"), indent=1)
