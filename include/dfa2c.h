@@ -183,6 +183,20 @@ int dfa2c_dense_attention_forward(const void* q, const void* k, const void* v, v
                                   int64_t n_heads, int64_t seq_len, int64_t head_dim,
                                   void* stream);
 
+/* attention_reference (inc/tensor.hpp:86-93; src/tensor.cpp:73-114, 268-295):
+ * the reference's ground-truth masked attention at the CALLER's precision —
+ * dtype DFA2C_F32 or DFA2C_F64, q/k/v/out device [n_heads, N, d] of that
+ * type, computed in that type by a SIMT kernel (no bf16, no tensor cores):
+ * scores, row max, exp, row sum, out = sum_j (w_j / sum) v_j. An independent
+ * checker for the bf16 path (run_bench's oracle gate, cmd_verify); results
+ * agree with the reference's sequential loops to rounding (~1e-6 relative in
+ * f32). active (host nb*nb bytes, nb = ceil(N/block)) may be NULL (no mask);
+ * an empty mask row -> DFA2C_FULLY_MASKED before any compute. head_dim <= 512.
+ * Asynchronous on `stream` (synchronises when a mask is given). */
+int dfa2c_attention_reference(const void* q, const void* k, const void* v, void* out, int32_t dtype,
+                              int64_t n_heads, int64_t seq_len, int64_t head_dim, const uint8_t* active,
+                              int64_t block, void* stream);
+
 /* ---- calibration RSE query ---------------------------------------------
  * rse (inc/calibrate.hpp:18-20; src/calibrate.cpp:18-87) for `n_heads`
  * contiguous heads of `numel` elements each (y_m, y_o device, dtype

@@ -127,6 +127,8 @@ _SIGS = {
                                                  c_int64, POINTER(c_uint8), c_int64, c_void_p]),
     "dfa2c_dense_attention_forward": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int64,
                                                 c_int64, c_void_p]),
+    "dfa2c_attention_reference": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_int32, c_int64, c_int64,
+                                            c_int64, POINTER(c_uint8), c_int64, c_void_p]),
     "dfa2c_rse": (c_int32, [c_void_p, c_void_p, c_int32, c_int64, c_int64, c_int32, POINTER(c_double),
                             c_void_p]),
     "dfa2c_rse_async": (c_int32, [c_void_p, c_void_p, c_int32, c_int64, c_int64, c_int32, c_void_p,

@@ -280,6 +280,24 @@ def _as_bf16_cuda(x, name: str):
 
 
 # --------------------------------------------------------------- cache
+def _device_out(out, like, shape_given, name="out"):
+    """Validates a caller-supplied device output buffer (CUDA, bf16,
+    contiguous, on q's device, shaped like the caller's q) and returns a view
+    with `like`'s (4-D) shape; None -> a fresh buffer."""
+    torch = _torch()
+    if out is None:
+        return torch.empty_like(like)
+    if not isinstance(out, torch.Tensor) or not out.is_cuda or out.dtype != torch.bfloat16:
+        raise ShapeError(f"{name} must be a CUDA bf16 tensor")
+    if not out.is_contiguous():
+        raise ShapeError(f"{name} must be contiguous")
+    if out.device != like.device:
+        raise ShapeError(f"{name} must be on q's device")
+    if tuple(out.shape) != tuple(shape_given):
+        raise ShapeError(f"{name} must have q's shape {tuple(shape_given)} (got {tuple(out.shape)})")
+    return out.view(like.shape)
+
+
 class HeadCache:
     """HeadCache (inc/cache.hpp:15-32), device resident.
 
@@ -398,7 +416,6 @@ def multi_strategy_attention(q, k, v, plan: LayerPlan, cache: Optional[HeadCache
     of the layer this call leaves alone (DFA2C_SKIP; e.g. the heads another
     GPU owns); their output rows are not written.
     """
-    torch = _torch()
     q = _as_bf16_cuda(q, "q")
     k = _as_bf16_cuda(k, "k")
     v = _as_bf16_cuda(v, "v")
@@ -411,15 +428,17 @@ def multi_strategy_attention(q, k, v, plan: LayerPlan, cache: Optional[HeadCache
         raise ShapeError("tensor shape disagrees with dims")
     if plan.n_heads() != dims.n_heads:
         raise ShapeError("plan must assign exactly one strategy per head")
-    if out is None:
-        out = torch.empty_like(q)
+    given = out
+    out4 = _device_out(out, q, q.shape[1:] if squeeze else q.shape)
     d = dims.c()
     kinds, wins = _plan_kinds(plan, skip_heads)
     check(lib().dfa2c_mha_forward(c_void_p(q.data_ptr()), c_void_p(k.data_ptr()), c_void_p(v.data_ptr()),
                                   q.shape[0], byref(d), block_size, kinds, wins,
                                   cache.handle if cache is not None else None, layer, t,
-                                  c_void_p(out.data_ptr()), c_void_p(_stream_ptr(stream))))
-    return out[0] if squeeze else out
+                                  c_void_p(out4.data_ptr()), c_void_p(_stream_ptr(stream))))
+    if given is not None:
+        return given  # the caller's buffer, in the caller's shape
+    return out4[0] if squeeze else out4
 
 
 def multi_strategy_attention_host(q, k, v, plan: LayerPlan, cache: Optional[HeadCache], layer: int, t: int,
@@ -469,8 +488,7 @@ def sparse_attention_forward(q, k, v, mask: BlockMask, out=None, stream=None):
     heads = 1 if q.dim() == 2 else q.shape[0]
     if mask.seq_len != n:
         raise ShapeError("mask sequence length disagrees with tensors")
-    if out is None:
-        out = torch.empty_like(q)
+    out = _device_out(out, q, q.shape)
     a = np.ascontiguousarray(mask.active, dtype=np.uint8)
     check(lib().dfa2c_sparse_attention_forward(
         c_void_p(q.data_ptr()), c_void_p(k.data_ptr()), c_void_p(v.data_ptr()), c_void_p(out.data_ptr()),
@@ -484,13 +502,46 @@ def dense_tiled_attention(q, k, v, out=None, stream=None):
     q = _as_bf16_cuda(q, "q")
     k = _as_bf16_cuda(k, "k")
     v = _as_bf16_cuda(v, "v")
+    if q.shape != k.shape or q.shape != v.shape or q.dim() not in (2, 3):
+        raise ShapeError("dense attention expects per-head [N, d] tensors")
     n, d = q.shape[-2], q.shape[-1]
     heads = 1 if q.dim() == 2 else q.shape[0]
-    if out is None:
-        out = torch.empty_like(q)
+    out = _device_out(out, q, q.shape)
     check(lib().dfa2c_dense_attention_forward(c_void_p(q.data_ptr()), c_void_p(k.data_ptr()),
                                               c_void_p(v.data_ptr()), c_void_p(out.data_ptr()), heads, n, d,
                                               c_void_p(_stream_ptr(stream))))
+    return out
+
+
+def attention_reference(q, k, v, mask: Optional[BlockMask] = None, stream=None):
+    """attention_reference (inc/tensor.hpp:86-93; src/tensor.cpp:73-114,
+    268-295) at the operands' own precision: q/k/v CUDA float32 or float64
+    [H, N, d] (or [N, d]); computed in that type by the SIMT reference kernel
+    (dfa2c_attention_reference), never through the bf16 path. The drop-in's
+    independent f32/f64 checker; agrees with the reference's sequential loops
+    to rounding."""
+    torch = _torch()
+    if q.dtype not in (torch.float32, torch.float64):
+        raise ShapeError("attention_reference computes in float32 or float64")
+    for name, x in (("q", q), ("k", k), ("v", v)):
+        if not isinstance(x, torch.Tensor) or not x.is_cuda or x.dtype != q.dtype:
+            raise ShapeError(f"{name} must be a CUDA tensor of q's dtype")
+    if q.shape != k.shape or q.shape != v.shape or q.dim() not in (2, 3):
+        raise ShapeError("attention expects [H, N, d] tensors")
+    q, k, v = q.contiguous(), k.contiguous(), v.contiguous()
+    n, d = q.shape[-2], q.shape[-1]
+    heads = 1 if q.dim() == 2 else q.shape[0]
+    out = torch.empty_like(q)
+    a = None
+    if mask is not None:
+        if mask.seq_len != n:
+            raise ShapeError("mask sequence length disagrees with tensors")
+        a = np.ascontiguousarray(mask.active, dtype=np.uint8)
+    check(lib().dfa2c_attention_reference(
+        c_void_p(q.data_ptr()), c_void_p(k.data_ptr()), c_void_p(v.data_ptr()), c_void_p(out.data_ptr()),
+        2 if q.dtype == torch.float64 else 1, heads, n, d,
+        a.ctypes.data_as(POINTER(c_uint8)) if a is not None else None, mask.block_size if mask is not None else 0,
+        c_void_p(_stream_ptr(stream))))
     return out
 
 

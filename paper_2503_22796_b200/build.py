@@ -20,7 +20,7 @@ LIB = os.path.join(HERE, "libdfa2_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
-CU_SOURCES = ["attn_sm100.cu", "rse_sm100.cu", "convert_sm100.cu"]
+CU_SOURCES = ["attn_sm100.cu", "rse_sm100.cu", "convert_sm100.cu", "reference_sm100.cu"]
 CPP_SOURCES = ["dfa2c.cpp", "json_lite.cpp", "plansolver.cpp"]
 
 

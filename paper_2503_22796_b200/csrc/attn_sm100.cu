@@ -919,7 +919,11 @@ __global__ void __launch_bounds__(384, 1)
                 float* xch = reinterpret_cast<float*>(smem + C::XCHG_OFF);
                 xch[(L * 2 + 0) * TILE_M + r] = m_ref;
                 xch[(L * 2 + 1) * TILE_M + r] = l;
+                // the other lane's O completed on ITS o_full barrier: order our
+                // cross-lane TMEM reads after it through the thread sync
+                tc_fence_before();
                 named_bar_sync(3, 256);
+                tc_fence_after();
                 const float mo = xch[((1 - L) * 2 + 0) * TILE_M + r], lo_ = xch[((1 - L) * 2 + 1) * TILE_M + r];
                 const float mA = L ? mo : m_ref, lA = L ? lo_ : l, mB = L ? m_ref : mo, lB = L ? l : lo_;
                 const float M = fmaxf(mA, mB);

@@ -39,6 +39,10 @@ cudaError_t launch_rse_multi(const void* const* ym, int M, const void* yo, int d
                              int64_t numel, int mode, double* out_dev, double* scratch, int nblk,
                              cudaStream_t stream);
 int rse_multi_max();
+int reference_max_head_dim();
+cudaError_t launch_attention_reference(const void* q, const void* k, const void* v, void* out, int dtype, int64_t H,
+                                       int64_t n, int64_t d, const uint8_t* mask, int64_t block, int64_t nb,
+                                       cudaStream_t stream);
 }  // namespace dfa2k
 
 using dfa2k::WorkItem;
@@ -202,11 +206,13 @@ void check_rows_nonempty(const uint8_t* m, int64_t nb) {
 
 // ------------------------------------------------------------ device plan
 // A work list on the device: one stream-ordered block from the library pool
-// holding the items, CTA ranges, tile words and masks. `used` is recorded
-// after every launch that reads it; on eviction the block is released on an
-// internal stream once that event has fired, so building or dropping a plan
-// never synchronises the device.
-void plan_release(int device, void* dev, cudaEvent_t used);
+// holding the items, CTA ranges, tile words and masks. Every launch that
+// reads it is fenced onto the device's retire stream (retire_after); on
+// eviction the block is freed on that stream, after the upload (`ready`) and
+// after every launch on any stream that was enqueued before the eviction, so
+// building or dropping a plan never synchronises the device.
+void plan_release(int device, void* dev, cudaEvent_t ready);
+void retire_after(int device, cudaStream_t stream);
 struct DevPlan {
     int grid = 0;
     int32_t n_groups = 0;  // split groups (counters per launch)
@@ -217,19 +223,15 @@ struct DevPlan {
     uint8_t* masks = nullptr;
     int32_t n_snap = 0;                                   // calibration plans: snapshots per query tile
     uint16_t snap_slots[dfa2k::MAX_SNAPS] = {};
+    std::vector<int64_t> shard_rows;                      // sharded plans: [world + 1] flattened row bounds
     int device = 0;
     void* dev = nullptr;
     size_t bytes = 0;
-    cudaEvent_t used = nullptr;
     cudaEvent_t ready = nullptr;  // the upload (on the building call's stream) has landed
-    ~DevPlan() {
-        plan_release(device, dev, used);
-        if (ready)
-            cudaEventDestroy(ready);
-    }
+    ~DevPlan() { plan_release(device, dev, ready); }
     // a launch on any stream first orders itself after the upload
     void acquire(cudaStream_t stream) const { DFA2C_CUDA_CHECK(cudaStreamWaitEvent(stream, ready, 0)); }
-    void release(cudaStream_t stream) const { DFA2C_CUDA_CHECK(cudaEventRecord(used, stream)); }
+    void release(cudaStream_t stream) const { retire_after(device, stream); }
 };
 
 // Head strategy for the scheduler: mask_id >= 0 => computed over that mask;
@@ -304,7 +306,6 @@ struct PlanStaging {
 };
 std::mutex g_staging_mu;
 std::map<int, PlanStaging> g_staging;
-std::map<int, cudaStream_t> g_free_streams;
 
 template <class Fill>
 void plan_upload(int device, cudaStream_t stream, void* dst, size_t bytes, Fill&& fill) {
@@ -334,30 +335,54 @@ void plan_upload(int device, cudaStream_t stream, void* dst, size_t bytes, Fill&
     DFA2C_CUDA_CHECK(cudaEventRecord(ps.ev[i], stream));
 }
 
-void plan_release(int device, void* dev, cudaEvent_t used) {
-    if (!dev && !used)
+// Per device: the retire stream (frees of evicted plans) and one event used
+// to fence launches onto it. cudaStreamWaitEvent captures the event's state
+// at the call, so the event can be re-recorded by the next launch at once.
+struct Retire {
+    std::mutex mu;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev = nullptr;
+};
+Retire& retire_of(int device) {
+    static std::mutex mu;
+    static std::map<int, std::unique_ptr<Retire>> m;
+    std::lock_guard<std::mutex> lk(mu);
+    auto& r = m[device];
+    if (!r) {
+        r = std::make_unique<Retire>();
+        int cur = 0;
+        cudaGetDevice(&cur);
+        cudaSetDevice(device);
+        DFA2C_CUDA_CHECK(cudaStreamCreateWithFlags(&r->stream, cudaStreamNonBlocking));
+        DFA2C_CUDA_CHECK(cudaEventCreateWithFlags(&r->ev, cudaEventDisableTiming));
+        cudaSetDevice(cur);
+    }
+    return *r;
+}
+
+void retire_after(int device, cudaStream_t stream) {
+    Retire& r = retire_of(device);
+    std::lock_guard<std::mutex> lk(r.mu);
+    DFA2C_CUDA_CHECK(cudaEventRecord(r.ev, stream));
+    DFA2C_CUDA_CHECK(cudaStreamWaitEvent(r.stream, r.ev, 0));
+}
+
+void plan_release(int device, void* dev, cudaEvent_t ready) {
+    if (!dev && !ready)
         return;
     int cur = 0;
     cudaGetDevice(&cur);
     cudaSetDevice(device);
-    cudaStream_t fs;
+    Retire& r = retire_of(device);
     {
-        std::lock_guard<std::mutex> lk(g_staging_mu);
-        auto it = g_free_streams.find(device);
-        if (it == g_free_streams.end()) {
-            cudaStream_t s_ = nullptr;
-            cudaStreamCreateWithFlags(&s_, cudaStreamNonBlocking);
-            it = g_free_streams.emplace(device, s_).first;
-        }
-        fs = it->second;
+        std::lock_guard<std::mutex> lk(r.mu);
+        if (ready)
+            cudaStreamWaitEvent(r.stream, ready, 0);  // the upload itself (a plan never launched)
+        if (dev)
+            cudaFreeAsync(dev, r.stream);  // after every launch fenced so far, on any stream
     }
-    if (dev) {
-        if (used)
-            cudaStreamWaitEvent(fs, used, 0);  // every launch that read the plan
-        cudaFreeAsync(dev, fs);
-    }
-    if (used)
-        cudaEventDestroy(used);
+    if (ready)
+        cudaEventDestroy(ready);
     cudaSetDevice(cur);
 }
 
@@ -669,7 +694,6 @@ std::unique_ptr<DevPlan> schedule_items(int device, std::vector<Cand>& cands, co
     const size_t o_tiles = up(o_cta + n_cta), n_tiles = tiles.size() * sizeof(uint32_t);
     const size_t o_masks = up(o_tiles + n_tiles), n_masks = mask_bytes.size();
     p->bytes = up(o_masks + n_masks);
-    DFA2C_CUDA_CHECK(cudaEventCreateWithFlags(&p->used, cudaEventDisableTiming));
     scratch_alloc(&p->dev, p->bytes, stream);
     char* d = static_cast<char*>(p->dev);
     p->items = reinterpret_cast<WorkItem*>(d + o_items);
@@ -1802,6 +1826,42 @@ int dfa2c_dense_attention_forward(const void* q, const void* k, const void* v, v
         s.cache = nullptr;
         plan_jobs(&dims, 128, kinds.data(), nullptr, false, s);
         run_forward(s, as_stream(stream));
+    });
+}
+
+int dfa2c_attention_reference(const void* q, const void* k, const void* v, void* out, int32_t dtype,
+                              int64_t n_heads, int64_t n, int64_t d, const uint8_t* active, int64_t block,
+                              void* stream) {
+    return guard([&] {
+        if (!q || !k || !v || !out)
+            fail(DFA2C_SHAPE, "attention_reference operands must not be NULL");
+        if (dtype != DFA2C_F32 && dtype != DFA2C_F64)
+            fail(DFA2C_SHAPE, "attention_reference computes in f32 or f64");
+        if (n_heads < 1 || n < 1 || d < 1)
+            fail(DFA2C_SHAPE, "attention needs heads, seq_len, head_dim >= 1");
+        if (d > dfa2k::reference_max_head_dim())
+            fail(DFA2C_UNSUPPORTED, "attention_reference supports head_dim <= " +
+                                        std::to_string(dfa2k::reference_max_head_dim()));
+        if (n_heads > 65535 || n > (int64_t{1} << 30))
+            fail(DFA2C_UNSUPPORTED, "attention_reference problem too large");
+        const cudaStream_t st = as_stream(stream);
+        uint8_t* dmask = nullptr;
+        int64_t nb = 1;
+        if (active) {
+            if (block < 1)
+                fail(DFA2C_SHAPE, "block_size must be >= 1");
+            nb = ceil_div(n, block);
+            check_rows_nonempty(active, nb);  // FullyMaskedRowError before any compute (tensor.cpp:97-99)
+            scratch_alloc(&dmask, static_cast<size_t>(nb * nb), st);
+            DFA2C_CUDA_CHECK(cudaMemcpyAsync(dmask, active, static_cast<size_t>(nb * nb), cudaMemcpyHostToDevice, st));
+        }
+        DFA2C_CUDA_CHECK(dfa2k::launch_attention_reference(q, k, v, out, dtype, n_heads, n, d, dmask,
+                                                           active ? block : n, nb, st));
+        g_launches.fetch_add(1);
+        if (dmask) {
+            DFA2C_CUDA_CHECK(cudaFreeAsync(dmask, st));
+            DFA2C_CUDA_CHECK(cudaStreamSynchronize(st));  // the host mask bytes may be freed on return
+        }
     });
 }
 

@@ -665,6 +665,23 @@ DFA2_API void dense_tiled_attention(const float* q, const float* k, const float*
     sparse_heads(q, k, v, out, 1, n, d, nullptr);
 }
 
+namespace {
+// the reference's ground truth at the operands' own precision (SIMT kernel)
+void reference_heads(const void* q, const void* k, const void* v, void* out, bool f64, int64_t heads, int64_t n,
+                     int64_t d, const BlockMask* mask) {
+    if (mask && mask->seq_len != n)
+        throw ShapeError("mask sequence length disagrees with tensors");
+    const size_t bytes = static_cast<size_t>(heads * n * d) * (f64 ? 8 : 4);
+    DevBuf dq(bytes), dk(bytes), dv(bytes), dout(bytes);
+    cuda_check(cudaMemcpy(dq.p, q, bytes, cudaMemcpyHostToDevice), "attention_reference upload");
+    cuda_check(cudaMemcpy(dk.p, k, bytes, cudaMemcpyHostToDevice), "attention_reference upload");
+    cuda_check(cudaMemcpy(dv.p, v, bytes, cudaMemcpyHostToDevice), "attention_reference upload");
+    check(dfa2c_attention_reference(dq.p, dk.p, dv.p, dout.p, f64 ? DFA2C_F64 : DFA2C_F32, heads, n, d,
+                                    mask ? mask->active.data() : nullptr, mask ? mask->block_size : 0, nullptr));
+    cuda_check(cudaMemcpy(out, dout.p, bytes, cudaMemcpyDeviceToHost), "attention_reference download");
+}
+}  // namespace
+
 DFA2_API Tensor attention_reference(const Tensor& q, const Tensor& k, const Tensor& v, const BlockMask* mask) {
     if (q.ndim() != 3 || k.ndim() != 3 || v.ndim() != 3)
         throw ShapeError("attention expects [H, N, d] tensors");
@@ -672,23 +689,76 @@ DFA2_API Tensor attention_reference(const Tensor& q, const Tensor& k, const Tens
         throw ShapeError("q/k/v shapes disagree");
     if (q.dtype() != k.dtype() || q.dtype() != v.dtype())
         throw ShapeError("q/k/v dtypes disagree");
+    if (mask && mask->seq_len != q.dim(1))
+        throw ShapeError("mask sequence length disagrees with tensors");
     q.check_finite("attention q");
     k.check_finite("attention k");
     v.check_finite("attention v");
-    const std::vector<float> qf = as_f32(q), kf = as_f32(k), vf = as_f32(v);
-    std::vector<float> of(qf.size());
-    sparse_heads(qf.data(), kf.data(), vf.data(), of.data(), q.dim(0), q.dim(1), q.dim(2), mask);
-    Tensor out = Tensor::from_f32(q.shape(), std::move(of));
-    return q.dtype() == Dtype::f64 ? out.to_f64() : out;
+    const bool f64 = q.dtype() == Dtype::f64;
+    Tensor out = Tensor::zeros(q.shape(), q.dtype());
+    if (f64)
+        reference_heads(q.f64(), k.f64(), v.f64(), out.f64(), true, q.dim(0), q.dim(1), q.dim(2), mask);
+    else
+        reference_heads(q.f32(), k.f32(), v.f32(), out.f32(), false, q.dim(0), q.dim(1), q.dim(2), mask);
+    out.check_finite("attention result");
+    return out;
+}
+
+DFA2_API void attention_reference_head_f32(const float* q, const float* k, const float* v, float* out, int64_t n,
+                                           int64_t d, const BlockMask* mask) {
+    reference_heads(q, k, v, out, false, 1, n, d, mask);
 }
 
 // ---------------------------------------------------------------- cache
-DFA2_API HeadCache::~HeadCache() {
+DFA2_API HeadCache::~HeadCache() { release_device(); }
+
+void HeadCache::release_device() {
     if (dev_)
         dfa2c_cache_destroy(dev_);
+    dev_ = nullptr;
+    heads_ = n_ = d_ = layers_ = 0;
 }
 
-DFA2_API dfa2c_cache* HeadCache::bind(int64_t n_heads, int64_t n, int64_t d) {
+DFA2_API HeadCache::HeadCache(const HeadCache& other) { *this = other; }
+
+DFA2_API HeadCache& HeadCache::operator=(const HeadCache& other) {
+    if (this == &other)
+        return *this;
+    // deep copy: every entry as a host f32 tensor (device-only slots read
+    // back first), uploaded to this cache's own slots on first GPU use
+    std::map<std::pair<int64_t, int64_t>, Slot> copy;
+    for (const auto& kv : other.slots_) {
+        Slot s;
+        s.produced_at = kv.second.produced_at;
+        s.host = other.fetch(kv.first.first, kv.first.second);
+        s.host_fresh = true;
+        s.on_device = false;
+        copy.emplace(kv.first, std::move(s));
+    }
+    release_device();
+    slots_ = std::move(copy);
+    return *this;
+}
+
+DFA2_API HeadCache::HeadCache(HeadCache&& other) noexcept { *this = std::move(other); }
+
+DFA2_API HeadCache& HeadCache::operator=(HeadCache&& other) noexcept {
+    if (this == &other)
+        return *this;
+    release_device();
+    slots_ = std::move(other.slots_);
+    other.slots_.clear();
+    dev_ = other.dev_;
+    heads_ = other.heads_;
+    n_ = other.n_;
+    d_ = other.d_;
+    layers_ = other.layers_;
+    other.dev_ = nullptr;
+    other.heads_ = other.n_ = other.d_ = other.layers_ = 0;
+    return *this;
+}
+
+DFA2_API dfa2c_cache* HeadCache::bind(int64_t n_heads, int64_t n, int64_t d) const {
     if (dev_) {
         if (n_heads != heads_ || n != n_ || d != d_)
             throw ShapeError("cached output shape disagrees with dims");
@@ -733,7 +803,7 @@ DFA2_API void HeadCache::store(int64_t layer, int64_t head, Tensor output, int64
         bind(heads_, n_, d_);  // upload now (bf16 slot)
 }
 
-DFA2_API const HeadCache::Slot& HeadCache::slot(int64_t layer, int64_t head) const {
+DFA2_API HeadCache::Slot& HeadCache::slot(int64_t layer, int64_t head) const {
     const auto it = slots_.find({layer, head});
     if (it == slots_.end())
         throw CacheMissError("no cached output for layer " + std::to_string(layer) + ", head " + std::to_string(head));
@@ -741,7 +811,7 @@ DFA2_API const HeadCache::Slot& HeadCache::slot(int64_t layer, int64_t head) con
 }
 
 DFA2_API const Tensor& HeadCache::fetch(int64_t layer, int64_t head) const {
-    const Slot& s = slot(layer, head);
+    Slot& s = slot(layer, head);
     if (!s.host_fresh) {
         DevBuf tmp(static_cast<size_t>(n_ * d_) * 2);
         check(dfa2c_cache_fetch(dev_, layer, head, tmp.p, nullptr));
@@ -902,7 +972,7 @@ DFA2_API std::vector<MethodCandidate> make_candidates(const std::vector<int64_t>
 }
 
 DFA2_API LayerInfluence influence_for_layer(const Tensor& q, const Tensor& k, const Tensor& v,
-                                            const std::vector<MethodCandidate>& methods, HeadCache& cache,
+                                            const std::vector<MethodCandidate>& methods, const HeadCache& cache,
                                             int64_t layer, int64_t t, const AttentionDims& dims, int64_t block_size,
                                             RseMode mode, CalibrationStats* stats) {
     if (methods.empty())

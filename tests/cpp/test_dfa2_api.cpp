@@ -188,6 +188,21 @@ TEST(cache_host_semantics, false) {  // test_cache.cpp
     CHECK_THROWS_AS(make_candidates({}, false), ShapeError);
 }
 
+TEST(cache_is_a_copyable_value_type, false) {  // reference cache.hpp:15-32 (implicit copy)
+    HeadCache c;
+    const Tensor a = gaussian({6, 4}, 2);
+    c.store(0, 1, a, 4);
+    HeadCache copy = c;  // deep copy
+    CHECK(copy.has(0, 1) && copy.produced_at(0, 1) == 4 && copy.fetch(0, 1) == a);
+    c.store(0, 1, gaussian({6, 4}, 3), 5);  // the copy does not alias the original
+    CHECK(copy.fetch(0, 1) == a && copy.produced_at(0, 1) == 4 && c.produced_at(0, 1) == 5);
+    HeadCache assigned;
+    assigned = copy;
+    CHECK(assigned.size() == 1 && assigned.fetch(0, 1) == a);
+    HeadCache moved = std::move(assigned);
+    CHECK(moved.size() == 1 && moved.fetch(0, 1) == a);
+}
+
 // ---------------------------------------------------------------- GPU
 TEST(mixed_plan_matches_per_head_oracles, true) {  // test_dispatch.cpp:63-88
     const AttentionDims d = dims_of(3, 64, 256, 44);
@@ -280,6 +295,50 @@ TEST(influence_for_layer_semantics, true) {  // test_calibrate.cpp:85-146
         CHECK(li.influence[h * 3 + 1] == 0.0);      // max window == Full bitwise
         CHECK(li.influence[h * 3 + 0] > 0.0);
     }
+}
+
+TEST(influence_takes_const_cache_and_copies_carry_device_slots, true) {  // calibrate.hpp:80-86
+    const AttentionDims d = dims_of(2, 64, 256, 32);
+    const int64_t n = d.seq_len();
+    const Tensor q = gaussian({2, n, 64}, 41), k = gaussian({2, n, 64}, 42), v = gaussian({2, n, 64}, 43);
+    HeadCache cache;
+    const Tensor out0 = multi_strategy_attention(q, k, v, LayerPlan::all_full(2), cache, 0, 0, d, 64);
+    const HeadCache& cref = cache;  // a const caller, as in the reference
+    const LayerInfluence li = influence_for_layer(q, k, v, make_candidates({0}, true), cref, 0, 1, d, 64,
+                                                  RseMode::standard, nullptr);
+    CHECK(std::isfinite(li.influence[1]) && std::isfinite(li.influence[3]));
+    HeadCache copy = cache;  // device-resident slots deep-copied through the host
+    CHECK(copy.fetch(0, 0) == head_slice(out0, 0) && copy.produced_at(0, 1) == 0);
+    const Tensor again = multi_strategy_attention(q, k, v, LayerPlan{{HeadStrategy::Cached(), HeadStrategy::Cached()}},
+                                                  copy, 0, 1, d, 64);
+    CHECK(again == out0);  // the copy's re-uploaded slots splice bit-exactly
+}
+
+TEST(attention_reference_is_f32_and_f64_accurate, true) {  // tensor.cpp:73-114, 268-295
+    const AttentionDims d = dims_of(2, 64, 200, 40);
+    const int64_t n = d.seq_len();
+    const Tensor q = gaussian({2, n, 64}, 51), k = gaussian({2, n, 64}, 52), v = gaussian({2, n, 64}, 53);
+    const BlockMask m = build_arrow_mask({d, 32, 1});
+    const Tensor r32 = attention_reference(q, k, v, &m);
+    const Tensor r64 = attention_reference(q.to_f64(), k.to_f64(), v.to_f64(), &m);
+    CHECK(r32.dtype() == Dtype::f32 && r64.dtype() == Dtype::f64);
+    for (int64_t h = 0; h < 2; ++h) {
+        const std::vector<double> want = oracle_head(head_slice(q, h).f32(), head_slice(k, h).f32(),
+                                                    head_slice(v, h).f32(), n, 64, &m);
+        const Tensor g32 = head_slice(r32, h), g64 = head_slice(r64, h);
+        double e32 = 0, e64 = 0, mx = 0;
+        for (size_t i = 0; i < want.size(); ++i) {
+            e32 = std::max(e32, std::abs(static_cast<double>(g32.f32()[i]) - want[i]));
+            e64 = std::max(e64, std::abs(g64.f64()[i] - want[i]));
+            mx = std::max(mx, std::abs(static_cast<double>(want[i])));
+        }
+        CHECK(e32 <= 1e-5 * mx);  // f32 precision, not bf16 (bf16 would be ~1e-3)
+        CHECK(e64 <= 1e-12 * mx);  // f64 to rounding
+    }
+    BlockMask bad = BlockMask::all_active(n, 32);
+    for (int64_t j = 0; j < bad.n_key_blocks; ++j)
+        bad.set(1, j, false);
+    CHECK_THROWS_AS(attention_reference(q, k, v, &bad), FullyMaskedRowError);
 }
 
 // dump-workload H d nv nt order L T B seed path: raw f32 q|k|v of every
