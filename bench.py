@@ -8,8 +8,14 @@ Workload (BASELINE.json configs[2]): one FLUX.1 2K joint-attention layer,
 paper's ~68% reduction plan "FLUX68" (6 Full, 8 Arrow(8), 4 Arrow(0),
 6 Cached) at t=1 with every cache slot filled at t=0.
 A step = one dfa2c_mha_forward call (ONE kernel launch) over one sample.
-With --gpus N (torchrun, one process per GPU) each rank runs its own sample
-(batch/sample sharding, no data-path collective): weak scaling.
+
+--gpus N: one process per GPU (this script re-launches itself under
+torch.distributed.run when WORLD_SIZE is unset). `value` is the batch-
+sharded layer (config 4's sharding: one FLUX sample per GPU, no data-path
+collective; weak scaling). The same line carries `row_sharded`: ONE sample
+split over the N GPUs by dfa2c_mha_forward_sharded (contiguous cost-
+balanced row ranges, one fused launch per rank, NCCL all-gather in place)
+— compute-only and compute + gather, strong scaling.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
 """
@@ -18,6 +24,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -33,20 +40,19 @@ H, NV, NT, D, BLOCK = 24, 16384, 512, 128, 128
 N = NV + NT
 PLAN = "F A8 C A0 F A8 C A8 F A8 C A0 F A8 C A0 F A8 C A8 F A8 C A0"
 CPU_SAMPLE_HEADS = list(range(H))  # the whole FLUX68 layer (6 F, 8 A8, 4 A0, 6 C): no extrapolation
+PARITY_MAX_REL, PARITY_MAX_RSE = 1e-2, 5e-5  # DESIGN.md §4, SURVEY.md §8c
 
 
 def dense_layer_flops() -> int:
     return H * 4 * D * N * N
 
 
-def config(extra=None):
-    c = {"workload": "FLUX.1 2K joint-attention layer (BASELINE configs[2])", "n_visual": NV, "n_text": NT,
-         "heads": H, "head_dim": D, "mask_block": BLOCK, "plan": "FLUX68: " + PLAN, "samples_per_gpu": 1,
-         "token_order": "visual_first",
-         "l2": "no flush; per-step inputs q/k/v/out = 415 MB > 126 MB L2"}
-    if extra:
-        c.update(extra)
-    return c
+def config():
+    """Identical for both arms (the driver compares them)."""
+    return {"workload": "FLUX.1 2K joint-attention layer (BASELINE configs[2])", "n_visual": NV, "n_text": NT,
+            "heads": H, "head_dim": D, "mask_block": BLOCK, "plan": "FLUX68: " + PLAN, "samples_per_gpu": 1,
+            "token_order": "visual_first",
+            "l2": "no flush; per-step inputs q/k/v/out = 415 MB > 126 MB L2"}
 
 
 def peaks():
@@ -112,11 +118,30 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def cpu_layer_sample(q, k, v, slots, threads=None, heads=None):
-    """The reference's own CPU kernels (oracle/_ref, compiled from
-    /root/reference sources) on heads CPU_SAMPLE_HEADS of the same layer:
-    Full -> dense_tiled_attention, Arrow(w) -> sparse_attention_forward,
-    Cached -> copy; DFA2_THREADS = all host cores. Returns (seconds, cores)."""
+def host_inputs(seed_base=0):
+    """The step's inputs, generated once on the host (seeded, bf16): q/k/v
+    [1, H, N, D] and the t=0 cache slots [H, N, D]. The GPU arm copies them
+    to HBM; the CPU legs read the same values widened to f32."""
+    import torch
+
+    g = torch.Generator().manual_seed(seed_base + 1)
+    q, k, v = (torch.randn(1, H, N, D, generator=g).to(torch.bfloat16) for _ in range(3))
+    slots = torch.randn(H, N, D, generator=g).to(torch.bfloat16)
+    return q, k, v, slots
+
+
+def as_f32_numpy(x):
+    import numpy as np
+
+    return np.ascontiguousarray(x.float().numpy().reshape(H, N, D))
+
+
+def cpu_layer(q, k, v, slots, threads=None, heads=None):
+    """The reference's own CPU kernels (oracle/_ref, compiled from the
+    unmodified /root/reference sources) over `heads` of the layer: Full ->
+    dense_tiled_attention, Arrow(w) -> sparse_attention_forward (both
+    parallel over query blocks), Cached -> copy; DFA2_THREADS = all host
+    cores. q/k/v/slots: f32 numpy [H, N, D]. Returns (seconds, cores, out)."""
     import numpy as np
 
     import oracle
@@ -136,25 +161,33 @@ def cpu_layer_sample(q, k, v, slots, threads=None, heads=None):
                                                    ptr(slots, c_float), ptr(out, c_float), H, D, NV, NT, 0, BLOCK,
                                                    ptr(kinds, c_int32), ptr(wins, c_int64), ptr(heads, c_int64),
                                                    len(heads)))
-    return time.perf_counter() - t0, cores
+    return time.perf_counter() - t0, cores, out
 
 
-def host_sample_inputs(seed_base=0):
-    """bf16-rounded f32 copies of the bench inputs for the CPU sample (only
-    the sampled heads are materialised; others stay zero and are not read)."""
+def parity(gpu_out, ref_out):
+    """Whole-layer parity of the GPU output against the reference CPU layer
+    on the same inputs: per head max|gpu-ref|/max|ref| and RSE (the
+    reference's rse, src/calibrate.cpp:18-87, in f64); Cached heads bitwise."""
     import numpy as np
-    import torch
 
-    def gen(seed, heads):
-        g = torch.Generator().manual_seed(seed)
-        x = torch.zeros(H, N, D, dtype=torch.float32)
-        full = torch.randn(len(heads), N, D, generator=g).to(torch.bfloat16).float()
-        for i, h in enumerate(heads):
-            x[h] = full[i]
-        return np.ascontiguousarray(x.numpy())
-
-    hs = CPU_SAMPLE_HEADS
-    return gen(seed_base + 1, hs), gen(seed_base + 2, hs), gen(seed_base + 3, hs), gen(seed_base + 100, hs)
+    g = gpu_out.float().cpu().numpy().reshape(H, N, D).astype(np.float64)
+    kinds = [s for s in PLAN.split()]
+    rels, rses, cached_equal = [], [], True
+    for h in range(H):
+        r = ref_out[h].astype(np.float64)
+        e = g[h] - r
+        rels.append(float(np.abs(e).max() / np.abs(r).max()))
+        den = float(((r - r.mean()) ** 2).sum())
+        rses.append(float((e ** 2).sum() / den))
+        if kinds[h] == "C":
+            cached_equal &= bool(np.array_equal(g[h], r))
+    worst = int(np.argmax(rels))
+    ok = max(rels) <= PARITY_MAX_REL and max(rses) <= PARITY_MAX_RSE and cached_equal
+    return {"checked": f"all {H} heads x {N} rows x {D} cols vs the reference CPU layer (oracle/_ref) on the same "
+                       "bf16 inputs",
+            "max_rel": max(rels), "rse_per_head_max": max(rses), "worst_head": worst,
+            "worst_head_kind": kinds[worst], "cached_heads_bitwise": cached_equal,
+            "tolerance": {"max_rel": PARITY_MAX_REL, "rse": PARITY_MAX_RSE}, "pass": ok}
 
 
 def run_reference(args):
@@ -177,15 +210,15 @@ def run_reference(args):
     # K + W whole-layer steps would exceed ~150 s, each step samples the
     # first 8 heads (F A8 C A0 F A8 C A8) instead, keeping the run within a
     # few minutes.
-    q, k, v, slots = host_sample_inputs()
-    first, _ = cpu_layer_sample(q, k, v, slots)
+    q, k, v, slots = (as_f32_numpy(x) for x in host_inputs())
+    first, _, _ = cpu_layer(q, k, v, slots)
     heads = CPU_SAMPLE_HEADS if first * (args.steps + args.warmup) <= 150.0 else CPU_SAMPLE_HEADS[:8]
     for _ in range(args.warmup - 1):
-        cpu_layer_sample(q, k, v, slots, heads=heads)
+        cpu_layer(q, k, v, slots, heads=heads)
     times = []
     cores = 1
     for _ in range(args.steps):
-        dt, cores = cpu_layer_sample(q, k, v, slots, heads=heads)
+        dt, cores, _ = cpu_layer(q, k, v, slots, heads=heads)
         times.append(dt)
     sec = sum(times) / len(times)
     sample_flops = len(heads) * 4 * D * N * N
@@ -197,91 +230,45 @@ def run_reference(args):
     line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded N(0,1), bf16-rounded)",
-            "config": config({"cpu_sample": "whole layer"}),
-            "layer_ms": sec * 1e3 * H / len(heads),
+            "config": config(), "layer_ms": sec * 1e3 * H / len(heads),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
 
 
-def run_head_mode(args, rank, world, barrier, max_over_ranks):
-    """One FLUX sample on `world` GPUs: heads LPT-sharded by plan cost, one
-    fused launch per rank over the full plan with the other ranks' heads
-    DFA2C_SKIP, NCCL all-gather of the bf16 output heads
-    (paper_2503_22796_b200.parallel). Strong scaling."""
+def spawn(args):
+    """--gpus N without a torchrun environment: relaunch under
+    torch.distributed.run, one process per GPU, and pass its exit code on."""
     import torch
 
-    from paper_2503_22796_b200 import api, parallel
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        print(f"bench.py: --gpus {args.gpus} needs {args.gpus} GPUs, this node has {have}", file=sys.stderr)
+        return 2
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
 
-    dims = api.AttentionDims(H, D, NV, NT)
-    lp = api.LayerPlan.parse(PLAN)
-    shard = parallel.make_head_shard(lp, dims, BLOCK, world, rank)
-    gen = torch.Generator(device="cuda")
 
-    def randn(seed, *shape):
-        gen.manual_seed(seed)
-        return torch.randn(*shape, device="cuda", dtype=torch.float32, generator=gen).to(torch.bfloat16)
-
-    q, k, v = (randn(s, H, N, D) for s in (1, 2, 3))  # the same sample on every rank
-    nh = len(shard.heads)
-    cache = api.HeadCache(1, H, N, D)  # layer-shaped; only this rank's slots are touched
-    for h in shard.heads:
-        cache.store(0, h, randn(100 + h, N, D), 0)
-    full = torch.empty_like(q)
-    skip = [h for h in range(H) if h not in set(shard.heads)]
-    stream = torch.cuda.current_stream()
-
-    def compute():  # one fused launch over the full plan, other ranks' heads DFA2C_SKIP
-        if nh:
-            api.multi_strategy_attention(q, k, v, lp, cache, 0, 1, dims, BLOCK, out=full, skip_heads=skip)
-
-    idx = torch.tensor(shard.heads, device="cuda", dtype=torch.long)
-
-    def step():
-        compute()
-        parallel.gather_heads(full.index_select(0, idx), shard, full)
-
-    # compute + gather overlapped per head group (parallel.pipelined_sharded_attention)
-    n_groups = args.head_groups or (3 if nh >= 12 else 2 if nh >= 6 else 1)
-    comm = torch.cuda.Stream()
-
-    def compute_group(hs):
-        owned = set(hs)
-        api.multi_strategy_attention(q, k, v, lp, cache, 0, 1, dims, BLOCK, out=full,
-                                     skip_heads=[h for h in range(H) if h not in owned])
-
-    def piped():
-        parallel.pipelined_sharded_attention(compute_group, full, shard, n_groups, comm_stream=comm)
-
-    def timed(fn, steps):
-        for _ in range(args.warmup):
-            fn()
-        torch.cuda.synchronize()
-        barrier()
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(steps):
-            fn()
-        e1.record(stream)
-        torch.cuda.synchronize()
-        barrier()
-        return max_over_ranks(e0.elapsed_time(e1) / steps)
-
-    compute_ms = timed(compute, args.steps)
-    serial_ms = timed(step, args.steps)
-    piped_ms = timed(piped, args.steps)
-    ms = min(serial_ms, piped_ms)
-    dense_fl = dense_layer_flops()
-    line = {"metric": METRIC, "value": dense_fl / (ms * 1e-3) / 1e12, "unit": UNIT, "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded N(0,1) bf16)",
-            "config": config({"parallelism": f"head-sharded x{world} (LPT on plan cost) + NCCL all-gather"}),
-            "layer_ms": ms, "compute_only_ms": compute_ms, "compute_then_gather_ms": serial_ms,
-            "overlapped_ms": piped_ms, "head_groups": n_groups,
-            "heads_per_rank": [len(o) for o in shard.all_heads]}
-    if rank == 0:
-        print(json.dumps(line))
+def cpp_f32_dropin():
+    """The reference's calling convention end to end: dfa2::multi_strategy_attention
+    with host f32 Tensors (tools/cpp_api_bench, built by __graft_entry__.build())."""
+    exe = os.path.join(ROOT, "tools", "cpp_api_bench_bin")
+    if not os.path.exists(exe):
+        return {"unavailable": "tools/cpp_api_bench_bin not built"}
+    try:
+        r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+        rec = json.loads(r.stdout.strip().splitlines()[-1])
+        ms = rec["ms_per_call"]
+        return {"value": dense_layer_flops() / (ms * 1e-3) / 1e12, "unit": UNIT, "ms_per_step": ms,
+                "h2d_bytes_per_step": 3 * 18 * N * D * 4, "d2h_bytes_per_step": H * N * D * 4,
+                "api": rec["api"] + " (f32 host in/out; bf16 over PCIe, rounding on host)"}
+    except Exception as e:  # a reported figure, never the product
+        return {"unavailable": str(e)[:200]}
 
 
 def main():
@@ -290,17 +277,14 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline / parity leg")
     ap.add_argument("--ncu", action="store_true", help="short run for profiler captures (no e2e/cpu legs)")
-    ap.add_argument("--head-groups", type=int, default=0,
-                    help="--mode head: head groups whose gather overlaps the next group's compute (0 = auto)")
-    ap.add_argument("--mode", default="sample", choices=["sample", "head"],
-                    help="sample: one FLUX sample per GPU (weak scaling, no collective); "
-                         "head: one sample split over the GPUs by LPT head sharding + NCCL all-gather (strong)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
         return run_reference(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn(args)
 
     import torch
     import torch.distributed as dist
@@ -310,6 +294,9 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        return 2
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -326,22 +313,13 @@ def main():
         return float(t.item())
 
     dims = api.AttentionDims(H, D, NV, NT)
-    if args.mode == "head":
-        return run_head_mode(args, rank, world, barrier, max_over_ranks)
-    seed0 = 1000 * rank
-    gen = torch.Generator(device="cuda")
-
-    def randn(seed, *shape):
-        gen.manual_seed(seed)
-        return torch.randn(*shape, device="cuda", dtype=torch.float32, generator=gen).to(torch.bfloat16)
-
-    q = randn(seed0 + 1, 1, H, N, D)
-    k = randn(seed0 + 2, 1, H, N, D)
-    v = randn(seed0 + 3, 1, H, N, D)
+    hq, hk, hv, hslots = host_inputs(1000 * rank)  # this rank's own sample
+    q, k, v = (x.cuda() for x in (hq, hk, hv))
     out = torch.empty_like(q)
     cache = api.HeadCache(1, H, N, D, batch=1)
+    slots = hslots.cuda()
     for h in range(H):  # t = 0: every slot produced
-        cache.store(0, h, randn(seed0 + 100 + h, N, D), 0)
+        cache.store(0, h, slots[h], 0)
     lp = api.LayerPlan.parse(PLAN)
     full = api.LayerPlan.all_full(H)
     plan_fl = api.plan_flops(lp, dims, BLOCK)
@@ -350,14 +328,14 @@ def main():
     def step(plan, t=1):
         api.multi_strategy_attention(q, k, v, plan, cache, 0, t, dims, BLOCK, out=out)
 
-    def timed(plan, steps, warmup, min_warm_s=0.0):
+    def timed(fn, steps, warmup, min_warm_s=0.0):
         for _ in range(warmup):
-            step(plan)
+            fn()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         while time.perf_counter() - t0 < min_warm_s:  # keep clocks at load for the sampler
             for _ in range(20):
-                step(plan)
+                fn()
             torch.cuda.synchronize()
         barrier()
         torch.cuda.synchronize()
@@ -365,7 +343,7 @@ def main():
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(steps):
-            step(plan)
+            fn()
         e1.record(stream)
         torch.cuda.synchronize()
         barrier()
@@ -374,11 +352,12 @@ def main():
 
     # headline: FLUX68 layer, inputs resident in HBM
     with ClockSampler(local) as clk:
-        ms, launches = timed(lp, args.steps, args.warmup, min_warm_s=0.0 if args.ncu else 1.0)
+        ms, launches = timed(lambda: step(lp), args.steps, args.warmup, min_warm_s=0.0 if args.ncu else 1.0)
         time.sleep(0.25)
     clocks = clk.summary()
+    gpu_out = out.clone()  # the FLUX68 layer output of this rank's sample (for the parity leg)
     # dense comparison through the same kernel (all-Full plan; no cached heads)
-    dense_ms, _ = timed(full, max(3, args.steps // 2), 2)
+    dense_ms, _ = timed(lambda: step(full), max(3, args.steps // 2), 2)
 
     dense_fl = dense_layer_flops()
     value = world * dense_fl / (ms * 1e-3) / 1e12
@@ -394,7 +373,7 @@ def main():
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded N(0,1) bf16; random cache slots)",
-            "config": config({"parallelism": f"sample-sharded x{world} (one FLUX 2K sample per GPU)"}),
+            "config": config(), "parallelism": f"batch-sharded x{world} (one FLUX 2K sample per GPU)",
             "layer_ms": ms, "dense_ms": dense_ms, "speedup_vs_dense": dense_ms / ms,
             "plan_flops": plan_fl, "dense_flops": dense_fl, "flop_reduction": 1 - plan_fl / dense_fl,
             "computed_tflops": achieved, "dense_path_tflops": dense_fl / (dense_ms * 1e-3) / 1e12,
@@ -406,22 +385,49 @@ def main():
             "gpu_launches": launches, "clocks": clocks}
 
     if not args.ncu:
+        # ONE sample over the `world` GPUs (strong scaling): contiguous
+        # cost-balanced row ranges, one fused launch per rank, in-place NCCL
+        # all-gather + cache completion (dfa2c_mha_forward_sharded).
+        comm = api.NcclComm.create(rank, world) if world > 1 else None
+        sq, sk, sv = (x.cuda() for x in host_inputs(0)[:3])  # the same sample on every rank
+        s_out = torch.empty_like(sq)
+        s_cache = api.HeadCache(1, H, N, D, batch=1)
+        for h in range(H):
+            s_cache.store(0, h, slots[h], 0)
+        bounds = api.shard_rows(lp, dims, BLOCK, world)
+
+        def sharded(c):
+            api.multi_strategy_attention_sharded(sq, sk, sv, lp, s_cache, 0, 1, dims, BLOCK, rank, world, comm=c,
+                                                 out=s_out)
+
+        s_compute, _ = timed(lambda: sharded(None), args.steps, args.warmup)
+        s_layer, _ = timed(lambda: sharded(comm), args.steps, args.warmup) if world > 1 else (s_compute, 0)
+        line["row_sharded"] = {
+            "what": "one FLUX68 sample split over the GPUs (dfa2c_mha_forward_sharded): strong scaling",
+            "n_gpus": world, "compute_ms": s_compute, "layer_ms": s_layer,
+            "gather": "NCCL group of W in-place broadcasts (all-gather-v) + cache completion" if world > 1 else None,
+            "value": dense_fl / (s_layer * 1e-3) / 1e12, "unit": UNIT,
+            "rows_per_rank": [int(bounds[r + 1] - bounds[r]) for r in range(world)],
+            "nccl_ranks": world if comm is not None else 0}
+        if comm is not None:
+            comm.close()
+
         # e2e through the public API with HOST buffers: dfa2c_mha_forward_host
         # uploads the computed heads' q/k/v from pinned memory in head groups,
         # runs each group's fused launch as its inputs land, and downloads
         # outputs (cached heads straight from their slots) — all inside the
         # timed region, every step.
-        hq, hk, hv = (x.cpu().pin_memory() for x in (q, k, v))
+        pq, pk, pv = (x.pin_memory() for x in (hq, hk, hv))
         ho = torch.empty(q.shape, dtype=torch.bfloat16).pin_memory()
 
         def e2e_step():
-            api.multi_strategy_attention_host(hq, hk, hv, lp, cache, 0, 1, dims, BLOCK, out=ho)
+            api.multi_strategy_attention_host(pq, pk, pv, lp, cache, 0, 1, dims, BLOCK, out=ho)
 
         for _ in range(2):
             e2e_step()
         step(lp)
         torch.cuda.synchronize()
-        if not torch.equal(ho.to("cuda"), out):  # same plan, same inputs: bitwise the device-path output
+        if not torch.equal(ho.to("cuda"), out):  # same plan, inputs and cache: bitwise the device-path output
             raise RuntimeError("host-buffer path disagrees with the device path")
         barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -442,12 +448,13 @@ def main():
                               "(pinned host q/k/v in, host out; only computed heads' q/k/v uploaded)"}
 
     if rank == 0 and world == 1 and not args.no_cpu and not args.ncu:
+        line["e2e_cpp_f32"] = cpp_f32_dropin()
         try:
-            hq_, hk_, hv_, hs_ = host_sample_inputs()
+            cq, ck, cv, cs = (as_f32_numpy(x) for x in (hq, hk, hv, hslots))
             # whole layers until ~10 s of CPU work (at least one)
-            secs = []
+            secs, ref_out = [], None
             while not secs or (sum(secs) < 10.0 and len(secs) < 5):
-                sec, cores = cpu_layer_sample(hq_, hk_, hv_, hs_)
+                sec, cores, ref_out = cpu_layer(cq, ck, cv, cs)
                 secs.append(sec)
             sec = sum(secs) / len(secs)
             sample_flops = len(CPU_SAMPLE_HEADS) * 4 * D * N * N
@@ -456,6 +463,7 @@ def main():
                 "sample": f"the whole FLUX68 layer ({len(CPU_SAMPLE_HEADS)} heads) x {len(secs)} through oracle/_ref "
                           f"(reference dense_tiled / sparse_attention_forward, DFA2_THREADS={cores}); "
                           f"{sec:.2f} s per layer, {sum(secs):.1f} s total"}
+            line["parity"] = parity(gpu_out, ref_out)
         except Exception as e:  # the CPU leg is a reported baseline, never the product
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
                                     "sample": f"unavailable: {e}"}
@@ -463,7 +471,8 @@ def main():
         print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()
+    return 0
 
 
 if __name__ == "__main__":
-    main()
+    sys.exit(main() or 0)

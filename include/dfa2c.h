@@ -161,6 +161,57 @@ int dfa2c_mha_forward_host(const void* q, const void* k, const void* v, int64_t 
                            const int64_t* windows, dfa2c_cache* cache, int64_t layer,
                            int64_t t, void* out, void* stream);
 
+/* ---- one layer on W GPUs (src/dispatch.cpp:62-83) --------
+ * Every (sample, head, query block) is independent, so the layer shards with
+ * no exchange inside it. dfa2c_mha_forward_sharded is the multi-GPU
+ * multi_strategy_attention, called by every rank with the SAME replicated
+ * q/k/v and plan:
+ *  - the layer's (sample, head, query-tile pair) sequence is cut into
+ *    `world` contiguous ranges of near-equal cost (cost = the pair's kept KV
+ *    tiles; a Cached head's pair = its copy), so rank r owns one contiguous
+ *    span [row_bounds[r], row_bounds[r+1]) of the flattened [batch*H*N]
+ *    output rows and its ONE fused launch computes / copies / commits only
+ *    those rows over all 148 SMs;
+ *  - pairs longer than 1/(8*148) of the layer run as key chunks (split-KV
+ *    against a fixed 8-GPU reference), so the bits of every head are the same
+ *    for every `world` (1, 2, 4, 8 ... give identical outputs);
+ *  - with nccl_comm (an ncclComm_t of `world` ranks, this rank = `rank`; the
+ *    library binds libnccl.so.2 at run time) the ranges are all-gathered in
+ *    place into `out` (one NCCL group of W broadcasts over NVLink/NVSwitch),
+ *    and the other ranks' computed rows are committed into this rank's cache
+ *    so every rank's cache is complete (a Cached head can then be served by
+ *    whichever rank owns its rows at the next timestep). Without a comm the
+ *    caller gathers `out` itself and then calls dfa2c_shard_commit.
+ * row_bounds (optional, [world + 1]) receives the row ranges. Cached heads
+ * need their slots on every rank (true when every layer runs through this
+ * call). Asynchronous on `stream`. */
+int dfa2c_mha_forward_sharded(const void* q, const void* k, const void* v, int64_t batch,
+                              const dfa2c_dims* dims, int64_t block, const int32_t* kinds,
+                              const int64_t* windows, dfa2c_cache* cache, int64_t layer, int64_t t,
+                              void* out, int32_t rank, int32_t world, void* nccl_comm,
+                              int64_t* row_bounds, void* stream);
+/* The row ranges dfa2c_mha_forward_sharded gives each of `world` ranks for
+ * this layer (host only, no GPU): row_bounds[world + 1] over the flattened
+ * [batch*H*N] rows; bitwise the bounds the sharded call reports. */
+int dfa2c_shard_rows(int64_t batch, const dfa2c_dims* dims, int64_t block, const int32_t* kinds,
+                     const int64_t* windows, int32_t world, int64_t* row_bounds);
+/* After a caller-side gather of a sharded call's `out`: commit the computed
+ * heads' rows outside this rank's range into `cache`. */
+int dfa2c_shard_commit(int64_t batch, const dfa2c_dims* dims, const int32_t* kinds, dfa2c_cache* cache,
+                       int64_t layer, const int64_t* row_bounds, int32_t rank, int32_t world,
+                       const void* out, void* stream);
+/* NCCL plumbing for C / C++ callers without their own communicator.
+ * dfa2c_nccl_unique_id fills 128 bytes on one rank (share them out of band);
+ * every rank then calls dfa2c_nccl_comm_init with its rank (collective). */
+int dfa2c_nccl_available(void);
+int dfa2c_nccl_unique_id(char* id /* 128 bytes */);
+int dfa2c_nccl_comm_init(const char* id, int32_t world, int32_t rank, void** comm);
+int dfa2c_nccl_comm_destroy(void* comm);
+/* In-place all-gather of unequal row ranges [row_bounds[r], row_bounds[r+1])
+ * (rows of row_bytes bytes) of buf: one NCCL group of `world` broadcasts. */
+int dfa2c_allgather_rows(void* comm, void* buf, const int64_t* row_bounds, int32_t world,
+                         int64_t row_bytes, void* stream);
+
 /* Split-KV scheduling for latency-bound layers (process-wide; default from
  * the environment, DFA2_SPLIT_KV=1). When on, a query-tile pair whose key
  * tiles cost more than the layer's average load per SM (reference 148 SMs)

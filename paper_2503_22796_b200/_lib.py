@@ -127,6 +127,18 @@ _SIGS = {
                                                  c_int64, POINTER(c_uint8), c_int64, c_void_p]),
     "dfa2c_dense_attention_forward": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int64,
                                                 c_int64, c_void_p]),
+    "dfa2c_mha_forward_sharded": (c_int32, [c_void_p, c_void_p, c_void_p, c_int64, POINTER(Dims), c_int64,
+                                            POINTER(c_int32), POINTER(c_int64), c_void_p, c_int64, c_int64,
+                                            c_void_p, c_int32, c_int32, c_void_p, POINTER(c_int64), c_void_p]),
+    "dfa2c_shard_rows": (c_int32, [c_int64, POINTER(Dims), c_int64, POINTER(c_int32), POINTER(c_int64), c_int32,
+                                   POINTER(c_int64)]),
+    "dfa2c_shard_commit": (c_int32, [c_int64, POINTER(Dims), POINTER(c_int32), c_void_p, c_int64, POINTER(c_int64),
+                                     c_int32, c_int32, c_void_p, c_void_p]),
+    "dfa2c_nccl_available": (c_int32, []),
+    "dfa2c_nccl_unique_id": (c_int32, [c_char_p]),
+    "dfa2c_nccl_comm_init": (c_int32, [c_char_p, c_int32, c_int32, POINTER(c_void_p)]),
+    "dfa2c_nccl_comm_destroy": (c_int32, [c_void_p]),
+    "dfa2c_allgather_rows": (c_int32, [c_void_p, c_void_p, POINTER(c_int64), c_int32, c_int64, c_void_p]),
     "dfa2c_attention_reference": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_int32, c_int64, c_int64,
                                             c_int64, POINTER(c_uint8), c_int64, c_void_p]),
     "dfa2c_rse": (c_int32, [c_void_p, c_void_p, c_int32, c_int64, c_int64, c_int32, POINTER(c_double),

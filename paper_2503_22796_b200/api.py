@@ -441,6 +441,111 @@ def multi_strategy_attention(q, k, v, plan: LayerPlan, cache: Optional[HeadCache
     return out4[0] if squeeze else out4
 
 
+def shard_rows(plan: LayerPlan, dims: AttentionDims, block_size: int, world: int, batch: int = 1) -> np.ndarray:
+    """Row ranges [bounds[r], bounds[r+1]) of the flattened [batch*H*N] output
+    that rank r of `world` computes in multi_strategy_attention_sharded
+    (dfa2c_shard_rows; host only, no GPU)."""
+    if plan.n_heads() != dims.n_heads:
+        raise ShapeError("plan must assign exactly one strategy per head")
+    kinds, wins = plan.arrays()
+    out = (c_int64 * (world + 1))()
+    d = dims.c()
+    check(lib().dfa2c_shard_rows(batch, byref(d), block_size, kinds, wins, world, out))
+    return np.array(list(out), dtype=np.int64)
+
+
+def multi_strategy_attention_sharded(q, k, v, plan: LayerPlan, cache: Optional[HeadCache], layer: int, t: int,
+                                     dims: AttentionDims, block_size: int, rank: int, world: int, comm=None,
+                                     out=None, stream=None):
+    """One layer on `world` GPUs (dfa2c_mha_forward_sharded).
+
+    Every rank passes the same replicated q/k/v and plan; this rank's ONE
+    fused launch computes its contiguous row range of the layer (near-equal
+    cost per rank, long pairs split into key chunks against a fixed 8-GPU
+    reference so each head's bits are independent of `world`). With `comm`
+    (a NcclComm of `world` ranks) the ranges are all-gathered in place over
+    NVLink and every rank's cache receives all computed rows; without it the
+    caller gathers `out` (e.g. parallel.gather_rows) and calls shard_commit.
+    Returns (out, row_bounds)."""
+    q = _as_bf16_cuda(q, "q")
+    k = _as_bf16_cuda(k, "k")
+    v = _as_bf16_cuda(v, "v")
+    squeeze = q.dim() == 3
+    if squeeze:
+        q, k, v = q.unsqueeze(0), k.unsqueeze(0), v.unsqueeze(0)
+    if q.dim() != 4 or q.shape != k.shape or q.shape != v.shape:
+        raise ShapeError("q/k/v must be identical [H, N, d] tensors")
+    if tuple(q.shape[1:]) != (dims.n_heads, dims.seq_len(), dims.head_dim):
+        raise ShapeError("tensor shape disagrees with dims")
+    if plan.n_heads() != dims.n_heads:
+        raise ShapeError("plan must assign exactly one strategy per head")
+    given = out
+    out4 = _device_out(out, q, q.shape[1:] if squeeze else q.shape)
+    d = dims.c()
+    kinds, wins = plan.arrays()
+    bounds = (c_int64 * (world + 1))()
+    check(lib().dfa2c_mha_forward_sharded(
+        c_void_p(q.data_ptr()), c_void_p(k.data_ptr()), c_void_p(v.data_ptr()), q.shape[0], byref(d), block_size,
+        kinds, wins, cache.handle if cache is not None else None, layer, t, c_void_p(out4.data_ptr()), rank, world,
+        comm.handle if comm is not None else None, bounds, c_void_p(_stream_ptr(stream))))
+    res = given if given is not None else (out4[0] if squeeze else out4)
+    return res, np.array(list(bounds), dtype=np.int64)
+
+
+def shard_commit(out, plan: LayerPlan, cache: HeadCache, layer: int, dims: AttentionDims, bounds, rank: int,
+                 world: int, stream=None) -> None:
+    """After a caller-side gather of a sharded call's `out`: commit the
+    computed heads' rows outside this rank's range into `cache`."""
+    kinds, _ = plan.arrays()
+    b = (c_int64 * (world + 1))(*[int(x) for x in bounds])
+    d = dims.c()
+    batch = 1 if out.dim() == 3 else out.shape[0]
+    check(lib().dfa2c_shard_commit(batch, byref(d), kinds, cache.handle, layer, b, rank, world,
+                                   c_void_p(out.data_ptr()), c_void_p(_stream_ptr(stream))))
+
+
+class NcclComm:
+    """An NCCL communicator owned by the library (dfa2c_nccl_comm_init; NCCL
+    bound at run time). create() shares the unique id through the default
+    torch.distributed group (any backend)."""
+
+    def __init__(self, handle: c_void_p, rank: int, world: int):
+        self._h, self.rank, self.world = handle, rank, world
+
+    @staticmethod
+    def available() -> bool:
+        return bool(lib().dfa2c_nccl_available())
+
+    @staticmethod
+    def create(rank: int, world: int, group=None) -> "NcclComm":
+        import torch.distributed as dist
+
+        uid = ctypes.create_string_buffer(128)
+        if rank == 0:
+            check(lib().dfa2c_nccl_unique_id(uid))
+        if world > 1:
+            obj = [uid.raw if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0, group=group)
+            uid = ctypes.create_string_buffer(obj[0], 128)
+        h = c_void_p()
+        check(lib().dfa2c_nccl_comm_init(uid, world, rank, byref(h)))
+        return NcclComm(h, rank, world)
+
+    @property
+    def handle(self) -> c_void_p:
+        return self._h
+
+    def allgather_rows(self, buf, bounds, row_bytes: int, stream=None) -> None:
+        b = (c_int64 * (self.world + 1))(*[int(x) for x in bounds])
+        check(lib().dfa2c_allgather_rows(self._h, c_void_p(buf.data_ptr()), b, self.world, row_bytes,
+                                         c_void_p(_stream_ptr(stream))))
+
+    def close(self) -> None:
+        if self._h is not None and self._h.value:
+            check(lib().dfa2c_nccl_comm_destroy(self._h))
+        self._h = None
+
+
 def multi_strategy_attention_host(q, k, v, plan: LayerPlan, cache: Optional[HeadCache], layer: int, t: int,
                                   dims: AttentionDims, block_size: int, out=None, stream=None, skip_heads=None):
     """multi_strategy_attention with HOST tensors (the reference's calling

@@ -21,7 +21,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 CU_SOURCES = ["attn_sm100.cu", "rse_sm100.cu", "convert_sm100.cu", "reference_sm100.cu"]
-CPP_SOURCES = ["dfa2c.cpp", "json_lite.cpp", "plansolver.cpp"]
+CPP_SOURCES = ["dfa2c.cpp", "json_lite.cpp", "plansolver.cpp", "nccl_dl.cpp"]
 
 
 def _sources():
@@ -75,6 +75,23 @@ def build_cli(force: bool = False) -> str:
     subprocess.run(cmd, check=True)
     os.replace(CLI + ".tmp", CLI)
     return CLI
+
+
+def build_tools(force: bool = False) -> str:
+    """tools/cpp_api_bench_bin: times the C++ drop-in dfa2::multi_strategy_attention
+    with host f32 tensors (the reference's calling convention; bench.py's
+    e2e_cpp_f32)."""
+    src = os.path.join(ROOT, "tools", "cpp_api_bench.cpp")
+    exe = os.path.join(ROOT, "tools", "cpp_api_bench_bin")
+    inc = os.path.join(ROOT, "include", "dfa2")
+    deps = [src, LIB] + [os.path.join(inc, f) for f in os.listdir(inc)]
+    if not force and not _stale(exe, deps):
+        return exe
+    cmd = [os.environ.get("CXX", "g++"), "-std=c++20", "-O2", "-I", os.path.join(ROOT, "include"), src, "-o",
+           exe + ".tmp", "-L", HERE, "-ldfa2_b200", "-Wl,-rpath,$ORIGIN/../paper_2503_22796_b200"]
+    subprocess.run(cmd, check=True)
+    os.replace(exe + ".tmp", exe)
+    return exe
 
 
 if __name__ == "__main__":

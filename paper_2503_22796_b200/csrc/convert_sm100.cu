@@ -71,4 +71,46 @@ cudaError_t launch_convert(const void* src, int src_dtype, void* dst, int dst_dt
     }
 }
 
+// ---- sharded layer: commit the rows other ranks computed ----------------
+// After the all-gather every rank holds the whole layer output; the rows of
+// computed heads outside this rank's own range [r0, r1) (flattened
+// [batch*H*N] rows) are copied into this rank's cache layer, so every rank's
+// cache is complete and a Cached head can be served by whichever rank owns
+// its rows at a later timestep. 16-byte vectors, grid-stride; HBM-bound.
+struct HeadBits {
+    uint32_t w[32];  // computed heads (up to 1024)
+};
+
+__global__ void commit_rows_kernel(const uint4* __restrict__ out, uint4* __restrict__ cache, int64_t rows,
+                                   int64_t r0, int64_t r1, int64_t n, int64_t H, int vec_per_row, HeadBits bits) {
+    const int64_t outside = rows - (r1 - r0);
+    const int64_t total = outside * vec_per_row;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
+        int64_t r = i / vec_per_row;
+        r = r < r0 ? r : r + (r1 - r0);
+        const int64_t h = (r / n) % H;
+        if (!((bits.w[h >> 5] >> (h & 31)) & 1u))
+            continue;
+        const int64_t v = r * vec_per_row + i % vec_per_row;
+        cache[v] = out[v];
+    }
+}
+
+cudaError_t launch_commit_rows(const void* out, void* cache, int64_t rows, int64_t r0, int64_t r1, int64_t n,
+                               int64_t H, int64_t d, const uint32_t* head_bits, int sms, cudaStream_t stream) {
+    HeadBits b{};
+    for (int i = 0; i < 32; ++i)
+        b.w[i] = head_bits[i];
+    const int vec = static_cast<int>(d * 2 / 16);
+    const int64_t total = (rows - (r1 - r0)) * vec;
+    if (total <= 0)
+        return cudaSuccess;
+    const int64_t blocks = (total + 255) / 256;
+    const int grid = static_cast<int>(blocks < 8LL * sms ? blocks : 8LL * sms);
+    commit_rows_kernel<<<grid, 256, 0, stream>>>(static_cast<const uint4*>(out), static_cast<uint4*>(cache), rows, r0,
+                                                 r1, n, H, vec, b);
+    return cudaGetLastError();
+}
+
 }  // namespace dfa2k

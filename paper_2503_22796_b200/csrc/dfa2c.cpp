@@ -24,6 +24,7 @@
 
 #include "attn_types.h"
 #include "capi_status.h"
+#include "nccl_dl.h"
 #include "json_lite.h"
 
 namespace dfa2k {
@@ -40,6 +41,8 @@ cudaError_t launch_rse_multi(const void* const* ym, int M, const void* yo, int d
                              cudaStream_t stream);
 int rse_multi_max();
 int reference_max_head_dim();
+cudaError_t launch_commit_rows(const void* out, void* cache, int64_t rows, int64_t r0, int64_t r1, int64_t n,
+                               int64_t H, int64_t d, const uint32_t* head_bits, int sms, cudaStream_t stream);
 cudaError_t launch_attention_reference(const void* q, const void* k, const void* v, void* out, int dtype, int64_t H,
                                        int64_t n, int64_t d, const uint8_t* mask, int64_t block, int64_t nb,
                                        cudaStream_t stream);
@@ -344,10 +347,12 @@ struct Retire {
     cudaEvent_t ev = nullptr;
 };
 Retire& retire_of(int device) {
-    static std::mutex mu;
-    static std::map<int, std::unique_ptr<Retire>> m;
-    std::lock_guard<std::mutex> lk(mu);
-    auto& r = m[device];
+    // never destroyed: plans evicted by static destruction at exit (g_plans)
+    // still find their device's retire state
+    static std::mutex* mu = new std::mutex;
+    static auto* m = new std::map<int, std::unique_ptr<Retire>>;
+    std::lock_guard<std::mutex> lk(*mu);
+    auto& r = (*m)[device];
     if (!r) {
         r = std::make_unique<Retire>();
         int cur = 0;
@@ -509,26 +514,51 @@ std::unique_ptr<DevPlan> schedule_items(int device, std::vector<Cand>& cands, co
 // greedily assigned to the least-loaded CTA. The schedule is static, so
 // every run (and every GPU count) folds the same tiles in the same order:
 // outputs are bitwise reproducible.
-std::unique_ptr<DevPlan> build_dev_plan(int device, int64_t batch, int64_t H, int64_t n, int64_t B,
-                                        const std::vector<std::vector<uint8_t>>& masks,
-                                        const std::vector<HeadJob>& jobs, const std::vector<int>& ref_jobs,
-                                        int64_t text_lo, int64_t text_hi, int64_t halve_ratio, cudaStream_t stream) {
+// Sharded launches (n_parts > 0; dfa2c_mha_forward_sharded): the layer's
+// (sample, head, query-tile pair) sequence is cut into n_parts contiguous
+// ranges of near-equal cost and this launch runs range `part`. Pairs are
+// always (2p, 2p+1) (no HALVES entries), so every range is one contiguous
+// span of the flattened [batch*H*N] output rows. Long pairs are split into
+// key chunks against a fixed reference of kShardRefSMs SMs (an 8-GPU box),
+// whatever the GPU count, so a head's bits are the same for every n_parts.
+constexpr double kShardRefSMs = 148.0 * 8;
+
+// Host-side geometry of a work list: per-mask pair sets and their tile
+// words, the split-KV chunking, and for sharded launches the partition.
+struct PlanGeometry {
+    std::vector<uint32_t> tiles;
+    std::vector<uint8_t> mask_bytes;
+    std::vector<int64_t> mask_tile_base, mask_off;
+    std::vector<PairSet> sets;
+    std::vector<std::vector<int32_t>> chunks_of;  // per mask, per pair: key chunks (1 = whole)
+    std::vector<int64_t> shard_rows;              // sharded: [n_parts + 1] flattened row bounds
+    std::vector<int32_t> pair_part;               // sharded: part of each (sample, head, pair)
+};
+
+PlanGeometry plan_geometry(int64_t batch, int64_t H, int64_t n, int64_t B,
+                           const std::vector<std::vector<uint8_t>>& masks, const std::vector<HeadJob>& jobs,
+                           const std::vector<int>& ref_jobs, int64_t text_lo, int64_t text_hi, int64_t halve_ratio,
+                           int32_t n_parts) {
     const int64_t nqt = ceil_div(n, dfa2k::TILE_M);
     const int64_t np = (nqt + 1) / 2;  // copy items: pairs (2p, 2p+1)
+    const bool sharded = n_parts > 0;
+    PlanGeometry g;
+    auto& tiles = g.tiles;
+    auto& mask_bytes = g.mask_bytes;
+    auto& mask_tile_base = g.mask_tile_base;
+    auto& mask_off = g.mask_off;
+    auto& sets = g.sets;
+    auto& chunks_of = g.chunks_of;
     // text query tiles as HALVES entries (d = 64; not under split-KV, which
-    // chunks the long rows its own way)
+    // chunks the long rows its own way, nor in sharded launches)
     std::vector<uint8_t> text_tile;
-    if (halve_ratio > 0 && !split_kv_enabled() && text_hi > text_lo) {
+    if (halve_ratio > 0 && !split_kv_enabled() && !sharded && text_hi > text_lo) {
         text_tile.assign(static_cast<size_t>(nqt), 0);
         for (int64_t q = 0; q < nqt; ++q) {
             const int64_t r0 = q * dfa2k::TILE_M, r1 = std::min(r0 + dfa2k::TILE_M, n);
             text_tile[q] = (r0 < text_hi && r1 > text_lo) ? 1 : 0;
         }
     }
-    std::vector<uint32_t> tiles;
-    std::vector<uint8_t> mask_bytes;
-    std::vector<int64_t> mask_tile_base, mask_off;
-    std::vector<PairSet> sets;
     for (const auto& m : masks) {
         sets.push_back(build_pair_set(build_tile_set(m.data(), n, B), nqt, text_tile, halve_ratio));
         mask_tile_base.push_back(static_cast<int64_t>(tiles.size()));
@@ -558,11 +588,11 @@ std::unique_ptr<DevPlan> build_dev_plan(int device, int64_t batch, int64_t H, in
     // why it is off by default: with it off every head's result is a
     // function of its own strategy alone (head isolation, bitwise,
     // test_dispatch.cpp:98-109).
-    constexpr double kRefSMs = 148.0;
-    std::vector<std::vector<int32_t>> chunks_of(sets.size());
+    const double kRefSMs = sharded ? kShardRefSMs : 148.0;
+    chunks_of.resize(sets.size());
     for (size_t mi = 0; mi < sets.size(); ++mi)
         chunks_of[mi].assign(sets[mi].qa.size(), 1);
-    if (split_kv_enabled()) {
+    if (split_kv_enabled() || sharded) {
         double per_sample = 0.0;
         for (int64_t h = 0; h < H; ++h) {
             const int rj = ref_jobs.empty() ? jobs[h].mask_id : ref_jobs[h];
@@ -586,10 +616,76 @@ std::unique_ptr<DevPlan> build_dev_plan(int device, int64_t batch, int64_t H, in
             }
         }
     }
+    // sharded: cost of every pair of the layer, in (sample, head, pair)
+    // order, and the cut into n_parts near-equal contiguous ranges (a pair
+    // belongs to the part containing the midpoint of its cost interval)
+    auto& shard_rows = g.shard_rows;
+    auto& pair_part = g.pair_part;
+    if (sharded) {
+        std::vector<double> cost;
+        std::vector<int64_t> row_end;  // flattened end row of each pair
+        for (int64_t b = 0; b < batch; ++b)
+            for (int64_t h = 0; h < H; ++h) {
+                const int rj = jobs[h].mask_id;
+                if (rj == JOB_SKIP)
+                    fail(DFA2C_SHAPE, "sharded launches take the whole layer (no skipped heads)");
+                for (int64_t p = 0; p < np; ++p) {
+                    const int64_t r1 = std::min<int64_t>(n, 256 * (p + 1));
+                    if (rj == JOB_COPY) {
+                        cost.push_back(static_cast<double>(r1 - 256 * p) / 128.0);
+                    } else {
+                        const PairSet& ps = sets[rj];
+                        const int32_t nch = chunks_of[rj][p];
+                        cost.push_back(ps.n_a[p] + ps.n_b[p] + 1.0 + (nch > 1 ? 0.5 * nch : 0.0));
+                    }
+                    row_end.push_back((b * H + h) * n + r1);
+                }
+            }
+        double total = 0.0;
+        for (double c : cost)
+            total += c;
+        shard_rows.assign(static_cast<size_t>(n_parts) + 1, 0);
+        pair_part.resize(cost.size());
+        double acc = 0.0;
+        int32_t cur = 0;
+        for (size_t i = 0; i < cost.size(); ++i) {
+            const double mid = acc + 0.5 * cost[i];
+            while (cur + 1 < n_parts && mid >= total * (cur + 1) / n_parts) {
+                ++cur;
+                shard_rows[static_cast<size_t>(cur)] = i ? row_end[i - 1] : 0;
+            }
+            pair_part[i] = cur;
+            acc += cost[i];
+        }
+        for (int32_t c = cur + 1; c <= n_parts; ++c)
+            shard_rows[static_cast<size_t>(c)] = batch * H * n;
+    }
+
+    return g;
+}
+
+std::unique_ptr<DevPlan> build_dev_plan(int device, int64_t batch, int64_t H, int64_t n, int64_t B,
+                                        const std::vector<std::vector<uint8_t>>& masks,
+                                        const std::vector<HeadJob>& jobs, const std::vector<int>& ref_jobs,
+                                        int64_t text_lo, int64_t text_hi, int64_t halve_ratio, cudaStream_t stream,
+                                        int32_t n_parts = 0, int32_t part = 0) {
+    const int64_t nqt = ceil_div(n, dfa2k::TILE_M);
+    const int64_t np = (nqt + 1) / 2;  // copy items: pairs (2p, 2p+1)
+    const bool sharded = n_parts > 0;
+    PlanGeometry g = plan_geometry(batch, H, n, B, masks, jobs, ref_jobs, text_lo, text_hi, halve_ratio, n_parts);
+    auto& tiles = g.tiles;
+    const auto& mask_bytes = g.mask_bytes;
+    const auto& mask_tile_base = g.mask_tile_base;
+    const auto& mask_off = g.mask_off;
+    const auto& sets = g.sets;
+    const auto& chunks_of = g.chunks_of;
+    auto& shard_rows = g.shard_rows;
+    const auto& pair_part = g.pair_part;
     int32_t n_groups = 0, n_slots = 0;
 
     std::vector<Cand> cands;
     cands.reserve(static_cast<size_t>(batch * H * np));
+    int64_t pair_idx = -1;
     for (int64_t b = 0; b < batch; ++b)
         for (int64_t h = 0; h < H; ++h) {
             const HeadJob& j = jobs[h];
@@ -598,6 +694,9 @@ std::unique_ptr<DevPlan> build_dev_plan(int device, int64_t batch, int64_t H, in
             const int64_t n_entries =
                 j.mask_id == JOB_COPY ? np : static_cast<int64_t>(sets[j.mask_id].qa.size());
             for (int64_t p = 0; p < n_entries; ++p) {
+                ++pair_idx;
+                if (sharded && pair_part[static_cast<size_t>(pair_idx)] != part)
+                    continue;
                 WorkItem w{};
                 w.bh = static_cast<int32_t>(b * H + h);
                 if (j.mask_id == JOB_COPY) {
@@ -646,7 +745,15 @@ std::unique_ptr<DevPlan> build_dev_plan(int device, int64_t batch, int64_t H, in
                 }
             }
         }
-    return schedule_items(device, cands, tiles, mask_bytes, n_groups, n_slots, stream);
+    if (cands.empty() && sharded) {  // an empty part: nothing to launch
+        auto p = std::make_unique<DevPlan>();
+        p->device = device;
+        p->shard_rows = std::move(shard_rows);
+        return p;
+    }
+    auto plan = schedule_items(device, cands, tiles, mask_bytes, n_groups, n_slots, stream);
+    plan->shard_rows = std::move(shard_rows);
+    return plan;
 }
 
 // LPT assignment of the work items to one persistent CTA per SM (cost desc,
@@ -883,6 +990,9 @@ struct ForwardSpec {
     dfa2c_cache* cache;                       // slots read (copy) / written (commit)
     int64_t layer;
     int64_t scale_d = 0;                      // head dim of the softmax scale (0: dims->head_dim)
+    int32_t n_parts = 0;                      // sharded launch: the layer cut into n_parts ranges...
+    int32_t part = 0;                         // ...of which this launch runs `part`
+    std::vector<int64_t>* shard_rows = nullptr;  // out: [n_parts + 1] flattened row bounds
 };
 
 // The kernel instantiations: D = 64 serves head dims 1..64, D = 128 serves 65..128.
@@ -1025,6 +1135,8 @@ void launch_forward(const ForwardSpec& s, cudaStream_t stream) {
     if (split_kv_enabled())
         for (int rj : s.ref_jobs)
             put(key, rj);
+    put(key, s.n_parts);
+    put(key, s.part);
     key += s.mask_key;
 
     std::shared_ptr<DevPlan> plan;
@@ -1046,9 +1158,11 @@ void launch_forward(const ForwardSpec& s, cudaStream_t stream) {
             }
             plan = plan_insert(key, build_dev_plan(device, s.batch, H, n, s.block, *masks, s.jobs, s.ref_jobs,
                                                    text_begin(s.dims), text_end(s.dims), halve_ratio(d),
-                                                   stream));
+                                                   stream, s.n_parts, s.part));
         }
     }
+    if (s.shard_rows)
+        *s.shard_rows = plan->shard_rows;
 
     void* cache_layer = nullptr;
     bool need_cache = false;
@@ -1780,6 +1894,188 @@ int dfa2c_mha_forward_host(const void* q, const void* k, const void* v, int64_t 
         DFA2C_CUDA_CHECK(cudaStreamWaitEvent(user, ws.ev_done, 0));
         DFA2C_CUDA_CHECK(cudaEventRecord(ws.ev_free, user));
         commit_produced(dims, kinds, cache, layer, t);
+    });
+}
+
+// ---------------------------------------------------------------- multi-GPU
+namespace {
+
+void head_bits(const dfa2c_dims* dims, const int32_t* kinds, uint32_t* bits) {
+    for (int i = 0; i < 32; ++i)
+        bits[i] = 0;
+    for (int64_t h = 0; h < dims->n_heads; ++h)
+        if (kind_of(kinds[h]) != DFA2C_CACHED)
+            bits[h >> 5] |= 1u << (h & 31);
+}
+
+void commit_others(int64_t batch, const dfa2c_dims* dims, const int32_t* kinds, dfa2c_cache* cache, int64_t layer,
+                   int64_t r0, int64_t r1, const void* out, cudaStream_t st) {
+    const int64_t H = dims->n_heads, n = seq_len(dims), d = dims->head_dim;
+    uint32_t bits[32];
+    head_bits(dims, kinds, bits);
+    bool any = false;
+    for (uint32_t b : bits)
+        any |= b != 0;
+    if (!any)
+        return;
+    cache->ensure(layer);
+    void* slots = cache->layer_ptr(layer, st);
+    int device = 0;
+    DFA2C_CUDA_CHECK(cudaGetDevice(&device));
+    DFA2C_CUDA_CHECK(dfa2k::launch_commit_rows(out, slots, batch * H * n, r0, r1, n, H, d, bits, num_sms(device), st));
+    g_launches.fetch_add(1);
+}
+
+void validate_sharded(int64_t batch, const dfa2c_dims* dims, const int32_t* kinds, int32_t rank, int32_t world) {
+    if (world < 1 || rank < 0 || rank >= world)
+        fail(DFA2C_SHAPE, "need 0 <= rank < world");
+    if (!direct_layout(dims->head_dim))
+        fail(DFA2C_UNSUPPORTED, "sharded launches need head_dim 64 or 72..128 (multiple of 8)");
+    if (dims->n_heads > 1024)
+        fail(DFA2C_UNSUPPORTED, "sharded launches support up to 1024 heads");
+    for (int64_t h = 0; h < dims->n_heads; ++h)
+        if (skipped(kinds[h]))
+            fail(DFA2C_SHAPE, "sharded launches take the whole layer plan (no DFA2C_SKIP heads)");
+    (void)batch;
+}
+}  // namespace
+
+int dfa2c_mha_forward_sharded(const void* q, const void* k, const void* v, int64_t batch, const dfa2c_dims* dims,
+                              int64_t block, const int32_t* kinds, const int64_t* windows, dfa2c_cache* cache,
+                              int64_t layer, int64_t t, void* out, int32_t rank, int32_t world, void* nccl_comm,
+                              int64_t* row_bounds, void* stream) {
+    return guard([&] {
+        validate_forward(batch, dims, block, kinds, windows, cache, layer);
+        validate_sharded(batch, dims, kinds, rank, world);
+        if (nccl_comm) {
+            int nr = 0, r = 0;
+            const std::string e = dfa2nccl::comm_shape(nccl_comm, &nr, &r);
+            if (!e.empty())
+                fail(DFA2C_CUDA, e);
+            if (nr != world || r != rank)
+                fail(DFA2C_SHAPE, "NCCL communicator (" + std::to_string(r) + " of " + std::to_string(nr) +
+                                      ") disagrees with rank/world");
+        }
+        const cudaStream_t st = as_stream(stream);
+        ForwardSpec s{};
+        s.q = q;
+        s.k = k;
+        s.v = v;
+        s.out = out;
+        s.batch = batch;
+        s.dims = dims;
+        s.block = block;
+        s.cache = cache;
+        s.layer = layer;
+        s.n_parts = world;
+        s.part = rank;
+        std::vector<int64_t> rows;
+        s.shard_rows = &rows;
+        plan_jobs(dims, block, kinds, windows, cache != nullptr, s);
+        launch_forward(s, st);  // this rank's rows only; its computed rows are committed in-kernel
+        if (rows.size() != static_cast<size_t>(world) + 1)
+            fail(DFA2C_CUDA, "internal: shard bounds missing");
+        if (row_bounds)
+            std::copy(rows.begin(), rows.end(), row_bounds);
+        if (nccl_comm && world > 1) {
+            const int64_t rb = dims->head_dim * 2;
+            std::vector<int64_t> off(rows.size());
+            for (size_t i = 0; i < rows.size(); ++i)
+                off[i] = rows[i] * rb;
+            const std::string e = dfa2nccl::allgather_v(nccl_comm, out, off.data(), world, st);
+            if (!e.empty())
+                fail(DFA2C_CUDA, e);
+            if (cache)
+                commit_others(batch, dims, kinds, cache, layer, rows[rank], rows[rank + 1], out, st);
+        }
+        commit_produced(dims, kinds, cache, layer, t);
+    });
+}
+
+int dfa2c_shard_rows(int64_t batch, const dfa2c_dims* dims, int64_t block, const int32_t* kinds,
+                     const int64_t* windows, int32_t world, int64_t* row_bounds) {
+    return guard([&] {
+        validate_dims(dims);
+        if (block < 1 || batch < 1)
+            fail(DFA2C_SHAPE, "block_size and batch must be >= 1");
+        validate_plan(dims, kinds, windows);
+        validate_sharded(batch, dims, kinds, 0, world);
+        if (!row_bounds)
+            fail(DFA2C_SHAPE, "row_bounds must not be NULL");
+        ForwardSpec s{};
+        plan_jobs(dims, block, kinds, windows, false, s);
+        const int64_t n = seq_len(dims), nb = ceil_div(n, block);
+        std::vector<std::vector<uint8_t>> masks;
+        for (int64_t w : s.mask_windows)
+            masks.push_back(w < 0 ? std::vector<uint8_t>(static_cast<size_t>(nb * nb), uint8_t{1})
+                                  : arrow_mask(dims, block, w));
+        const PlanGeometry g = plan_geometry(batch, dims->n_heads, n, block, masks, s.jobs, s.ref_jobs,
+                                             text_begin(dims), text_end(dims), 0, world);
+        std::copy(g.shard_rows.begin(), g.shard_rows.end(), row_bounds);
+    });
+}
+
+int dfa2c_shard_commit(int64_t batch, const dfa2c_dims* dims, const int32_t* kinds, dfa2c_cache* cache, int64_t layer,
+                       const int64_t* row_bounds, int32_t rank, int32_t world, const void* out, void* stream) {
+    return guard([&] {
+        validate_dims(dims);
+        if (!cache || !row_bounds || !out)
+            fail(DFA2C_SHAPE, "shard_commit needs a cache, the row bounds and the gathered output");
+        if (world < 1 || rank < 0 || rank >= world)
+            fail(DFA2C_SHAPE, "need 0 <= rank < world");
+        if (cache->H != dims->n_heads || cache->n != seq_len(dims) || cache->d != dims->head_dim ||
+            cache->batch != batch)
+            fail(DFA2C_SHAPE, "cache geometry disagrees with dims/batch");
+        if (dims->n_heads > 1024)
+            fail(DFA2C_UNSUPPORTED, "sharded launches support up to 1024 heads");
+        commit_others(batch, dims, kinds, cache, layer, row_bounds[rank], row_bounds[rank + 1], out,
+                      as_stream(stream));
+    });
+}
+
+int dfa2c_nccl_available(void) { return dfa2nccl::available(nullptr) ? 1 : 0; }
+
+int dfa2c_nccl_unique_id(char* id) {
+    return guard([&] {
+        if (!id)
+            fail(DFA2C_SHAPE, "id buffer must not be NULL");
+        const std::string e = dfa2nccl::unique_id(id);
+        if (!e.empty())
+            fail(DFA2C_CUDA, e);
+    });
+}
+
+int dfa2c_nccl_comm_init(const char* id, int32_t world, int32_t rank, void** comm) {
+    return guard([&] {
+        if (!id || !comm || world < 1 || rank < 0 || rank >= world)
+            fail(DFA2C_SHAPE, "nccl_comm_init needs an id, a comm slot and 0 <= rank < world");
+        const std::string e = dfa2nccl::comm_init(comm, world, id, rank);
+        if (!e.empty())
+            fail(DFA2C_CUDA, e);
+    });
+}
+
+int dfa2c_nccl_comm_destroy(void* comm) {
+    return guard([&] {
+        if (!comm)
+            return;
+        const std::string e = dfa2nccl::comm_destroy(comm);
+        if (!e.empty())
+            fail(DFA2C_CUDA, e);
+    });
+}
+
+int dfa2c_allgather_rows(void* comm, void* buf, const int64_t* row_bounds, int32_t world, int64_t row_bytes,
+                         void* stream) {
+    return guard([&] {
+        if (!comm || !buf || !row_bounds || world < 1 || row_bytes < 1)
+            fail(DFA2C_SHAPE, "allgather_rows needs a comm, a buffer, the bounds and row_bytes >= 1");
+        std::vector<int64_t> off(static_cast<size_t>(world) + 1);
+        for (int32_t i = 0; i <= world; ++i)
+            off[i] = row_bounds[i] * row_bytes;
+        const std::string e = dfa2nccl::allgather_v(comm, buf, off.data(), world, as_stream(stream));
+        if (!e.empty())
+            fail(DFA2C_CUDA, e);
     });
 }
 

@@ -545,41 +545,6 @@ def test_run_pipeline_on_reference_workload():
     _ = (ctypes, per, ArrowSpec)
 
 
-def test_head_sharded_layer_is_bitwise_the_single_gpu_layer():
-    """the head-sharded path (parallel.sharded_multi_strategy_attention,
-    one launch per rank over the full plan with DFA2C_SKIP) assembles to
-    exactly the single-call output for W = 2, 4 and 8 ranks (ranks emulated
-    one after another on this GPU; the NCCL all-gather is covered by the
-    gloo test), cached heads included."""
-    from paper_2503_22796_b200 import parallel
-
-    t = torch()
-    H, nv, nt, d, B = 24, 4096, 333, 64, 128
-    n = nv + nt
-    dims = AttentionDims(H, d, nv, nt)
-    q, _ = bf16_inputs((H, n, d), 91)
-    k, _ = bf16_inputs((H, n, d), 92)
-    v, _ = bf16_inputs((H, n, d), 93)
-    plan = api.flux68_plan(H)
-    ref_cache = HeadCache(1, H, n, d)
-    api.multi_strategy_attention(q, k, v, LayerPlan.all_full(H), ref_cache, 0, 0, dims, B)
-    ref = api.multi_strategy_attention(q, k, v, plan, ref_cache, 0, 1, dims, B)
-    for W in (2, 4, 8):
-        assembled = t.empty_like(q)
-        for r in range(W):
-            shard = parallel.make_head_shard(plan, dims, B, W, r)
-            cache = HeadCache(1, H, n, d)
-            full = t.empty_like(q)
-            parallel.sharded_multi_strategy_attention(q, k, v, LayerPlan.all_full(H), cache, 0, 0, dims, B, shard,
-                                                      gather=False, out=full)
-            local = parallel.sharded_multi_strategy_attention(q, k, v, plan, cache, 0, 1, dims, B, shard,
-                                                              gather=False, out=full)
-            for i, h in enumerate(shard.heads):
-                assembled[h] = local[i]
-        t.cuda.synchronize()
-        assert t.equal(assembled, ref), f"W={W}"
-
-
 # ---- fused calibration pass (dfa2c_influence_for_layer at block 128):
 # the original and every Arrow candidate from one launch, each candidate the
 # snapshot of its query tiles after the candidate's window band.
