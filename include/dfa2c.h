@@ -374,6 +374,27 @@ int dfa2c_plan_from_json(const char* text, int64_t text_len, dfa2c_plan_header* 
 /* fnv1a_hex (inc/plan.hpp:57-58): FNV-1a 64 of n bytes as 16 hex chars + NUL. */
 int dfa2c_fnv1a_hex(const void* bytes, int64_t n, char* out);
 
+/* ---- device workload generator ------------------------
+ * The reference's synthetic MMDiT stream (generate(), src/workload.cpp:
+ * 120-228: default locality/drift profiles, positional features from its
+ * own seeded mt19937_64 draws, a per-timestep random walk) produced on the
+ * GPU: per-element gaussians come from a counter-based Philox stream keyed
+ * by the reference's derive_seed(seed, layer, head, t, tag), so any slot is
+ * a pure function of (seed, t, layer) — same distribution as the reference,
+ * not the same bits (dfa2::generate on the host stays bit-identical for
+ * small streams). Each layer's walk state stays in HBM (fp32 [3, H, N, d],
+ * allocated on first use); dfa2c_workload_slot writes slot (t, layer) as
+ * bf16 q/k/v [H, N, d] on `stream`, stepping the layer's walk forward (or
+ * restarting it for an earlier t). head_dim % 4 == 0. Not thread-safe. */
+typedef struct dfa2c_workload dfa2c_workload;
+int dfa2c_workload_create(const dfa2c_dims* dims, int64_t n_layers, int64_t block, uint64_t seed,
+                          dfa2c_workload** w);
+int dfa2c_workload_destroy(dfa2c_workload* w);
+int dfa2c_workload_profile(const dfa2c_workload* w, int64_t layer, int64_t head, double* locality,
+                           double* drift);
+int dfa2c_workload_slot(dfa2c_workload* w, int64_t t, int64_t layer, void* q, void* k, void* v,
+                        void* stream);
+
 /* Kernel launches issued by this library since load (evidence counter). */
 int64_t dfa2c_launch_count(void);
 /* Debug: device buffer (int64 [2][4096][8]) receiving per-tile clock64 stamps

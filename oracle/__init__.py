@@ -103,6 +103,9 @@ def ref() -> ctypes.CDLL:
                                                                              _P(c_float), _P(c_int64)],
             "ref_generate": [c_int64] * 4 + [c_int, c_int64, c_int64, c_int64, c_uint64, _P(c_float), _P(c_float),
                                              _P(c_float)],
+            "ref_calibrate_model": [c_int64] * 4 + [c_int, c_int64, c_int64, c_int64, c_uint64, _P(c_int64), c_int64,
+                                                    c_int, c_double, c_double, _P(c_int32), _P(c_int64), _P(c_double),
+                                                    _P(c_double)],
             "ref_plan_aggregate": [c_int64] * 4 + [c_int, c_int64, c_int64, c_int64, _P(c_int32), _P(c_int64),
                                                    _P(c_int64), _P(c_int64), _P(c_double)],
             "ref_layer_sample": [_P(c_float)] * 5 + [c_int64] * 4 + [c_int, c_int64, _P(c_int32), _P(c_int64),

@@ -276,6 +276,42 @@ REF_API int ref_generate(int64_t H, int64_t d, int64_t nv, int64_t nt, int order
     });
 }
 
+// calibrate_model (calibrate.cpp:255-348) on the reference's own generated
+// workload (workload.cpp:120-228): the selected plan [T*L*H] (kinds,
+// windows) and the per-(t, layer) solver objective and budget spent.
+REF_API int ref_calibrate_model(int64_t H, int64_t d, int64_t nv, int64_t nt, int order,
+                                int64_t L, int64_t T, int64_t B, uint64_t seed,
+                                const int64_t* windows, int64_t n_windows, int include_cached,
+                                double delta, double coeff, int32_t* kinds, int64_t* wins,
+                                double* objective, double* budget) {
+    return guard([&] {
+        dfa2::WorkloadConfig cfg;
+        cfg.dims = make_dims(H, d, nv, nt, order);
+        cfg.n_layers = L;
+        cfg.n_timesteps = T;
+        cfg.block_size = B;
+        cfg.seed = seed;
+        const dfa2::Workload w = dfa2::generate(cfg);
+        dfa2::CalibrationConfig cc;
+        cc.methods = dfa2::make_candidates(std::vector<int64_t>(windows, windows + n_windows),
+                                           include_cached != 0);
+        cc.delta = delta;
+        cc.coeff = coeff;
+        const dfa2::CalibrationResult r = dfa2::calibrate_model(w, cc);
+        for (int64_t s = 0; s < T * L; ++s) {
+            const dfa2::LayerPlan& lp = r.plan.layers[static_cast<size_t>(s)];
+            for (int64_t h = 0; h < H; ++h) {
+                const dfa2::HeadStrategy& st = lp.strategies[static_cast<size_t>(h)];
+                kinds[s * H + h] = st.kind == dfa2::StrategyKind::full ? 0
+                                   : st.kind == dfa2::StrategyKind::arrow ? 1 : 2;
+                wins[s * H + h] = st.kind == dfa2::StrategyKind::arrow ? st.window_blocks : 0;
+            }
+            if (objective) objective[s] = r.stats.objective[static_cast<size_t>(s)];
+            if (budget) budget[s] = r.stats.budget_spent[static_cast<size_t>(s)];
+        }
+    });
+}
+
 // CompressionPlan::aggregate_sparsity (plan.cpp:58-73) over a [T*L*H] plan.
 REF_API int ref_plan_aggregate(int64_t H, int64_t d, int64_t nv, int64_t nt, int order,
                                int64_t T, int64_t L, int64_t B, const int32_t* kinds,

@@ -139,6 +139,10 @@ _SIGS = {
     "dfa2c_nccl_comm_init": (c_int32, [c_char_p, c_int32, c_int32, POINTER(c_void_p)]),
     "dfa2c_nccl_comm_destroy": (c_int32, [c_void_p]),
     "dfa2c_allgather_rows": (c_int32, [c_void_p, c_void_p, POINTER(c_int64), c_int32, c_int64, c_void_p]),
+    "dfa2c_workload_create": (c_int32, [POINTER(Dims), c_int64, c_int64, ctypes.c_uint64, POINTER(c_void_p)]),
+    "dfa2c_workload_destroy": (c_int32, [c_void_p]),
+    "dfa2c_workload_profile": (c_int32, [c_void_p, c_int64, c_int64, POINTER(c_double), POINTER(c_double)]),
+    "dfa2c_workload_slot": (c_int32, [c_void_p, c_int64, c_int64, c_void_p, c_void_p, c_void_p, c_void_p]),
     "dfa2c_attention_reference": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_int32, c_int64, c_int64,
                                             c_int64, POINTER(c_uint8), c_int64, c_void_p]),
     "dfa2c_rse": (c_int32, [c_void_p, c_void_p, c_int32, c_int64, c_int64, c_int32, POINTER(c_double),

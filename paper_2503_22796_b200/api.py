@@ -1308,6 +1308,45 @@ def run_pipeline(q_stream, k_stream, v_stream, plan: CompressionPlan, batch: int
     return stats
 
 
+class DeviceWorkload:
+    """The reference's synthetic drifting Q/K/V stream (generate(),
+    src/workload.cpp:120-228) produced on the GPU (dfa2c_workload_*):
+    slot(t, layer) returns bf16 CUDA q, k, v [H, N, d]. Same model and
+    profiles as the reference; per-element noise from a counter-based Philox
+    stream (a pure function of (seed, t, layer)), so FLUX-scale schedules
+    cost HBM time, not host time."""
+
+    def __init__(self, dims: AttentionDims, n_layers: int, block_size: int, seed: int = 1234):
+        self.dims, self.n_layers, self.block_size, self.seed = dims, n_layers, block_size, seed
+        h = c_void_p()
+        d = dims.c()
+        check(lib().dfa2c_workload_create(byref(d), n_layers, block_size, seed, byref(h)))
+        self._h = h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                lib().dfa2c_workload_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+    def profile(self, layer: int, head: int):
+        loc, drift = c_double(), c_double()
+        check(lib().dfa2c_workload_profile(self._h, layer, head, byref(loc), byref(drift)))
+        return loc.value, drift.value
+
+    def slot(self, t: int, layer: int, out=None, stream=None):
+        torch = _torch()
+        shape = (self.dims.n_heads, self.dims.seq_len(), self.dims.head_dim)
+        q, k, v = out if out is not None else tuple(
+            torch.empty(shape, dtype=torch.bfloat16, device="cuda") for _ in range(3))
+        check(lib().dfa2c_workload_slot(self._h, t, layer, c_void_p(q.data_ptr()), c_void_p(k.data_ptr()),
+                                        c_void_p(v.data_ptr()), c_void_p(_stream_ptr(stream))))
+        return q, k, v
+
+
 def flux68_plan(n_heads: int = 24) -> LayerPlan:
     """The survey's FLUX68 head pattern: head h,
     g = h // 4, r = h % 4 -> r0 Full, r1 Arrow(8), r2 Cached,

@@ -20,8 +20,8 @@ LIB = os.path.join(HERE, "libdfa2_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
-CU_SOURCES = ["attn_sm100.cu", "rse_sm100.cu", "convert_sm100.cu", "reference_sm100.cu"]
-CPP_SOURCES = ["dfa2c.cpp", "json_lite.cpp", "plansolver.cpp", "nccl_dl.cpp"]
+CU_SOURCES = ["attn_sm100.cu", "rse_sm100.cu", "convert_sm100.cu", "reference_sm100.cu", "workload_sm100.cu"]
+CPP_SOURCES = ["dfa2c.cpp", "json_lite.cpp", "plansolver.cpp", "nccl_dl.cpp", "workload_dev.cpp"]
 
 
 def _sources():
