@@ -64,6 +64,12 @@ def test_shard_rows_cover_and_balance(nv, nt, d, plan_text):
         assert max(loads) <= 1.02 * total / W + 300, (W, loads)
 
 
+def test_sample_sharding():
+    from paper_2503_22796_b200 import parallel
+
+    assert parallel.shard_samples(8, 8, 3) == [3] and parallel.shard_samples(5, 2, 1) == [1, 3]
+
+
 def test_shard_rows_batch_and_validation():
     plan = LayerPlan.parse("F A0 C")
     dims = AttentionDims(3, 64, 1024, 77)
