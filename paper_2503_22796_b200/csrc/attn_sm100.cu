@@ -101,6 +101,11 @@ struct Cfg {
 #ifndef DFA2_TRACE
 #define DFA2_TRACE 0
 #endif
+// d = 128: commit V(u-1)'s "empty" barrier right after its last PV instead of
+// after the step's last S MMA (the next V load then starts ~one S earlier)
+#ifndef DFA2_EARLY_VFREE
+#define DFA2_EARLY_VFREE 1
+#endif
 
 // Row max: keys 0..63 are loaded and reduced (8 chains) while keys 64..127
 // are still in flight from TMEM (1), or everything loads first (0).
@@ -111,7 +116,7 @@ struct Cfg {
 #define DFA2_STAMP(L_, j_, k_)                                                          \
     do {                                                                                \
         if (DFA2_TRACE && args.trace && blockIdx.x == 0 && (j_) < 4096)                 \
-            if (DFA2_TRACE == 1 || (k_) < 3)                                                  \
+            if (DFA2_TRACE == 1 || DFA2_TRACE == 3 || (k_) < 3)                               \
                 args.trace[((static_cast<int>(L_) * 4096) + static_cast<int>(j_)) * 8 + (k_)] = clock64(); \
     } while (0)
 
@@ -131,6 +136,9 @@ __device__ __forceinline__ uint32_t p_col(int lane) {
 template <int D>
 constexpr uint32_t P_HI = D == 64 ? 32u : 64u;
 
+#ifndef DFA2_POLY_NOSEL
+#define DFA2_POLY_NOSEL 1
+#endif
 // Two exp2s on the FMA/ALU pipes with packed fp32x2 arithmetic: x = j + f,
 // j = floor(x) by the round-down magic-number add, 2^f by a degree-3
 // minimax polynomial (max rel. error 8.6e-5, far below the bf16 rounding P
@@ -144,8 +152,16 @@ __device__ __forceinline__ float2 ex2_poly2(float2 x) {
     float2 p = __ffma2_rn(make_float2(0.0770652f, 0.0770652f), f, make_float2(0.227647f, 0.227647f));
     p = __ffma2_rn(p, f, make_float2(0.69511634f, 0.69511634f));
     p = __ffma2_rn(p, f, make_float2(1.0f, 1.0f));
+#if DFA2_POLY_NOSEL
+    // no select: at the clamp (x <= -127) t = -127 and f = 0, so p = 1.0 and
+    // the exponent add wraps 0x3F800000 + (-127 << 23) to exactly +0.0;
+    // (-127, -126) gives denormals below 1.2e-38 (P rounds to bf16 anyway)
+    return make_float2(__uint_as_float(__float_as_uint(p.x) + (__float_as_uint(t.x) << 23)),
+                       __uint_as_float(__float_as_uint(p.y) + (__float_as_uint(t.y) << 23)));
+#else
     return make_float2(x.x < -126.f ? 0.f : __uint_as_float(__float_as_uint(p.x) + (__float_as_uint(t.x) << 23)),
                        x.y < -126.f ? 0.f : __uint_as_float(__float_as_uint(p.y) + (__float_as_uint(t.y) << 23)));
+#endif
 }
 
 // Per-row 128-column validity bitmap for a partial tile: key < N and the
@@ -242,6 +258,18 @@ __device__ __forceinline__ void softmax_tile(uint32_t sc, uint32_t oc, float sl2
                                              uint32_t bar_sfree, uint32_t bar_pfree, int pf_parity,
                                              long long* stamp = nullptr) {
     constexpr bool SEP = Cfg<D>::SEP_P;
+#ifdef DFA2_FAKE_SOFTMAX  // timing experiment only: P is whatever S was (garbage)
+    if (SEP) {
+        tc_fence_before();
+        mbar_arrive(bar_sfree);
+    }
+    if (SEP && pf_parity >= 0) mbar_wait(bar_pfree, static_cast<uint32_t>(pf_parity));
+    tc_fence_before();
+    mbar_arrive(bar_half);
+    mbar_arrive(bar_full);
+    l = 1.f;
+    return;
+#endif
     bool pfree_done = !SEP || pf_parity < 0;
     auto wait_pfree = [&] {
         if (!pfree_done) {
@@ -494,7 +522,9 @@ __global__ void __launch_bounds__(384, 1)
                     }
                     const int kt = static_cast<int>(args.tiles[w.tile_begin + kc.j] & TILE_INDEX_MASK);
                     const int st = kcount % KS;
+                    if (DFA2_TRACE == 3 && lane == 0) DFA2_STAMP(2, kcount, 0);
                     mbar_wait(k_empty(st), ((kcount / KS) & 1) ^ 1);
+                    if (DFA2_TRACE == 3 && lane == 0) DFA2_STAMP(2, kcount, 1);
                     if (elect_one()) {
                         mbar_arrive_expect_tx(k_full(st), C::TILE_BYTES);
 #pragma unroll
@@ -509,7 +539,9 @@ __global__ void __launch_bounds__(384, 1)
                 const WorkItem& w = items[vc.it];
                 const int kt = static_cast<int>(args.tiles[w.tile_begin + vc.j] & TILE_INDEX_MASK);
                 const int st = vcount % VS;
+                if (DFA2_TRACE == 3 && lane == 0) DFA2_STAMP(2, vcount, 2);
                 mbar_wait(v_empty(st), ((vcount / VS) & 1) ^ 1);
+                if (DFA2_TRACE == 3 && lane == 0) DFA2_STAMP(2, vcount, 3);
                 if (elect_one()) {
                     mbar_arrive_expect_tx(v_full(st), C::TILE_BYTES);
 #pragma unroll
@@ -547,8 +579,12 @@ __global__ void __launch_bounds__(384, 1)
             bool first_pv = true, any_s = false;
             uint32_t prev = 0;
             const int U = w.n_tiles;
+            uint32_t word_next = U > 0 ? __ldg(args.tiles + w.tile_begin) : 0u;
             for (int u = 0; u <= U; ++u) {
-                const uint32_t word = u < U ? args.tiles[w.tile_begin + u] : 0u;
+                // the next step's word is loaded a step ahead (its L2 latency
+                // would otherwise sit on the issue path of every step)
+                const uint32_t word = word_next;
+                word_next = u + 1 < U ? __ldg(args.tiles + w.tile_begin + u + 1) : 0u;
                 const int vst = vcount % VS;
                 const int kst = kcount % KS;
                 auto do_s = [&] {
@@ -671,13 +707,17 @@ __global__ void __launch_bounds__(384, 1)
                 bool first_pv[2] = {true, true};
                 uint32_t prev = 0;
                 const int U = w.n_tiles;
+                uint32_t word_next = U > 0 ? __ldg(args.tiles + w.tile_begin) : 0u;
                 for (int u = 0; u <= U; ++u) {
-                    const uint32_t word = u < U ? args.tiles[w.tile_begin + u] : 0u;
+                    // the next step's word is loaded a step ahead (its L2 latency
+                    // would otherwise sit on the issue path of every step)
+                    const uint32_t word = word_next;
+                    word_next = u + 1 < U ? __ldg(args.tiles + w.tile_begin + u + 1) : 0u;
                     const int vst = vcount % VS;
                     const int kst = kcount % KS;
                     const uint32_t v_addr = sbase + C::V_OFF + vst * C::TILE_BYTES;
                     const uint32_t k_addr = sbase + C::K_OFF + kst * C::TILE_BYTES;
-                    bool v_ready = false, k_ready = false;
+                    bool v_ready = false, k_ready = false, v_freed = false;
                     // lane by lane: O_L += P_L(u-1) V(u-1), then S_L = Q_L K(u)^T, so
                     // lane A's next S overlaps lane B's softmax and vice versa.
 #pragma unroll
@@ -685,10 +725,11 @@ __global__ void __launch_bounds__(384, 1)
                         const uint32_t need = L ? TILE_NEED_B : TILE_NEED_A;
                         auto issue_pv = [&] {
                             if (!v_ready) {
+                                if (DFA2_TRACE == 3 && lane == 0) DFA2_STAMP(3, vcount, 0);
                                 mbar_wait(v_full(vst), (vcount / VS) & 1);
                                 v_ready = true;
                             }
-                            if (DFA2_TRACE == 1 && lane == 0) DFA2_STAMP(L, pcnt[L], 7);
+                            if ((DFA2_TRACE == 1 || DFA2_TRACE == 3) && lane == 0) DFA2_STAMP(L, pcnt[L], 7);
                             // keys 64..127 (P in cols [64,96)) as soon as that half is ready,
                             // then keys 0..63 (cols [0,32))
                             const uint64_t vdesc = smem_desc_sw128(v_addr, C::BOX_BYTES, 1024);
@@ -730,7 +771,7 @@ __global__ void __launch_bounds__(384, 1)
                                 mbar_wait(k_full(kst), (kcount / KS) & 1);
                                 k_ready = true;
                             }
-                            if (DFA2_TRACE == 1 && lane == 0) DFA2_STAMP(L, scount[L], 6);
+                            if ((DFA2_TRACE == 1 || DFA2_TRACE == 3) && lane == 0) DFA2_STAMP(L, scount[L], 6);
                             tc_fence_after();
                             const uint64_t qdesc = smem_desc_sw128(qbase + L * C::TILE_BYTES, 16, 1024);
                             const uint64_t kdesc = smem_desc_sw128(k_addr, 16, 1024);
@@ -754,14 +795,25 @@ __global__ void __launch_bounds__(384, 1)
                             if (do_pv)
                                 issue_pv();
                         } else {
-                            if (do_pv)
+                            if (do_pv) {
                                 issue_pv();
+                                // V(u-1) is free once its last PV completes: release it
+                                // before this lane's S so the producer's next V load
+                                // does not also wait for that S
+                                if (DFA2_EARLY_VFREE && (L == 1 || !(prev & TILE_NEED_B))) {
+                                    if (elect_one())
+                                        mma_commit(v_empty(vst));
+                                    __syncwarp();
+                                    v_freed = true;
+                                }
+                            }
                             if (do_s)
                                 issue_s();
                         }
                     }
+                    if (DFA2_TRACE == 3 && lane == 0) DFA2_STAMP(3, kcount, 1);
                     if (elect_one()) {
-                        if (u >= 1)
+                        if (u >= 1 && !v_freed)
                             mma_commit(v_empty(vst));  // V(u-1) free once its PVs complete
                         if (u < U) {
                             mma_commit(k_empty(kst));  // K(u) free once its S MMAs complete
@@ -770,6 +822,7 @@ __global__ void __launch_bounds__(384, 1)
                         }
                     }
                     __syncwarp();
+                    if (DFA2_TRACE == 3 && lane == 0) DFA2_STAMP(3, kcount, 2);
                     if (u >= 1)
                         ++vcount;
                     if (u < U)
@@ -876,8 +929,11 @@ __global__ void __launch_bounds__(384, 1)
             };
             const uint32_t snap_bit = L ? TILE_SNAP_B : TILE_SNAP_A;
             int sidx = 0;
+            uint32_t word_next = __ldg(args.tiles + w.tile_begin);
             for (int u = 0; u < w.n_tiles; ++u) {
-                const uint32_t word = args.tiles[w.tile_begin + u];
+                const uint32_t word = word_next;
+                if (u + 1 < w.n_tiles)
+                    word_next = __ldg(args.tiles + w.tile_begin + u + 1);
                 if (!(word & need_bit))
                     continue;
                 uint32_t vm[4] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu};

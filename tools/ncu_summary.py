@@ -18,7 +18,9 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "sm__warps_active.avg.per_cycle_active", "launch__registers_per_thread",
         "sm__cycles_elapsed.avg.per_second", "lts__t_sector_hit_rate.pct",
         "dram__throughput.avg.pct_of_peak_sustained_elapsed", "launch__grid_size", "launch__block_size",
-        "smsp__inst_executed.sum", "launch__shared_mem_per_block_dynamic"]
+        "smsp__inst_executed.sum", "launch__shared_mem_per_block_dynamic",
+        "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active", "smsp__issue_active.avg.pct_of_peak_sustained_active",
+        "lts__throughput.avg.pct_of_peak_sustained_elapsed", "l1tex__m_xbar2l1tex_read_bytes.sum"]
 
 
 def raw(rep):
