@@ -411,6 +411,23 @@ def main():
             "nccl_ranks": world if comm is not None else 0}
         if comm is not None:
             comm.close()
+        if world == 1:
+            # strong scaling emulated on this GPU: each rank r of W runs exactly
+            # the launch its own GPU would (same row range, no gather), timed
+            # alone; the per-GPU compute at W GPUs is the max over ranks
+            emu = {}
+            for W in (2, 4, 8):
+                per = []
+                for r in range(W):
+                    fn = lambda: api.multi_strategy_attention_sharded(sq, sk, sv, lp, s_cache, 0, 1, dims, BLOCK,
+                                                                      r, W, out=s_out)
+                    per.append(timed(fn, max(5, args.steps // 2), 3)[0])
+                emu[str(W)] = {"per_rank_compute_ms": per, "max_ms": max(per),
+                               "x_ideal_vs_1gpu_layer": max(per) * W / ms}
+            line["row_sharded"]["emulated_ranks"] = {
+                "what": "per-GPU compute of the row-sharded layer at W GPUs, every rank's launch timed alone on "
+                        "this GPU (gather not included); x_ideal_vs_1gpu_layer = max_ms * W / layer_ms",
+                "worlds": emu}
 
         # e2e through the public API with HOST buffers: dfa2c_mha_forward_host
         # uploads the computed heads' q/k/v from pinned memory in head groups,

@@ -1047,11 +1047,30 @@ __global__ void __launch_bounds__(384, 1)
                 auto ml = [&](int c, int which) {
                     return __ldcg(args.part_ml + ((static_cast<size_t>(slot0 + c) * 2 + L) * 2 + which) * TILE_M + r);
                 };
+                // the first CW chunks' (max, sum) are loaded together and kept
+                // in registers (a split pair has 2-4 chunks at FLUX sizes), so
+                // the fold's global round trips do not serialise per chunk; the
+                // arithmetic and its order are the same for every chunk count
+                constexpr int CW = 8;
+                const int nc = w.nchunk;
+                float mcv[CW], lcv[CW];
+#pragma unroll
+                for (int c = 0; c < CW; ++c) {
+                    mcv[c] = c < nc ? ml(c, 0) : -INFINITY;
+                    lcv[c] = c < nc ? ml(c, 1) : 0.f;
+                }
                 float m = -INFINITY;
-                for (int c = 0; c < w.nchunk; ++c)
+#pragma unroll
+                for (int c = 0; c < CW; ++c)
+                    m = fmaxf(m, mcv[c]);
+                for (int c = CW; c < nc; ++c)
                     m = fmaxf(m, ml(c, 0));
                 float lsum = 0.f;
-                for (int c = 0; c < w.nchunk; ++c) {
+#pragma unroll
+                for (int c = 0; c < CW; ++c)
+                    if (mcv[c] != -INFINITY)
+                        lsum += exp2f(mcv[c] - m) * lcv[c];
+                for (int c = CW; c < nc; ++c) {
                     const float mc = ml(c, 0);
                     if (mc != -INFINITY)
                         lsum += exp2f(mc - m) * ml(c, 1);
@@ -1062,8 +1081,14 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
                     for (int i = 0; i < 64; ++i)
                         acc[i] = 0.f;
-                    for (int c = 0; c < w.nchunk; ++c) {
-                        const float mc = ml(c, 0);
+                    for (int c = 0; c < nc; ++c) {
+                        float mc = -INFINITY;
+#pragma unroll
+                        for (int j = 0; j < CW; ++j)
+                            if (j == c)
+                                mc = mcv[j];
+                        if (c >= CW)
+                            mc = ml(c, 0);
                         if (mc == -INFINITY)
                             continue;  // this lane folded no tile in chunk c
                         const float wc = exp2f(mc - m);

@@ -521,7 +521,35 @@ std::unique_ptr<DevPlan> schedule_items(int device, std::vector<Cand>& cands, co
 // span of the flattened [batch*H*N] output rows. Long pairs are split into
 // key chunks against a fixed reference of kShardRefSMs SMs (an 8-GPU box),
 // whatever the GPU count, so a head's bits are the same for every n_parts.
-constexpr double kShardRefSMs = 148.0 * 8;
+double shard_ref_sms() {
+    static const double v = [] {
+        const char* e = std::getenv("DFA2_SHARD_REF_SMS");  // A/B only
+        return e ? std::atof(e) : 148.0 * 8;
+    }();
+    return v;
+}
+
+// Key-chunk boundaries of a split pair: chunk c gets a share of the union
+// tiles proportional to (nch - c), e.g. 1/2, 1/3, 1/6 for three chunks.
+// Unequal chunks give the LPT assignment small items to fill the CTAs that
+// the large ones leave short: a sharded rank whose range is all Full pairs
+// (192 equal chunks on 148 SMs at 8 GPUs) otherwise ends one whole chunk
+// late on a third of its SMs. Every chunk keeps at least one tile; the cut
+// depends only on (U, nch), so results stay independent of the GPU count.
+std::vector<int32_t> chunk_bounds(int32_t U, int32_t nch) {
+    std::vector<int32_t> cut(static_cast<size_t>(nch) + 1, 0);
+    const int64_t W = int64_t{nch} * (nch + 1) / 2;
+    int64_t acc = 0;
+    for (int32_t c = 0; c < nch; ++c) {
+        acc += nch - c;
+        int64_t b = (acc * U + W / 2) / W;
+        b = std::max<int64_t>(b, cut[c] + 1);            // non-empty
+        b = std::min<int64_t>(b, U - (nch - 1 - c));      // room for the rest
+        cut[c + 1] = static_cast<int32_t>(b);
+    }
+    cut[nch] = U;
+    return cut;
+}
 
 // Host-side geometry of a work list: per-mask pair sets and their tile
 // words, the split-KV chunking, and for sharded launches the partition.
@@ -588,7 +616,7 @@ PlanGeometry plan_geometry(int64_t batch, int64_t H, int64_t n, int64_t B,
     // why it is off by default: with it off every head's result is a
     // function of its own strategy alone (head isolation, bitwise,
     // test_dispatch.cpp:98-109).
-    const double kRefSMs = sharded ? kShardRefSMs : 148.0;
+    const double kRefSMs = sharded ? shard_ref_sms() : 148.0;
     chunks_of.resize(sets.size());
     for (size_t mi = 0; mi < sets.size(); ++mi)
         chunks_of[mi].assign(sets[mi].qa.size(), 1);
@@ -724,10 +752,10 @@ std::unique_ptr<DevPlan> build_dev_plan(int device, int64_t batch, int64_t H, in
                         continue;
                     }
                     const int32_t U = w.n_tiles, begin = w.tile_begin;
+                    const std::vector<int32_t> cut = chunk_bounds(U, nch);
                     for (int32_t c = 0; c < nch; ++c) {
                         WorkItem cw = w;
-                        const int32_t lo = static_cast<int32_t>(int64_t{c} * U / nch);
-                        const int32_t hi = static_cast<int32_t>(int64_t{c + 1} * U / nch);
+                        const int32_t lo = cut[c], hi = cut[c + 1];
                         cw.tile_begin = begin + lo;
                         cw.n_tiles = hi - lo;
                         cw.flags |= dfa2k::ITEM_SPLIT;
