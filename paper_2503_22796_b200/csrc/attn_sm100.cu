@@ -32,6 +32,8 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
+
 #include "attn_types.h"
 #include "sm100_ptx.cuh"
 
@@ -120,7 +122,28 @@ struct Cfg {
                 args.trace[((static_cast<int>(L_) * 4096) + static_cast<int>(j_)) * 8 + (k_)] = clock64(); \
     } while (0)
 
+// Read-once / write-once TMA traffic (Q tiles, cached slots read for copies,
+// outputs and cache commits) is tagged L2::evict_first so the K/V tiles that
+// every query-tile pair of a head re-streams keep their L2 residency.
+#ifndef DFA2_L2_HINTS
+#define DFA2_L2_HINTS 1
+#endif
+
 namespace {
+
+__device__ __forceinline__ void tma_load_q(uint32_t dst, const CUtensorMap* map, uint32_t bar, int32_t c0, int32_t c1,
+                                           int32_t c2) {
+    if (DFA2_L2_HINTS)
+        tma_load_3d_hint(dst, map, bar, c0, c1, c2, policy_evict_first());
+    else
+        tma_load_3d(dst, map, bar, c0, c1, c2);
+}
+__device__ __forceinline__ void tma_store_o(const CUtensorMap* map, uint32_t src, int32_t c0, int32_t c1, int32_t c2) {
+    if (DFA2_L2_HINTS)
+        tma_store_3d_hint(map, src, c0, c1, c2, policy_evict_first());
+    else
+        tma_store_3d(map, src, c0, c1, c2);
+}
 
 __device__ __forceinline__ uint32_t s_col(int lane) { return lane ? 128u : 0u; }
 template <int D>
@@ -510,10 +533,10 @@ __global__ void __launch_bounds__(384, 1)
                             mbar_arrive_expect_tx(q_full(qs), nq * C::TILE_BYTES);
 #pragma unroll
                             for (int b = 0; b < C::BOXES; ++b) {
-                                tma_load_3d(qaddr + b * C::BOX_BYTES, &tmq, q_full(qs), b * 64, w.qtile_a * TILE_M,
-                                            w.bh);
+                                tma_load_q(qaddr + b * C::BOX_BYTES, &tmq, q_full(qs), b * 64, w.qtile_a * TILE_M,
+                                           w.bh);
                                 if (nq == 2)
-                                    tma_load_3d(qaddr + C::TILE_BYTES + b * C::BOX_BYTES, &tmq, q_full(qs), b * 64,
+                                    tma_load_q(qaddr + C::TILE_BYTES + b * C::BOX_BYTES, &tmq, q_full(qs), b * 64,
                                                 w.qtile_b * TILE_M, w.bh);
                             }
                         }
@@ -865,10 +888,10 @@ __global__ void __launch_bounds__(384, 1)
                     for (int b = 0; b < D / 64; ++b) {
                         bulk_wait_read0();  // staging free
                         mbar_arrive_expect_tx(c_full(L), C::BOX_BYTES);
-                        tma_load_3d(stg, &tmc, c_full(L), b * 64, qt * TILE_M, w.bh);
+                        tma_load_q(stg, &tmc, c_full(L), b * 64, qt * TILE_M, w.bh);
                         mbar_wait(c_full(L), ccnt & 1);
                         ++ccnt;
-                        tma_store_3d(&tmo, stg, b * 64, qt * TILE_M, w.bh);
+                        tma_store_o(&tmo, stg, b * 64, qt * TILE_M, w.bh);
                         bulk_commit();
                     }
                 }
@@ -904,9 +927,9 @@ __global__ void __launch_bounds__(384, 1)
                 named_bar_sync(1 + L, 128);
                 if (issuer) {
                     if (!multi) {
-                        tma_store_3d(&tmo, stg, b * 64, qt * TILE_M, w.bh);  // rows >= N are clipped
+                        tma_store_o(&tmo, stg, b * 64, qt * TILE_M, w.bh);  // rows >= N are clipped
                         if (commit)
-                            tma_store_3d(&tmc, stg, b * 64, qt * TILE_M, w.bh);
+                            tma_store_o(&tmc, stg, b * 64, qt * TILE_M, w.bh);
                     } else {
                         if (dst & SNAP_ORIGINAL)
                             tma_store_3d(&tmc, stg, b * 64, qt * TILE_M, w.bh);
@@ -1125,15 +1148,19 @@ template <int D>
 cudaError_t launch_d(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const CUtensorMap& to,
                      const CUtensorMap& tc, const AttnArgs& args, int grid, cudaStream_t stream) {
     using C = Cfg<D>;
-    static int configured_for = -1;  // device the smem attribute was set on
+    // the smem attribute is per (function, device): set once per device; the
+    // bitmask is atomic, so host threads driving different GPUs (one per
+    // rank) never race on it (a redundant set is harmless)
+    static std::atomic<uint64_t> configured{0};
     int dev = 0;
     cudaGetDevice(&dev);
-    if (configured_for != dev) {
+    const uint64_t bit = dev < 64 ? uint64_t{1} << dev : 0;
+    if (!bit || !(configured.load(std::memory_order_acquire) & bit)) {
         const cudaError_t e =
             cudaFuncSetAttribute(attn_fwd_sm100<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_BYTES);
         if (e != cudaSuccess)
             return e;
-        configured_for = dev;
+        configured.fetch_or(bit, std::memory_order_acq_rel);
     }
     attn_fwd_sm100<D><<<grid, C::THREADS, C::SMEM_BYTES, stream>>>(tq, tk, tv, to, tc, args);
     return cudaGetLastError();

@@ -21,6 +21,9 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <mutex>
+#include <set>
+#include <utility>
 
 #include "sm100_ptx.cuh"
 
@@ -387,17 +390,24 @@ __global__ void rse_finalize(const T* __restrict__ yo, const double* __restrict_
 }
 
 namespace {
+// true the first time a (kernel, device) pair is seen: the smem attribute is
+// then set once instead of on every launch; thread-safe (one host thread per
+// GPU), a rare duplicate set is harmless
+template <int KIND>
+bool needs_smem_attr(const void* fn) {
+    static std::mutex mu;
+    static std::set<std::pair<const void*, int>> seen;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    return seen.insert({fn, dev}).second;
+}
+
 template <typename T, bool LIT>
 void launch_partial(const dim3& grid, const T* m, const T* o, int64_t numel, int64_t chunk, int vec_ok,
                     double* scratch, cudaStream_t stream) {
-    static uint64_t configured = 0;  // bit per device the smem attribute was set on
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (dev >= 64 || !((configured >> dev) & 1u)) {
+    if (needs_smem_attr<0>(reinterpret_cast<const void*>(rse_partial<T, LIT>)))
         cudaFuncSetAttribute(rse_partial<T, LIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, RSE_SMEM);
-        if (dev < 64)
-            configured |= uint64_t{1} << dev;
-    }
     rse_partial<T, LIT><<<grid, RSE_THREADS + 32, RSE_SMEM, stream>>>(m, o, numel, chunk, vec_ok, scratch);
 }
 
@@ -430,7 +440,8 @@ void launch_multi_typed(const void* const* ym, int M, const void* yo, int64_t n_
     const dim3 grid(nblk, static_cast<unsigned>(n_heads));
     const uint32_t smem = rse_multi_smem(M);
     auto kern = mode == 0 ? rse_multi_partial<T, false> : rse_multi_partial<T, true>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, rse_multi_smem(RSE_MAXM));
+    if (needs_smem_attr<1>(reinterpret_cast<const void*>(kern)))
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, rse_multi_smem(RSE_MAXM));
     kern<<<grid, RSE_THREADS + 32, smem, stream>>>(c, M, static_cast<const T*>(yo), numel, chunk, vec_ok, scratch);
     const int sets = static_cast<int>(M * n_heads);
     rse_finalize<T><<<(sets + 7) / 8, 256, 0, stream>>>(static_cast<const T*>(yo), scratch, nblk, sets,
