@@ -117,7 +117,7 @@ struct Cfg {
 // trace[((lane * 4096) + tile) * 8 + slot] = clock64() for CTA 0 (debug builds)
 #define DFA2_STAMP(L_, j_, k_)                                                          \
     do {                                                                                \
-        if (DFA2_TRACE && args.trace && blockIdx.x == 0 && (j_) < 4096)                 \
+        if (DFA2_TRACE && DFA2_TRACE != 4 && args.trace && blockIdx.x == 0 && (j_) < 4096) \
             if (DFA2_TRACE == 1 || DFA2_TRACE == 3 || (k_) < 3)                               \
                 args.trace[((static_cast<int>(L_) * 4096) + static_cast<int>(j_)) * 8 + (k_)] = clock64(); \
     } while (0)
@@ -502,6 +502,15 @@ __global__ void __launch_bounds__(384, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    // DFA2_TRACE == 4: per-CTA start / end (globaltimer ns) and the end of
+    // each lane's softmax work, to see the schedule's tail
+    auto gtime = [] {
+        uint64_t t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        return static_cast<long long>(t);
+    };
+    if (DFA2_TRACE == 4 && args.trace && threadIdx.x == 0)
+        args.trace[blockIdx.x * 4 + 0] = gtime();
 
     const int it0 = args.cta_begin[blockIdx.x];
     const int it1 = args.cta_begin[blockIdx.x + 1];
@@ -1128,9 +1137,13 @@ __global__ void __launch_bounds__(384, 1)
             bulk_wait0();  // every bulk store of this lane has completed
     }
 
+    if (DFA2_TRACE == 4 && args.trace && (threadIdx.x == 128 || threadIdx.x == 256))
+        args.trace[blockIdx.x * 4 + 1 + (threadIdx.x >> 8)] = gtime();  // lane A / B softmax done
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+    if (DFA2_TRACE == 4 && args.trace && threadIdx.x == 0)
+        args.trace[blockIdx.x * 4 + 3] = gtime();
     if (warp == 2)
         tmem_dealloc(tmem, C::TMEM_COLS);
 }
