@@ -888,6 +888,13 @@ __global__ void __launch_bounds__(384, 1)
         uint32_t scnt = 0, icnt = 0, ccnt = 0;
         for (int it = it0; it < it1; ++it) {
             const WorkItem w = items[it];
+            if (DFA2_TRACE == 4 && args.trace && L == 0 && r == 0 && it < 8192) {  // per-item start (lane A)
+                long long* ti = args.trace + 148 * 4 + static_cast<size_t>(it) * 4;
+                ti[0] = gtime();
+                ti[1] = static_cast<long long>(w.n_tiles) | (static_cast<long long>(w.flags) << 16) |
+                        (w.qtile_b < 0 ? (1ll << 30) : 0ll);
+                ti[2] = blockIdx.x;
+            }
             if (w.flags & ITEM_COPY) {
                 // Cached head: out <- stored slot, one 128-row tile per lane,
                 // 64-column boxes through the lane's staging buffer by TMA.

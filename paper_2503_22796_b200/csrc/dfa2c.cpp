@@ -416,7 +416,11 @@ inline uint32_t tag_lane(uint32_t c, int lane) {
 }
 
 // text_tile[q]: query tile q runs as a HALVES entry candidate (empty: none)
-PairSet build_pair_set(const TileSet& ts, int64_t nqt, const std::vector<uint8_t>& text_tile, int64_t ratio) {
+// halve_single: a query tile left without a partner (odd tile count) runs as
+// a HALVES entry too, so it keeps both lanes busy instead of folding its whole
+// key row on one lane (d = 64, SD3's ragged 35th tile).
+PairSet build_pair_set(const TileSet& ts, int64_t nqt, const std::vector<uint8_t>& text_tile, int64_t ratio,
+                       bool halve_single) {
     PairSet ps;
     ps.row_ptr.push_back(0);
     ps.words.reserve(ts.cols.size());
@@ -463,9 +467,19 @@ PairSet build_pair_set(const TileSet& ts, int64_t nqt, const std::vector<uint8_t
         ps.halves.push_back(1);
         ps.row_ptr.push_back(static_cast<int64_t>(ps.words.size()));
     };
+    auto add_single = [&](int64_t q) {
+        if (halve_single && ts.row_ptr[q + 1] - ts.row_ptr[q] >= 2)
+            add_halves(q);
+        else
+            add_pair(q, -1);
+    };
     if (text_tile.empty()) {
-        for (int64_t q = 0; q < nqt; q += 2)
-            add_pair(q, q + 1 < nqt ? q + 1 : -1);
+        for (int64_t q = 0; q < nqt; q += 2) {
+            if (q + 1 < nqt)
+                add_pair(q, q + 1);
+            else
+                add_single(q);
+        }
         return ps;
     }
     // Halve only when the text rows are the mask's long pole: their key
@@ -495,8 +509,21 @@ PairSet build_pair_set(const TileSet& ts, int64_t nqt, const std::vector<uint8_t
         }
     }
     if (pending >= 0)
-        add_pair(pending, -1);
+        add_single(pending);
     return ps;
+}
+
+// Scheduling cost of a pair-set entry in lane-tile units: a step of the
+// shared K/V stream costs one period whether one or both lanes fold it, so a
+// pair costs 2 x its union length (a single-lane entry as much as a full
+// pair); a HALVES entry's steps alternate between the lanes, each ~0.6 of a
+// pair step (measured per item with -DDFA2_TRACE=4, tools/cta_tail.py
+// --items: 1.05 vs 1.77 us per step at d = 64), so 1.2 per folded tile.
+// +1 for the item's ramp.
+double entry_cost(const PairSet& ps, size_t p) {
+    if (ps.halves[p])
+        return 1.2 * (ps.n_a[p] + ps.n_b[p]) + 1.0;
+    return 2.0 * static_cast<double>(ps.row_ptr[p + 1] - ps.row_ptr[p]) + 1.0;
 }
 
 struct Cand {
@@ -588,7 +615,8 @@ PlanGeometry plan_geometry(int64_t batch, int64_t H, int64_t n, int64_t B,
         }
     }
     for (const auto& m : masks) {
-        sets.push_back(build_pair_set(build_tile_set(m.data(), n, B), nqt, text_tile, halve_ratio));
+        sets.push_back(build_pair_set(build_tile_set(m.data(), n, B), nqt, text_tile, halve_ratio,
+                                      halve_ratio > 0 && !split_kv_enabled() && !sharded));
         mask_tile_base.push_back(static_cast<int64_t>(tiles.size()));
         tiles.insert(tiles.end(), sets.back().words.begin(), sets.back().words.end());
         mask_off.push_back(static_cast<int64_t>(mask_bytes.size()));
@@ -630,13 +658,13 @@ PlanGeometry plan_geometry(int64_t batch, int64_t H, int64_t n, int64_t B,
             }
             const PairSet& ps = sets[rj];
             for (size_t p = 0; p < ps.qa.size(); ++p)
-                per_sample += ps.n_a[p] + ps.n_b[p] + 1.0;
+                per_sample += entry_cost(ps, p);
         }
         const double avg = std::max(per_sample / kRefSMs, 1.0);
         for (size_t mi = 0; mi < sets.size(); ++mi) {
             const PairSet& ps = sets[mi];
             for (size_t p = 0; p < ps.qa.size(); ++p) {
-                const double cost = ps.n_a[p] + ps.n_b[p] + 1.0;
+                const double cost = entry_cost(ps, p);
                 const int64_t len = ps.row_ptr[p + 1] - ps.row_ptr[p];
                 if (cost > avg && len >= 8)
                     chunks_of[mi][p] = static_cast<int32_t>(
@@ -664,7 +692,7 @@ PlanGeometry plan_geometry(int64_t batch, int64_t H, int64_t n, int64_t B,
                     } else {
                         const PairSet& ps = sets[rj];
                         const int32_t nch = chunks_of[rj][p];
-                        cost.push_back(ps.n_a[p] + ps.n_b[p] + 1.0 + (nch > 1 ? 0.5 * nch : 0.0));
+                        cost.push_back(entry_cost(ps, p) + (nch > 1 ? 0.5 * nch : 0.0));
                     }
                     row_end.push_back((b * H + h) * n + r1);
                 }
@@ -748,7 +776,7 @@ std::unique_ptr<DevPlan> build_dev_plan(int device, int64_t batch, int64_t H, in
                         fail(DFA2C_FULLY_MASKED, "query tile " + std::to_string(w.qtile_b) + " has no active key tiles");
                     const int32_t nch = chunks_of[j.mask_id][p];
                     if (nch <= 1) {
-                        cands.push_back({w, (ps.n_a[p] + ps.n_b[p]) * (dfa2k::TILE_N / 128.0) + 1.0});
+                        cands.push_back({w, entry_cost(ps, p)});
                         continue;
                     }
                     const int32_t U = w.n_tiles, begin = w.tile_begin;
@@ -763,10 +791,8 @@ std::unique_ptr<DevPlan> build_dev_plan(int device, int64_t batch, int64_t H, in
                         cw.chunk = c;
                         cw.nchunk = nch;
                         cw.part = n_slots + c;
-                        int64_t fold = 0;
-                        for (int32_t u = cw.tile_begin; u < cw.tile_begin + cw.n_tiles; ++u)
-                            fold += ((tiles[u] & dfa2k::TILE_NEED_A) != 0) + ((tiles[u] & dfa2k::TILE_NEED_B) != 0);
-                        cands.push_back({cw, static_cast<double>(fold) + 1.5});
+                        // a chunk's steps cost one period each (split pairs are never HALVES)
+                        cands.push_back({cw, 2.0 * cw.n_tiles + 1.5});
                     }
                     ++n_groups;
                     n_slots += nch;
