@@ -1141,11 +1141,100 @@ void run_padded(const ForwardSpec& s, cudaStream_t st) {
         DFA2C_CUDA_CHECK(cudaFreeAsync(x, st));
 }
 
+// Head dims above 128 (the reference accepts any d >= 1, src/tensor.cpp:
+// 225-230): the tcgen05 kernel's TMEM budget (two lanes of S + O) holds
+// d <= 128, so wider heads run through the SIMT attention kernel
+// (reference_sm100.cu, one warp per query row) in f32 on the bf16 inputs,
+// head by head with the head's own block mask, and the result is rounded to
+// bf16 like the fused path's. Cached heads and cache commits are copies on
+// the same stream. Correct for any plan; not the performance path.
+void run_wide(const ForwardSpec& s, cudaStream_t st) {
+    const int64_t n = seq_len(s.dims), d = s.dims->head_dim, H = s.dims->n_heads;
+    if (s.batch < 1)
+        fail(DFA2C_SHAPE, "batch must be >= 1");
+    if (s.n_parts > 0)
+        fail(DFA2C_UNSUPPORTED, "sharded launches need head_dim <= 128");
+    check_ptr(s.q, "q");
+    check_ptr(s.k, "k");
+    check_ptr(s.v, "v");
+    check_ptr(s.out, "out");
+    const int64_t nb = ceil_div(n, s.block);
+    const size_t head_elems = static_cast<size_t>(n * d);
+    const size_t head_bytes = head_elems * 2;
+    int device = 0;
+    DFA2C_CUDA_CHECK(cudaGetDevice(&device));
+    const int sms = num_sms(device);
+    // distinct masks on the device (null: every key of every row)
+    std::vector<void*> dmasks;
+    const size_t n_masks = std::max(s.masks.size(), s.mask_windows.size());
+    for (size_t m = 0; m < n_masks; ++m) {
+        std::vector<uint8_t> bytes;
+        if (!s.masks.empty())
+            bytes = s.masks[m];
+        else if (s.mask_windows[m] >= 0)
+            bytes = arrow_mask(s.dims, s.block, s.mask_windows[m]);
+        void* dm = nullptr;
+        if (!bytes.empty()) {
+            for (int64_t r = 0; r < nb; ++r)  // FullyMaskedRowError before any compute
+                if (std::none_of(bytes.begin() + r * nb, bytes.begin() + (r + 1) * nb, [](uint8_t x) { return x; }))
+                    fail(DFA2C_FULLY_MASKED, "query block " + std::to_string(r) + " has no active key blocks");
+            scratch_alloc(&dm, bytes.size(), st);
+            DFA2C_CUDA_CHECK(cudaMemcpyAsync(dm, bytes.data(), bytes.size(), cudaMemcpyHostToDevice, st));
+        }
+        dmasks.push_back(dm);
+    }
+    void* cache_layer = nullptr;
+    for (const HeadJob& j : s.jobs)
+        if ((j.mask_id == JOB_COPY || j.commit) && !cache_layer) {
+            if (!s.cache)
+                fail(DFA2C_CACHE_MISS, "cached heads need a cache");
+            s.cache->ensure(s.layer);
+            cache_layer = s.cache->layer_ptr(s.layer, st);
+        }
+    void *qf = nullptr, *kf = nullptr, *vf = nullptr, *of = nullptr;
+    for (void** p : {&qf, &kf, &vf, &of})
+        scratch_alloc(p, head_elems * 4, st);
+    for (int64_t b = 0; b < s.batch; ++b)
+        for (int64_t h = 0; h < H; ++h) {
+            const HeadJob& j = s.jobs[h];
+            const size_t off = static_cast<size_t>(b * H + h) * head_bytes;
+            char* o = static_cast<char*>(s.out) + off;
+            if (j.mask_id == JOB_SKIP)
+                continue;
+            if (j.mask_id == JOB_COPY) {
+                DFA2C_CUDA_CHECK(cudaMemcpyAsync(o, static_cast<const char*>(cache_layer) + off, head_bytes,
+                                                 cudaMemcpyDeviceToDevice, st));
+                continue;
+            }
+            const std::pair<const void*, void*> ins[3] = {{s.q, qf}, {s.k, kf}, {s.v, vf}};
+            for (const auto& [src, dst] : ins)
+                DFA2C_CUDA_CHECK(dfa2k::launch_convert(static_cast<const char*>(src) + off, DFA2C_BF16, dst, DFA2C_F32,
+                                                       static_cast<int64_t>(head_elems), sms, st));
+            DFA2C_CUDA_CHECK(dfa2k::launch_attention_reference(qf, kf, vf, of, DFA2C_F32, 1, n, d,
+                                                               static_cast<const uint8_t*>(dmasks[j.mask_id]),
+                                                               s.block, nb, st));
+            DFA2C_CUDA_CHECK(dfa2k::launch_convert(of, DFA2C_F32, o, DFA2C_BF16, static_cast<int64_t>(head_elems),
+                                                   sms, st));
+            if (j.commit)
+                DFA2C_CUDA_CHECK(cudaMemcpyAsync(static_cast<char*>(cache_layer) + off, o, head_bytes,
+                                                 cudaMemcpyDeviceToDevice, st));
+        }
+    for (void* x : {qf, kf, vf, of})
+        DFA2C_CUDA_CHECK(cudaFreeAsync(x, st));
+    for (void* dm : dmasks)
+        if (dm)
+            DFA2C_CUDA_CHECK(cudaFreeAsync(dm, st));
+    g_launches.fetch_add(1);
+}
+
 void run_forward(const ForwardSpec& s, cudaStream_t stream) {
     const int64_t d = s.dims->head_dim;
-    if (d < 1 || d > 128)
-        fail(DFA2C_UNSUPPORTED, "head_dim must be in [1, 128] on the sm_100a path (got " + std::to_string(d) + ")");
-    if (direct_layout(d))
+    if (d < 1 || d > dfa2k::reference_max_head_dim())
+        fail(DFA2C_UNSUPPORTED, "head_dim must be in [1, " + std::to_string(dfa2k::reference_max_head_dim()) +
+                                    "] (got " + std::to_string(d) + ")");
+    if (d > 128)
+        run_wide(s, stream);
+    else if (direct_layout(d))
         launch_forward(s, stream);
     else
         run_padded(s, stream);

@@ -185,6 +185,38 @@ def test_padded_head_dim_cache_semantics():
         check_close(to_np(o1[h]), oracle_head(q1n[h], q1n[h], q1n[h], dims, B, lp.strategies[h]))
 
 
+@pytest.mark.parametrize("d", [160, 256, 512])
+def test_wide_head_dims_through_the_simt_path(d):
+    """head_dim > 128 (the reference accepts any d >= 1, src/tensor.cpp:225-230)
+    runs head by head through the SIMT attention kernel in f32 on the bf16
+    inputs: same plan semantics (Full / Arrow / Cached, commits, FullyMasked)
+    and the same tolerance against the f64 oracle."""
+    t = torch()
+    H, nv, nt, B = 3, 300, 40, 64
+    n = nv + nt
+    dims = AttentionDims(H, d, nv, nt)
+    cache = HeadCache(1, H, n, d)
+    q, qn = bf16_inputs((H, n, d), 71)
+    k, kn = bf16_inputs((H, n, d), 72)
+    v, vn = bf16_inputs((H, n, d), 73)
+    o0 = api.multi_strategy_attention(q, k, v, LayerPlan.all_full(H), cache, 0, 0, dims, B)
+    lp = LayerPlan.parse("A1 C F")
+    o1 = api.multi_strategy_attention(q, k, v, lp, cache, 0, 1, dims, B)
+    t.cuda.synchronize()
+    assert t.equal(o1[1], o0[1])                          # Cached: the stored slot, bitwise
+    assert t.equal(o1[2], o0[2])                          # deterministic: Full again, same bits
+    assert [cache.produced_at(0, h) for h in range(H)] == [1, 0, 1]
+    assert t.equal(cache.fetch(0, 0), o1[0])              # commit == output
+    for h in (0, 2):
+        check_close(to_np(o1[h]), oracle_head(qn[h], kn[h], vn[h], dims, B, lp.strategies[h]), f"d={d} head {h}")
+    # a mask with an empty block row fails before any compute
+    nb = (n + B - 1) // B
+    active = np.ones(nb * nb, np.uint8)
+    active[nb:2 * nb] = 0
+    with pytest.raises(FullyMaskedRowError):
+        api.sparse_attention_forward(q[0], k[0], v[0], BlockMask(B, n, nb, nb, active))
+
+
 def test_cache_miss_is_raised_before_any_compute():
     t = torch()
     H, n, d = 3, 300, 64
