@@ -1,8 +1,9 @@
 """compute-sanitizer (memcheck, racecheck, synccheck) over small layers of
 every kernel path: d = 64 and 128, Full / Arrow / Cached items with cache
 commits, split-KV chunks and their combine, the fused calibration pass, a
-mask block other than the tile (element masking), and text rows halved
-across the two lanes."""
+mask block other than the tile (element masking), text rows halved across
+the two lanes, row-sharded launches (unequal key chunks) and the SIMT path
+for head_dim > 128."""
 import os
 import shutil
 import subprocess
@@ -34,6 +35,19 @@ for d in (64, 128):
 dims = api.AttentionDims(2, 64, 4096, 333)
 q, k, v = (torch.randn(2, 4429, 64, device="cuda").to(torch.bfloat16) for _ in range(3))
 api.multi_strategy_attention(q, k, v, api.LayerPlan.parse("A0 A1"), None, 0, 0, dims, 128)
+# row-sharded launches (unequal key chunks and their combine), ranks of 2 and 4
+dims = api.AttentionDims(4, 128, 1024, 77)
+q, k, v = (torch.randn(4, 1101, 128, device="cuda").to(torch.bfloat16) for _ in range(3))
+cache = api.HeadCache(1, 4, 1101, 128)
+api.multi_strategy_attention(q, k, v, api.LayerPlan.all_full(4), cache, 0, 0, dims, 128)
+for world in (2, 4):
+    for rank in range(world):
+        api.multi_strategy_attention_sharded(q, k, v, api.LayerPlan.parse("F A0 C A2"), cache, 0, 1, dims, 128,
+                                             rank, world)
+# head_dim > 128 (SIMT path)
+dims = api.AttentionDims(2, 160, 200, 40)
+q, k, v = (torch.randn(2, 240, 160, device="cuda").to(torch.bfloat16) for _ in range(3))
+api.multi_strategy_attention(q, k, v, api.LayerPlan.parse("F A0"), None, 0, 0, dims, 64)
 torch.cuda.synchronize()
 print("case ok")
 ''' % ROOT
