@@ -402,13 +402,35 @@ def main():
 
         s_compute, _ = timed(lambda: sharded(None), args.steps, args.warmup)
         s_layer, _ = timed(lambda: sharded(comm), args.steps, args.warmup) if world > 1 else (s_compute, 0)
+        p2p = None
+        if world > 1:
+            # the same layer assembled over peer memory: each rank's kernel
+            # stores its rows into every rank's buffer (CUDA IPC over
+            # NVLink), no collective; a step ends when every rank's launch
+            # has completed (device sync + barrier inside the timed region)
+            from paper_2503_22796_b200 import parallel
+
+            peers = parallel.PeerOutputs(s_out, rank, world)
+
+            def p2p_step():
+                api.multi_strategy_attention_sharded_p2p(sq, sk, sv, lp, s_cache, 0, 1, dims, BLOCK, rank, world,
+                                                         peers.outs)
+                torch.cuda.synchronize()
+                barrier()
+
+            p2p_ms, _ = timed(p2p_step, args.steps, args.warmup)
+            barrier()
+            peers.close()
+            p2p = {"layer_ms": p2p_ms, "value": dense_fl / (p2p_ms * 1e-3) / 1e12, "unit": UNIT,
+                   "how": "dfa2c_mha_forward_sharded_p2p: output boxes stored to every rank's buffer from the "
+                          "kernel epilogue (CUDA IPC / NVLink), no NCCL; includes a device sync + barrier per step"}
         line["row_sharded"] = {
             "what": "one FLUX68 sample split over the GPUs (dfa2c_mha_forward_sharded): strong scaling",
             "n_gpus": world, "compute_ms": s_compute, "layer_ms": s_layer,
             "gather": "NCCL group of W in-place broadcasts (all-gather-v) + cache completion" if world > 1 else None,
             "value": dense_fl / (s_layer * 1e-3) / 1e12, "unit": UNIT,
             "rows_per_rank": [int(bounds[r + 1] - bounds[r]) for r in range(world)],
-            "nccl_ranks": world if comm is not None else 0}
+            "nccl_ranks": world if comm is not None else 0, "p2p_assembly": p2p}
         if comm is not None:
             comm.close()
         if world == 1:
@@ -417,13 +439,23 @@ def main():
             # alone; the per-GPU compute at W GPUs is the max over ranks
             emu = {}
             for W in (2, 4, 8):
-                per = []
+                per, per_p2p = [], []
+                bufs = [s_out] + [torch.empty_like(s_out) for _ in range(W - 1)]
                 for r in range(W):
                     fn = lambda: api.multi_strategy_attention_sharded(sq, sk, sv, lp, s_cache, 0, 1, dims, BLOCK,
                                                                       r, W, out=s_out)
                     per.append(timed(fn, max(5, args.steps // 2), 3)[0])
+                    # the peer-memory variant: every output box also stored to the W-1 other
+                    # ranks' buffers (here on this GPU's HBM instead of NVLink)
+                    extra = iter(bufs[1:])
+                    outs = [s_out if j == r else next(extra) for j in range(W)]  # outs[r]: this rank's own
+                    fp = lambda: api.multi_strategy_attention_sharded_p2p(sq, sk, sv, lp, s_cache, 0, 1, dims,
+                                                                          BLOCK, r, W, outs)
+                    per_p2p.append(timed(fp, max(5, args.steps // 2), 3)[0])
+                del bufs
                 emu[str(W)] = {"per_rank_compute_ms": per, "max_ms": max(per),
-                               "x_ideal_vs_1gpu_layer": max(per) * W / ms}
+                               "x_ideal_vs_1gpu_layer": max(per) * W / ms,
+                               "p2p_per_rank_ms": per_p2p, "p2p_max_ms": max(per_p2p)}
             line["row_sharded"]["emulated_ranks"] = {
                 "what": "per-GPU compute of the row-sharded layer at W GPUs, every rank's launch timed alone on "
                         "this GPU (gather not included); x_ideal_vs_1gpu_layer = max_ms * W / layer_ms",

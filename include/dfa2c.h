@@ -190,6 +190,27 @@ int dfa2c_mha_forward_sharded(const void* q, const void* k, const void* v, int64
                               const int64_t* windows, dfa2c_cache* cache, int64_t layer, int64_t t,
                               void* out, int32_t rank, int32_t world, void* nccl_comm,
                               int64_t* row_bounds, void* stream);
+/* The same sharded layer assembled over PEER MEMORY instead of a collective:
+ * outs[world] holds every rank's output buffer as mapped in this process
+ * (outs[rank] is this rank's own; the others opened with dfa2c_ipc_open).
+ * This rank's ONE fused launch stores each output box of its row range to
+ * its own out AND to every peer's, from the kernel epilogue over NVLink, so
+ * the transfer overlaps the computation tile by tile and no all-gather runs.
+ * Once every rank's launch has completed (the caller's cross-rank sync), all
+ * outs hold the whole layer, bitwise the single-GPU sharded result; call
+ * dfa2c_shard_commit to complete this rank's cache with the other rows.
+ * world <= 8. Asynchronous on `stream`. */
+int dfa2c_mha_forward_sharded_p2p(const void* q, const void* k, const void* v, int64_t batch,
+                                  const dfa2c_dims* dims, int64_t block, const int32_t* kinds,
+                                  const int64_t* windows, dfa2c_cache* cache, int64_t layer, int64_t t,
+                                  void* const* outs, int32_t rank, int32_t world, int64_t* row_bounds,
+                                  void* stream);
+/* CUDA IPC for the peer buffers: a 64-byte handle + byte offset of a device
+ * pointer (any pointer inside an allocation), its mapping in another process
+ * (peer access enabled lazily), and the unmapping (same offset). */
+int dfa2c_ipc_handle(const void* ptr, char* handle /* 64 bytes */, int64_t* offset);
+int dfa2c_ipc_open(const char* handle, int64_t offset, void** ptr);
+int dfa2c_ipc_close(void* ptr, int64_t offset);
 /* The row ranges dfa2c_mha_forward_sharded gives each of `world` ranks for
  * this layer (host only, no GPU): row_bounds[world + 1] over the flattened
  * [batch*H*N] rows; bitwise the bounds the sharded call reports. */

@@ -130,6 +130,12 @@ _SIGS = {
     "dfa2c_mha_forward_sharded": (c_int32, [c_void_p, c_void_p, c_void_p, c_int64, POINTER(Dims), c_int64,
                                             POINTER(c_int32), POINTER(c_int64), c_void_p, c_int64, c_int64,
                                             c_void_p, c_int32, c_int32, c_void_p, POINTER(c_int64), c_void_p]),
+    "dfa2c_mha_forward_sharded_p2p": (c_int32, [c_void_p, c_void_p, c_void_p, c_int64, POINTER(Dims), c_int64,
+                                                POINTER(c_int32), POINTER(c_int64), c_void_p, c_int64, c_int64,
+                                                POINTER(c_void_p), c_int32, c_int32, POINTER(c_int64), c_void_p]),
+    "dfa2c_ipc_handle": (c_int32, [c_void_p, c_char_p, POINTER(c_int64)]),
+    "dfa2c_ipc_open": (c_int32, [c_char_p, c_int64, POINTER(c_void_p)]),
+    "dfa2c_ipc_close": (c_int32, [c_void_p, c_int64]),
     "dfa2c_shard_rows": (c_int32, [c_int64, POINTER(Dims), c_int64, POINTER(c_int32), POINTER(c_int64), c_int32,
                                    POINTER(c_int64)]),
     "dfa2c_shard_commit": (c_int32, [c_int64, POINTER(Dims), POINTER(c_int32), c_void_p, c_int64, POINTER(c_int64),

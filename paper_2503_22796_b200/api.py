@@ -492,6 +492,46 @@ def multi_strategy_attention_sharded(q, k, v, plan: LayerPlan, cache: Optional[H
     return res, np.array(list(bounds), dtype=np.int64)
 
 
+def multi_strategy_attention_sharded_p2p(q, k, v, plan: LayerPlan, cache: Optional[HeadCache], layer: int, t: int,
+                                         dims: AttentionDims, block_size: int, rank: int, world: int, outs,
+                                         stream=None):
+    """The sharded layer assembled over peer memory (dfa2c_mha_forward_sharded_p2p):
+    `outs` lists every rank's output buffer as mapped in this process (a
+    tensor for this rank; tensors or raw device pointers for the peers, e.g.
+    from parallel.PeerOutputs). This rank's launch stores its rows into all
+    of them from the kernel epilogue; after every rank's launch has completed
+    (the caller's cross-rank sync) each out holds the whole layer. Returns
+    the row bounds."""
+    q = _as_bf16_cuda(q, "q")
+    k = _as_bf16_cuda(k, "k")
+    v = _as_bf16_cuda(v, "v")
+    if q.dim() == 3:
+        q, k, v = q.unsqueeze(0), k.unsqueeze(0), v.unsqueeze(0)
+    if q.dim() != 4 or q.shape != k.shape or q.shape != v.shape:
+        raise ShapeError("q/k/v must be identical [H, N, d] tensors")
+    if tuple(q.shape[1:]) != (dims.n_heads, dims.seq_len(), dims.head_dim):
+        raise ShapeError("tensor shape disagrees with dims")
+    if plan.n_heads() != dims.n_heads or len(outs) != world:
+        raise ShapeError("plan must cover every head and outs every rank")
+    ptrs = []
+    for r, o in enumerate(outs):
+        if isinstance(o, int):
+            ptrs.append(o)
+            continue
+        if o.dtype != _torch().bfloat16 or not o.is_cuda or not o.is_contiguous() or o.numel() != q.numel():
+            raise ShapeError(f"outs[{r}] must be a contiguous bf16 CUDA tensor shaped like q")
+        ptrs.append(o.data_ptr())
+    arr = (c_void_p * world)(*ptrs)
+    d = dims.c()
+    kinds, wins = plan.arrays()
+    bounds = (c_int64 * (world + 1))()
+    check(lib().dfa2c_mha_forward_sharded_p2p(
+        c_void_p(q.data_ptr()), c_void_p(k.data_ptr()), c_void_p(v.data_ptr()), q.shape[0], byref(d), block_size,
+        kinds, wins, cache.handle if cache is not None else None, layer, t, arr, rank, world, bounds,
+        c_void_p(_stream_ptr(stream))))
+    return np.array(list(bounds), dtype=np.int64)
+
+
 def shard_commit(out, plan: LayerPlan, cache: HeadCache, layer: int, dims: AttentionDims, bounds, rank: int,
                  world: int, stream=None) -> None:
     """After a caller-side gather of a sharded call's `out`: commit the

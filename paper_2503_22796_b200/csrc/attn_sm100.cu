@@ -434,7 +434,8 @@ template <int D>
 __global__ void __launch_bounds__(384, 1)
     attn_fwd_sm100(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtensorMap tmk,
                    const __grid_constant__ CUtensorMap tmv, const __grid_constant__ CUtensorMap tmo,
-                   const __grid_constant__ CUtensorMap tmc, const AttnArgs args) {
+                   const __grid_constant__ CUtensorMap tmc, const AttnArgs args,
+                   const __grid_constant__ PeerMaps peers) {
     using C = Cfg<D>;
     constexpr int KS = C::KSTAGES;
     constexpr int VS = C::VSTAGES;
@@ -908,6 +909,8 @@ __global__ void __launch_bounds__(384, 1)
                         mbar_wait(c_full(L), ccnt & 1);
                         ++ccnt;
                         tma_store_o(&tmo, stg, b * 64, qt * TILE_M, w.bh);
+                        for (int p = 0; p < args.n_peers; ++p)
+                            tma_store_o(&peers.m[p], stg, b * 64, qt * TILE_M, w.bh);
                         bulk_commit();
                     }
                 }
@@ -946,6 +949,8 @@ __global__ void __launch_bounds__(384, 1)
                         tma_store_o(&tmo, stg, b * 64, qt * TILE_M, w.bh);  // rows >= N are clipped
                         if (commit)
                             tma_store_o(&tmc, stg, b * 64, qt * TILE_M, w.bh);
+                        for (int p = 0; p < args.n_peers; ++p)  // the other ranks' copies of the layer
+                            tma_store_o(&peers.m[p], stg, b * 64, qt * TILE_M, w.bh);
                     } else {
                         if (dst & SNAP_ORIGINAL)
                             tma_store_3d(&tmc, stg, b * 64, qt * TILE_M, w.bh);
@@ -1159,14 +1164,15 @@ __global__ void __launch_bounds__(384, 1)
     const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap,                     \
         const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap,                 \
         const __grid_constant__ CUtensorMap
-template __global__ void attn_fwd_sm100<64>(DFA2_MAPS, const AttnArgs);
-template __global__ void attn_fwd_sm100<128>(DFA2_MAPS, const AttnArgs);
+template __global__ void attn_fwd_sm100<64>(DFA2_MAPS, const AttnArgs, const __grid_constant__ PeerMaps);
+template __global__ void attn_fwd_sm100<128>(DFA2_MAPS, const AttnArgs, const __grid_constant__ PeerMaps);
 #undef DFA2_MAPS
 
 namespace {
 template <int D>
 cudaError_t launch_d(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const CUtensorMap& to,
-                     const CUtensorMap& tc, const AttnArgs& args, int grid, cudaStream_t stream) {
+                     const CUtensorMap& tc, const AttnArgs& args, const PeerMaps& peers, int grid,
+                     cudaStream_t stream) {
     using C = Cfg<D>;
     // the smem attribute is per (function, device): set once per device; the
     // bitmask is atomic, so host threads driving different GPUs (one per
@@ -1182,7 +1188,7 @@ cudaError_t launch_d(const CUtensorMap& tq, const CUtensorMap& tk, const CUtenso
             return e;
         configured.fetch_or(bit, std::memory_order_acq_rel);
     }
-    attn_fwd_sm100<D><<<grid, C::THREADS, C::SMEM_BYTES, stream>>>(tq, tk, tv, to, tc, args);
+    attn_fwd_sm100<D><<<grid, C::THREADS, C::SMEM_BYTES, stream>>>(tq, tk, tv, to, tc, args, peers);
     return cudaGetLastError();
 }
 }  // namespace
@@ -1190,10 +1196,10 @@ cudaError_t launch_d(const CUtensorMap& tq, const CUtensorMap& tk, const CUtenso
 // Host-side launcher (called from dfa2c.cpp). `to` / `tc` map the output and
 // the cache layer buffer with the same [batch*H, N, d] geometry as q/k/v.
 cudaError_t launch_attn(int d, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
-                        const CUtensorMap& to, const CUtensorMap& tc, const AttnArgs& args, int grid,
-                        cudaStream_t stream) {
-    return d == 128 ? launch_d<128>(tq, tk, tv, to, tc, args, grid, stream)
-                    : launch_d<64>(tq, tk, tv, to, tc, args, grid, stream);
+                        const CUtensorMap& to, const CUtensorMap& tc, const AttnArgs& args, const PeerMaps& peers,
+                        int grid, cudaStream_t stream) {
+    return d == 128 ? launch_d<128>(tq, tk, tv, to, tc, args, peers, grid, stream)
+                    : launch_d<64>(tq, tk, tv, to, tc, args, peers, grid, stream);
 }
 
 }  // namespace dfa2k

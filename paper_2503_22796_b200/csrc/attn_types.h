@@ -2,6 +2,7 @@
 // (dfa2c.cpp) and the sm_100a fused head-wise attention kernel.
 #pragma once
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_bf16.h>
 
 namespace dfa2k {
@@ -71,9 +72,18 @@ struct AttnArgs {
     float* part_o;             // split items: [slots][2 lanes][D][128] unnormalised O
     float* part_ml;            // split items: [slots][2 lanes][2][128] reference max, row sum
     int* counters;             // split groups: [groups][2 lanes] chunks finished (zeroed per launch)
+    int32_t n_peers;           // sharded P2P launches: other ranks' out buffers (PeerMaps) to store to
     int32_t snap_stride;       // ITEM_MULTI: rows of `to` between candidate outputs (= batch*H)
     int32_t n_snap;            // ITEM_MULTI: snapshots per query tile (window bands + the full row)
     uint16_t snap_slots[MAX_SNAPS];
+};
+
+// Sharded launches that assemble the layer over peer memory: the TMA maps of
+// the other ranks' output buffers (opened through CUDA IPC on the NVLink
+// box); every output box this rank stores goes to each of them as well.
+constexpr int MAX_PEERS = 7;  // world <= 8
+struct PeerMaps {
+    CUtensorMap m[MAX_PEERS];
 };
 
 constexpr int TILE_M = 128;  // query rows per tile (tcgen05 M)

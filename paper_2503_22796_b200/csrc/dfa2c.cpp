@@ -29,8 +29,8 @@
 
 namespace dfa2k {
 cudaError_t launch_attn(int d, const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv,
-                        const CUtensorMap& to, const CUtensorMap& tc, const AttnArgs& args, int grid,
-                        cudaStream_t stream);
+                        const CUtensorMap& to, const CUtensorMap& tc, const AttnArgs& args, const PeerMaps& peers,
+                        int grid, cudaStream_t stream);
 int rse_ctas_per_sm();
 cudaError_t launch_convert(const void* src, int src_dtype, void* dst, int dst_dtype, int64_t n, int sms,
                            cudaStream_t stream);
@@ -1047,6 +1047,7 @@ struct ForwardSpec {
     int32_t n_parts = 0;                      // sharded launch: the layer cut into n_parts ranges...
     int32_t part = 0;                         // ...of which this launch runs `part`
     std::vector<int64_t>* shard_rows = nullptr;  // out: [n_parts + 1] flattened row bounds
+    std::vector<void*> peer_outs;                // sharded P2P: the other ranks' out buffers (this process's mappings)
 };
 
 // The kernel instantiations: D = 64 serves head dims 1..64, D = 128 serves 65..128.
@@ -1348,7 +1349,16 @@ void launch_forward(const ForwardSpec& s, cudaStream_t stream) {
         DFA2C_CUDA_CHECK(cudaMemsetAsync(a.counters, 0, static_cast<size_t>(plan->n_groups) * 2 * sizeof(int), stream));
     }
     plan->acquire(stream);
-    DFA2C_CUDA_CHECK(dfa2k::launch_attn(kernel_dim(d), tq, tk, tv, to, tc, a, plan->grid, stream));
+    dfa2k::PeerMaps peers;
+    std::memset(&peers, 0, sizeof peers);
+    if (s.peer_outs.size() > static_cast<size_t>(dfa2k::MAX_PEERS))
+        fail(DFA2C_UNSUPPORTED, "at most " + std::to_string(dfa2k::MAX_PEERS) + " peer outputs");
+    for (size_t i = 0; i < s.peer_outs.size(); ++i) {
+        check_ptr(s.peer_outs[i], "peer out");
+        peers.m[i] = make_map(s.peer_outs[i], bh, n, d, dfa2k::TILE_M);
+    }
+    a.n_peers = static_cast<int32_t>(s.peer_outs.size());
+    DFA2C_CUDA_CHECK(dfa2k::launch_attn(kernel_dim(d), tq, tk, tv, to, tc, a, peers, plan->grid, stream));
     plan->release(stream);
     if (plan->n_groups > 0) {
         DFA2C_CUDA_CHECK(cudaFreeAsync(a.part_o, stream));
@@ -1574,7 +1584,9 @@ void run_influence_fused(const void* q, const void* k, const void* v, const dfa2
     a.n_snap = plan->n_snap;
     std::copy(plan->snap_slots, plan->snap_slots + dfa2k::MAX_SNAPS, a.snap_slots);
     plan->acquire(stream);
-    DFA2C_CUDA_CHECK(dfa2k::launch_attn(kernel_dim(d), tq, tk, tv, to, tc, a, plan->grid, stream));
+    dfa2k::PeerMaps no_peers;
+    std::memset(&no_peers, 0, sizeof no_peers);
+    DFA2C_CUDA_CHECK(dfa2k::launch_attn(kernel_dim(d), tq, tk, tv, to, tc, a, no_peers, plan->grid, stream));
     plan->release(stream);
     g_launches.fetch_add(1);
 }
@@ -2132,6 +2144,100 @@ int dfa2c_mha_forward_sharded(const void* q, const void* k, const void* v, int64
                 commit_others(batch, dims, kinds, cache, layer, rows[rank], rows[rank + 1], out, st);
         }
         commit_produced(dims, kinds, cache, layer, t);
+    });
+}
+
+int dfa2c_mha_forward_sharded_p2p(const void* q, const void* k, const void* v, int64_t batch,
+                                  const dfa2c_dims* dims, int64_t block, const int32_t* kinds,
+                                  const int64_t* windows, dfa2c_cache* cache, int64_t layer, int64_t t,
+                                  void* const* outs, int32_t rank, int32_t world, int64_t* row_bounds,
+                                  void* stream) {
+    return guard([&] {
+        validate_forward(batch, dims, block, kinds, windows, cache, layer);
+        validate_sharded(batch, dims, kinds, rank, world);
+        if (!outs)
+            fail(DFA2C_SHAPE, "outs must hold every rank's output buffer");
+        if (world - 1 > dfa2k::MAX_PEERS)
+            fail(DFA2C_UNSUPPORTED, "peer-memory assembly supports up to " + std::to_string(dfa2k::MAX_PEERS + 1) +
+                                        " ranks");
+        const cudaStream_t st = as_stream(stream);
+        ForwardSpec s{};
+        s.q = q;
+        s.k = k;
+        s.v = v;
+        s.out = outs[rank];
+        s.batch = batch;
+        s.dims = dims;
+        s.block = block;
+        s.cache = cache;
+        s.layer = layer;
+        s.n_parts = world;
+        s.part = rank;
+        for (int32_t r = 0; r < world; ++r)
+            if (r != rank) {
+                if (!outs[r] || outs[r] == outs[rank])
+                    fail(DFA2C_SHAPE, "outs must be distinct non-NULL buffers");
+                s.peer_outs.push_back(outs[r]);
+            }
+        std::vector<int64_t> rows;
+        s.shard_rows = &rows;
+        plan_jobs(dims, block, kinds, windows, cache != nullptr, s);
+        // this rank's rows, stored to its own out and, box by box from the
+        // epilogue, to every peer's out over NVLink (no collective); its
+        // computed rows are committed to its cache in-kernel
+        launch_forward(s, st);
+        if (rows.size() != static_cast<size_t>(world) + 1)
+            fail(DFA2C_CUDA, "internal: shard bounds missing");
+        if (row_bounds)
+            std::copy(rows.begin(), rows.end(), row_bounds);
+        commit_produced(dims, kinds, cache, layer, t);
+    });
+}
+
+int dfa2c_ipc_handle(const void* ptr, char* handle, int64_t* offset) {
+    return guard([&] {
+        if (!ptr || !handle || !offset)
+            fail(DFA2C_SHAPE, "ptr, handle and offset must not be NULL");
+        // the IPC handle names the whole allocation: find its base (the
+        // driver entry point, as for the tensor maps: no libcuda link)
+        using RangeFn = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+        static RangeFn range = [] {
+            cudaDriverEntryPointQueryResult q{};
+            void* p = nullptr;
+            return cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) == cudaSuccess &&
+                           q == cudaDriverEntryPointSuccess
+                       ? reinterpret_cast<RangeFn>(p)
+                       : nullptr;
+        }();
+        CUdeviceptr base = 0;
+        size_t size = 0;
+        if (!range || range(&base, &size, reinterpret_cast<CUdeviceptr>(ptr)) != CUDA_SUCCESS)
+            fail(DFA2C_CUDA, "cuMemGetAddressRange failed (not a device allocation?)");
+        cudaIpcMemHandle_t h;
+        DFA2C_CUDA_CHECK(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)));
+        static_assert(sizeof h == 64, "cudaIpcMemHandle_t is 64 bytes");
+        std::memcpy(handle, &h, sizeof h);
+        *offset = static_cast<int64_t>(reinterpret_cast<CUdeviceptr>(ptr) - base);
+    });
+}
+
+int dfa2c_ipc_open(const char* handle, int64_t offset, void** ptr) {
+    return guard([&] {
+        if (!handle || !ptr || offset < 0)
+            fail(DFA2C_SHAPE, "handle and ptr must not be NULL, offset >= 0");
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, handle, sizeof h);
+        void* base = nullptr;
+        DFA2C_CUDA_CHECK(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+        *ptr = static_cast<char*>(base) + offset;
+    });
+}
+
+int dfa2c_ipc_close(void* ptr, int64_t offset) {
+    return guard([&] {
+        if (!ptr)
+            fail(DFA2C_SHAPE, "ptr must not be NULL");
+        DFA2C_CUDA_CHECK(cudaIpcCloseMemHandle(static_cast<char*>(ptr) - offset));
     });
 }
 

@@ -60,6 +60,48 @@ def gather_rows(out, bounds, rank: int, world: int, group=None):
     return out
 
 
+class PeerOutputs:
+    """Every rank's output buffer mapped into this process through CUDA IPC
+    (dfa2c_ipc_handle / dfa2c_ipc_open; handles exchanged over the given
+    torch.distributed group), for api.multi_strategy_attention_sharded_p2p:
+    the fused kernel then writes each rank's rows into all ranks' buffers
+    over NVLink, so the layer is assembled without a collective."""
+
+    def __init__(self, out, rank: int, world: int, group=None):
+        import ctypes
+
+        import torch.distributed as dist
+
+        lib = api.lib()
+        h = ctypes.create_string_buffer(64)
+        off = ctypes.c_int64()
+        api.check(lib.dfa2c_ipc_handle(ctypes.c_void_p(out.data_ptr()), h, ctypes.byref(off)))
+        mine = (h.raw, off.value)
+        allh = [None] * world
+        if world > 1:
+            dist.all_gather_object(allh, mine, group=group)
+        else:
+            allh = [mine]
+        self.rank, self.world = rank, world
+        self._opened = []  # (ptr, offset) this process mapped
+        self.outs = []
+        for r in range(world):
+            if r == rank:
+                self.outs.append(out)
+                continue
+            p = ctypes.c_void_p()
+            api.check(lib.dfa2c_ipc_open(allh[r][0], allh[r][1], ctypes.byref(p)))
+            self._opened.append((p.value, allh[r][1]))
+            self.outs.append(p.value)
+
+    def close(self):
+        import ctypes
+
+        for p, off in self._opened:
+            api.check(api.lib().dfa2c_ipc_close(ctypes.c_void_p(p), off))
+        self._opened = []
+
+
 def sharded_multi_strategy_attention(q, k, v, plan: api.LayerPlan, cache: Optional[api.HeadCache], layer: int,
                                      t: int, dims: api.AttentionDims, block_size: int, rank: int, world: int,
                                      comm: Optional[api.NcclComm] = None, group=None, out=None, gather: bool = True):

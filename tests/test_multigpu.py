@@ -270,3 +270,117 @@ def test_two_processes_assemble_the_single_rank_bits():
     for r in range(2):
         for t in range(len(STEPS)):
             assert np.array_equal(res[r][t], ref[t].cpu().view(torch.int16).numpy()), (r, t)
+
+
+# ------------------------------------------------ assembly over peer memory
+def _p2p_emulated_ranks(W, q, k, v, dims, B):
+    """The STEPS timesteps with W ranks emulated on this GPU, assembled over
+    peer memory: each rank owns an output buffer, and its fused launch stores
+    its rows into every rank's buffer from the epilogue
+    (dfa2c_mha_forward_sharded_p2p); then each rank completes its cache."""
+    import torch
+
+    H, n, d = dims.n_heads, dims.seq_len(), dims.head_dim
+    caches = [HeadCache(1, H, n, d) for _ in range(W)]
+    per_t = []
+    for t, text in enumerate(STEPS):
+        plan = LayerPlan.parse(text)
+        bufs = [torch.full_like(q.unsqueeze(0), float("nan")) for _ in range(W)]
+        bounds = None
+        for r in range(W):
+            bounds = api.multi_strategy_attention_sharded_p2p(q, k, v, plan, caches[r], 0, t, dims, B, r, W, bufs)
+        torch.cuda.synchronize()  # every "rank" has finished: every buffer holds the layer
+        for r in range(W):
+            api.shard_commit(bufs[r], plan, caches[r], 0, dims, bounds, r, W)
+        torch.cuda.synchronize()
+        per_t.append([b[0].clone() for b in bufs])
+    return per_t, caches
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("nv,nt,d", [(2048, 77, 64), (2048, 256, 128)])
+def test_p2p_assembly_gives_every_rank_the_single_rank_bits(nv, nt, d):
+    import torch
+
+    H, B = 12, 128
+    dims = AttentionDims(H, d, nv, nt)
+    n = dims.seq_len()
+    q, k, v = (_inputs(H, n, d, s) for s in (1, 2, 3))
+    ref, ref_caches = _emulated_ranks(1, q, k, v, dims, B)
+    for W in (2, 4, 8):
+        per_t, caches = _p2p_emulated_ranks(W, q, k, v, dims, B)
+        for t in range(len(STEPS)):
+            for r in range(W):
+                assert torch.equal(per_t[t][r], ref[t]), f"W={W} t={t} rank {r}"
+        for r in range(W):
+            for h in range(H):
+                assert torch.equal(caches[r].fetch(0, h), ref_caches[0].fetch(0, h)), (W, r, h)
+    with pytest.raises(api.ShapeError):  # every rank's buffer, distinct
+        buf = torch.empty_like(q.unsqueeze(0))
+        api.multi_strategy_attention_sharded_p2p(q, k, v, LayerPlan.all_full(H), None, 0, 0, dims, B, 0, 2,
+                                                 [buf, buf])
+
+
+def _p2p_process_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2503_22796_b200 import parallel
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)  # both ranks on the one GPU of this box (same-device CUDA IPC)
+        H, nv, nt, d, B = 12, 2048, 77, 64, 128
+        dims = AttentionDims(H, d, nv, nt)
+        n = dims.seq_len()
+        qq, kk, vv = (_inputs(H, n, d, s) for s in (1, 2, 3))
+        cache = HeadCache(1, H, n, d)
+        out = torch.empty(1, H, n, d, dtype=torch.bfloat16, device="cuda")
+        peers = parallel.PeerOutputs(out, rank, world)
+        results = []
+        try:
+            for t, text in enumerate(STEPS):
+                plan = LayerPlan.parse(text)
+                dist.barrier()  # nobody writes a buffer its owner is still reading
+                bounds = api.multi_strategy_attention_sharded_p2p(qq, kk, vv, plan, cache, 0, t, dims, B, rank,
+                                                                  world, peers.outs)
+                torch.cuda.synchronize()
+                dist.barrier()  # every rank's launch has completed: `out` holds the whole layer
+                api.shard_commit(out, plan, cache, 0, dims, bounds, rank, world)
+                torch.cuda.synchronize()
+                results.append(out[0].cpu())
+        finally:
+            dist.barrier()
+            peers.close()
+        q.put((rank, [r.view(torch.int16).numpy() for r in results]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_two_processes_assemble_over_cuda_ipc():
+    """world_size 2, one process per rank; each rank's fused kernel writes its
+    rows into the other process's output buffer (CUDA IPC), no gather: both
+    processes end with the single-rank bits, three timesteps."""
+    import torch
+    import torch.multiprocessing as mp
+
+    H, nv, nt, d, B = 12, 2048, 77, 64, 128
+    dims = AttentionDims(H, d, nv, nt)
+    n = dims.seq_len()
+    q, k, v = (_inputs(H, n, d, s) for s in (1, 2, 3))
+    ref, _ = _emulated_ranks(1, q, k, v, dims, B)
+    ctx = mp.get_context("spawn")
+    qu = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_p2p_process_worker, args=(r, 2, port, qu)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(qu.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for r in range(2):
+        for t in range(len(STEPS)):
+            assert np.array_equal(res[r][t], ref[t].cpu().view(torch.int16).numpy()), (r, t)
