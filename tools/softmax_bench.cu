@@ -37,11 +37,11 @@ __device__ __forceinline__ float2 ex2_poly2(float2 x) {
                        __uint_as_float(__float_as_uint(p.y) + (__float_as_uint(t.y) << 23)));
 }
 
-template <int EMU, int DEG>
-__global__ void __launch_bounds__(256, 1) row_kernel(const float* in, float* out, long long* clk, int iters) {
-    float s[128];
+template <int EMU, int DEG, int EL = 128>
+__global__ void __launch_bounds__(512, 1) row_kernel(const float* in, float* out, long long* clk, int iters) {
+    float s[EL];
 #pragma unroll
-    for (int i = 0; i < 128; ++i) s[i] = in[(threadIdx.x * 131 + i) & 4095];
+    for (int i = 0; i < EL; ++i) s[i] = in[(threadIdx.x * 131 + i) & 4095];
     const float2 scale2 = make_float2(0.127f, 0.127f);
     float m = 0.5f;
     uint32_t acc = 0;
@@ -52,7 +52,7 @@ __global__ void __launch_bounds__(256, 1) row_kernel(const float* in, float* out
         const float2 neg_m = make_float2(-m, -m);
         float2 sum = make_float2(0.f, 0.f);
 #pragma unroll
-        for (int i = 0; i < 64; ++i) {
+        for (int i = 0; i < EL / 2; ++i) {
             const float2 x = __ffma2_rn(make_float2(s[2 * i], s[2 * i + 1]), scale2, neg_m);
             float2 p;
             if (EMU > 0 && (i % (EMU > 0 ? EMU : 1)) == EMU - 1)
@@ -68,30 +68,40 @@ __global__ void __launch_bounds__(256, 1) row_kernel(const float* in, float* out
     const long long t1 = clock64();
     out[blockIdx.x * blockDim.x + threadIdx.x] = l + __uint_as_float(acc & 0x3FFFFFFF) * 1e-30f;
     if (threadIdx.x % 32 == 0)
-        clk[blockIdx.x * 8 + threadIdx.x / 32] = t1 - t0;
+        clk[blockIdx.x * 16 + threadIdx.x / 32] = t1 - t0;
 }
 
-template <int EMU, int DEG>
+template <int EMU, int DEG, int EL = 128>
 void run(const float* in, float* out, long long* clk, long long* h, int threads) {
     const int iters = 400;
-    row_kernel<EMU, DEG><<<148, threads>>>(in, out, clk, iters);
-    row_kernel<EMU, DEG><<<148, threads>>>(in, out, clk, iters);
+    row_kernel<EMU, DEG, EL><<<148, threads>>>(in, out, clk, iters);
+    row_kernel<EMU, DEG, EL><<<148, threads>>>(in, out, clk, iters);
     cudaDeviceSynchronize();
-    cudaMemcpy(h, clk, 148 * 8 * sizeof(long long), cudaMemcpyDeviceToHost);
+    cudaMemcpy(h, clk, 148 * 16 * sizeof(long long), cudaMemcpyDeviceToHost);
     double mx = 0;
     for (int b = 0; b < 148; ++b)
-        for (int w = 0; w < threads / 32; ++w) mx = h[b * 8 + w] > mx ? h[b * 8 + w] : mx;
-    printf("EMU %d deg %d  warps/SMSP %d : %.0f clk per 128-element row (%.2f MUFU-clk floor ratio)\n", EMU, DEG,
-           threads / 128, mx / iters, (mx / iters) / (threads / 128 * 1024.0 * (EMU ? 1.0 - 1.0 / EMU : 1.0)));
+        for (int w = 0; w < threads / 32; ++w) mx = h[b * 16 + w] > mx ? h[b * 16 + w] : mx;
+    // SMSP time per 128 elements of one row: (warps per SMSP) x EL elements per warp-iteration
+    const double rows_per_iter = threads / 128.0 * EL / 128.0;
+    printf("EMU %d deg %d  elems/thread %3d warps/SMSP %d : %.0f clk per 128-element row of SMSP time\n", EMU, DEG,
+           EL, threads / 128, mx / iters / rows_per_iter);
 }
 
 int main() {
     float *in, *out;
-    long long *clk, h[148 * 8];
+    long long *clk, h[148 * 16];
     cudaMalloc(&in, 4096 * 4);
-    cudaMalloc(&out, 148 * 256 * 4);
-    cudaMalloc(&clk, 148 * 8 * 8);
+    cudaMalloc(&out, 148 * 512 * 4);
+    cudaMalloc(&clk, 148 * 16 * 8);
     cudaMemset(in, 0, 4096 * 4);
+    for (int th : {256, 512}) {
+        run<3, 3, 64>(in, out, clk, h, th);
+        run<4, 3, 64>(in, out, clk, h, th);
+    }
+    for (int th : {128, 256, 384, 512}) {
+        run<3, 3>(in, out, clk, h, th);
+        run<4, 3>(in, out, clk, h, th);
+    }
     for (int th : {128, 256}) {
         run<0, 3>(in, out, clk, h, th);
         run<8, 3>(in, out, clk, h, th);
