@@ -73,6 +73,7 @@ struct AttnArgs {
     float* part_ml;            // split items: [slots][2 lanes][2][128] reference max, row sum
     int* counters;             // split groups: [groups][2 lanes] chunks finished (zeroed per launch)
     int32_t n_peers;           // sharded P2P launches: other ranks' out buffers (PeerMaps) to store to
+    int32_t copies_last;       // every CTA's copy items form the tail of its list (the copy-tail ring)
     int32_t snap_stride;       // ITEM_MULTI: rows of `to` between candidate outputs (= batch*H)
     int32_t n_snap;            // ITEM_MULTI: snapshots per query tile (window bands + the full row)
     uint16_t snap_slots[MAX_SNAPS];

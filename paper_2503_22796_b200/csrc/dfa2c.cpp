@@ -220,6 +220,7 @@ struct DevPlan {
     int grid = 0;
     int32_t n_groups = 0;  // split groups (counters per launch)
     int32_t n_slots = 0;   // partial-output slots (one per split chunk)
+    bool copies_last = false;  // every CTA's copy items are the tail of its list
     WorkItem* items = nullptr;
     int32_t* cta_begin = nullptr;
     uint32_t* tiles = nullptr;
@@ -556,6 +557,15 @@ double shard_ref_sms() {
     return v;
 }
 
+// DFA2_COPY_TAIL=0 keeps one staging box per lane for trailing copies (A/B)
+bool copy_tail_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("DFA2_COPY_TAIL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 // Key-chunk boundaries of a split pair: chunk c gets a share of the union
 // tiles proportional to (nch - c), e.g. 1/2, 1/3, 1/6 for three chunks.
 // Unequal chunks give the LPT assignment small items to fill the CTAs that
@@ -838,13 +848,21 @@ std::unique_ptr<DevPlan> schedule_items(int device, std::vector<Cand>& cands, co
     }
     std::vector<WorkItem> items;
     std::vector<int32_t> cta_begin(static_cast<size_t>(grid + 1), 0);
+    bool copies_last = true;  // copies cost the least, so LPT leaves them at the end of every CTA
     for (int c = 0; c < grid; ++c) {
+        bool seen_copy = false;
+        for (const WorkItem& w : per_cta[c]) {
+            const bool copy = (w.flags & dfa2k::ITEM_COPY) != 0;
+            copies_last = copies_last && (copy || !seen_copy);
+            seen_copy = seen_copy || copy;
+        }
         items.insert(items.end(), per_cta[c].begin(), per_cta[c].end());
         cta_begin[c + 1] = static_cast<int32_t>(items.size());
     }
 
     auto p = std::make_unique<DevPlan>();
     p->grid = grid;
+    p->copies_last = copies_last;
     p->n_groups = n_groups;
     p->n_slots = n_slots;
     p->device = device;
@@ -1333,6 +1351,7 @@ void launch_forward(const ForwardSpec& s, cudaStream_t stream) {
     a.out = static_cast<__nv_bfloat16*>(s.out);
     a.cache = static_cast<__nv_bfloat16*>(cache_layer);
     a.n = static_cast<int32_t>(n);
+    a.copies_last = plan->copies_last && copy_tail_enabled() ? 1 : 0;
     a.block = static_cast<int32_t>(std::min<int64_t>(s.block, int64_t{1} << 30));
     a.nb = static_cast<int32_t>(ceil_div(n, s.block));
     a.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(s.scale_d ? s.scale_d : d)));
