@@ -2,7 +2,7 @@
  * attention path on B200 (sm_100a).
  *
  * The reference (/root/reference/proj) exposes this path as the namespace
- * `dfa2` C++ free-function API (include/dfa2/*.hpp, linked statically as
+ * `dfa2` C++ free-function API (include/dfa2/ *.hpp headers, linked statically as
  * dfa2_core). This header is the thin C layer the host C++ (include/dfa2/)
  * and any FFI (ctypes, cgo, JNI) call. Plain pointers,
  * sizes and integer status codes; no C++ or torch types cross it.
