@@ -573,12 +573,15 @@ bool copy_tail_enabled() {
 // (192 equal chunks on 148 SMs at 8 GPUs) otherwise ends one whole chunk
 // late on a third of its SMs. Every chunk keeps at least one tile; the cut
 // depends only on (U, nch), so results stay independent of the GPU count.
-std::vector<int32_t> chunk_bounds(int32_t U, int32_t nch) {
+// Latency-mode split-KV (not sharded) keeps equal chunks: there the longest
+// chunk is the launch's critical path (a single head: 1.03x dense-vs-arrow
+// with unequal chunks against 1.5x+ with equal ones).
+std::vector<int32_t> chunk_bounds(int32_t U, int32_t nch, bool unequal) {
     std::vector<int32_t> cut(static_cast<size_t>(nch) + 1, 0);
-    const int64_t W = int64_t{nch} * (nch + 1) / 2;
+    const int64_t W = unequal ? int64_t{nch} * (nch + 1) / 2 : nch;
     int64_t acc = 0;
     for (int32_t c = 0; c < nch; ++c) {
-        acc += nch - c;
+        acc += unequal ? nch - c : 1;
         int64_t b = (acc * U + W / 2) / W;
         b = std::max<int64_t>(b, cut[c] + 1);            // non-empty
         b = std::min<int64_t>(b, U - (nch - 1 - c));      // room for the rest
@@ -790,7 +793,7 @@ std::unique_ptr<DevPlan> build_dev_plan(int device, int64_t batch, int64_t H, in
                         continue;
                     }
                     const int32_t U = w.n_tiles, begin = w.tile_begin;
-                    const std::vector<int32_t> cut = chunk_bounds(U, nch);
+                    const std::vector<int32_t> cut = chunk_bounds(U, nch, sharded);
                     for (int32_t c = 0; c < nch; ++c) {
                         WorkItem cw = w;
                         const int32_t lo = cut[c], hi = cut[c + 1];
