@@ -362,6 +362,9 @@ __global__ void __launch_bounds__(RSE_THREADS + 32) rse_multi_partial(CandPtrs<T
 template <typename T>
 __global__ void rse_finalize(const T* __restrict__ yo, const double* __restrict__ part, int nblk,
                              int n_heads, int ref_heads, int64_t numel, int mode, double* __restrict__ out) {
+    // launched as a programmatic dependent of the partial kernel: resident
+    // early, it waits here until every partial CTA has written its sums
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     const int h = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
     if (h >= n_heads)
@@ -390,6 +393,25 @@ __global__ void rse_finalize(const T* __restrict__ yo, const double* __restrict_
 }
 
 namespace {
+// rse_finalize as a programmatic dependent launch: its launch latency
+// overlaps the partial kernel's tail (griddepcontrol.wait orders its reads
+// after every partial CTA's writes)
+template <typename T>
+void launch_finalize(int blocks, const T* yo, const double* part, int nblk, int n_heads, int ref_heads,
+                     int64_t numel, int mode, double* out, cudaStream_t stream) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(blocks));
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, rse_finalize<T>, yo, part, nblk, n_heads, ref_heads, numel, mode, out);
+}
+
 // true the first time a (kernel, device) pair is seen: the smem attribute is
 // then set once instead of on every launch; thread-safe (one host thread per
 // GPU), a rare duplicate set is harmless
@@ -422,8 +444,8 @@ void launch_typed(const void* ym, const void* yo, int64_t n_heads, int64_t numel
     else
         launch_partial<T, true>(grid, m, o, numel, chunk, vec_ok, scratch, stream);
     const int fin_blocks = static_cast<int>((n_heads + 7) / 8);
-    rse_finalize<T><<<fin_blocks, 256, 0, stream>>>(o, scratch, nblk, static_cast<int>(n_heads),
-                                                   static_cast<int>(n_heads), numel, mode, out_dev);
+    launch_finalize<T>(fin_blocks, o, scratch, nblk, static_cast<int>(n_heads), static_cast<int>(n_heads), numel,
+                       mode, out_dev, stream);
 }
 }  // namespace
 
@@ -444,8 +466,8 @@ void launch_multi_typed(const void* const* ym, int M, const void* yo, int64_t n_
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, rse_multi_smem(RSE_MAXM));
     kern<<<grid, RSE_THREADS + 32, smem, stream>>>(c, M, static_cast<const T*>(yo), numel, chunk, vec_ok, scratch);
     const int sets = static_cast<int>(M * n_heads);
-    rse_finalize<T><<<(sets + 7) / 8, 256, 0, stream>>>(static_cast<const T*>(yo), scratch, nblk, sets,
-                                                       static_cast<int>(n_heads), numel, mode, out_dev);
+    launch_finalize<T>((sets + 7) / 8, static_cast<const T*>(yo), scratch, nblk, sets, static_cast<int>(n_heads),
+                       numel, mode, out_dev, stream);
 }
 }  // namespace
 
