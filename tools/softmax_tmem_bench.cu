@@ -12,7 +12,18 @@
 #include "sm100_ptx.cuh"
 using namespace dfa2k;
 
-template <int EL, int EMU>
+__device__ __forceinline__ void tmem_ld64(uint32_t taddr, uint32_t* r) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x64.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,"
+        "%32,%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,%43,%44,%45,%46,%47,"
+        "%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63}, [%64];"
+        : DFA2_R8(0), DFA2_R8(8), DFA2_R8(16), DFA2_R8(24), DFA2_R8(32), DFA2_R8(40), DFA2_R8(48), DFA2_R8(56)
+        : "r"(taddr));
+}
+
+template <int EL, int EMU, bool WIDE_LD = false>
 __global__ void __launch_bounds__(EL == 128 ? 256 : 512, 1) step(float* out, long long* clk, int iters) {
     __shared__ uint32_t slot;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -39,9 +50,15 @@ __global__ void __launch_bounds__(EL == 128 ? 256 : 512, 1) step(float* out, lon
     const long long t0 = clock64();
     for (int it = 0; it < iters; ++it) {
         uint32_t s[EL];
+        if (WIDE_LD) {
 #pragma unroll
-        for (int c = 0; c < EL; c += 32)
-            tmem_ld32(base + c, s + c);
+            for (int c = 0; c < EL; c += 64)
+                tmem_ld64(base + c, s + c);
+        } else {
+#pragma unroll
+            for (int c = 0; c < EL; c += 32)
+                tmem_ld32(base + c, s + c);
+        }
         tmem_ld_wait();
         float mm[8];
 #pragma unroll
@@ -98,19 +115,19 @@ __global__ void __launch_bounds__(EL == 128 ? 256 : 512, 1) step(float* out, lon
         tmem_dealloc(tmem, 512);
 }
 
-template <int EL, int EMU>
+template <int EL, int EMU, bool WIDE_LD = false>
 void run(float* out, long long* clk, long long* h, int warps) {
     const int iters = 400;
-    step<EL, EMU><<<148, warps * 32>>>(out, clk, iters);
-    step<EL, EMU><<<148, warps * 32>>>(out, clk, iters);
+    step<EL, EMU, WIDE_LD><<<148, warps * 32>>>(out, clk, iters);
+    step<EL, EMU, WIDE_LD><<<148, warps * 32>>>(out, clk, iters);
     cudaDeviceSynchronize();
     cudaMemcpy(h, clk, 148 * 16 * sizeof(long long), cudaMemcpyDeviceToHost);
     double mx = 0;
     for (int b = 0; b < 148; ++b)
         for (int w = 0; w < warps; ++w) mx = h[b * 16 + w] > mx ? h[b * 16 + w] : mx;
     const double rows = warps / 4.0 * EL / 128.0;  // 128-score rows per SMSP per iteration
-    std::printf("keys/row %3d EMU %d warps/SMSP %d: %.0f clk per iteration, %.0f SMSP clk per 128 scores\n", EL, EMU,
-                warps / 4, mx / iters, mx / iters / rows);
+    std::printf("keys/row %3d EMU %d warps/SMSP %d ld %s: %.0f clk per iteration, %.0f SMSP clk per 128 scores\n", EL,
+                EMU, warps / 4, WIDE_LD ? "x64" : "x32", mx / iters, mx / iters / rows);
 }
 
 int main() {
@@ -119,7 +136,9 @@ int main() {
     cudaMalloc(&out, 148 * 512 * 4);
     cudaMalloc(&clk, 148 * 16 * 8);
     run<128, 3>(out, clk, h, 8);   // the kernel today: 2 lanes x 128-key rows
+    run<128, 3, true>(out, clk, h, 8);
     run<128, 3>(out, clk, h, 4);
+    run<128, 3, true>(out, clk, h, 4);
     run<64, 3>(out, clk, h, 16);   // 4 lanes x 64-key rows
     run<64, 3>(out, clk, h, 8);
     run<128, 8>(out, clk, h, 8);
