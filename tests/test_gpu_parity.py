@@ -217,6 +217,28 @@ def test_wide_head_dims_through_the_simt_path(d):
         api.sparse_attention_forward(q[0], k[0], v[0], BlockMask(B, n, nb, nb, active))
 
 
+def test_wide_head_dims_batched_and_through_the_host_path():
+    """head_dim > 128 with batch 2 on the device path and through the
+    host-buffer path (head groups, skipped heads): same bits both ways."""
+    t = torch()
+    Bt, H, nv, nt, d, B = 2, 3, 256, 30, 192, 64
+    n = nv + nt
+    dims = AttentionDims(H, d, nv, nt)
+    q, qn = bf16_inputs((Bt, H, n, d), 81)
+    k, kn = bf16_inputs((Bt, H, n, d), 82)
+    v, vn = bf16_inputs((Bt, H, n, d), 83)
+    lp = LayerPlan.parse("F A0 A2")
+    dev = api.multi_strategy_attention(q, k, v, lp, None, 0, 0, dims, B)
+    host = api.multi_strategy_attention_host(q.cpu().pin_memory(), k.cpu().pin_memory(), v.cpu().pin_memory(), lp,
+                                             None, 0, 0, dims, B)
+    t.cuda.synchronize()
+    assert t.equal(host.to("cuda"), dev)
+    for b in range(Bt):
+        for h in range(H):
+            check_close(to_np(dev[b, h]), oracle_head(qn[b, h], kn[b, h], vn[b, h], dims, B, lp.strategies[h]),
+                        f"sample {b} head {h}")
+
+
 def test_cache_miss_is_raised_before_any_compute():
     t = torch()
     H, n, d = 3, 300, 64

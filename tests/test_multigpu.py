@@ -321,6 +321,28 @@ def test_p2p_assembly_gives_every_rank_the_single_rank_bits(nv, nt, d):
                                                  [buf, buf])
 
 
+@pytest.mark.gpu
+def test_p2p_assembly_batched_without_cache():
+    """Batch 2, no cache (no commits, no Cached heads): W = 3 emulated ranks
+    assemble over their buffers to the single-rank sharded bits."""
+    import torch
+
+    Bt, H, nv, nt, d, B = 2, 6, 1024, 77, 128, 128
+    dims = AttentionDims(H, d, nv, nt)
+    n = dims.seq_len()
+    g = torch.Generator(device="cuda").manual_seed(7)
+    q, k, v = (torch.randn(Bt, H, n, d, device="cuda", generator=g).to(torch.bfloat16) for _ in range(3))
+    plan = LayerPlan.parse("F A0 A2 F A8 A1")
+    ref, _ = api.multi_strategy_attention_sharded(q, k, v, plan, None, 0, 0, dims, B, 0, 1)
+    W = 3
+    bufs = [torch.full_like(q, float("nan")) for _ in range(W)]
+    for r in range(W):
+        api.multi_strategy_attention_sharded_p2p(q, k, v, plan, None, 0, 0, dims, B, r, W, bufs)
+    torch.cuda.synchronize()
+    for r in range(W):
+        assert torch.equal(bufs[r], ref), r
+
+
 def _p2p_process_worker(rank, world, port, q):
     import torch
     import torch.distributed as dist
