@@ -118,6 +118,40 @@ struct Cfg {
 #ifndef DFA2_SPLITLD
 #define DFA2_SPLITLD 1
 #endif
+// Keys 0..63 stay in registers from the max pass to their exps (1), or are
+// re-read from TMEM after the keys-64..127 half (0), per head dim. Keeping
+// them needs the softmax warpgroups' register budget raised (setmaxnreg,
+// DFA2_REGS_*). Interleaved A/B (tools/ab_interleaved.py): d = 128 FLUX68
+// -2.2%, all-Full -2.1%; d = 64 SD3 arrows +1.5% (so off there).
+// Hardware warpgroup -> role (warpgroups 0,1,2 in hardware order):
+// 0: control, lane A, lane B (lane B above lane A, control lowest);
+// 1: lane A, lane B, control (control highest); 2: control, lane B, lane A;
+// 3: lane B, lane A, control. Interleaved A/B: map 1 is 2% faster at d = 64
+// (SD3), 2% slower at d = 128 than map 0.
+#ifndef DFA2_WARPMAP64
+#define DFA2_WARPMAP64 1
+#endif
+#ifndef DFA2_WARPMAP128
+#define DFA2_WARPMAP128 0
+#endif
+template <int D>
+constexpr int WARPMAP = D == 64 ? DFA2_WARPMAP64 : DFA2_WARPMAP128;
+#ifndef DFA2_KEEPLO128
+#define DFA2_KEEPLO128 1
+#endif
+#ifndef DFA2_KEEPLO64
+#define DFA2_KEEPLO64 0
+#endif
+template <int D>
+constexpr bool KEEPLO = D == 64 ? DFA2_KEEPLO64 : DFA2_KEEPLO128;
+#ifndef DFA2_REGS_SOFTMAX
+#define DFA2_REGS_SOFTMAX 216
+#endif
+#ifndef DFA2_REGS_OTHER
+#define DFA2_REGS_OTHER 72
+#endif
+static_assert(DFA2_REGS_OTHER + 2 * DFA2_REGS_SOFTMAX <= 3 * 168,
+              "setmaxnreg must not ask for more than the CTA's 384 x 168 registers");
 // trace[((lane * 4096) + tile) * 8 + slot] = clock64() for CTA 0 (debug builds)
 #define DFA2_STAMP(L_, j_, k_)                                                          \
     do {                                                                                \
@@ -307,8 +341,8 @@ __device__ __forceinline__ void softmax_tile(uint32_t sc, uint32_t oc, float sl2
     };
     uint32_t hi[64];
     float mx;
+    uint32_t lo[64];  // keys 0..63 (re-loaded below unless KEEPLO<D>)
     {
-        uint32_t lo[64];
 #if DFA2_SPLITLD
         // keys 0..63 first; their max chains run while keys 64..127 load
         tmem_ld32(sc, lo);
@@ -334,6 +368,10 @@ __device__ __forceinline__ void softmax_tile(uint32_t sc, uint32_t oc, float sl2
                 mm[j] = fmaxf(mm[j], fmaxf(__uint_as_float(hi[c + 2 * j]), __uint_as_float(hi[c + 2 * j + 1])));
         mx = fmaxf(fmaxf(fmaxf(mm[0], mm[1]), fmaxf(mm[2], mm[3])), fmaxf(fmaxf(mm[4], mm[5]), fmaxf(mm[6], mm[7]))) *
              sl2;
+        if (KEEPLO<D> && SEP) {  // S fully in registers: the lane's next S may overwrite it
+            tc_fence_before();
+            mbar_arrive(bar_sfree);
+        }
 #else
         tmem_ld32(sc, lo);
         tmem_ld32(sc + 32, lo + 32);
@@ -395,11 +433,12 @@ __device__ __forceinline__ void softmax_tile(uint32_t sc, uint32_t oc, float sl2
     mbar_arrive(bar_half);
     DFA2_SSTAMP(6);
     // keys 0..63 re-read (cols [0,64) untouched so far) -> cols [0,32)
-    uint32_t lo[64];
-    tmem_ld32(sc, lo);
-    tmem_ld32(sc + 32, lo + 32);
-    tmem_ld_wait();
-    if (SEP) {  // S fully read: the lane's next S may overwrite it
+    if (!KEEPLO<D>) {
+        tmem_ld32(sc, lo);
+        tmem_ld32(sc + 32, lo + 32);
+        tmem_ld_wait();
+    }
+    if (SEP && !KEEPLO<D>) {  // S fully read: the lane's next S may overwrite it
         tc_fence_before();
         mbar_arrive(bar_sfree);
     }
@@ -448,7 +487,17 @@ __global__ void __launch_bounds__(384, 1)
     if (sbase & 1023u)
         __trap();
 
-    const int warp = threadIdx.x >> 5;
+    // Logical warp roles: 0 producer, 1 (and 3 at d = 64) MMA issue, 2 TMEM
+    // allocation, 4..7 softmax lane A, 8..11 lane B. The SMSP scheduler
+    // favours the highest warp id among eligible warps, so which hardware
+    // warpgroup takes which role sets the issue priority between the MMA
+    // issuer and the two softmax warps sharing its SMSP (WARPMAP<D>). The
+    // TMEM lane quarter of a softmax warp (hardware warp % 4) equals logical
+    // warp % 4 under every map.
+    const int hg = static_cast<int>(threadIdx.x >> 7);
+    constexpr int WM = WARPMAP<D>;
+    const int lg = WM == 0 ? hg : WM == 1 ? (hg + 1) % 3 : WM == 2 ? (hg == 0 ? 0 : 3 - hg) : 2 - hg;
+    const int warp = lg * 4 + static_cast<int>((threadIdx.x >> 5) & 3);
     const int lane = threadIdx.x & 31;
 
     const uint32_t bars = sbase + C::BAR_OFF;
@@ -524,6 +573,10 @@ __global__ void __launch_bounds__(384, 1)
     const int it1 = args.cta_begin[blockIdx.x + 1];
     const WorkItem* items = args.items;
 
+    if (warp < 4) {
+    // warpgroup 0 (producer / MMA issue) hands registers to the softmax warpgroups
+    if (KEEPLO<D>)
+        regs_dec<DFA2_REGS_OTHER>();
     if (warp == 0) {
         // ------------------------------------------------ TMA producer
         // The whole warp walks the schedule (warp-uniform control flow keeps
@@ -879,8 +932,11 @@ __global__ void __launch_bounds__(384, 1)
                 ++qcount;
             }
         }
-    } else if (warp >= 4) {
+    }
+    } else {
         // ------------------------------------------------ softmax lanes
+        if (KEEPLO<D>)
+            regs_inc<DFA2_REGS_SOFTMAX>();
         const int L = (warp - 4) >> 2;              // 0 = lane A, 1 = lane B
         const int wq = warp & 3;                    // TMEM lane quarter
         const int r = wq * 32 + lane;               // row within the query tile
@@ -1212,8 +1268,8 @@ __global__ void __launch_bounds__(384, 1)
             bulk_wait0();  // every bulk store of this lane has completed
     }
 
-    if (DFA2_TRACE == 4 && args.trace && (threadIdx.x == 128 || threadIdx.x == 256))
-        args.trace[blockIdx.x * 4 + 1 + (threadIdx.x >> 8)] = gtime();  // lane A / B softmax done
+    if (DFA2_TRACE == 4 && args.trace && (warp == 4 || warp == 8) && lane == 0)
+        args.trace[blockIdx.x * 4 + 1 + (warp >> 3)] = gtime();  // lane A / B softmax done
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
