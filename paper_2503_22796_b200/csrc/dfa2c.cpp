@@ -484,7 +484,7 @@ PairSet build_pair_set(const TileSet& ts, int64_t nqt, const std::vector<uint8_t
         return ps;
     }
     // Halve only when the text rows are the mask's long pole: their key
-    // chains are more than 5x the average chain of the other query tiles
+    // chains are more than ratio/10 x the average chain of the other query tiles
     // (narrow arrow windows). A property of the mask alone, so heads with
     // the same strategy are treated alike and Full == Arrow(max) holds.
     int64_t other_len = 0, n_other = 0, text_len = 0;
@@ -497,7 +497,7 @@ PairSet build_pair_set(const TileSet& ts, int64_t nqt, const std::vector<uint8_t
             ++n_other;
         }
     }
-    const bool halve = n_other > 0 && text_len * n_other > ratio * other_len;
+    const bool halve = n_other > 0 && 10 * text_len * n_other > ratio * other_len;
     int64_t pending = -1;  // the other tiles pair up in order
     for (int64_t q = 0; q < nqt; ++q) {
         if (halve && text_tile[q] && ts.row_ptr[q + 1] - ts.row_ptr[q] >= 2) {
@@ -1262,14 +1262,17 @@ void run_forward(const ForwardSpec& s, cudaStream_t stream) {
         run_padded(s, stream);
 }
 
-// Text rows run on both lanes when their key chains exceed this many times
-// the mask's average chain (0: never): d = 64 from 5x.
+// Text rows run on both lanes when their key chains exceed this many tenths
+// of the mask's average chain (0: never): d = 64 from 5x.
+#ifndef DFA2_HALVES64_DEFAULT
+#define DFA2_HALVES64_DEFAULT 50
+#endif
 int64_t halve_ratio(int64_t d) {
     static const int64_t r128 = [] {
         const char* e = std::getenv("DFA2_HALVES128");
-        return e ? std::atoll(e) : 0;
+        return e ? 10 * std::atoll(e) : 0;
     }();
-    return kernel_dim(d) == 64 ? 5 : r128;
+    return kernel_dim(d) == 64 ? DFA2_HALVES64_DEFAULT : r128;
 }
 
 void launch_forward(const ForwardSpec& s, cudaStream_t stream) {
