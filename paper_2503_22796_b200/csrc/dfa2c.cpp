@@ -826,6 +826,76 @@ std::unique_ptr<DevPlan> build_dev_plan(int device, int64_t batch, int64_t H, in
 // LPT assignment of the work items to one persistent CTA per SM (cost desc,
 // then (bh, pair) so concurrently running CTAs share a head's K/V in L2) and
 // upload of the device plan.
+// LPT leaves a tail when a CTA holds only ~3 items: the CTAs given one of
+// the few long items (text-row pairs) later also receive a short one when
+// everything else is full (SD3 Arrow(8): the costliest CTA 17% above the
+// average). Improvement moves on the costliest CTA until none helps: move
+// one of its items to a lightly loaded CTA, or swap it for a cheaper item
+// there, whichever lowers the larger of the two loads the most. Only the
+// item -> CTA assignment changes (every item's result is independent of
+// where it runs), so results are bitwise unchanged. Deterministic: ties go
+// to the lowest index.
+void refine_schedule(std::vector<std::vector<const Cand*>>& bins, std::vector<double>& load) {
+    const int m = static_cast<int>(bins.size());
+    if (m < 2)
+        return;
+    constexpr int kLight = 16;  // lightest CTAs tried as partners
+    const int max_iters = 4 * m;
+    std::vector<int> order(static_cast<size_t>(m));
+    for (int iter = 0; iter < max_iters; ++iter) {
+        int cm = 0;
+        for (int c = 1; c < m; ++c)
+            if (load[c] > load[cm])
+                cm = c;
+        const double L = load[cm];
+        for (int c = 0; c < m; ++c)
+            order[c] = c;
+        const int k = std::min(kLight, m);
+        std::partial_sort(order.begin(), order.begin() + k, order.end(), [&](int a, int b) {
+            return load[a] != load[b] ? load[a] < load[b] : a < b;
+        });
+        double best = L - 1e-9;
+        int bi = -1, bc = -1, bj = -1;
+        for (int i = 0; i < static_cast<int>(bins[cm].size()); ++i) {
+            const double ci = bins[cm][i]->cost;
+            for (int t = 0; t < k; ++t) {
+                const int c = order[t];
+                if (c == cm)
+                    continue;
+                const double mv = std::max(L - ci, load[c] + ci);
+                if (mv < best) {
+                    best = mv;
+                    bi = i, bc = c, bj = -1;
+                }
+                for (int j = 0; j < static_cast<int>(bins[c].size()); ++j) {
+                    const double cj = bins[c][j]->cost;
+                    if (cj >= ci)
+                        continue;
+                    const double sw = std::max(L - ci + cj, load[c] - cj + ci);
+                    if (sw < best) {
+                        best = sw;
+                        bi = i, bc = c, bj = j;
+                    }
+                }
+            }
+        }
+        if (bi < 0)
+            return;
+        const Cand* x = bins[cm][bi];
+        bins[cm].erase(bins[cm].begin() + bi);
+        load[cm] -= x->cost;
+        if (bj >= 0) {
+            const Cand* y = bins[bc][bj];
+            bins[bc].erase(bins[bc].begin() + bj);
+            load[bc] -= y->cost;
+            bins[cm].push_back(y);
+            load[cm] += y->cost;
+        }
+        bins[bc].push_back(x);
+        load[bc] += x->cost;
+    }
+}
+
 std::unique_ptr<DevPlan> schedule_items(int device, std::vector<Cand>& cands, const std::vector<uint32_t>& tiles,
                                         const std::vector<uint8_t>& mask_bytes, int32_t n_groups, int32_t n_slots,
                                         cudaStream_t stream) {
@@ -841,13 +911,27 @@ std::unique_ptr<DevPlan> schedule_items(int device, std::vector<Cand>& cands, co
     std::priority_queue<Slot, std::vector<Slot>, std::greater<Slot>> pq;
     for (int c = 0; c < grid; ++c)
         pq.push({0.0, c});
-    std::vector<std::vector<WorkItem>> per_cta(static_cast<size_t>(grid));
+    std::vector<std::vector<const Cand*>> bins(static_cast<size_t>(grid));
+    std::vector<double> load(static_cast<size_t>(grid), 0.0);
     for (const Cand& c : cands) {
         Slot s = pq.top();
         pq.pop();
-        per_cta[s.second].push_back(c.w);
+        bins[s.second].push_back(&c);
         s.first += c.cost;
+        load[s.second] = s.first;
         pq.push(s);
+    }
+    refine_schedule(bins, load);
+    std::vector<std::vector<WorkItem>> per_cta(static_cast<size_t>(grid));
+    for (int c = 0; c < grid; ++c) {
+        // costliest first within a CTA (LPT's order), copies last (the kernel's
+        // copy tail streams a CTA's trailing copies through its freed rings)
+        std::stable_sort(bins[c].begin(), bins[c].end(), [](const Cand* a, const Cand* b) {
+            const bool ca = (a->w.flags & dfa2k::ITEM_COPY) != 0, cb = (b->w.flags & dfa2k::ITEM_COPY) != 0;
+            return ca != cb ? cb : a->cost > b->cost;
+        });
+        for (const Cand* x : bins[c])
+            per_cta[c].push_back(x->w);
     }
     std::vector<WorkItem> items;
     std::vector<int32_t> cta_begin(static_cast<size_t>(grid + 1), 0);
