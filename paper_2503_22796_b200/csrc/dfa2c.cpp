@@ -1351,10 +1351,13 @@ void run_forward(const ForwardSpec& s, cudaStream_t stream) {
 #ifndef DFA2_HALVES64_DEFAULT
 #define DFA2_HALVES64_DEFAULT 50
 #endif
+#ifndef DFA2_HALVES128_DEFAULT
+#define DFA2_HALVES128_DEFAULT 0
+#endif
 int64_t halve_ratio(int64_t d) {
     static const int64_t r128 = [] {
         const char* e = std::getenv("DFA2_HALVES128");
-        return e ? 10 * std::atoll(e) : 0;
+        return e ? 10 * std::atoll(e) : DFA2_HALVES128_DEFAULT;
     }();
     return kernel_dim(d) == 64 ? DFA2_HALVES64_DEFAULT : r128;
 }

@@ -30,9 +30,16 @@ SHAPES = {"flux": (24, 16384, 512, 128), "sd3": (24, 4096, 333, 64)}
 B = 128
 
 
+MIXED = {  # a late-timestep layer: most heads Cached, a few narrow arrows (latency-bound)
+    "LATE": " ".join((["C"] * 5 + ["A0"]) * 4),
+}
+
+
 def plan_of(name, H):
     if name == "FLUX68":
         return "flux", FLUX68
+    if name in MIXED:
+        return "flux", MIXED[name]
     shape, kind = name.split("_")
     return shape, " ".join([kind] * H)
 
