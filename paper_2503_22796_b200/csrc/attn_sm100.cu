@@ -150,6 +150,18 @@ constexpr bool KEEPLO = D == 64 ? DFA2_KEEPLO64 : DFA2_KEEPLO128;
 #ifndef DFA2_REGS_OTHER
 #define DFA2_REGS_OTHER 72
 #endif
+#ifndef DFA2_REGS_SOFTMAX64
+#define DFA2_REGS_SOFTMAX64 DFA2_REGS_SOFTMAX
+#endif
+#ifndef DFA2_REGS_OTHER64
+#define DFA2_REGS_OTHER64 DFA2_REGS_OTHER
+#endif
+template <int D>
+constexpr uint32_t REGS_SOFTMAX = D == 64 ? DFA2_REGS_SOFTMAX64 : DFA2_REGS_SOFTMAX;
+template <int D>
+constexpr uint32_t REGS_OTHER = D == 64 ? DFA2_REGS_OTHER64 : DFA2_REGS_OTHER;
+static_assert(DFA2_REGS_OTHER64 + 2 * DFA2_REGS_SOFTMAX64 <= 3 * 168,
+              "setmaxnreg must not ask for more than the CTA's 384 x 168 registers");
 static_assert(DFA2_REGS_OTHER + 2 * DFA2_REGS_SOFTMAX <= 3 * 168,
               "setmaxnreg must not ask for more than the CTA's 384 x 168 registers");
 // trace[((lane * 4096) + tile) * 8 + slot] = clock64() for CTA 0 (debug builds)
@@ -576,7 +588,7 @@ __global__ void __launch_bounds__(384, 1)
     if (warp < 4) {
     // warpgroup 0 (producer / MMA issue) hands registers to the softmax warpgroups
     if (KEEPLO<D>)
-        regs_dec<DFA2_REGS_OTHER>();
+        regs_dec<REGS_OTHER<D>>();
     if (warp == 0) {
         // ------------------------------------------------ TMA producer
         // The whole warp walks the schedule (warp-uniform control flow keeps
@@ -936,7 +948,7 @@ __global__ void __launch_bounds__(384, 1)
     } else {
         // ------------------------------------------------ softmax lanes
         if (KEEPLO<D>)
-            regs_inc<DFA2_REGS_SOFTMAX>();
+            regs_inc<REGS_SOFTMAX<D>>();
         const int L = (warp - 4) >> 2;              // 0 = lane A, 1 = lane B
         const int wq = warp & 3;                    // TMEM lane quarter
         const int r = wq * 32 + lane;               // row within the query tile
