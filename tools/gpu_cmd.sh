@@ -1,1 +1,2 @@
-timeout 1200 python tools/ab_interleaved.py paper_2503_22796_b200/libdfa2_b200.so build/ab_k64_184.so build/ab_k64_200.so --rounds 14 --plans sd3_F,sd3_A16,sd3_A8,sd3_A2,sd3_A0 2>&1 | tee gpurun_out/ab_k64regs.txt
+timeout 900 python tools/configs_bench.py --only 4 --out gpurun_out/cfg4_nosplit.json 2>&1 | grep cfg4 | cut -c1-400
+DFA2_SPLIT_KV=1 timeout 900 python tools/configs_bench.py --only 4 --out gpurun_out/cfg4_split.json 2>&1 | grep cfg4 | cut -c1-400
