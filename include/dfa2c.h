@@ -421,6 +421,12 @@ int64_t dfa2c_launch_count(void);
 /* Debug: device buffer (int64 [2][4096][8]) receiving per-tile clock64 stamps
  * of CTA 0 from kernels built with -DDFA2_TRACE=1 (NULL disables). */
 void dfa2c_debug_set_trace(void* dev_buffer);
+/* Debug / test hook (no device work): the work-list scheduler's CTA
+ * assignment for items of the given costs over n_ctas CTAs — LPT, then with
+ * refine != 0 the move / swap improvement of the costliest CTA. cta_of[i]
+ * receives item i's CTA, *max_load the costliest CTA's load. */
+int dfa2c_debug_schedule(const double* costs, int64_t n, int32_t n_ctas, int32_t refine, int32_t* cta_of,
+                         double* max_load);
 
 #ifdef __cplusplus
 }

@@ -97,6 +97,8 @@ _SIGS = {
     "dfa2c_version": (c_char_p, []),
     "dfa2c_launch_count": (c_int64, []),
     "dfa2c_debug_set_trace": (None, [c_void_p]),
+    "dfa2c_debug_schedule": (c_int32, [POINTER(c_double), c_int64, c_int32, c_int32, POINTER(c_int32),
+                                       POINTER(c_double)]),
     "dfa2c_arrow_mask": (c_int32, [POINTER(Dims), c_int64, c_int64, POINTER(c_uint8), POINTER(c_int64)]),
     "dfa2c_mask_stats": (c_int32, [POINTER(c_uint8), c_int64, c_int64, c_int64, POINTER(c_int64),
                                    POINTER(c_int64), POINTER(c_double)]),

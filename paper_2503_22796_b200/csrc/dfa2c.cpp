@@ -896,17 +896,9 @@ void refine_schedule(std::vector<std::vector<const Cand*>>& bins, std::vector<do
     }
 }
 
-std::unique_ptr<DevPlan> schedule_items(int device, std::vector<Cand>& cands, const std::vector<uint32_t>& tiles,
-                                        const std::vector<uint8_t>& mask_bytes, int32_t n_groups, int32_t n_slots,
-                                        cudaStream_t stream) {
-    std::stable_sort(cands.begin(), cands.end(), [](const Cand& a, const Cand& b) {
-        if (a.cost != b.cost)
-            return a.cost > b.cost;
-        if (a.w.bh != b.w.bh)
-            return a.w.bh < b.w.bh;
-        return a.w.qtile_a < b.w.qtile_a;
-    });
-    const int grid = static_cast<int>(std::min<int64_t>(num_sms(device), static_cast<int64_t>(cands.size())));
+// LPT over `grid` CTAs of candidates already sorted costliest first, then
+// (refine) the move / swap improvement above.
+std::vector<std::vector<const Cand*>> assign_ctas(const std::vector<Cand>& cands, int grid, bool refine) {
     using Slot = std::pair<double, int>;
     std::priority_queue<Slot, std::vector<Slot>, std::greater<Slot>> pq;
     for (int c = 0; c < grid; ++c)
@@ -921,7 +913,23 @@ std::unique_ptr<DevPlan> schedule_items(int device, std::vector<Cand>& cands, co
         load[s.second] = s.first;
         pq.push(s);
     }
-    refine_schedule(bins, load);
+    if (refine)
+        refine_schedule(bins, load);
+    return bins;
+}
+
+std::unique_ptr<DevPlan> schedule_items(int device, std::vector<Cand>& cands, const std::vector<uint32_t>& tiles,
+                                        const std::vector<uint8_t>& mask_bytes, int32_t n_groups, int32_t n_slots,
+                                        cudaStream_t stream) {
+    std::stable_sort(cands.begin(), cands.end(), [](const Cand& a, const Cand& b) {
+        if (a.cost != b.cost)
+            return a.cost > b.cost;
+        if (a.w.bh != b.w.bh)
+            return a.w.bh < b.w.bh;
+        return a.w.qtile_a < b.w.qtile_a;
+    });
+    const int grid = static_cast<int>(std::min<int64_t>(num_sms(device), static_cast<int64_t>(cands.size())));
+    std::vector<std::vector<const Cand*>> bins = assign_ctas(cands, grid, true);
     std::vector<std::vector<WorkItem>> per_cta(static_cast<size_t>(grid));
     for (int c = 0; c < grid; ++c) {
         // costliest first within a CTA (LPT's order), copies last (the kernel's
@@ -1832,6 +1840,35 @@ const char* dfa2c_last_error(void) { return g_err.c_str(); }
 const char* dfa2c_version(void) { return "dfa2c 0.1 (sm_100a tcgen05/TMA fused head-wise attention)"; }
 int64_t dfa2c_launch_count(void) { return g_launches.load(); }
 void dfa2c_debug_set_trace(void* dev_buffer) { g_trace = static_cast<long long*>(dev_buffer); }
+
+int dfa2c_debug_schedule(const double* costs, int64_t n, int32_t n_ctas, int32_t refine, int32_t* cta_of,
+                         double* max_load) {
+    return guard([&] {
+        if (n < 0 || n_ctas < 1 || (n > 0 && (!costs || !cta_of)) || !max_load)
+            fail(DFA2C_SHAPE, "need n >= 0, n_ctas >= 1 and non-NULL buffers");
+        std::vector<Cand> cands(static_cast<size_t>(n));
+        for (int64_t i = 0; i < n; ++i) {
+            if (!(costs[i] >= 0.0))
+                fail(DFA2C_SHAPE, "costs must be >= 0");
+            cands[i].w = WorkItem{};
+            cands[i].w.bh = static_cast<int32_t>(i);
+            cands[i].cost = costs[i];
+        }
+        std::stable_sort(cands.begin(), cands.end(), [](const Cand& a, const Cand& b) { return a.cost > b.cost; });
+        const int grid = static_cast<int>(std::min<int64_t>(n_ctas, std::max<int64_t>(n, 1)));
+        const auto bins = assign_ctas(cands, grid, refine != 0);
+        double mx = 0.0;
+        for (int c = 0; c < grid; ++c) {
+            double l = 0.0;
+            for (const Cand* x : bins[c]) {
+                cta_of[x->w.bh] = c;
+                l += x->cost;
+            }
+            mx = std::max(mx, l);
+        }
+        *max_load = mx;
+    });
+}
 
 int dfa2c_arrow_mask(const dfa2c_dims* dims, int64_t block, int64_t window, uint8_t* active, int64_t* nb) {
     return guard([&] {

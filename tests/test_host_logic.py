@@ -172,3 +172,58 @@ def test_flux68_tile_counts():
         assert not any(int(c) >> 31 for c in cols)  # block-aligned: no element masking at FLUX 2K
     # 134,368 computed 128x128 tiles of 418,176 dense
     assert total * kv_tile() == 134368 * 128 and 24 * 132 * 132 == 418176
+
+
+def _schedule(costs, m, refine):
+    import ctypes
+
+    from paper_2503_22796_b200 import _lib
+    c = np.ascontiguousarray(costs, dtype=np.float64)
+    cta = np.full(len(c), -1, dtype=np.int32)
+    mx = ctypes.c_double()
+    _lib.check(_lib.lib().dfa2c_debug_schedule(c.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), len(c), m,
+                                               int(refine), cta.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                                               ctypes.byref(mx)))
+    return cta, mx.value
+
+
+def _sd3_arrow_costs(w, H=24):
+    # the scheduler's cost model for an SD3 Arrow(w) layer (32 visual + 3 text
+    # query tiles): pairs 2 x union + 1, the trailing text tile as HALVES
+    out = []
+    for _ in range(H):
+        for p in range(16):
+            lo, hi = max(0, 2 * p - w), min(31, 2 * p + 1 + w)
+            out.append(2 * (hi - lo + 1 + 3) + 1)
+        out += [2 * 35 + 1, 1.2 * 35 + 1]
+    return out
+
+
+def test_schedule_refinement_lowers_the_costliest_cta_and_keeps_every_item():
+    # SD3 Arrow(8): LPT leaves the costliest CTA 17% above the mean; the
+    # move / swap refinement brings it under 8% (late round 2)
+    costs = _sd3_arrow_costs(8)
+    mean = sum(costs) / 148
+    cta0, lpt = _schedule(costs, 148, False)
+    cta1, ref = _schedule(costs, 148, True)
+    assert lpt / mean > 1.15 and ref / mean < 1.08 and ref <= lpt
+    for cta in (cta0, cta1):
+        assert cta.min() >= 0 and cta.max() < 148  # every item placed exactly once
+        loads = np.bincount(cta, weights=costs, minlength=148)
+        assert loads.sum() == pytest.approx(sum(costs))
+    assert np.bincount(cta1, weights=costs, minlength=148).max() == pytest.approx(ref)
+    # deterministic, and never worse than LPT on random cost mixes
+    assert np.array_equal(_schedule(costs, 148, True)[0], cta1)
+    rng = np.random.default_rng(5)
+    for _ in range(20):
+        c = rng.choice([3.0, 15.0, 43.0, 71.0, 265.0], size=int(rng.integers(1, 900)))
+        m = int(rng.integers(1, 160))
+        assert _schedule(c, m, True)[1] <= _schedule(c, m, False)[1] + 1e-9
+        assert _schedule(c, m, True)[1] >= max(c.max(), c.sum() / min(m, len(c))) - 1e-9
+
+
+def test_schedule_hook_rejects_bad_arguments():
+    with pytest.raises(ShapeError):
+        _schedule([1.0, -2.0], 4, True)
+    with pytest.raises(ShapeError):
+        _schedule([1.0], 0, True)
