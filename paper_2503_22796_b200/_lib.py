@@ -199,7 +199,10 @@ def lib() -> ctypes.CDLL:
                 f"{LIB_PATH} is missing: build it with `python -m paper_2503_22796_b200.build` "
                 "(there is no CPU fallback for the attention path)")
         L = ctypes.CDLL(LIB_PATH)
+        ab_build = os.path.abspath(LIB_PATH) != os.path.join(HERE, "libdfa2_b200.so")
         for name, (res, args) in _SIGS.items():
+            if ab_build and not hasattr(L, name):
+                continue  # an older A/B build without a newer entry point
             fn = getattr(L, name)
             fn.restype = res
             fn.argtypes = args

@@ -839,7 +839,16 @@ void refine_schedule(std::vector<std::vector<const Cand*>>& bins, std::vector<do
     const int m = static_cast<int>(bins.size());
     if (m < 2)
         return;
-    constexpr int kLight = 16;  // lightest CTAs tried as partners
+    size_t n_items = 0;
+    for (const auto& b : bins)
+        n_items += b.size();
+    // Few items per CTA (SD3-size layers) is where LPT's tail is large and
+    // the search is cheap: every CTA is a partner, and one item of the
+    // costliest CTA may also trade for two cheaper ones (SD3 Arrow(8): 6.8%
+    // -> 3.3% over the mean in the cost model). With many items per CTA
+    // (FLUX) LPT is already within ~2%: the 16 lightest CTAs, single swaps.
+    const bool deep = n_items <= static_cast<size_t>(6 * m);
+    const int kLight = deep ? m : 16;  // lightest CTAs tried as partners
     const int max_iters = 4 * m;
     std::vector<int> order(static_cast<size_t>(m));
     for (int iter = 0; iter < max_iters; ++iter) {
@@ -855,7 +864,7 @@ void refine_schedule(std::vector<std::vector<const Cand*>>& bins, std::vector<do
             return load[a] != load[b] ? load[a] < load[b] : a < b;
         });
         double best = L - 1e-9;
-        int bi = -1, bc = -1, bj = -1;
+        int bi = -1, bc = -1, bj = -1, bk = -1;
         for (int i = 0; i < static_cast<int>(bins[cm].size()); ++i) {
             const double ci = bins[cm][i]->cost;
             for (int t = 0; t < k; ++t) {
@@ -865,16 +874,29 @@ void refine_schedule(std::vector<std::vector<const Cand*>>& bins, std::vector<do
                 const double mv = std::max(L - ci, load[c] + ci);
                 if (mv < best) {
                     best = mv;
-                    bi = i, bc = c, bj = -1;
+                    bi = i, bc = c, bj = -1, bk = -1;
                 }
-                for (int j = 0; j < static_cast<int>(bins[c].size()); ++j) {
+                const int nc = static_cast<int>(bins[c].size());
+                for (int j = 0; j < nc; ++j) {
                     const double cj = bins[c][j]->cost;
                     if (cj >= ci)
                         continue;
                     const double sw = std::max(L - ci + cj, load[c] - cj + ci);
                     if (sw < best) {
                         best = sw;
-                        bi = i, bc = c, bj = j;
+                        bi = i, bc = c, bj = j, bk = -1;
+                    }
+                    if (!deep || nc > 8)
+                        continue;
+                    for (int q = j + 1; q < nc; ++q) {  // two of c's items for one of cm's
+                        const double cjk = cj + bins[c][q]->cost;
+                        if (cjk >= ci)
+                            continue;
+                        const double s2 = std::max(L - ci + cjk, load[c] - cjk + ci);
+                        if (s2 < best) {
+                            best = s2;
+                            bi = i, bc = c, bj = j, bk = q;
+                        }
                     }
                 }
             }
@@ -885,6 +907,14 @@ void refine_schedule(std::vector<std::vector<const Cand*>>& bins, std::vector<do
         bins[cm].erase(bins[cm].begin() + bi);
         load[cm] -= x->cost;
         if (bj >= 0) {
+            // bk > bj: erase the later one first so bj stays valid
+            if (bk >= 0) {
+                const Cand* z = bins[bc][bk];
+                bins[bc].erase(bins[bc].begin() + bk);
+                load[bc] -= z->cost;
+                bins[cm].push_back(z);
+                load[cm] += z->cost;
+            }
             const Cand* y = bins[bc][bj];
             bins[bc].erase(bins[bc].begin() + bj);
             load[bc] -= y->cost;
