@@ -1,1 +1,1 @@
-timeout 1200 python tools/ab_interleaved.py build/ab_refine.so paper_2503_22796_b200/libdfa2_b200.so --rounds 14 --plans sd3_F,sd3_A16,sd3_A8,sd3_A4,sd3_A2,sd3_A0,FLUX68,flux_A8 2>&1 | tee gpurun_out/ab_deep.txt
+DFA2_RANDOM_LAYERS=400 timeout 2400 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -p no:cacheprovider -k random 2>&1 | tail -3 | tee gpurun_out/random400.txt
