@@ -1,1 +1,3 @@
-DFA2_RANDOM_LAYERS=400 timeout 2400 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -p no:cacheprovider -k random 2>&1 | tail -3 | tee gpurun_out/random400.txt
+timeout 600 python bench.py --steps 20 --warmup 5 --no-cpu > gpurun_out/bench_power.json 2> gpurun_out/bench_power.err; tail -2 gpurun_out/bench_power.err
+python -c "import json;d=json.loads(open('gpurun_out/bench_power.json').read().strip().splitlines()[-1]);print(d['clocks'], d['layer_ms'], d['dense_ms'])"
+nvidia-smi --query-gpu=power.limit,power.max_limit,power.default_limit,enforced.power.limit --format=csv
