@@ -221,6 +221,21 @@ class LayerPlan:
     def n_heads(self) -> int:
         return len(self.strategies)
 
+    def __getstate__(self):  # the ctypes cache does not pickle (plans cross process groups)
+        st = dict(self.__dict__)
+        st.pop("_arr_cache", None)
+        return st
+
+    def _arrays_cached(self):
+        # the per-call ctypes arrays of an unchanged plan (read-only use): a
+        # layer call's host cost is otherwise dominated by rebuilding them
+        key = tuple(self.strategies)
+        c = self.__dict__.get("_arr_cache")
+        if c is None or c[0] != key:
+            c = (key, self.arrays())
+            self.__dict__["_arr_cache"] = c
+        return c[1]
+
     def arrays(self):
         kinds = (c_int32 * max(1, len(self.strategies)))(*[_KIND_CODE[s.kind] for s in self.strategies])
         wins = (c_int64 * max(1, len(self.strategies)))(*[s.window_blocks for s in self.strategies])
@@ -262,8 +277,12 @@ def _torch():
 
 def _stream_ptr(stream=None) -> Optional[int]:
     torch = _torch()
-    s = stream if stream is not None else torch.cuda.current_stream()
-    return s.cuda_stream
+    if stream is not None:
+        return stream.cuda_stream
+    raw = getattr(torch._C, "_cuda_getCurrentRawStream", None)  # the current stream without a Stream object
+    if raw is not None:
+        return raw(torch._C._cuda_getDevice())
+    return torch.cuda.current_stream().cuda_stream
 
 
 def _as_bf16_cuda(x, name: str):
@@ -291,11 +310,11 @@ def _device_out(out, like, shape_given, name="out"):
         raise ShapeError(f"{name} must be a CUDA bf16 tensor")
     if not out.is_contiguous():
         raise ShapeError(f"{name} must be contiguous")
-    if out.device != like.device:
+    if out.get_device() != like.get_device():
         raise ShapeError(f"{name} must be on q's device")
-    if tuple(out.shape) != tuple(shape_given):
+    if out.shape != shape_given and tuple(out.shape) != tuple(shape_given):
         raise ShapeError(f"{name} must have q's shape {tuple(shape_given)} (got {tuple(out.shape)})")
-    return out.view(like.shape)
+    return out if out.shape == like.shape else out.view(like.shape)
 
 
 class HeadCache:
@@ -371,6 +390,8 @@ class HeadCache:
 
 # --------------------------------------------------------------- attention
 def _plan_kinds(plan: LayerPlan, skip_heads):
+    if not skip_heads:
+        return plan._arrays_cached()
     kinds, wins = plan.arrays()
     for h in skip_heads or ():
         if not 0 <= h < plan.n_heads():

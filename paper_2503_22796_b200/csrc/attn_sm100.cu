@@ -1276,6 +1276,68 @@ __global__ void __launch_bounds__(384, 1)
                 }
             }
         }
+        if (args.n_copy_tiles > 0) {
+            // Copy pool: the layer's Cached-head copies are not in any CTA's
+            // list; every CTA that has finished its compute drains the pool,
+            // each lane claiming RING 64-column boxes at a time from one
+            // counter, so copies fill whatever compute leaves idle and the
+            // copy bandwidth evens out over the SMs (a static split left
+            // the slowest CTAs 12% behind the average). Every box goes from
+            // its cache slot to out (and the peers) through the lane's ring
+            // in the freed Q / K / V window, as in the per-CTA copy tail.
+            if (issuer)
+                bulk_wait_read0();
+            named_bar_sync(3, 256);  // both lanes' compute is done: the rings are free
+            if (issuer) {
+                // a tile's rows are contiguous in the [bh, N, d] layout of both
+                // the cache and out: 1-D bulk copies of up to BOX_BYTES each
+                const uint32_t tile_bytes = static_cast<uint32_t>(TILE_M * args.row_bytes);
+                const int bpt = static_cast<int>((tile_bytes + C::BOX_BYTES - 1) / C::BOX_BYTES);
+                const int total = args.n_copy_tiles * bpt;
+                const uint64_t pol = policy_evict_first();
+                const char* csrc = reinterpret_cast<const char*>(args.cache);
+                for (;;) {
+                    const int base = atomicAdd(args.copy_ctr, C::RING);
+                    if (base >= total)
+                        break;
+                    const int got = min(C::RING, total - base);
+                    int64_t boff[C::RING];
+                    uint32_t blen[C::RING];
+                    bulk_wait_read0();  // the previous batch's stores have read the ring
+#pragma unroll
+                    for (int i = 0; i < C::RING; ++i) {
+                        blen[i] = 0;
+                        if (i >= got)
+                            continue;
+                        const int box = base + i;
+                        const int2 ct = args.copy_tiles[box / bpt];
+                        const int rows = min(TILE_M, args.n - ct.y * TILE_M);
+                        const int64_t off = static_cast<int64_t>(box % bpt) * C::BOX_BYTES;
+                        const int64_t left = static_cast<int64_t>(rows) * args.row_bytes - off;
+                        if (left <= 0)
+                            continue;  // a ragged tile's missing box
+                        blen[i] = static_cast<uint32_t>(left < static_cast<int64_t>(C::BOX_BYTES) ? left : static_cast<int64_t>(C::BOX_BYTES));
+                        boff[i] = (static_cast<int64_t>(ct.x) * args.n + static_cast<int64_t>(ct.y) * TILE_M) *
+                                      args.row_bytes + off;
+                        const uint32_t addr = sbase + static_cast<uint32_t>(L * C::RING + i) * C::BOX_BYTES;
+                        mbar_arrive_expect_tx(ring_full(L, i), blen[i]);
+                        bulk_load_1d_hint(addr, csrc + boff[i], blen[i], ring_full(L, i), pol);
+                    }
+#pragma unroll
+                    for (int i = 0; i < C::RING; ++i) {
+                        if (blen[i] == 0)
+                            continue;
+                        const uint32_t addr = sbase + static_cast<uint32_t>(L * C::RING + i) * C::BOX_BYTES;
+                        mbar_wait(ring_full(L, i), ring_phase[i]);
+                        ring_phase[i] ^= 1u;
+                        bulk_store_1d_hint(reinterpret_cast<char*>(args.out) + boff[i], addr, blen[i], pol);
+                        for (int p = 0; p < args.n_peers; ++p)
+                            bulk_store_1d_hint(static_cast<char*>(peers.ptr[p]) + boff[i], addr, blen[i], pol);
+                        bulk_commit();
+                    }
+                }
+            }
+        }
         if (issuer)
             bulk_wait0();  // every bulk store of this lane has completed
     }
@@ -1287,6 +1349,15 @@ __global__ void __launch_bounds__(384, 1)
     tc_fence_after();
     if (DFA2_TRACE == 4 && args.trace && threadIdx.x == 0)
         args.trace[blockIdx.x * 4 + 3] = gtime();
+    if (args.n_copy_tiles > 0 && threadIdx.x == 0) {
+        // the last CTA out re-zeroes this launch's pool counter slot (every
+        // CTA's claims precede its increment here), ready for its next use
+        __threadfence();
+        if (atomicAdd(args.copy_ctr + 1, 1) == static_cast<int>(gridDim.x) - 1) {
+            atomicExch(args.copy_ctr, 0);
+            atomicExch(args.copy_ctr + 1, 0);
+        }
+    }
     if (warp == 2)
         tmem_dealloc(tmem, C::TMEM_COLS);
 }

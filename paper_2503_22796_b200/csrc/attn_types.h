@@ -4,6 +4,7 @@
 #include <cstdint>
 #include <cuda.h>
 #include <cuda_bf16.h>
+#include <vector_types.h>
 
 namespace dfa2k {
 
@@ -74,6 +75,10 @@ struct AttnArgs {
     int* counters;             // split groups: [groups][2 lanes] chunks finished (zeroed per launch)
     int32_t n_peers;           // sharded P2P launches: other ranks' out buffers (PeerMaps) to store to
     int32_t copies_last;       // every CTA's copy items form the tail of its list (the copy-tail ring)
+    const int2* copy_tiles;    // copy pool: (bh, query tile) of every Cached-head tile of the launch
+    int32_t n_copy_tiles;      //   (0: copies are per-CTA list items)
+    int32_t row_bytes;         //   bytes per row of out / cache (d x 2)
+    int* copy_ctr;             //   [2]: boxes claimed, CTAs done (zero at launch; the last CTA re-zeroes)
     int32_t snap_stride;       // ITEM_MULTI: rows of `to` between candidate outputs (= batch*H)
     int32_t n_snap;            // ITEM_MULTI: snapshots per query tile (window bands + the full row)
     uint16_t snap_slots[MAX_SNAPS];
@@ -85,6 +90,7 @@ struct AttnArgs {
 constexpr int MAX_PEERS = 7;  // world <= 8
 struct PeerMaps {
     CUtensorMap m[MAX_PEERS];
+    void* ptr[MAX_PEERS];  // the same buffers as raw pointers (the copy pool's 1-D bulk stores)
 };
 
 constexpr int TILE_M = 128;  // query rows per tile (tcgen05 M)

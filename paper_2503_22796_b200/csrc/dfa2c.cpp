@@ -221,6 +221,8 @@ struct DevPlan {
     int32_t n_groups = 0;  // split groups (counters per launch)
     int32_t n_slots = 0;   // partial-output slots (one per split chunk)
     bool copies_last = false;  // every CTA's copy items are the tail of its list
+    int32_t n_copy_tiles = 0;  // copy pool: Cached-head tiles drained by every CTA
+    int2* copy_tiles = nullptr;
     WorkItem* items = nullptr;
     int32_t* cta_begin = nullptr;
     uint32_t* tiles = nullptr;
@@ -564,6 +566,43 @@ bool copy_tail_enabled() {
         return !(e && e[0] == '0');
     }();
     return on;
+}
+
+// Cached-head copies as one pool drained by every CTA once its compute is
+// done (DFA2_COPY_POOL=0: LPT places them as list items, copied in each
+// CTA's tail).
+#ifndef DFA2_COPY_POOL_DEFAULT
+#define DFA2_COPY_POOL_DEFAULT 1
+#endif
+bool copy_pool_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("DFA2_COPY_POOL");
+        return e ? e[0] != '0' : DFA2_COPY_POOL_DEFAULT != 0;
+    }();
+    return on && copy_tail_enabled();
+}
+
+// Per-launch copy-pool counters: a ring of zeroed [claimed, done] pairs per
+// device; launch k uses slot k mod kCopySlots and its last CTA re-zeroes it,
+// so no memset sits between launches.
+constexpr int kCopySlots = 1 << 16;
+int* copy_counter_slot(int device) {
+    static std::mutex mu;
+    static int* base[64] = {};
+    static std::atomic<uint32_t> seq[64];
+    if (device < 0 || device >= 64)
+        fail(DFA2C_UNSUPPORTED, "device index out of range");
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        if (!base[device]) {
+            int* p = nullptr;
+            DFA2C_CUDA_CHECK(cudaMalloc(&p, sizeof(int) * 2 * kCopySlots));
+            DFA2C_CUDA_CHECK(cudaMemset(p, 0, sizeof(int) * 2 * kCopySlots));
+            DFA2C_CUDA_CHECK(cudaDeviceSynchronize());
+            base[device] = p;
+        }
+    }
+    return base[device] + 2 * (seq[device].fetch_add(1) % kCopySlots);
 }
 
 // Key-chunk boundaries of a split pair: chunk c gets a share of the union
@@ -958,7 +997,24 @@ std::unique_ptr<DevPlan> schedule_items(int device, std::vector<Cand>& cands, co
             return a.w.bh < b.w.bh;
         return a.w.qtile_a < b.w.qtile_a;
     });
-    const int grid = static_cast<int>(std::min<int64_t>(num_sms(device), static_cast<int64_t>(cands.size())));
+    // copy pool: the Cached-head tiles leave the lists (LPT balances the
+    // compute alone; every CTA drains the pool when its compute is done)
+    std::vector<int2> copy_tiles;
+    if (copy_pool_enabled()) {
+        std::vector<Cand> compute;
+        for (const Cand& c : cands) {
+            if (c.w.flags & dfa2k::ITEM_COPY) {
+                copy_tiles.push_back(make_int2(c.w.bh, c.w.qtile_a));
+                if (c.w.qtile_b >= 0)
+                    copy_tiles.push_back(make_int2(c.w.bh, c.w.qtile_b));
+            } else {
+                compute.push_back(c);
+            }
+        }
+        cands.swap(compute);
+    }
+    const int64_t units = static_cast<int64_t>(cands.size() + copy_tiles.size());
+    const int grid = static_cast<int>(std::min<int64_t>(num_sms(device), units));
     std::vector<std::vector<const Cand*>> bins = assign_ctas(cands, grid, true);
     std::vector<std::vector<WorkItem>> per_cta(static_cast<size_t>(grid));
     for (int c = 0; c < grid; ++c) {
@@ -988,25 +1044,30 @@ std::unique_ptr<DevPlan> schedule_items(int device, std::vector<Cand>& cands, co
     auto p = std::make_unique<DevPlan>();
     p->grid = grid;
     p->copies_last = copies_last;
+    p->n_copy_tiles = static_cast<int32_t>(copy_tiles.size());
     p->n_groups = n_groups;
     p->n_slots = n_slots;
     p->device = device;
-    // one block: [items | cta_begin | tiles | masks], 256-byte aligned parts
+    // one block: [items | cta_begin | copy tiles | tiles | masks], 256-byte aligned parts
     auto up = [](size_t x) { return (x + 255) / 256 * 256; };
     const size_t o_items = 0, n_items = items.size() * sizeof(WorkItem);
     const size_t o_cta = up(o_items + n_items), n_cta = cta_begin.size() * sizeof(int32_t);
-    const size_t o_tiles = up(o_cta + n_cta), n_tiles = tiles.size() * sizeof(uint32_t);
+    const size_t o_copy = up(o_cta + n_cta), n_copy = copy_tiles.size() * sizeof(int2);
+    const size_t o_tiles = up(o_copy + n_copy), n_tiles = tiles.size() * sizeof(uint32_t);
     const size_t o_masks = up(o_tiles + n_tiles), n_masks = mask_bytes.size();
     p->bytes = up(o_masks + n_masks);
     scratch_alloc(&p->dev, p->bytes, stream);
     char* d = static_cast<char*>(p->dev);
     p->items = reinterpret_cast<WorkItem*>(d + o_items);
     p->cta_begin = reinterpret_cast<int32_t*>(d + o_cta);
+    p->copy_tiles = reinterpret_cast<int2*>(d + o_copy);
     p->tiles = reinterpret_cast<uint32_t*>(d + o_tiles);
     p->masks = reinterpret_cast<uint8_t*>(d + o_masks);
     plan_upload(device, stream, p->dev, p->bytes, [&](char* h) {
         std::memcpy(h + o_items, items.data(), n_items);
         std::memcpy(h + o_cta, cta_begin.data(), n_cta);
+        if (n_copy)
+            std::memcpy(h + o_copy, copy_tiles.data(), n_copy);
         std::memcpy(h + o_tiles, tiles.data(), n_tiles);
         std::memcpy(h + o_masks, mask_bytes.data(), n_masks);
     });
@@ -1073,7 +1134,36 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 // [rows=batch*H][n][d] bf16, box {64 cols, box_rows rows, 1}, 128-byte
 // swizzle: the canonical K-major SW128 UMMA layout (and MN-major for V).
+CUtensorMap encode_map(const void* base, int64_t bh, int64_t n, int64_t d, int box_rows);
+
+// Encoding is a pure host computation of the descriptor, and steady-state
+// callers pass the same buffers every layer: a small per-thread cache keyed
+// by (base, shape, box) saves ~0.5-1 us per map (five per launch).
 CUtensorMap make_map(const void* base, int64_t bh, int64_t n, int64_t d, int box_rows) {
+    struct Entry {
+        const void* base;
+        int64_t bh, n, d;
+        int box;
+        CUtensorMap m;
+    };
+    constexpr int kEntries = 16;
+    thread_local Entry cache[kEntries];
+    thread_local int next = 0;
+    for (const Entry& e : cache)
+        if (e.base == base && base && e.bh == bh && e.n == n && e.d == d && e.box == box_rows)
+            return e.m;
+    Entry& e = cache[next];
+    next = (next + 1) % kEntries;
+    e.m = encode_map(base, bh, n, d, box_rows);
+    e.base = base;
+    e.bh = bh;
+    e.n = n;
+    e.d = d;
+    e.box = box_rows;
+    return e.m;
+}
+
+CUtensorMap encode_map(const void* base, int64_t bh, int64_t n, int64_t d, int box_rows) {
     CUtensorMap m;
     const cuuint64_t dims[3] = {static_cast<cuuint64_t>(d), static_cast<cuuint64_t>(n),
                                 static_cast<cuuint64_t>(bh)};
@@ -1483,6 +1573,10 @@ void launch_forward(const ForwardSpec& s, cudaStream_t stream) {
     a.cache = static_cast<__nv_bfloat16*>(cache_layer);
     a.n = static_cast<int32_t>(n);
     a.copies_last = plan->copies_last && copy_tail_enabled() ? 1 : 0;
+    a.n_copy_tiles = plan->n_copy_tiles;
+    a.copy_tiles = plan->copy_tiles;
+    a.row_bytes = static_cast<int32_t>(d * 2);
+    a.copy_ctr = plan->n_copy_tiles > 0 ? copy_counter_slot(device) : nullptr;
     a.block = static_cast<int32_t>(std::min<int64_t>(s.block, int64_t{1} << 30));
     a.nb = static_cast<int32_t>(ceil_div(n, s.block));
     a.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(s.scale_d ? s.scale_d : d)));
@@ -1506,6 +1600,7 @@ void launch_forward(const ForwardSpec& s, cudaStream_t stream) {
     for (size_t i = 0; i < s.peer_outs.size(); ++i) {
         check_ptr(s.peer_outs[i], "peer out");
         peers.m[i] = make_map(s.peer_outs[i], bh, n, d, dfa2k::TILE_M);
+        peers.ptr[i] = s.peer_outs[i];
     }
     a.n_peers = static_cast<int32_t>(s.peer_outs.size());
     DFA2C_CUDA_CHECK(dfa2k::launch_attn(kernel_dim(d), tq, tk, tv, to, tc, a, peers, plan->grid, stream));
@@ -1732,6 +1827,8 @@ void run_influence_fused(const void* q, const void* k, const void* v, const dfa2
     a.trace = g_trace;
     a.snap_stride = static_cast<int32_t>(H);
     a.n_snap = plan->n_snap;
+    if (plan->n_copy_tiles)
+        fail(DFA2C_UNSUPPORTED, "calibration plans have no cached heads");
     std::copy(plan->snap_slots, plan->snap_slots + dfa2k::MAX_SNAPS, a.snap_slots);
     plan->acquire(stream);
     dfa2k::PeerMaps no_peers;
