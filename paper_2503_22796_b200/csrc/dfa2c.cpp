@@ -586,23 +586,27 @@ bool copy_pool_enabled() {
 // device; launch k uses slot k mod kCopySlots and its last CTA re-zeroes it,
 // so no memset sits between launches.
 constexpr int kCopySlots = 1 << 16;
-int* copy_counter_slot(int device) {
+// The ring is allocated when the first plan with copies is built (never
+// under CUDA-graph capture, which reuses built plans only).
+int* copy_counter_base(int device) {
     static std::mutex mu;
     static int* base[64] = {};
-    static std::atomic<uint32_t> seq[64];
     if (device < 0 || device >= 64)
         fail(DFA2C_UNSUPPORTED, "device index out of range");
-    {
-        std::lock_guard<std::mutex> lk(mu);
-        if (!base[device]) {
-            int* p = nullptr;
-            DFA2C_CUDA_CHECK(cudaMalloc(&p, sizeof(int) * 2 * kCopySlots));
-            DFA2C_CUDA_CHECK(cudaMemset(p, 0, sizeof(int) * 2 * kCopySlots));
-            DFA2C_CUDA_CHECK(cudaDeviceSynchronize());
-            base[device] = p;
-        }
+    std::lock_guard<std::mutex> lk(mu);
+    if (!base[device]) {
+        int* p = nullptr;
+        DFA2C_CUDA_CHECK(cudaMalloc(&p, sizeof(int) * 2 * kCopySlots));
+        DFA2C_CUDA_CHECK(cudaMemset(p, 0, sizeof(int) * 2 * kCopySlots));
+        DFA2C_CUDA_CHECK(cudaDeviceSynchronize());
+        base[device] = p;
     }
-    return base[device] + 2 * (seq[device].fetch_add(1) % kCopySlots);
+    return base[device];
+}
+int* copy_counter_slot(int device) {
+    static std::atomic<uint32_t> seq[64];
+    int* base = copy_counter_base(device);
+    return base + 2 * (seq[device].fetch_add(1) % kCopySlots);
 }
 
 // Key-chunk boundaries of a split pair: chunk c gets a share of the union
@@ -1045,6 +1049,8 @@ std::unique_ptr<DevPlan> schedule_items(int device, std::vector<Cand>& cands, co
     p->grid = grid;
     p->copies_last = copies_last;
     p->n_copy_tiles = static_cast<int32_t>(copy_tiles.size());
+    if (!copy_tiles.empty())
+        copy_counter_base(device);
     p->n_groups = n_groups;
     p->n_slots = n_slots;
     p->device = device;
@@ -1093,6 +1099,26 @@ size_t max_plans() {  // DFA2_PLAN_CACHE_MAX overrides the count (tests exercise
         return x > 0 ? static_cast<size_t>(x) : kMaxPlans;
     }();
     return v;
+}
+
+bool stream_capturing(cudaStream_t stream) {
+    cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+    DFA2C_CUDA_CHECK(cudaStreamIsCapturing(stream, &st));
+    return st != cudaStreamCaptureStatusNone;
+}
+
+// A plan captured into a CUDA graph: the graph orders itself after the
+// plan's upload through an external event-wait node (a plain stream wait on
+// an uncaptured event would invalidate the capture), and the plan stays
+// allocated for the process lifetime.
+std::mutex g_pinned_mu;
+std::vector<std::shared_ptr<DevPlan>> g_pinned;
+void pin_for_capture(const std::shared_ptr<DevPlan>& plan, cudaStream_t stream) {
+    if (plan->ready)
+        DFA2C_CUDA_CHECK(cudaStreamWaitEvent(stream, plan->ready, cudaEventWaitExternal));
+    std::lock_guard<std::mutex> lk(g_pinned_mu);
+    if (std::find(g_pinned.begin(), g_pinned.end(), plan) == g_pinned.end())
+        g_pinned.push_back(plan);
 }
 
 std::shared_ptr<DevPlan> plan_insert(const std::string& key, std::unique_ptr<DevPlan> p) {
@@ -1253,6 +1279,16 @@ struct dfa2c_cache {
         } else {
             order_after_ready(layer, st);
         }
+        return layer_buf[layer];
+    }
+    // Under CUDA-graph capture: the buffer must exist and be initialised
+    // (no stream ordering can be captured against its allocation).
+    void* layer_ptr_captured(int64_t layer, cudaStream_t st) {
+        if (!layer_buf[layer])
+            fail(DFA2C_UNSUPPORTED, "CUDA-graph capture: the cache layer is not allocated yet (run the layer "
+                                    "once without capture first)");
+        if (layer_ready[layer])  // an external event-wait node in the graph
+            DFA2C_CUDA_CHECK(cudaStreamWaitEvent(st, layer_ready[layer], cudaEventWaitExternal));
         return layer_buf[layer];
     }
     void order_after_ready(int64_t layer, cudaStream_t st) const {
@@ -1522,12 +1558,21 @@ void launch_forward(const ForwardSpec& s, cudaStream_t stream) {
     put(key, s.part);
     key += s.mask_key;
 
+    // CUDA-graph capture: a launch on a capturing stream must not touch
+    // uncaptured work (no waits on the plan's upload or on other streams),
+    // so it needs a work list a plain call already built and uploaded; that
+    // plan is pinned for the life of the process, since the graph holds its
+    // device memory.
+    const bool capturing = stream_capturing(stream);
     std::shared_ptr<DevPlan> plan;
     {
         std::lock_guard<std::mutex> lk(g_plan_mu);
         auto it = g_plans.find(key);
         if (it != g_plans.end()) {
             plan = it->second;
+        } else if (capturing) {
+            fail(DFA2C_UNSUPPORTED, "CUDA-graph capture of a layer needs one plain call with the same plan and "
+                                    "shapes first (it builds and uploads the work list)");
         } else {
             // masks are only materialised when the work list has to be built
             std::vector<std::vector<uint8_t>> built;
@@ -1555,7 +1600,7 @@ void launch_forward(const ForwardSpec& s, cudaStream_t stream) {
         if (!s.cache)
             fail(DFA2C_CACHE_MISS, "cached heads need a cache");
         s.cache->ensure(s.layer);
-        cache_layer = s.cache->layer_ptr(s.layer, stream);
+        cache_layer = capturing ? s.cache->layer_ptr_captured(s.layer, stream) : s.cache->layer_ptr(s.layer, stream);
     }
 
     const int64_t bh = s.batch * H;
@@ -1592,7 +1637,10 @@ void launch_forward(const ForwardSpec& s, cudaStream_t stream) {
         scratch_alloc(&a.counters, static_cast<size_t>(plan->n_groups) * 2 * sizeof(int), stream);
         DFA2C_CUDA_CHECK(cudaMemsetAsync(a.counters, 0, static_cast<size_t>(plan->n_groups) * 2 * sizeof(int), stream));
     }
-    plan->acquire(stream);
+    if (capturing)
+        pin_for_capture(plan, stream);
+    else
+        plan->acquire(stream);
     dfa2k::PeerMaps peers;
     std::memset(&peers, 0, sizeof peers);
     if (s.peer_outs.size() > static_cast<size_t>(dfa2k::MAX_PEERS))
@@ -1604,7 +1652,8 @@ void launch_forward(const ForwardSpec& s, cudaStream_t stream) {
     }
     a.n_peers = static_cast<int32_t>(s.peer_outs.size());
     DFA2C_CUDA_CHECK(dfa2k::launch_attn(kernel_dim(d), tq, tk, tv, to, tc, a, peers, plan->grid, stream));
-    plan->release(stream);
+    if (!capturing)
+        plan->release(stream);
     if (plan->n_groups > 0) {
         DFA2C_CUDA_CHECK(cudaFreeAsync(a.part_o, stream));
         DFA2C_CUDA_CHECK(cudaFreeAsync(a.part_ml, stream));

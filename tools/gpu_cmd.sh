@@ -1,4 +1,1 @@
-timeout 300 python tools/api_overhead.py 2>&1 | head -3
-timeout 120 python tools/allc_probe.py flux; timeout 120 python tools/allc_probe.py sd3
-timeout 300 python tools/hbm_paths.py 2>&1 | tail -3
-timeout 1500 python -m pytest tests -m gpu -q -x -p no:cacheprovider 2>&1 | tail -2
+timeout 900 python tools/configs_bench.py --only 1,2,3 --out gpurun_out/configs_r02i.json 2>&1 | grep -E "^cfg" | cut -c1-300
