@@ -1,4 +1,2 @@
-timeout 1500 python -m pytest tests -m gpu -q -x -p no:cacheprovider 2>&1 | tail -2
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
-timeout 900 python bench.py > gpurun_out/bench_r02j.json 2> gpurun_out/bench_r02j.err; tail -2 gpurun_out/bench_r02j.err
-python -c "import json;d=json.loads(open('gpurun_out/bench_r02j.json').read().strip().splitlines()[-1]);print(d['ms_per_step'], d['roofline']['frac'], d['e2e']['ms_per_step'], d['clocks'], d['parity']['pass'], d.get('e2e_cpp_f32',{}).get('ms_per_step'))"
+timeout 1200 python tools/ab_interleaved.py build/ab_cur.so paper_2503_22796_b200/libdfa2_b200.so --rounds 14 --plans FLUX68,flux_F,sd3_F,sd3_A16,sd3_A8,sd3_A4,sd3_A2,sd3_A0 2>&1 | tee gpurun_out/ab_splitld2.txt
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_graphs.py -m gpu -q -x -p no:cacheprovider 2>&1 | tail -1
