@@ -220,6 +220,9 @@ __device__ __forceinline__ uint32_t p_col(int lane) {
 template <int D>
 constexpr uint32_t P_HI = D == 64 ? 32u : 64u;
 
+#ifndef DFA2_SUM_CHAINS
+#define DFA2_SUM_CHAINS 1
+#endif
 #ifndef DFA2_POLY_NOSEL
 #define DFA2_POLY_NOSEL 1
 #endif
@@ -304,6 +307,13 @@ template <int D>
 __device__ __forceinline__ void softmax_half(const uint32_t* s, float2 scale2, float2 neg_m, float2& sum,
                                              uint32_t dst) {
     constexpr int EMU = D == 64 ? DFA2_EMU_EVERY64 : DFA2_EMU_EVERY128;
+    // DFA2_SUM_CHAINS independent row-sum accumulators (the FADD2 chain is
+    // otherwise one dependency through every pair of the half)
+    constexpr int NS = DFA2_SUM_CHAINS;
+    float2 acc[NS];
+#pragma unroll
+    for (int j = 0; j < NS; ++j)
+        acc[j] = j == 0 ? sum : make_float2(0.f, 0.f);
 #pragma unroll
     for (int cc = 0; cc < 2; ++cc) {
         uint32_t pk[16];
@@ -318,11 +328,15 @@ __device__ __forceinline__ void softmax_half(const uint32_t* s, float2 scale2, f
             } else {
                 p = make_float2(ex2_approx(x.x), ex2_approx(x.y));
             }
-            sum = __fadd2_rn(sum, p);
+            acc[i % NS] = __fadd2_rn(acc[i % NS], p);
             pk[i] = pack_bf16x2(p.x, p.y);
         }
         tmem_st16(dst + 16 * cc, pk);
     }
+#pragma unroll
+    for (int j = 1; j < NS; ++j)
+        acc[0] = __fadd2_rn(acc[0], acc[j]);
+    sum = acc[0];
 }
 
 // DFA2_TRACE == 2: in-softmax stamps (slots 3..7 of the lane's trace rows)
