@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <immintrin.h>
 #include <sys/mman.h>
 #include <chrono>
 #include <cstdlib>
@@ -234,7 +235,7 @@ struct Seg {
 
 // f32 -> bf16, round to nearest even (NaN -> 0x7FFF), bitwise what the
 // device conversion (__float2bfloat16_rn, dfa2c_convert) gives.
-void round_f32_to_bf16(const float* src, uint16_t* dst, size_t n) {
+void round_f32_to_bf16_scalar(const float* src, uint16_t* dst, size_t n) {
     for (size_t i = 0; i < n; ++i) {
         uint32_t u;
         std::memcpy(&u, src + i, 4);
@@ -243,11 +244,68 @@ void round_f32_to_bf16(const float* src, uint16_t* dst, size_t n) {
         dst[i] = nan ? uint16_t{0x7FFF} : static_cast<uint16_t>(r);
     }
 }
-void widen_bf16_to_f32(const uint16_t* src, float* dst, size_t n) {
+void widen_bf16_to_f32_scalar(const uint16_t* src, float* dst, size_t n) {
     for (size_t i = 0; i < n; ++i) {
         const uint32_t u = static_cast<uint32_t>(src[i]) << 16;
         std::memcpy(dst + i, &u, 4);
     }
+}
+// The same conversions 16 lanes at a time (AVX-512F/BW, picked at run time):
+// the host side of the drop-in's f32 calling convention is bound by these
+// passes over the tensors.
+__attribute__((target("avx512f,avx512bw"))) void round_f32_to_bf16_avx512(const float* src, uint16_t* dst,
+                                                                         size_t n) {
+    const __m512i bias = _mm512_set1_epi32(0x7FFF), one = _mm512_set1_epi32(1);
+    const __m512i absmask = _mm512_set1_epi32(0x7FFFFFFF), inf = _mm512_set1_epi32(0x7F800000);
+    const __m512i qnan = _mm512_set1_epi32(0x7FFF);
+    size_t i = 0;
+    // streaming (non-temporal) stores once dst is 32-byte aligned: the pinned
+    // chunk is read next by the DMA engine, not by this core
+    for (; i < n && (reinterpret_cast<uintptr_t>(dst + i) & 31u); ++i)
+        round_f32_to_bf16_scalar(src + i, dst + i, 1);
+    for (; i + 16 <= n; i += 16) {
+        const __m512i u = _mm512_loadu_si512(src + i);
+        const __m512i lsb = _mm512_and_si512(_mm512_srli_epi32(u, 16), one);
+        __m512i r = _mm512_srli_epi32(_mm512_add_epi32(_mm512_add_epi32(u, bias), lsb), 16);
+        const __mmask16 nan = _mm512_cmpgt_epu32_mask(_mm512_and_si512(u, absmask), inf);
+        r = _mm512_mask_mov_epi32(r, nan, qnan);
+        _mm256_stream_si256(reinterpret_cast<__m256i*>(dst + i), _mm512_cvtepi32_epi16(r));
+    }
+    _mm_sfence();
+    round_f32_to_bf16_scalar(src + i, dst + i, n - i);
+}
+__attribute__((target("avx512f,avx512bw"))) void widen_bf16_to_f32_avx512(const uint16_t* src, float* dst,
+                                                                         size_t n) {
+    size_t i = 0;
+    // streaming stores into the caller's f32 tensor (no read-for-ownership of
+    // the destination lines) once it is 64-byte aligned
+    for (; i < n && (reinterpret_cast<uintptr_t>(dst + i) & 63u); ++i)
+        widen_bf16_to_f32_scalar(src + i, dst + i, 1);
+    for (; i + 16 <= n; i += 16) {
+        const __m256i h = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(src + i));
+        _mm512_stream_si512(reinterpret_cast<__m512i*>(dst + i), _mm512_slli_epi32(_mm512_cvtepu16_epi32(h), 16));
+    }
+    _mm_sfence();
+    widen_bf16_to_f32_scalar(src + i, dst + i, n - i);
+}
+bool have_avx512bw() {
+    static const bool ok = [] {
+        __builtin_cpu_init();
+        return __builtin_cpu_supports("avx512f") && __builtin_cpu_supports("avx512bw");
+    }();
+    return ok;
+}
+void round_f32_to_bf16(const float* src, uint16_t* dst, size_t n) {
+    if (have_avx512bw())
+        round_f32_to_bf16_avx512(src, dst, n);
+    else
+        round_f32_to_bf16_scalar(src, dst, n);
+}
+void widen_bf16_to_f32(const uint16_t* src, float* dst, size_t n) {
+    if (have_avx512bw())
+        widen_bf16_to_f32_avx512(src, dst, n);
+    else
+        widen_bf16_to_f32_scalar(src, dst, n);
 }
 
 // Host <-> device mover for the reference's pageable host tensors: the

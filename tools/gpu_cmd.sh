@@ -1,1 +1,6 @@
-timeout 1200 python tools/ab_interleaved.py build/ab_cur2.so build/ab_sum2.so build/ab_sum4.so --rounds 14 --plans FLUX68,flux_F,sd3_F,sd3_A8,sd3_A0 2>&1 | tee gpurun_out/ab_sumchains.txt
+for l in build/ab_scalarconv.so paper_2503_22796_b200/libdfa2_b200.so build/ab_scalarconv.so paper_2503_22796_b200/libdfa2_b200.so; do
+  cp $l /tmp/libdfa2_b200.so
+  echo "== $l"
+  LD_PRELOAD=/tmp/libdfa2_b200.so DFA2_HOST_PROFILE=1 timeout 300 tools/cpp_api_bench_bin 2>&1 | tail -2
+done
+timeout 1200 python -m pytest tests/test_cpp_api.py -q -x -p no:cacheprovider 2>&1 | tail -1
