@@ -314,8 +314,17 @@ void widen_bf16_to_f32(const uint16_t* src, float* dst, size_t n) {
 // flight on a copy stream. Synchronous for the caller, like the reference.
 class HostMover {
 public:
-    static constexpr size_t kChunk = size_t{32} << 20;
-    static constexpr int kBufs = 3;
+#ifndef DFA2_MOVER_CHUNK_MB
+#define DFA2_MOVER_CHUNK_MB 32
+#endif
+#ifndef DFA2_MOVER_BUFS
+#define DFA2_MOVER_BUFS 3
+#endif
+#ifndef DFA2_MOVER_TASK_KB
+#define DFA2_MOVER_TASK_KB 1024
+#endif
+    static constexpr size_t kChunk = size_t{DFA2_MOVER_CHUNK_MB} << 20;
+    static constexpr int kBufs = DFA2_MOVER_BUFS;
     ~HostMover() {
         for (int i = 0; i < kBufs; ++i) {
             if (pin_[i])
@@ -353,7 +362,7 @@ public:
         HostPool& pool = HostPool::get();
         auto host_copy = [&](char* pinned, size_t lo, size_t hi, bool into_pinned) {
             // split the chunk into ~1 MB tasks over the pool
-            const size_t len = hi - lo, task = size_t{1} << 20;
+            const size_t len = hi - lo, task = size_t{DFA2_MOVER_TASK_KB} << 10;
             const size_t ntask = (len + task - 1) / task;
             pool.parallel_for(ntask, [&](size_t t) {
                 const size_t a = lo + t * task, b = std::min(hi, a + task);
