@@ -960,3 +960,41 @@ def test_d64_text_rows_halved_across_lanes(order):
     o = to_np(a)
     for h, s_ in enumerate(LayerPlan.parse("A0 A0 F").strategies):
         check_close(o[h][rows], oracle_head(qn[h], kn[h], vn[h], dims, B, s_, rows), f"head {h} {s_}")
+
+
+_COPY_MODES_SCRIPT = r"""
+import sys, torch
+sys.path.insert(0, sys.argv[1])
+from paper_2503_22796_b200 import api
+g = torch.Generator(device="cuda").manual_seed(3)
+H, NV, NT, D = 8, 2048, 200, int(sys.argv[2])
+N = NV + NT
+dims = api.AttentionDims(H, D, NV, NT)
+q, k, v = (torch.randn(1, H, N, D, device="cuda", generator=g).to(torch.bfloat16) for _ in range(3))
+cache = api.HeadCache(1, H, N, D)
+out = torch.empty_like(q)
+api.multi_strategy_attention(q, k, v, api.LayerPlan.all_full(H), cache, 0, 0, dims, 128, out=out)
+for plan in ("F C A2 C C A0 F C", "C C C C C C C C"):
+    api.multi_strategy_attention(q, k, v, api.LayerPlan.parse(plan), cache, 0, 1, dims, 128, out=out)
+    torch.cuda.synchronize()
+    sys.stdout.buffer.write(out.view(torch.int16).cpu().numpy().tobytes())
+"""
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("D", [64, 128])
+def test_copy_pool_and_per_cta_copies_give_the_same_bits(D, tmp_path):
+    """The copy pool (default) and the per-CTA copy items (DFA2_COPY_POOL=0,
+    with and without the copy tail) write the same layer."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for env in ({}, {"DFA2_COPY_POOL": "0"}, {"DFA2_COPY_POOL": "0", "DFA2_COPY_TAIL": "0"}):
+        r = subprocess.run([sys.executable, "-c", _COPY_MODES_SCRIPT, root, str(D)], capture_output=True,
+                           env={**os.environ, **env}, timeout=300)
+        assert r.returncode == 0, r.stderr.decode()[-2000:]
+        outs.append(r.stdout)
+    assert len(outs[0]) > 0 and outs[0] == outs[1] == outs[2]

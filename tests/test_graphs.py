@@ -77,3 +77,4 @@ def test_capturing_a_plan_never_run_is_refused():
     g2.replay()
     torch.cuda.synchronize()
     assert torch.equal(out, ref)
+
