@@ -167,6 +167,13 @@ constexpr bool KEEPLO = D == 64 ? DFA2_KEEPLO64 : DFA2_KEEPLO128;
 #ifndef DFA2_REGS_OTHER64
 #define DFA2_REGS_OTHER64 DFA2_REGS_OTHER
 #endif
+// setmaxnreg split between the control and softmax warpgroups: always with
+// KEEPLO, else on request (DFA2_REGSPLIT64)
+#ifndef DFA2_REGSPLIT64
+#define DFA2_REGSPLIT64 0
+#endif
+template <int D>
+constexpr bool REGSPLIT = KEEPLO<D> || (D == 64 && DFA2_REGSPLIT64);
 template <int D>
 constexpr uint32_t REGS_SOFTMAX = D == 64 ? DFA2_REGS_SOFTMAX64 : DFA2_REGS_SOFTMAX;
 template <int D>
@@ -612,7 +619,7 @@ __global__ void __launch_bounds__(384, 1)
 
     if (warp < 4) {
     // warpgroup 0 (producer / MMA issue) hands registers to the softmax warpgroups
-    if (KEEPLO<D>)
+    if (REGSPLIT<D>)
         regs_dec<REGS_OTHER<D>>();
     if (warp == 0) {
         // ------------------------------------------------ TMA producer
@@ -972,7 +979,7 @@ __global__ void __launch_bounds__(384, 1)
     }
     } else {
         // ------------------------------------------------ softmax lanes
-        if (KEEPLO<D>)
+        if (REGSPLIT<D>)
             regs_inc<REGS_SOFTMAX<D>>();
         const int L = (warp - 4) >> 2;              // 0 = lane A, 1 = lane B
         const int wq = warp & 3;                    // TMEM lane quarter
