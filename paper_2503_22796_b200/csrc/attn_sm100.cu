@@ -199,6 +199,19 @@ static_assert(DFA2_REGS_OTHER + 2 * DFA2_REGS_SOFTMAX <= 3 * 168,
 
 namespace {
 
+// the producer / MMA-issue warps' barrier waits (DFA2_CTL_SLEEP: hardware
+// sleep until the phase completes, so they take no issue slots from the
+// softmax warps of their SMSP while they wait)
+#ifndef DFA2_CTL_SLEEP
+#define DFA2_CTL_SLEEP 0
+#endif
+__device__ __forceinline__ void mbar_wait_ctl(uint32_t bar, uint32_t parity) {
+    if (DFA2_CTL_SLEEP)
+        mbar_wait_sleep(bar, parity);
+    else
+        mbar_wait(bar, parity);
+}
+
 __device__ __forceinline__ void tma_load_q(uint32_t dst, const CUtensorMap* map, uint32_t bar, int32_t c0, int32_t c1,
                                            int32_t c2) {
     if (DFA2_L2_HINTS)
@@ -641,7 +654,7 @@ __global__ void __launch_bounds__(384, 1)
                     if (kc.j == 0) {
                         const int qs = qcount % C::QBUF;
                         const uint32_t qaddr = sbase + C::Q_OFF + qs * 2 * C::TILE_BYTES;
-                        mbar_wait(q_empty(qs), ((qcount / C::QBUF) & 1) ^ 1);
+                        mbar_wait_ctl(q_empty(qs), ((qcount / C::QBUF) & 1) ^ 1);
                         const int nq = w.qtile_b >= 0 ? 2 : 1;
                         if (elect_one()) {
                             mbar_arrive_expect_tx(q_full(qs), nq * C::TILE_BYTES);
@@ -660,7 +673,7 @@ __global__ void __launch_bounds__(384, 1)
                     const int kt = static_cast<int>(args.tiles[w.tile_begin + kc.j] & TILE_INDEX_MASK);
                     const int st = kcount % KS;
                     if (DFA2_TRACE == 3 && lane == 0) DFA2_STAMP(2, kcount, 0);
-                    mbar_wait(k_empty(st), ((kcount / KS) & 1) ^ 1);
+                    mbar_wait_ctl(k_empty(st), ((kcount / KS) & 1) ^ 1);
                     if (DFA2_TRACE == 3 && lane == 0) DFA2_STAMP(2, kcount, 1);
                     if (elect_one()) {
                         mbar_arrive_expect_tx(k_full(st), C::TILE_BYTES);
@@ -677,7 +690,7 @@ __global__ void __launch_bounds__(384, 1)
                 const int kt = static_cast<int>(args.tiles[w.tile_begin + vc.j] & TILE_INDEX_MASK);
                 const int st = vcount % VS;
                 if (DFA2_TRACE == 3 && lane == 0) DFA2_STAMP(2, vcount, 2);
-                mbar_wait(v_empty(st), ((vcount / VS) & 1) ^ 1);
+                mbar_wait_ctl(v_empty(st), ((vcount / VS) & 1) ^ 1);
                 if (DFA2_TRACE == 3 && lane == 0) DFA2_STAMP(2, vcount, 3);
                 if (elect_one()) {
                     mbar_arrive_expect_tx(v_full(st), C::TILE_BYTES);
@@ -710,7 +723,7 @@ __global__ void __launch_bounds__(384, 1)
                 continue;
             const int qs = qcount % C::QBUF;
             const uint32_t qbase = sbase + C::Q_OFF + qs * 2 * C::TILE_BYTES;
-            mbar_wait(q_full(qs), (qcount / C::QBUF) & 1);
+            mbar_wait_ctl(q_full(qs), (qcount / C::QBUF) & 1);
             tc_fence_after();
             const bool has_lane = L == 0 || w.qtile_b >= 0;
             bool first_pv = true, any_s = false;
@@ -728,9 +741,9 @@ __global__ void __launch_bounds__(384, 1)
                 if (u < U) {
                     if (word & need) {
                         if (C::SEP_P && scount >= 1) {  // the lane's softmax has read its previous S
-                            mbar_wait(s_free(L), (scount - 1) & 1);
+                            mbar_wait_ctl(s_free(L), (scount - 1) & 1);
                         }
-                        mbar_wait(k_full(kst), (kcount / KS) & 1);
+                        mbar_wait_ctl(k_full(kst), (kcount / KS) & 1);
                         tc_fence_after();
                         const uint64_t qdesc = smem_desc_sw128(qbase + L * C::TILE_BYTES, 16, 1024);
                         const uint64_t kdesc = smem_desc_sw128(sbase + C::K_OFF + kst * C::TILE_BYTES, 16, 1024);
@@ -751,7 +764,7 @@ __global__ void __launch_bounds__(384, 1)
                     } else {
                         // the tile must be loaded before this use's arrival, or the
                         // arrival could complete the slot's previous phase
-                        mbar_wait(k_full(kst), (kcount / KS) & 1);
+                        mbar_wait_ctl(k_full(kst), (kcount / KS) & 1);
                         if (elect_one()) {
                             mbar_arrive(k_empty(kst));
                             if (u == U - 1) {
@@ -768,9 +781,9 @@ __global__ void __launch_bounds__(384, 1)
                 auto do_pv = [&] {
                 if (u >= 1) {
                     if (prev & need) {
-                        mbar_wait(v_full(vst), (vcount / VS) & 1);
+                        mbar_wait_ctl(v_full(vst), (vcount / VS) & 1);
                         const uint64_t vdesc = smem_desc_sw128(sbase + C::V_OFF + vst * C::TILE_BYTES, C::BOX_BYTES, 1024);
-                        mbar_wait(p_half(L), pcnt & 1);
+                        mbar_wait_ctl(p_half(L), pcnt & 1);
                         tc_fence_after();
                         if (elect_one()) {
 #pragma unroll
@@ -779,7 +792,7 @@ __global__ void __launch_bounds__(384, 1)
                                             vdesc + (kk * 2048 >> 4), IDESC_O, (!first_pv || kk > 4) ? 1u : 0u);
                         }
                         __syncwarp();
-                        mbar_wait(p_full(L), pcnt & 1);
+                        mbar_wait_ctl(p_full(L), pcnt & 1);
                         tc_fence_after();
                         if (elect_one()) {
 #pragma unroll
@@ -796,7 +809,7 @@ __global__ void __launch_bounds__(384, 1)
                         first_pv = false;
                         ++pcnt;
                     } else {
-                        mbar_wait(v_full(vst), (vcount / VS) & 1);
+                        mbar_wait_ctl(v_full(vst), (vcount / VS) & 1);
                         if (elect_one())
                             mbar_arrive(v_empty(vst));
                         __syncwarp();
@@ -839,7 +852,7 @@ __global__ void __launch_bounds__(384, 1)
                     continue;
                 const int qs = qcount % C::QBUF;
                 const uint32_t qbase = sbase + C::Q_OFF + qs * 2 * C::TILE_BYTES;
-                mbar_wait(q_full(qs), (qcount / C::QBUF) & 1);
+                mbar_wait_ctl(q_full(qs), (qcount / C::QBUF) & 1);
                 tc_fence_after();
                 bool first_pv[2] = {true, true};
                 uint32_t prev = 0;
@@ -863,14 +876,14 @@ __global__ void __launch_bounds__(384, 1)
                         auto issue_pv = [&] {
                             if (!v_ready) {
                                 if (DFA2_TRACE == 3 && lane == 0) DFA2_STAMP(3, vcount, 0);
-                                mbar_wait(v_full(vst), (vcount / VS) & 1);
+                                mbar_wait_ctl(v_full(vst), (vcount / VS) & 1);
                                 v_ready = true;
                             }
                             if ((DFA2_TRACE == 1 || DFA2_TRACE == 3) && lane == 0) DFA2_STAMP(L, pcnt[L], 7);
                             // keys 64..127 (P in cols [64,96)) as soon as that half is ready,
                             // then keys 0..63 (cols [0,32))
                             const uint64_t vdesc = smem_desc_sw128(v_addr, C::BOX_BYTES, 1024);
-                            mbar_wait(p_half(L), pcnt[L] & 1);
+                            mbar_wait_ctl(p_half(L), pcnt[L] & 1);
                             tc_fence_after();
                             if (lane == 0) DFA2_STAMP(L, pcnt[L], 3);
                             if (elect_one()) {
@@ -880,7 +893,7 @@ __global__ void __launch_bounds__(384, 1)
                                                 vdesc + (kk * 2048 >> 4), IDESC_O, (!first_pv[L] || kk > 4) ? 1u : 0u);
                             }
                             __syncwarp();
-                            mbar_wait(p_full(L), pcnt[L] & 1);
+                            mbar_wait_ctl(p_full(L), pcnt[L] & 1);
                             tc_fence_after();
                             if (elect_one()) {
 #pragma unroll
@@ -901,11 +914,11 @@ __global__ void __launch_bounds__(384, 1)
                         };
                         auto issue_s = [&] {
                             if (C::SEP_P && scount[L] >= 1) {  // the lane's softmax has read its last S
-                                mbar_wait(s_free(L), (scount[L] - 1) & 1);
+                                mbar_wait_ctl(s_free(L), (scount[L] - 1) & 1);
                                 tc_fence_after();
                             }
                             if (!k_ready) {
-                                mbar_wait(k_full(kst), (kcount / KS) & 1);
+                                mbar_wait_ctl(k_full(kst), (kcount / KS) & 1);
                                 k_ready = true;
                             }
                             if ((DFA2_TRACE == 1 || DFA2_TRACE == 3) && lane == 0) DFA2_STAMP(L, scount[L], 6);
@@ -1159,6 +1172,8 @@ __global__ void __launch_bounds__(384, 1)
                 softmax_tile<D>(sc, oc, sl2, m_ref, l, first, p_half(L), p_full(L), pc, s_free(L), p_free(L),
                                 scnt == 0 ? -1 : static_cast<int>((scnt - 1) & 1), stamp);
                 if (r == 0) DFA2_STAMP(L, scnt, 2);
+                if (DFA2_TRACE == 5 && lane == 0 && args.trace && blockIdx.x == 0 && scnt < 4096)
+                    args.trace[((L * 4096) + scnt) * 8 + 4 + wq] = clock64();  // each warp's softmax end
                 ++scnt;
                 first = false;
                 if (word & snap_bit) {

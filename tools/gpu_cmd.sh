@@ -1,1 +1,1 @@
-for r in 1 2 3 4 5; do DFA2_HOST_STREAMS=1 timeout 300 python tools/e2e_probe.py --steps 40; timeout 300 python tools/e2e_probe.py --steps 40; done
+timeout 1200 python tools/ab_interleaved.py build/ab_cur6.so build/ab_ctlsleep.so --rounds 14 --plans FLUX68,flux_F,flux_A8,sd3_F,sd3_A8,sd3_A2,sd3_A0,flux_C 2>&1 | tee gpurun_out/ab_ctlsleep.txt
