@@ -139,6 +139,14 @@ constexpr bool SPLITLD = D == 64 ? DFA2_SPLITLD64 : DFA2_SPLITLD128;
 // 1: lane A, lane B, control (control highest); 2: control, lane B, lane A;
 // 3: lane B, lane A, control. Interleaved A/B: map 1 is 2% faster at d = 64
 // (SD3), 2% slower at d = 128 than map 0.
+// logical control warps of the producer and the TMEM allocator (0 and 2;
+// the MMA issuers are 1, and 3 at d = 64): which SMSP each busy role sits on
+#ifndef DFA2_PRODUCER_WARP
+#define DFA2_PRODUCER_WARP 0
+#endif
+#ifndef DFA2_ALLOC_WARP
+#define DFA2_ALLOC_WARP 2
+#endif
 #ifndef DFA2_WARPMAP64
 #define DFA2_WARPMAP64 1
 #endif
@@ -601,14 +609,14 @@ __global__ void __launch_bounds__(384, 1)
         }
         fence_mbar_init();
     }
-    if (warp == 0 && lane == 0) {
+    if (warp == DFA2_PRODUCER_WARP && lane == 0) {
         tma_prefetch_desc(&tmq);
         tma_prefetch_desc(&tmk);
         tma_prefetch_desc(&tmv);
         tma_prefetch_desc(&tmo);
         tma_prefetch_desc(&tmc);
     }
-    if (warp == 2) {
+    if (warp == DFA2_ALLOC_WARP) {
         tmem_alloc(smem_u32(tmem_slot), C::TMEM_COLS);
         tmem_relinquish();
     }
@@ -634,7 +642,7 @@ __global__ void __launch_bounds__(384, 1)
     // warpgroup 0 (producer / MMA issue) hands registers to the softmax warpgroups
     if (REGSPLIT<D>)
         regs_dec<REGS_OTHER<D>>();
-    if (warp == 0) {
+    if (warp == DFA2_PRODUCER_WARP) {
         // ------------------------------------------------ TMA producer
         // The whole warp walks the schedule (warp-uniform control flow keeps
         // coordinates in uniform registers); one elected lane issues.
@@ -1405,7 +1413,7 @@ __global__ void __launch_bounds__(384, 1)
             atomicExch(args.copy_ctr + 1, 0);
         }
     }
-    if (warp == 2)
+    if (warp == DFA2_ALLOC_WARP)
         tmem_dealloc(tmem, C::TMEM_COLS);
 }
 
