@@ -38,8 +38,29 @@
 namespace dfa2 {
 
 namespace detail {
+namespace {
+constexpr std::size_t kHuge = std::size_t{2} << 20;
+// Freed large buffers are kept (up to 8 / 2 GB) and handed back for the same
+// rounded size: the drop-in returns a fresh output Tensor every call, and
+// without reuse each call re-faults (and the kernel re-zeroes) its 208 MB.
+struct BigCache {
+    std::mutex mu;
+    std::vector<std::pair<std::size_t, void*>> free;
+    std::size_t bytes = 0;
+    static constexpr std::size_t kMaxBytes = std::size_t{2} << 30;
+    static constexpr std::size_t kMaxEntries = 8;
+    ~BigCache() {
+        for (auto& [n, p] : free)
+            std::free(p);
+    }
+};
+BigCache& big_cache() {
+    static BigCache* c = new BigCache;  // never destroyed: tensors may outlive static destruction
+    return *c;
+}
+}  // namespace
+
 DFA2_API void* host_alloc(std::size_t bytes) {
-    constexpr std::size_t kHuge = std::size_t{2} << 20;
     if (bytes < kHuge) {
         void* p = std::malloc(bytes ? bytes : 1);
         if (!p)
@@ -47,13 +68,36 @@ DFA2_API void* host_alloc(std::size_t bytes) {
         return p;
     }
     const std::size_t rounded = (bytes + kHuge - 1) / kHuge * kHuge;
+    {
+        BigCache& c = big_cache();
+        std::lock_guard<std::mutex> lk(c.mu);
+        for (std::size_t i = 0; i < c.free.size(); ++i)
+            if (c.free[i].first == rounded) {
+                void* p = c.free[i].second;
+                c.bytes -= rounded;
+                c.free.erase(c.free.begin() + static_cast<std::ptrdiff_t>(i));
+                return p;
+            }
+    }
     void* p = std::aligned_alloc(kHuge, rounded);
     if (!p)
         throw std::bad_alloc();
     madvise(p, rounded, MADV_HUGEPAGE);  // advisory: transparent huge pages where enabled
     return p;
 }
-DFA2_API void host_free(void* p, std::size_t) noexcept { std::free(p); }
+DFA2_API void host_free(void* p, std::size_t bytes) noexcept {
+    if (p && bytes >= kHuge) {
+        const std::size_t rounded = (bytes + kHuge - 1) / kHuge * kHuge;
+        BigCache& c = big_cache();
+        std::lock_guard<std::mutex> lk(c.mu);
+        if (c.free.size() < BigCache::kMaxEntries && c.bytes + rounded <= BigCache::kMaxBytes) {
+            c.free.push_back({rounded, p});
+            c.bytes += rounded;
+            return;
+        }
+    }
+    std::free(p);
+}
 }  // namespace detail
 
 DFA2_API void throw_status(int status) {
