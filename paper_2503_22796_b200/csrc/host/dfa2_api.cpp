@@ -385,7 +385,12 @@ public:
     enum Mode { kCopy, kRound };
     void up(const void* src, void* dst_dev, size_t bytes) { move({Seg{src, dst_dev, bytes}}, true); }
     void down(const void* src_dev, void* dst, size_t bytes) { move({Seg{src_dev, dst, bytes}}, false); }
-    void move(const std::vector<Seg>& segs, bool to_device, Mode mode = kCopy) {
+    // on_issued(hi, copy_stream): called after the DMAs of the flat bytes
+    // [0, hi) have been enqueued (uploads), so a caller can order work on
+    // another stream after them (an event on copy_stream) while the pool
+    // keeps filling the next chunks.
+    using Issued = std::function<void(size_t, cudaStream_t)>;
+    void move(const std::vector<Seg>& segs, bool to_device, Mode mode = kCopy, const Issued& on_issued = {}) {
         init();
         cuda_check(cudaDeviceSynchronize(), "sync");  // device-side producers of the sources are done
         // the transfer as a flat byte range [0, total) over the segments
@@ -444,6 +449,8 @@ public:
                                                cudaMemcpyHostToDevice, st_),
                                "upload");
                 });
+                if (on_issued)
+                    on_issued(hi, st_);
             } else {
                 pieces(lo, hi, [&](const Seg& sg, size_t off, size_t n, size_t at) {
                     cuda_check(cudaMemcpyAsync(pin_[b] + at, static_cast<const char*>(sg.src) + off, n,
@@ -499,7 +506,7 @@ struct UpPiece {
     int64_t n;
     void* dst;
 };
-void upload_bf16_many(const std::vector<UpPiece>& ps) {
+void upload_bf16_many(const std::vector<UpPiece>& ps, const HostMover::Issued& on_issued = {}) {
     // rounded to bf16 by the pool while it fills the pinned chunks: half the
     // PCIe bytes of an f32 upload, and no device-side conversion
     std::vector<Seg> segs;
@@ -507,7 +514,7 @@ void upload_bf16_many(const std::vector<UpPiece>& ps) {
         if (p.n > 0)
             segs.push_back(Seg{p.src, p.dst, static_cast<size_t>(p.n) * 2});
     if (!segs.empty())
-        g_mover.move(segs, true, HostMover::kRound);
+        g_mover.move(segs, true, HostMover::kRound, on_issued);
 }
 
 void download_bf16(const void* src, int64_t n, float* dst) {
@@ -984,35 +991,68 @@ DFA2_API Tensor multi_strategy_attention(const Tensor& q, const Tensor& k, const
     void* dv = sv.get(static_cast<size_t>(numel) * 2);
     void* dout = so.get(static_cast<size_t>(numel) * 2);
     // only computed heads' inputs cross PCIe (a Cached head reads its slot),
-    // one transfer per run of consecutive computed heads
+    // in ONE pipelined transfer ordered by head group: as soon as a group's
+    // last chunk is enqueued, the group's launch is enqueued behind it (an
+    // event on the copy stream), so the GPU computes group g while the host
+    // rounds group g+1 and only the last group's compute is exposed
     const int64_t hs = n * d;
-    std::vector<UpPiece> ups;
-    for (int64_t h0 = 0; h0 < H;) {
-        if (plan.strategies[h0].kind == StrategyKind::cached) {
-            ++h0;
-            continue;
-        }
-        int64_t h1 = h0 + 1;
-        while (h1 < H && plan.strategies[h1].kind != StrategyKind::cached)
-            ++h1;
-        ups.push_back({q.f32() + h0 * hs, (h1 - h0) * hs, static_cast<char*>(dq) + h0 * hs * 2});
-        ups.push_back({k.f32() + h0 * hs, (h1 - h0) * hs, static_cast<char*>(dk) + h0 * hs * 2});
-        ups.push_back({v.f32() + h0 * hs, (h1 - h0) * hs, static_cast<char*>(dv) + h0 * hs * 2});
-        h0 = h1;
-    }
-    const bool prof = std::getenv("DFA2_HOST_PROFILE") != nullptr;
-    auto now = [] { return std::chrono::steady_clock::now(); };
-    auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
-    const auto t0 = now();
-    upload_bf16_many(ups);
-    if (prof) cudaDeviceSynchronize();
-    const auto t1 = now();
     std::vector<int32_t> kinds;
     std::vector<int64_t> wins;
     plan_arrays(plan, kinds, wins);
     const dfa2c_dims cd = cdims(dims);
-    check(dfa2c_mha_forward(dq, dk, dv, 1, &cd, block_size, kinds.data(), wins.data(), dev, layer, t, dout,
-                            nullptr));
+    std::vector<int64_t> computed;
+    for (int64_t h = 0; h < H; ++h)
+        if (plan.strategies[h].kind != StrategyKind::cached)
+            computed.push_back(h);
+    constexpr size_t kGroups = 4;
+    const size_t G = std::max<size_t>(1, std::min(kGroups, computed.size()));
+    std::vector<UpPiece> ups;
+    std::vector<size_t> group_end(G, 0);  // flat (bf16) bytes through each group
+    std::vector<std::vector<int32_t>> group_kinds(G, kinds);
+    size_t flat = 0;
+    for (size_t g = 0; g < G; ++g) {
+        std::vector<bool> in(static_cast<size_t>(H), g == 0);  // group 0 also copies the Cached heads
+        for (int64_t h = 0; h < H; ++h)
+            if (g == 0 && plan.strategies[h].kind != StrategyKind::cached)
+                in[static_cast<size_t>(h)] = false;
+        for (size_t i = computed.size() * g / G; i < computed.size() * (g + 1) / G; ++i) {
+            const int64_t h = computed[i];
+            in[static_cast<size_t>(h)] = true;
+            for (const auto& [src, dst] :
+                 {std::pair<const float*, void*>{q.f32(), dq}, {k.f32(), dk}, {v.f32(), dv}}) {
+                ups.push_back({src + h * hs, hs, static_cast<char*>(dst) + h * hs * 2});
+                flat += static_cast<size_t>(hs) * 2;
+            }
+        }
+        group_end[g] = flat;
+        for (int64_t h = 0; h < H; ++h)
+            if (!in[static_cast<size_t>(h)])
+                group_kinds[g][h] |= DFA2C_SKIP;
+    }
+    thread_local cudaEvent_t ev_group = [] {
+        cudaEvent_t e;
+        cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+        return e;
+    }();
+    size_t next = 0;
+    auto launch_ready = [&](size_t issued, cudaStream_t copy_stream) {
+        while (next < G && group_end[next] <= issued) {
+            if (copy_stream) {
+                cuda_check(cudaEventRecord(ev_group, copy_stream), "event");
+                cuda_check(cudaStreamWaitEvent(nullptr, ev_group, 0), "wait");
+            }
+            check(dfa2c_mha_forward(dq, dk, dv, 1, &cd, block_size, group_kinds[next].data(), wins.data(), dev,
+                                    layer, t, dout, nullptr));
+            ++next;
+        }
+    };
+    const bool prof = std::getenv("DFA2_HOST_PROFILE") != nullptr;
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+    const auto t0 = now();
+    upload_bf16_many(ups, launch_ready);
+    launch_ready(flat, nullptr);  // groups without uploads (all-Cached layers); move() already synced
+    const auto t1 = now();
     if (prof) cudaDeviceSynchronize();
     const auto t2 = now();
     Tensor out = Tensor::uninitialized_f32(q.shape());  // the download writes every element
@@ -1020,8 +1060,8 @@ DFA2_API Tensor multi_strategy_attention(const Tensor& q, const Tensor& k, const
     download_bf16(dout, numel, out.f32());
     const auto t4 = now();
     if (prof)
-        std::fprintf(stderr, "[dfa2 host] upload %.2f ms, kernel %.2f ms, out alloc %.2f ms, download %.2f ms\n",
-                     ms(t0, t1), ms(t1, t2), ms(t2, t3), ms(t3, t4));
+        std::fprintf(stderr, "[dfa2 host] upload + launches %.2f ms, rest of the kernels %.2f ms, out alloc %.2f ms, "
+                     "download %.2f ms\n", ms(t0, t1), ms(t1, t2), ms(t2, t3), ms(t3, t4));
     for (int64_t h = 0; h < H; ++h)
         if (plan.strategies[h].kind != StrategyKind::cached)
             CacheAccess::committed(cache, layer, h, t);
