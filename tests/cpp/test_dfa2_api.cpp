@@ -131,6 +131,26 @@ static double max_rel(const float* got, const std::vector<double>& want) {
 }
 
 // ---------------------------------------------------------------- host-only
+TEST(large_tensor_storage_is_reused_and_zeros_still_zero, false) {
+    // freed large buffers are kept for reuse (no per-call page faults of
+    // fresh outputs); zeros() must still zero a recycled buffer
+    const int64_t n = int64_t{3} << 20;  // 12 MB of f32
+    const float* first = nullptr;
+    {
+        Tensor t = Tensor::zeros({n});
+        float* p = t.f32();
+        for (int64_t i = 0; i < n; i += 4099)
+            p[i] = 7.0f;  // garbage left behind
+        first = p;
+    }
+    Tensor z = Tensor::zeros({n});
+    CHECK(z.f32() == first);  // the same storage came back
+    bool all_zero = true;
+    for (int64_t i = 0; i < n; ++i)
+        all_zero = all_zero && z.f32()[i] == 0.0f;
+    CHECK(all_zero);
+}
+
 TEST(arrow_mask_known_answers, false) {  // test_arrow.cpp:53-92
     const BlockMask m = build_arrow_mask({dims_of(1, 16, 512, 128), 128, 0});
     CHECK(m.n_query_blocks == 5 && m.n_key_blocks == 5);
