@@ -2296,8 +2296,11 @@ int dfa2c_mha_forward_host(const void* q, const void* k, const void* v, int64_t 
         // near-equal head count; each group is copied in as maximal runs of
         // consecutive heads (one 2-D copy per run and tensor: width = run
         // bytes, height = batch, pitch = one sample).
-        constexpr int kGroups = 6;
-        static_assert(kGroups <= HostPipe::kMaxGroups, "event slots");
+        static const int kGroups = [] {  // DFA2_HOST_GROUPS (1..8; A/B knob)
+            const char* e = std::getenv("DFA2_HOST_GROUPS");
+            const int g = e ? std::atoi(e) : 6;
+            return std::max(1, std::min(g, HostPipe::kMaxGroups));
+        }();
         std::vector<int64_t> computed;
         for (int64_t h = 0; h < H; ++h)
             if (!skipped(kinds[h]) && kinds[h] != DFA2C_CACHED)

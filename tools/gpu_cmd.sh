@@ -1,1 +1,1 @@
-for r in 1 2 3 4; do timeout 300 python tools/e2e_probe.py --steps 40; DFA2_HOST_GROUPS_DESC=1 timeout 300 python tools/e2e_probe.py --steps 40 | sed 's/^/desc /'; done
+for r in 1 2 3; do for g in 6 8 4 3; do DFA2_HOST_GROUPS=$g timeout 300 python tools/e2e_probe.py --steps 40 | sed "s/^/groups $g /"; done; done
