@@ -1,1 +1,5 @@
-for r in 1 2 3; do for g in 6 8 4 3; do DFA2_HOST_GROUPS=$g timeout 300 python tools/e2e_probe.py --steps 40 | sed "s/^/groups $g /"; done; done
+P="F F F F F F A8 A8 A8 A8 A8 A8 A0 A0 A0 A0 A0 A0 C C C C C C"
+for r in 1 2; do for l in build/ab_eqgroups.so paper_2503_22796_b200/libdfa2_b200.so; do
+  DFA2_LIB=$l timeout 300 python tools/e2e_probe.py --steps 30 | sed "s|^|$(basename $l) |"
+  DFA2_LIB=$l timeout 300 python tools/e2e_probe.py --steps 30 --plan "$P" | sed "s|^|$(basename $l) |"
+done; done
